@@ -1,0 +1,176 @@
+/*
+ * es.h — C ABI of the B200-native evosax hot path (libes_b200.so).
+ *
+ * One generation of the ask → evaluate → tell loop of PAPER.md §2.1 (Listing 1) for the
+ * diagonal-Gaussian ES family of Table 1 — OpenAI-ES, PGPE, SNES and
+ * Sep-CMA-ES — batched over R independent runs (the paper's vmap over seeds or
+ * hyperparameters) and optionally population-sharded over W GPUs with NCCL (the paper's
+ * Future Work). The arithmetic is frozen in NUMERICS.md (N1–N15).
+ *
+ * Conventions (all entry points):
+ *   - Minimisation. Fitness is "lower is better".
+ *   - Every call is asynchronous and stream-ordered on the cudaStream_t given (NULL = legacy
+ *     default stream); no call synchronises the device unless it is handed host memory.
+ *   - Buffer arguments may be DEVICE pointers (no copy) or HOST pointers (pinned or pageable; the
+ *     library stages them through device scratch with cudaMemcpyAsync and, for host outputs,
+ *     synchronises the stream before returning). Layouts are row-major and dense.
+ *   - Arguments are validated before any launch or state change; on error nothing is modified.
+ *   - No C++ exception crosses the ABI. One context is used by one host thread at a time.
+ *   - Member j of run r on rank w is global member w*(N/W) + j (antithetic pairs never straddle
+ *     ranks). Noise is a pure function of (seed_r, direction, generation, dim): results are
+ *     independent of R, W and launch shape (NUMERICS N2).
+ */
+#ifndef ES_B200_H
+#define ES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *es_stream_t; /* == cudaStream_t */
+
+typedef enum { ES_OPENAI_ES = 0, ES_PGPE = 1, ES_SNES = 2, ES_SEP_CMA_ES = 3 } es_algo_t;
+
+typedef enum {
+  ES_FIT_SPHERE = 0,     /* Σ x_d²                                  (P:212 BBOB)      */
+  ES_FIT_ROSENBROCK = 1, /* Σ 100(x_{d+1} − x_d²)² + (1 − x_d)²                              */
+  ES_FIT_RASTRIGIN = 2,  /* 10D + Σ (x_d² − 10 cos 2πx_d), cancellation-free form (N7)         */
+  ES_FIT_MLP = 3         /* synthetic tanh-MLP regression fitness (N14)     */
+} es_fitness_t;
+
+typedef enum {
+  ES_SUCCESS = 0,
+  ES_ERR_INVALID_ARG = 1, /* bad sizes / hyperparameters / NULL pointers                         */
+  ES_ERR_BAD_STATE = 2,   /* call order violated (tell without ask, problem not set, ...)       */
+  ES_ERR_CUDA = 3,        /* CUDA launch or runtime error; message in es_last_error            */
+  ES_ERR_NCCL = 4,        /* NCCL error; the context is unusable afterwards                     */
+  ES_ERR_OOM = 5,         /* device allocation failed                                           */
+  ES_ERR_UNSUPPORTED = 6  /* valid request outside what this build implements                   */
+} es_status_t;
+
+/* Hyperparameters of one run. Defaults: PAPER.md App. B "Ant" column (P:285–286, P:301–308,
+ * P:323–332). Fields an algorithm does not use are ignored. */
+typedef struct {
+  uint64_t seed;              /* Philox key of the run (N1, N2)                                */
+  float init_min, init_max;   /* mean_0 ~ U[init_min, init_max] from the INIT stream (N6)       */
+  float sigma_init;           /* σ_0: scalar (OpenAI-ES, Sep-CMA-ES) or every σ_d (PGPE, SNES) */
+  float sigma_decay, sigma_limit; /* σ ← max(σ·decay, limit) per generation (OpenAI-ES, PGPE)  */
+  float lrate_init, lrate_decay, lrate_limit; /* Adam learning-rate schedule (OpenAI-ES, PGPE)  */
+  float beta1, beta2, eps;    /* Adam: 0.9, 0.999, 1e-8                                 */
+  float sigma_lrate;          /* PGPE σ learning rate: 0.2                              */
+  float sigma_max_change;     /* PGPE relative σ clip: 0.2                              */
+  float temperature;          /* SNES β                                          */
+  float elite_ratio;          /* Sep-CMA-ES μ = ⌊elite_ratio·N⌋                         */
+  int32_t shaping;            /* 0 = centered rank; 1 = raw fitness (OpenAI-ES,
+                                 PGPE only; for gradient tests)                                 */
+} es_run_params_t;
+
+/* Fields readable with es_get / writable with es_set (checkpoint / resume). Shapes per context. */
+typedef enum {
+  ES_FIELD_MEAN = 0,     /* float [R][D]                                                     */
+  ES_FIELD_SIGMA_D = 1,  /* float [R][D]  per-dimension σ (PGPE, SNES)                       */
+  ES_FIELD_ADAM_M = 2,   /* float [R][D]  (OpenAI-ES, PGPE)                                   */
+  ES_FIELD_ADAM_V = 3,   /* float [R][D]                                                     */
+  ES_FIELD_P_SIGMA = 4,  /* float [R][D]  Sep-CMA-ES evolution path p_σ                      */
+  ES_FIELD_P_C = 5,      /* float [R][D]  Sep-CMA-ES evolution path p_c                       */
+  ES_FIELD_C = 6,        /* float [R][D]  Sep-CMA-ES diagonal covariance                      */
+  ES_FIELD_BEST_X = 7,   /* float [R][D]  best member so far                           */
+  ES_FIELD_BEST_F = 8,   /* float [R]     best fitness so far                          */
+  ES_FIELD_SIGMA = 9,    /* float [R]     scalar σ (OpenAI-ES, Sep-CMA-ES)                    */
+  ES_FIELD_LRATE = 10,   /* float [R]     current Adam learning rate                          */
+  ES_FIELD_GEN = 11,     /* uint32 [R]    completed tells t                                   */
+  ES_FIELD_SHAPED = 12,  /* float [R][N]  last tell's shaped fitness: c_j (N10) or ω_j (N11)  */
+  ES_FIELD_RANK_S = 13,  /* int32 [R][N]  last tell's tie-group start s_j (N9)               */
+  ES_FIELD_RANK_E = 14,  /* int32 [R][N]  last tell's tie-group end e_j (N9)                 */
+  ES_FIELD_PERM = 15,    /* int32 [R][N]  member at each sorted position (N9)                */
+  ES_FIELD_FITNESS = 16, /* float [R][N]  last tell's full (gathered) fitness                 */
+  ES_NUM_FIELDS = 17
+} es_field_t;
+
+typedef struct es_ctx es_ctx_t;
+
+/* Create a context: allocates the R runs' state on the current device and initialises it
+ * (Listing 1 `strategy.initialize`; N6). popsize N is the GLOBAL population; each rank
+ * owns N/W members (= N/(2W) antithetic pairs or N/W directions). For world_size > 1,
+ * nccl_unique_id points at the 128-byte ncclUniqueId that rank 0 created and broadcast
+ * (e.g. via torch.distributed); it must be NULL when world_size == 1.
+ * Errors: ES_ERR_INVALID_ARG if N < 2, D < 1, R < 1, N odd (OpenAI-ES/PGPE), N mod W != 0,
+ * N/W odd (OpenAI-ES/PGPE), ⌊elite_ratio·N⌋ < 1 (Sep-CMA-ES), negative σ_init, non-positive
+ * lrate_init (OpenAI-ES/PGPE), world_rank outside [0, W); ES_ERR_UNSUPPORTED if N > 16384;
+ * ES_ERR_OOM / ES_ERR_CUDA / ES_ERR_NCCL on allocation / runtime failure. *out is NULL on error.
+ * Ownership: the context owns every state buffer and the NCCL communicator. */
+es_status_t es_init(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t popsize,
+                    int64_t num_dims, const es_run_params_t *params /* host [num_runs] */,
+                    int32_t world_rank, int32_t world_size, const void *nccl_unique_id,
+                    es_stream_t stream);
+
+/* ask: write this rank's population x = m + σ·z (N6), float [R][N/W][D]. Idempotent within
+ * a generation. Errors: ES_ERR_INVALID_ARG for NULL x. */
+es_status_t es_ask(es_ctx_t *ctx, float *x, es_stream_t stream);
+
+/* evaluate: fitness[n] = f(x[n]) for n rows of length D (N7; MLP: N14).
+ * Context-free for the BBOB functions (ctx may be NULL); ES_FIT_MLP needs a context on which
+ * es_set_mlp_problem was called and D equal to its parameter count. x float [n][D], fitness
+ * float [n]. Errors: ES_ERR_INVALID_ARG (n < 0, D < 1, unknown fn), ES_ERR_BAD_STATE (MLP
+ * problem not set). */
+es_status_t es_eval_bbob(es_ctx_t *ctx, es_fitness_t fn, const float *x, int64_t n, int64_t num_dims,
+                    float *fitness, es_stream_t stream);
+
+/* tell: update every run from this rank's fitness slice, float [R][N/W]. Performs the
+ * all-gather of fitness (W>1), ranks/shapes (N9–N11), best tracking, the regenerating reduction
+ * over directions (N12; z is never stored — x is NOT an input, a documented departure from
+ * P:96's tell(x, fitness, ...)), the all-reduce of the direction sums (W>1), the update and
+ * t ← t+1. Errors: ES_ERR_BAD_STATE if no es_ask since the last tell; ES_ERR_INVALID_ARG for
+ * NULL fitness. */
+es_status_t es_tell(es_ctx_t *ctx, const float *fitness, es_stream_t stream);
+
+/* Synthetic fitness for tell-only sweeps (N15): fitness[r][j], j over this rank's members. */
+es_status_t es_synth_fitness(es_ctx_t *ctx, float *fitness, es_stream_t stream);
+
+/* Copy a state field out (es_get) or in (es_set); dst/src may be host or device. Errors:
+ * ES_ERR_INVALID_ARG for an unknown field or one this algorithm does not keep. */
+es_status_t es_get(es_ctx_t *ctx, es_field_t field, void *dst, es_stream_t stream);
+es_status_t es_set(es_ctx_t *ctx, es_field_t field, const void *src, es_stream_t stream);
+
+/* MLP fitness problem (N14): widths[0..n_widths) layer widths (input first), `batch` inputs
+ * drawn from the DATA stream of data_seed, teacher weights from the TEACHER stream. Flattening of
+ * a parameter vector: per layer W as [in][out] row-major then b[out], layers in order.
+ * Errors: ES_ERR_INVALID_ARG for n_widths < 2, widths not multiples of 16, batch not 128. */
+es_status_t es_set_mlp_problem(es_ctx_t *ctx, const int32_t *widths, int32_t n_widths,
+                               int32_t batch, uint64_t data_seed, es_stream_t stream);
+
+/* Number of parameters of an MLP with these widths (Σ in·out + out); -1 on bad input. */
+int64_t es_mlp_num_params(const int32_t *widths, int32_t n_widths);
+
+/* Sizes of the context: R, N (global), N/W (local), D, P (global directions), W, rank. */
+es_status_t es_shape(const es_ctx_t *ctx, int64_t out[7]);
+
+/* Number of kernels this library launched on behalf of the context since creation. */
+int64_t es_kernel_launches(const es_ctx_t *ctx);
+
+/* Diagnostics for the parity tests: evaluate one NUMERICS primitive elementwise on the device.
+ *   which = 0  Philox4x32-10 (N1): in uint32 [n][6] = (c0, c1, c2, c3, k0, k1) → out uint32 [n][4]
+ *   which = 1  LN (N4):            in float [n]                                 → out float [n]
+ *   which = 2  SINCOS2PI (N5):     in float [n]                                 → out float [n][2]
+ *   which = 3  normals (N2):       in uint32 [n][6] = (q, i, t, tag, k0, k1)    → out float [n][4]
+ * in/out are device pointers. Errors: ES_ERR_INVALID_ARG for unknown `which` or n < 0. */
+es_status_t es_debug_primitive(int32_t which, const void *in, void *out, int64_t n,
+                               es_stream_t stream);
+
+es_status_t es_destroy(es_ctx_t *ctx);
+
+/* Last error message of the context (or of the calling thread when ctx is NULL). */
+const char *es_last_error(const es_ctx_t *ctx);
+const char *es_status_string(es_status_t s);
+
+/* Size of ncclUniqueId and a helper creating one (rank 0), so that bindings need no NCCL. */
+int32_t es_nccl_unique_id_size(void);
+es_status_t es_nccl_get_unique_id(void *out /* host, es_nccl_unique_id_size() bytes */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ES_B200_H */

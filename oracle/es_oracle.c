@@ -119,6 +119,26 @@ void orc_direction(uint64_t seed, uint32_t i, uint32_t t, int64_t D, float *z) {
   }
 }
 
+/* z of direction i at generation t for the run's dimensions (global indices when r->dims). */
+static void run_direction(const orc_run_t *r, uint32_t i, uint32_t t, float *z) {
+  if (!r->dims) {
+    orc_direction(r->p.seed, i, t, r->num_dims, z);
+    return;
+  }
+  float n[4];
+  int64_t cur = -1;
+  for (int64_t d = 0; d < r->num_dims; ++d) {
+    int64_t g = r->dims[d];
+    if (g / 4 != cur) {
+      cur = g / 4;
+      orc_normals4(r->p.seed, (uint32_t)cur, i, t, 0u, n);
+    }
+    z[d] = n[g % 4];
+  }
+}
+
+static int64_t gdim(const orc_run_t *r, int64_t d) { return r->dims ? r->dims[d] : d; }
+
 /* ---------------- N6 init / ask ---------------- */
 static int is_antithetic(int algo) { return algo == ORC_OPENAI_ES || algo == ORC_PGPE; }
 
@@ -138,9 +158,10 @@ int orc_init(orc_run_t *r) {
   uint32_t key[2] = {(uint32_t)p->seed, (uint32_t)(p->seed >> 32)};
   float *mean = vf(r, ORC_V_MEAN);
   for (int64_t d = 0; d < D; ++d) {
-    uint32_t ctr[4] = {(uint32_t)(d / 4), 0u, 0u, 1u}, o[4];
+    int64_t g = gdim(r, d);
+    uint32_t ctr[4] = {(uint32_t)(g / 4), 0u, 0u, 1u}, o[4];
     orc_philox4x32_10(ctr, key, o);
-    mean[d] = fmaf(p->init_max - p->init_min, orc_u_b(o[d % 4]), p->init_min);
+    mean[d] = fmaf(p->init_max - p->init_min, orc_u_b(o[g % 4]), p->init_min);
   }
   for (int64_t d = 0; d < D; ++d) {
     vf(r, ORC_V_SIGMA)[d] = p->sigma_init;
@@ -160,7 +181,8 @@ int orc_init(orc_run_t *r) {
   r->mu = 0;
   r->mueff = r->c_sigma = r->d_sigma = r->c_c = r->c_1 = r->c_mu = r->chi_d = 0.0;
   r->eta_sigma = 0.0;
-  double Dd = (double)D;
+  if (!r->dims) r->full_dims = D;
+  double Dd = (double)r->full_dims;
   if (r->algo == ORC_SNES) {
     /* N11 SNES utilities: w = softmax(beta * (rank/N - 0.5)), rank(best) = N-1 */
     double *u = (double *)malloc(sizeof(double) * (size_t)N);
@@ -212,7 +234,7 @@ void orc_member(const orc_run_t *r, int32_t j, float *x) {
   uint32_t i = anti ? (uint32_t)(j / 2) : (uint32_t)j;
   int neg = anti && (j % 2 == 1);
   float *z = (float *)malloc(sizeof(float) * (size_t)D);
-  orc_direction(r->p.seed, i, r->t, D, z);
+  run_direction(r, i, r->t, z);
   for (int64_t d = 0; d < D; ++d) {
     float s;
     switch (r->algo) {
@@ -331,7 +353,7 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
     for (int32_t i = 0; i < P; ++i) {
       double a = (double)sh[2 * i] - (double)sh[2 * i + 1];
       double h = ((double)sh[2 * i] + (double)sh[2 * i + 1]) * 0.5 - bbar;
-      orc_direction(r->p.seed, (uint32_t)i, r->t, D, z);
+      run_direction(r, (uint32_t)i, r->t, z);
       for (int64_t d = 0; d < D; ++d) {
         G0[d] += a * (double)z[d];
         if (r->algo == ORC_PGPE) G1[d] += h * ((double)z[d] * (double)z[d] - 1.0);
@@ -342,7 +364,7 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
     for (int32_t j = 0; j < N; ++j) {
       double w = (double)sh[j];
       if (sh[j] == 0.0f) continue; /* outside the elite (Sep-CMA); contributes exactly 0 */
-      orc_direction(r->p.seed, (uint32_t)j, r->t, D, z);
+      run_direction(r, (uint32_t)j, r->t, z);
       for (int64_t d = 0; d < D; ++d) {
         double zd = (double)z[d];
         G0[d] += w * zd;
@@ -431,7 +453,7 @@ int orc_tell(orc_run_t *r, const float *f) {
     double norm = sqrt(norm2);
     float sig_new = r->sigma * (float)exp((r->c_sigma / r->d_sigma) * (norm / r->chi_d - 1.0));
     double lhs = norm / sqrt(1.0 - pow(1.0 - r->c_sigma, 2.0 * (double)(r->t + 1)));
-    int hs = lhs < (1.4 + 2.0 / ((double)D + 1.0)) * r->chi_d;
+    int hs = lhs < (1.4 + 2.0 / ((double)r->full_dims + 1.0)) * r->chi_d;
     const float omcc = (float)(1.0 - r->c_c);
     const float kc = hs ? (float)sqrt(r->c_c * (2.0 - r->c_c) * r->mueff) : 0.0f;
     const float aC = (float)(1.0 - r->c_1 - r->c_mu +

@@ -51,6 +51,13 @@ typedef struct {
   double mueff, c_sigma, d_sigma, c_c, c_1, c_mu, chi_d, eta_sigma;
   float *vec;        /* caller-owned [ORC_NV][D] */
   float *wpos;       /* caller-owned [N] position weights (SNES / Sep-CMA) */
+  /* Optional dimension subset: when dims != NULL the run holds only the num_dims global dimensions
+   * dims[0..num_dims) of a problem with full_dims dimensions (noise counters use the global
+   * index; D-dependent constants use full_dims). Exact for every per-dimension quantity of
+   * OpenAI-ES / PGPE / SNES (their updates are elementwise given the ranks); Sep-CMA-ES's global
+   * ||p_sigma|| needs dims == NULL. Used to check full-size GPU runs on sampled dimensions. */
+  const int64_t *dims;
+  int64_t full_dims;
 } orc_run_t;
 
 /* N1–N5 primitives */

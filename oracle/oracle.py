@@ -48,7 +48,8 @@ class RunT(C.Structure):
                 ("mu", C.c_int32), ("mueff", C.c_double), ("c_sigma", C.c_double),
                 ("d_sigma", C.c_double), ("c_c", C.c_double), ("c_1", C.c_double),
                 ("c_mu", C.c_double), ("chi_d", C.c_double), ("eta_sigma", C.c_double),
-                ("vec", C.POINTER(C.c_float)), ("wpos", C.POINTER(C.c_float))]
+                ("vec", C.POINTER(C.c_float)), ("wpos", C.POINTER(C.c_float)),
+                ("dims", C.POINTER(C.c_int64)), ("full_dims", C.c_int64)]
 
 
 _lib = None
@@ -178,9 +179,14 @@ DEFAULTS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=0.999,
 class Run:
     """One oracle run (state owned by numpy arrays)."""
 
-    def __init__(self, algo, popsize, num_dims, seed=0, **params):
+    def __init__(self, algo, popsize, num_dims, seed=0, dims=None, **params):
+        """dims: optional sorted global dimension indices (num_dims is then the full D)."""
         kw = dict(DEFAULTS)
         kw.update(params)
+        full = num_dims
+        if dims is not None:
+            self.dims = np.ascontiguousarray(dims, dtype=np.int64)
+            num_dims = len(self.dims)
         self.vec = np.zeros((NV, num_dims), dtype=np.float32)
         self.wpos = np.zeros(popsize, dtype=np.float32)
         self.r = RunT()
@@ -188,6 +194,9 @@ class Run:
         self.r.p = Params(seed=seed, **kw)
         self.r.vec = _p(self.vec, C.c_float)
         self.r.wpos = _p(self.wpos, C.c_float)
+        if dims is not None:
+            self.r.dims = _p(self.dims, C.c_int64)
+        self.r.full_dims = full
         if lib().orc_init(C.byref(self.r)) != 0:
             raise ValueError("oracle init rejected the arguments")
 

@@ -1,0 +1,15 @@
+"""B200-native hot path of evosax (arXiv:2212.04180): batched diagonal-Gaussian ES generations
+(OpenAI-ES, PGPE, SNES, Sep-CMA-ES) on hand-written sm_100a kernels behind the C ABI include/es.h.
+"""
+from ._lib import (MLP, OPENAI_ES, PGPE, RASTRIGIN, ROSENBROCK, SEP_CMA_ES, SNES, SPHERE, ESError,
+                   lib)
+
+__all__ = ["OPENAI_ES", "PGPE", "SNES", "SEP_CMA_ES", "SPHERE", "ROSENBROCK", "RASTRIGIN", "MLP",
+           "ESError", "lib", "Strategy", "eval_bbob"]
+
+
+def __getattr__(name):
+    if name in ("Strategy", "eval_bbob"):
+        from . import strategy
+        return getattr(strategy, name)
+    raise AttributeError(name)

@@ -1,0 +1,544 @@
+// es_api.cu — the C ABI (include/es.h): context lifetime, argument validation, host-side constant
+// tables (binary64, NUMERICS N11/N12), host↔device staging, NCCL plumbing and the launch sequence
+// of one generation. No exception crosses the ABI; every CUDA/NCCL failure becomes a status code.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/es.h"
+#include "es_internal.h"
+
+namespace esb {
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
+void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
+                         cudaStream_t st, std::string* err);
+void mlp_problem_destroy(void* prob);
+int64_t mlp_problem_dims(const void* prob);
+cudaError_t launch_primitive(int which, const void* in, void* out, int64_t n, cudaStream_t st);
+}  // namespace esb
+
+using namespace esb;
+
+struct es_ctx {
+  DevState s{};
+  std::vector<RunScal> host_rs;
+  ncclComm_t comm = nullptr;
+  bool asked = false;
+  bool broken = false;
+  int nchunk = 1;
+  float* fgather = nullptr;     // [W][R][Nloc]
+  float* fstage = nullptr;      // [R][Nloc] staging of host fitness
+  float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
+  void* mlp = nullptr;
+  int64_t launches = 0;
+  std::vector<void*> allocs;
+  std::string err;
+};
+
+static thread_local std::string g_err;
+
+static es_status_t fail(es_ctx* c, es_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_OR(c, expr)                                                                     \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return fail((c), _e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA, "%s: %s", \
+                  #expr, cudaGetErrorString(_e));                                           \
+  } while (0)
+
+#define NCCL_OR(c, expr)                                                                \
+  do {                                                                                 \
+    ncclResult_t _r = (expr);                                                          \
+    if (_r != ncclSuccess) {                                                           \
+      if (c) (c)->broken = true;                                                       \
+      return fail((c), ES_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(_r));           \
+    }                                                                                  \
+  } while (0)
+
+static cudaError_t dalloc(es_ctx* c, void** p, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) c->allocs.push_back(*p);
+  return e;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static bool antithetic(int algo) { return algo == OPENAI_ES || algo == PGPE; }
+
+// ---- host constant tables (binary64; NUMERICS N11, N12) ------------------------------------
+static void snes_weights(int N, double beta, std::vector<float>& out) {
+  std::vector<double> u(N);
+  for (int p = 0; p < N; ++p) u[p] = beta * ((double)(N - 1 - p) / N - 0.5);
+  double z = 0.0;
+  for (int p = 0; p < N; ++p) z += std::exp(u[p] - u[0]);
+  for (int p = 0; p < N; ++p) out[p] = (float)(std::exp(u[p] - u[0]) / z);
+}
+
+static void sepcma_setup(int N, int64_t D, float elite, RunScal& rs, std::vector<float>& out) {
+  const int mu = (int)std::floor((double)elite * (double)N);   // P:286 elite ratio
+  std::vector<double> w(N, 0.0);
+  double sum = 0.0, sum2 = 0.0;
+  for (int p = 0; p < mu; ++p) {
+    w[p] = std::log((N + 1) / 2.0) - std::log((double)(p + 1));
+    sum += w[p];
+  }
+  for (int p = 0; p < N; ++p) {
+    w[p] /= sum;
+    sum2 += w[p] * w[p];
+    out[p] = (float)w[p];
+  }
+  const double mueff = 1.0 / sum2, Dd = (double)D;
+  rs.mu = mu;
+  rs.mueff = mueff;
+  rs.c_sigma = (mueff + 2.0) / (Dd + mueff + 5.0);
+  rs.d_sigma = 1.0 + 2.0 * std::max(0.0, std::sqrt((mueff - 1.0) / (Dd + 1.0)) - 1.0) + rs.c_sigma;
+  rs.c_c = (4.0 + mueff / Dd) / (Dd + 4.0 + 2.0 * mueff / Dd);
+  const double c1 = 2.0 / ((Dd + 1.3) * (Dd + 1.3) + mueff);
+  const double cmu = std::min(1.0 - c1, 2.0 * (mueff - 2.0 + 1.0 / mueff) /
+                                            ((Dd + 2.0) * (Dd + 2.0) + mueff));
+  rs.c_1 = c1 * (Dd + 2.0) / 3.0;      // Ros & Hansen (2008): separable learning-rate boost
+  rs.c_mu = cmu * (Dd + 2.0) / 3.0;
+  rs.chi_d = std::sqrt(Dd) * (1.0 - 1.0 / (4.0 * Dd) + 1.0 / (21.0 * Dd * Dd));
+}
+
+extern "C" {
+
+const char* es_status_string(es_status_t s) {
+  switch (s) {
+    case ES_SUCCESS: return "success";
+    case ES_ERR_INVALID_ARG: return "invalid argument";
+    case ES_ERR_BAD_STATE: return "bad state";
+    case ES_ERR_CUDA: return "CUDA error";
+    case ES_ERR_NCCL: return "NCCL error";
+    case ES_ERR_OOM: return "out of device memory";
+    case ES_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* es_last_error(const es_ctx_t* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int32_t es_nccl_unique_id_size(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+es_status_t es_nccl_get_unique_id(void* out) {
+  if (!out) return fail(nullptr, ES_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, ES_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(out, &id, sizeof id);
+  return ES_SUCCESS;
+}
+
+int64_t es_kernel_launches(const es_ctx_t* ctx) { return ctx ? ctx->launches : -1; }
+
+es_status_t es_shape(const es_ctx_t* c, int64_t out[7]) {
+  if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  out[0] = c->s.R; out[1] = c->s.N; out[2] = c->s.Nloc; out[3] = c->s.D; out[4] = c->s.P;
+  out[5] = c->s.W; out[6] = c->s.rank;
+  return ES_SUCCESS;
+}
+
+es_status_t es_destroy(es_ctx_t* c) {
+  if (!c) return ES_SUCCESS;
+  cudaDeviceSynchronize();
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->mlp) mlp_problem_destroy(c->mlp);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+  return ES_SUCCESS;
+}
+
+es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_t D,
+                    const es_run_params_t* params, int32_t rank, int32_t W, const void* uid,
+                    es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!out) return fail(nullptr, ES_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if ((int)algo < 0 || (int)algo > 3) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
+  if (!params) return fail(nullptr, ES_ERR_INVALID_ARG, "params is NULL");
+  if (R < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_runs must be >= 1");
+  if (N < 2) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be >= 2");
+  if (D < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be >= 1");
+  if (D >= (int64_t(1) << 34)) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be < 2^34");
+  if (W < 1 || rank < 0 || rank >= W) return fail(nullptr, ES_ERR_INVALID_ARG, "bad rank/world_size");
+  if ((W > 1) != (uid != nullptr))
+    return fail(nullptr, ES_ERR_INVALID_ARG, "nccl_unique_id must be given iff world_size > 1");
+  if (N % W) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be divisible by world_size");
+  if (antithetic(algo) && ((N % 2) || ((N / W) % 2)))
+    return fail(nullptr, ES_ERR_INVALID_ARG, "antithetic strategies need an even popsize per rank");
+  if (N > 16384) return fail(nullptr, ES_ERR_UNSUPPORTED, "popsize > 16384 is not implemented");
+  for (int r = 0; r < R; ++r) {
+    const es_run_params_t& p = params[r];
+    if (!(p.sigma_init >= 0.0f)) return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: sigma_init < 0", r);
+    if (antithetic(algo) && !(p.lrate_init > 0.0f))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: lrate_init must be > 0", r);
+    if (algo == ES_SEP_CMA_ES && (int)std::floor((double)p.elite_ratio * N) < 1)
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: floor(elite_ratio*N) < 1", r);
+    if (algo == ES_SEP_CMA_ES && !(p.elite_ratio <= 1.0f))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: elite_ratio > 1", r);
+    if (p.shaping != 0 && !(p.shaping == 1 && antithetic(algo)))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: raw shaping only for OpenAI-ES/PGPE", r);
+  }
+  es_ctx* c = new (std::nothrow) es_ctx();
+  if (!c) return fail(nullptr, ES_ERR_OOM, "host allocation failed");
+  DevState& s = c->s;
+  s.algo = algo; s.R = R; s.N = N; s.W = W; s.rank = rank; s.Nloc = N / W; s.D = D;
+  s.Q = (D + 3) / 4;
+  s.P = antithetic(algo) ? N / 2 : N;
+  auto bail = [&](es_status_t e) { std::string m = c->err; es_destroy(c); g_err = m; return e; };
+#define TRY(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) {                                                                  \
+      fail(c, _e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA, "%s: %s", #expr,     \
+           cudaGetErrorString(_e));                                                           \
+      return bail(_e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA);               \
+    }                                                                                         \
+  } while (0)
+  const size_t RD = (size_t)R * D, RN = (size_t)R * N;
+  const int a = (int)algo;
+  bool need[NVEC] = {true, a == PGPE || a == SNES, antithetic(a), antithetic(a),
+                     a == SEP_CMA_ES, a == SEP_CMA_ES, a == SEP_CMA_ES, true};
+  for (int f = 0; f < NVEC; ++f) {
+    s.vec[f] = nullptr;
+    if (need[f]) TRY(dalloc(c, (void**)&s.vec[f], RD * sizeof(float)));
+  }
+  TRY(dalloc(c, (void**)&s.rs, R * sizeof(RunScal)));
+  TRY(dalloc(c, (void**)&s.gs, R * sizeof(GenScal)));
+  TRY(dalloc(c, (void**)&s.wpos, RN * sizeof(float)));
+  TRY(dalloc(c, (void**)&s.fit, RN * sizeof(float)));
+  TRY(dalloc(c, (void**)&s.shaped, RN * sizeof(float)));
+  TRY(dalloc(c, (void**)&s.rs_s, RN * sizeof(int32_t)));
+  TRY(dalloc(c, (void**)&s.rs_e, RN * sizeof(int32_t)));
+  TRY(dalloc(c, (void**)&s.perm, RN * sizeof(int32_t)));
+  TRY(dalloc(c, (void**)&s.dir, RN * sizeof(uint32_t)));
+  TRY(dalloc(c, (void**)&s.coefA, RN * sizeof(double)));
+  TRY(dalloc(c, (void**)&s.coefB, RN * sizeof(double)));
+  TRY(dalloc(c, (void**)&s.G, 2 * RD * sizeof(double)));
+  c->nchunk = tell_pick_nchunk(s);
+  const int bpr = tell_blocks_per_run(s);
+  if (c->nchunk > 1) TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->nchunk * 2 * RD * sizeof(double)));
+  TRY(dalloc(c, (void**)&s.arrive, (size_t)R * bpr * sizeof(uint32_t)));
+  TRY(dalloc(c, (void**)&s.normpart, (size_t)R * bpr * sizeof(double)));
+  if (W > 1) TRY(dalloc(c, (void**)&c->fgather, RN * sizeof(float)));
+  // per-run scalars and weight tables, computed on the host in binary64
+  c->host_rs.assign(R, RunScal{});
+  std::vector<float> wpos(RN, 0.0f), wr(N);
+  for (int r = 0; r < R; ++r) {
+    const es_run_params_t& p = params[r];
+    RunScal& rs = c->host_rs[r];
+    rs.seed = p.seed; rs.t = 0; rs.lr = p.lrate_init; rs.sigma = p.sigma_init;
+    rs.best_f = INFINITY; rs.shaping = p.shaping; rs.b1pow = 1.0; rs.b2pow = 1.0;
+    rs.init_min = p.init_min; rs.init_max = p.init_max; rs.sigma_init = p.sigma_init;
+    rs.sigma_decay = p.sigma_decay; rs.sigma_limit = p.sigma_limit;
+    rs.lrate_decay = p.lrate_decay; rs.lrate_limit = p.lrate_limit;
+    rs.beta1 = p.beta1; rs.beta2 = p.beta2; rs.eps = p.eps;
+    rs.sigma_lrate = p.sigma_lrate; rs.sigma_max_change = p.sigma_max_change;
+    std::fill(wr.begin(), wr.end(), 0.0f);
+    if (algo == ES_SNES) {
+      snes_weights(N, (double)p.temperature, wr);
+      rs.eta_sigma = (3.0 + std::log((double)D)) / (5.0 * std::sqrt((double)D));
+    } else if (algo == ES_SEP_CMA_ES) {
+      sepcma_setup(N, D, p.elite_ratio, rs, wr);
+    }
+    std::copy(wr.begin(), wr.end(), wpos.begin() + (size_t)r * N);
+  }
+  TRY(cudaMemcpyAsync(s.rs, c->host_rs.data(), R * sizeof(RunScal), cudaMemcpyHostToDevice, st));
+  TRY(cudaMemcpyAsync(s.wpos, wpos.data(), RN * sizeof(float), cudaMemcpyHostToDevice, st));
+  TRY(cudaMemsetAsync(s.arrive, 0, (size_t)R * bpr * sizeof(uint32_t), st));
+  TRY(cudaMemsetAsync(s.G, 0, 2 * RD * sizeof(double), st));
+  TRY(cudaMemsetAsync(s.coefB, 0, RN * sizeof(double), st));
+  TRY(launch_init(s, st));
+  c->launches += 1;
+  TRY(cudaStreamSynchronize(st));   // host tables above are stack-owned
+  if (W > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclResult_t nr = ncclCommInitRank(&c->comm, W, id, rank);
+    if (nr != ncclSuccess) {
+      fail(c, ES_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+      return bail(ES_ERR_NCCL);
+    }
+  }
+#undef TRY
+  *out = c;
+  return ES_SUCCESS;
+}
+
+es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !x) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
+  const DevState& s = c->s;
+  const size_t bytes = (size_t)s.R * s.Nloc * s.D * sizeof(float);
+  float* dst = x;
+  const bool host = !is_device_ptr(x);
+  if (host) {
+    if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, bytes));
+    dst = c->xstage;
+  }
+  CUDA_OR(c, launch_ask(s, dst, st));
+  c->launches += 1;
+  if (host) {
+    CUDA_OR(c, cudaMemcpyAsync(x, dst, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_OR(c, cudaStreamSynchronize(st));
+  }
+  c->asked = true;
+  return ES_SUCCESS;
+}
+
+es_status_t es_synth_fitness(es_ctx_t* c, float* f, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  const DevState& s = c->s;
+  const size_t bytes = (size_t)s.R * s.Nloc * sizeof(float);
+  float* dst = f;
+  const bool host = !is_device_ptr(f);
+  if (host) {
+    if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, bytes));
+    dst = c->fstage;
+  }
+  CUDA_OR(c, launch_synth(s, dst, st));
+  c->launches += 1;
+  if (host) {
+    CUDA_OR(c, cudaMemcpyAsync(f, dst, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_OR(c, cudaStreamSynchronize(st));
+  }
+  c->asked = true;   // synthetic fitness stands in for ask + evaluate of this generation
+  return ES_SUCCESS;
+}
+
+es_status_t es_eval_bbob(es_ctx_t* c, es_fitness_t fn, const float* x, int64_t n, int64_t D,
+                         float* f, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!x || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (n < 0 || D < 1) return fail(c, ES_ERR_INVALID_ARG, "bad sizes n=%lld D=%lld", (long long)n, (long long)D);
+  if ((int)fn < 0 || (int)fn > 3) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
+  if (fn == ES_FIT_MLP) {
+    if (!c || !c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
+    if (mlp_problem_dims(c->mlp) != D)
+      return fail(c, ES_ERR_INVALID_ARG, "D=%lld != MLP parameter count %lld", (long long)D,
+                  (long long)mlp_problem_dims(c->mlp));
+  }
+  if (n == 0) return ES_SUCCESS;
+  const bool xh = !is_device_ptr(x), fh = !is_device_ptr(f);
+  const float* xd = x;
+  float* fd = f;
+  void* tmpx = nullptr;
+  void* tmpf = nullptr;
+  if (xh) {
+    CUDA_OR(c, cudaMalloc(&tmpx, (size_t)n * D * sizeof(float)));
+    CUDA_OR(c, cudaMemcpyAsync(tmpx, x, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st));
+    xd = (const float*)tmpx;
+  }
+  if (fh) {
+    if (c && (size_t)n <= (size_t)c->s.R * c->s.Nloc) {
+      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, (size_t)c->s.R * c->s.Nloc * sizeof(float)));
+      fd = c->fstage;
+    } else {
+      CUDA_OR(c, cudaMalloc(&tmpf, (size_t)n * sizeof(float)));
+      fd = (float*)tmpf;
+    }
+  }
+  cudaError_t e = fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, n, fd, st)
+                                   : launch_eval_bbob((int)fn, xd, n, D, fd, st);
+  if (e != cudaSuccess) return fail(c, ES_ERR_CUDA, "eval launch: %s", cudaGetErrorString(e));
+  if (c) c->launches += 1;
+  if (fh) {
+    CUDA_OR(c, cudaMemcpyAsync(f, fd, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CUDA_OR(c, cudaStreamSynchronize(st));
+  }
+  if (tmpx || tmpf) {
+    CUDA_OR(c, cudaStreamSynchronize(st));
+    if (tmpx) cudaFree(tmpx);
+    if (tmpf) cudaFree(tmpf);
+  }
+  return ES_SUCCESS;
+}
+
+es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !fitness) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
+  if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_tell without a preceding es_ask");
+  const DevState& s = c->s;
+  const size_t nloc = (size_t)s.R * s.Nloc;
+  const float* fl = fitness;
+  if (!is_device_ptr(fitness)) {
+    if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
+    CUDA_OR(c, cudaMemcpyAsync(c->fstage, fitness, nloc * sizeof(float), cudaMemcpyHostToDevice, st));
+    fl = c->fstage;
+  }
+  const float* fsrc = fl;
+  if (s.W > 1) {   // a5: every rank obtains all N fitness values
+    NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
+    fsrc = c->fgather;
+  }
+  CUDA_OR(c, launch_rank(s, fsrc, st));
+  c->launches += 1;
+  if (s.W == 1) {
+    CUDA_OR(c, launch_tell_reduce(s, true, c->nchunk, st));
+    c->launches += 1;
+  } else {
+    CUDA_OR(c, launch_tell_reduce(s, false, c->nchunk, st));
+    const size_t cnt = (size_t)(s.algo == OPENAI_ES ? 1 : 2) * s.R * s.D;   // a8 (P:226 pmean)
+    NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
+    CUDA_OR(c, launch_tell_update(s, st));
+    c->launches += 2;
+  }
+  if (s.algo == SEP_CMA_ES) {
+    int nk = 0;
+    CUDA_OR(c, launch_sepcma_finish(s, st, &nk));
+    c->launches += nk;
+  }
+  c->asked = false;
+  return ES_SUCCESS;
+}
+
+static bool field_ok(const es_ctx* c, int f, void** base, size_t* elem, size_t* count, bool* scal,
+                     size_t* off) {
+  const DevState& s = c->s;
+  *scal = false;
+  *elem = 4;
+  if (f >= 0 && f < NVEC) {
+    *base = s.vec[f];
+    *count = (size_t)s.R * s.D;
+    return s.vec[f] != nullptr;
+  }
+  const size_t RN = (size_t)s.R * s.N;
+  switch (f) {
+    case ES_FIELD_BEST_F: *scal = true; *off = offsetof(RunScal, best_f); return true;
+    case ES_FIELD_SIGMA: *scal = true; *off = offsetof(RunScal, sigma); return !(s.algo == PGPE || s.algo == SNES);
+    case ES_FIELD_LRATE: *scal = true; *off = offsetof(RunScal, lr); return antithetic(s.algo);
+    case ES_FIELD_GEN: *scal = true; *off = offsetof(RunScal, t); return true;
+    case ES_FIELD_SHAPED: *base = s.shaped; *count = RN; return true;
+    case ES_FIELD_RANK_S: *base = s.rs_s; *count = RN; return true;
+    case ES_FIELD_RANK_E: *base = s.rs_e; *count = RN; return true;
+    case ES_FIELD_PERM: *base = s.perm; *count = RN; return true;
+    case ES_FIELD_FITNESS: *base = s.fit; *count = RN; return true;
+  }
+  return false;
+}
+
+es_status_t es_get(es_ctx_t* c, es_field_t field, void* dst, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !dst) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  void* base = nullptr;
+  size_t elem, count = 0, off = 0;
+  bool scal;
+  if (!field_ok(c, field, &base, &elem, &count, &scal, &off))
+    return fail(c, ES_ERR_INVALID_ARG, "field %d not kept by this algorithm", field);
+  if (scal)
+    CUDA_OR(c, cudaMemcpy2DAsync(dst, 4, (char*)c->s.rs + off, sizeof(RunScal), 4, c->s.R,
+                                 cudaMemcpyDefault, st));
+  else
+    CUDA_OR(c, cudaMemcpyAsync(dst, base, count * elem, cudaMemcpyDefault, st));
+  if (!is_device_ptr(dst)) CUDA_OR(c, cudaStreamSynchronize(st));
+  return ES_SUCCESS;
+}
+
+es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !src) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (field >= ES_FIELD_SHAPED) return fail(c, ES_ERR_INVALID_ARG, "field %d is read-only", field);
+  void* base = nullptr;
+  size_t elem, count = 0, off = 0;
+  bool scal;
+  if (!field_ok(c, field, &base, &elem, &count, &scal, &off))
+    return fail(c, ES_ERR_INVALID_ARG, "field %d not kept by this algorithm", field);
+  if (scal)
+    CUDA_OR(c, cudaMemcpy2DAsync((char*)c->s.rs + off, sizeof(RunScal), src, 4, 4, c->s.R,
+                                 cudaMemcpyDefault, st));
+  else
+    CUDA_OR(c, cudaMemcpyAsync(base, src, count * elem, cudaMemcpyDefault, st));
+  if (field == ES_FIELD_GEN) {
+    // Adam's β^t products are a pure function of t (t exact double multiplications, N12): rebuild
+    // them so that a resumed run continues bit-identically.
+    std::vector<uint32_t> t(c->s.R);
+    CUDA_OR(c, cudaStreamSynchronize(st));
+    CUDA_OR(c, cudaMemcpy(t.data(), src, c->s.R * sizeof(uint32_t), cudaMemcpyDefault));
+    std::vector<double> p(2 * (size_t)c->s.R);
+    for (int r = 0; r < c->s.R; ++r) {
+      double b1 = 1.0, b2 = 1.0;
+      for (uint32_t k = 0; k < t[r]; ++k) {
+        b1 = b1 * (double)c->host_rs[r].beta1;
+        b2 = b2 * (double)c->host_rs[r].beta2;
+      }
+      p[2 * r] = b1;
+      p[2 * r + 1] = b2;
+    }
+    CUDA_OR(c, cudaMemcpy2DAsync((char*)c->s.rs + offsetof(RunScal, b1pow), sizeof(RunScal),
+                                 p.data(), 16, 16, c->s.R, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_OR(c, cudaStreamSynchronize(st));
+  return ES_SUCCESS;
+}
+
+es_status_t es_debug_primitive(int32_t which, const void* in, void* out, int64_t n,
+                               es_stream_t stream_) {
+  if (which < 0 || which > 3 || n < 0) return fail(nullptr, ES_ERR_INVALID_ARG, "bad which/n");
+  if (n > 0 && (!in || !out)) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  CUDA_OR(nullptr, launch_primitive(which, in, out, n, (cudaStream_t)stream_));
+  return ES_SUCCESS;
+}
+
+int64_t es_mlp_num_params(const int32_t* widths, int32_t nw) {
+  if (!widths || nw < 2) return -1;
+  int64_t n = 0;
+  for (int l = 0; l + 1 < nw; ++l) {
+    if (widths[l] < 1 || widths[l + 1] < 1) return -1;
+    n += (int64_t)widths[l] * widths[l + 1] + widths[l + 1];
+  }
+  return n;
+}
+
+es_status_t es_set_mlp_problem(es_ctx_t* c, const int32_t* widths, int32_t nw, int32_t batch,
+                               uint64_t seed, es_stream_t stream_) {
+  if (!c || !widths) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (nw < 2 || nw > 16) return fail(c, ES_ERR_INVALID_ARG, "need 2..16 layer widths");
+  std::string err;
+  void* p = mlp_problem_create(widths, nw, batch, seed, (cudaStream_t)stream_, &err);
+  if (!p) return fail(c, err.rfind("unsupported", 0) == 0 ? ES_ERR_UNSUPPORTED : ES_ERR_INVALID_ARG,
+                      "%s", err.c_str());
+  if (c->mlp) mlp_problem_destroy(c->mlp);
+  c->mlp = p;
+  return ES_SUCCESS;
+}
+
+}  // extern "C"

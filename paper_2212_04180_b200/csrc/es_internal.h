@@ -1,0 +1,91 @@
+// es_internal.h — device data layout and kernel entry points of libes_b200 (not part of the ABI).
+//
+// HBM layout (per context, all dense, 256-B aligned allocations):
+//   vec[f]      float [R][D] for each state field f the algorithm keeps (mean, σ_d, Adam m/v,
+//               p_σ, p_c, C, best_x) — structure-of-arrays so that every kernel streams float4.
+//   rs          RunScal [R]   per-run scalars + hyperparameters (device-resident, so a captured
+//               CUDA graph of a generation replays with no host round trip).
+//   gs          GenScal [R]   this generation's scalars, written by the rank kernel.
+//   wpos        float [R][N]  position weights w_p (SNES / Sep-CMA, N11).
+//   shaped/s/e/perm [R][N]    ranking results of the last tell (N9–N11).
+//   dir, coefA, coefB [R][N]  per-entry tell coefficients: direction index and its weights.
+//   Gpart       double [R][2][D] (+ chunk partials) reduction workspace.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace esb {
+
+enum Algo : int { OPENAI_ES = 0, PGPE = 1, SNES = 2, SEP_CMA_ES = 3 };
+enum Field : int {
+  F_MEAN = 0, F_SIGMA_D = 1, F_ADAM_M = 2, F_ADAM_V = 3, F_PSIGMA = 4, F_PC = 5, F_C = 6,
+  F_BEST_X = 7, NVEC = 8
+};
+
+struct alignas(16) RunScal {
+  uint64_t seed;
+  uint32_t t;
+  int32_t mu;
+  float lr, sigma, best_f;
+  int32_t shaping;
+  double b1pow, b2pow;
+  float init_min, init_max, sigma_init, sigma_decay, sigma_limit, lrate_decay, lrate_limit;
+  float beta1, beta2, eps, sigma_lrate, sigma_max_change;
+  double c_sigma, d_sigma, c_c, c_1, c_mu, chi_d, mueff, eta_sigma;
+};
+
+struct alignas(16) GenScal {
+  uint32_t t;          // generation being told (pre-increment)
+  int32_t jbest;       // member at sorted position 0
+  int32_t improved;    // f[jbest] < best_f before this tell
+  int32_t nentries;    // coefficient entries carrying weight (P, or Sep-CMA's weighted positions)
+  float lr, sigma;     // pre-decay learning rate and scalar σ
+  float bc1, bc2;      // Adam bias corrections 1 − β^{t+1}
+  double bbar;         // PGPE baseline
+  float sigma_new;     // Sep-CMA σ' (written by the norm kernel)
+  int32_t hsig;        // Sep-CMA h_σ
+};
+
+struct DevState {
+  int algo, R, N, Nloc, W, rank;
+  int64_t D, Q;        // Q = ceil(D/4) quads
+  int P;               // global directions
+  float* vec[NVEC];
+  RunScal* rs;
+  GenScal* gs;
+  float* wpos;
+  float* fit;          // [R][N] gathered fitness, run-major
+  float* shaped;
+  int32_t* rs_s;
+  int32_t* rs_e;
+  int32_t* perm;
+  uint32_t* dir;       // [R][N]
+  double* coefA;       // [R][N]
+  double* coefB;       // [R][N]
+  double* G;           // [2][R][D] reduced sums (W>1 path, and Sep-CMA Z/Q)
+  double* Gchunk;      // [nchunk][R][2][D] partials when the direction range is split
+  uint32_t* arrive;    // [R][blocks_per_run] last-block counters
+  double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
+};
+
+// Launch helpers (return cudaGetLastError()).
+cudaError_t launch_init(const DevState& s, cudaStream_t st);
+cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st);
+cudaError_t launch_eval_bbob(int fn, const float* x, int64_t n, int64_t D, float* f,
+                             cudaStream_t st);
+cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st);
+cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
+// Tell: regenerate-and-reduce over this rank's entries. fused=true (W == 1) applies the update in
+// the same kernel; otherwise the sums land in s.G for the all-reduce and launch_tell_update
+// applies them. Sep-CMA-ES additionally needs launch_sepcma_finish (global ‖p_σ‖, σ, h_σ, p_c, C).
+// Each returns the number of kernels it launched through *nk.
+cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st);
+cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
+cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
+int tell_blocks_per_run(const DevState& s);
+int tell_pick_nchunk(const DevState& s);
+constexpr int kTellThreads = 128;
+int sm_count();
+
+}  // namespace esb

@@ -1,0 +1,162 @@
+// k_ask.cu — K1 init, K2 ask (Philox noise fused with antithetic mirroring and x = m + σz), and
+// the synthetic-fitness generator of the tell sweep.
+//
+// K2 mapping: one thread owns (run r, quad q = 4 consecutive dims) and a chunk of directions; it
+// loads m and the per-dim scale once, then per direction makes ONE Philox call (4 normals) and
+// writes one float4 per member row (two rows per direction for antithetic pairs). Consecutive
+// threads own consecutive quads, so each warp store is a 512-B contiguous segment of one row.
+// Bound: the HBM write of x (4·N·D bytes) for antithetic strategies; the Philox/Box–Muller issue
+// rate for SNES / Sep-CMA (one direction per member). See DESIGN.md §Kernels.
+#include <algorithm>
+
+#include "es_internal.h"
+#include "noise.cuh"
+
+namespace esb {
+
+static constexpr int kAskThreads = 128;
+
+__global__ void __launch_bounds__(256) init_kernel(DevState s) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)s.R * s.Q) return;
+  const int r = (int)(gid / s.Q);
+  const uint32_t q = (uint32_t)(gid % s.Q);
+  const RunScal& rs = s.rs[r];
+  const Philox ph(rs.seed);
+  const uint4 o = ph(q, 0u, 0u, TAG_INIT);
+  const float span = __fsub_rn(rs.init_max, rs.init_min);
+  const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t d = 4 * (int64_t)q + k;
+    if (d >= s.D) break;
+    const int64_t idx = (int64_t)r * s.D + d;
+    const float m = __fmaf_rn(span, uni_b(ow[k]), rs.init_min);   // N6
+    s.vec[F_MEAN][idx] = m;
+    s.vec[F_BEST_X][idx] = m;
+    if (s.vec[F_SIGMA_D]) s.vec[F_SIGMA_D][idx] = rs.sigma_init;
+    if (s.vec[F_ADAM_M]) { s.vec[F_ADAM_M][idx] = 0.0f; s.vec[F_ADAM_V][idx] = 0.0f; }
+    if (s.vec[F_PSIGMA]) {
+      s.vec[F_PSIGMA][idx] = 0.0f;
+      s.vec[F_PC][idx] = 0.0f;
+      s.vec[F_C][idx] = 1.0f;
+    }
+  }
+}
+
+cudaError_t launch_init(const DevState& s, cudaStream_t st) {
+  const int64_t n = (int64_t)s.R * s.Q;
+  init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
+  return cudaGetLastError();
+}
+
+// Per-dimension scale of the sample for this algorithm (N6): x = fma(±scale, z, m).
+template <int ALGO>
+__device__ __forceinline__ float ask_scale(const DevState& s, const RunScal& rs, int64_t idx) {
+  if (ALGO == OPENAI_ES) return rs.sigma;
+  if (ALGO == PGPE || ALGO == SNES) return s.vec[F_SIGMA_D][idx];
+  return __fmul_rn(rs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
+}
+
+template <int ALGO, bool V4>
+__global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
+                                                           int bpr, int dpt) {
+  constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+  const int r = blockIdx.x / bpr;
+  const int64_t q = (int64_t)(blockIdx.x % bpr) * kAskThreads + threadIdx.x;
+  if (q >= s.Q) return;
+  const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
+  const int i0 = blockIdx.y * dpt;
+  const int i1 = min(Ploc, i0 + dpt);
+  if (i0 >= i1) return;
+  const RunScal& rs = s.rs[r];
+  const Philox ph(rs.seed);
+  const uint32_t t = rs.t;
+  const int64_t base = (int64_t)r * s.D + 4 * q;
+  float m[4], sc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool ok = 4 * q + k < s.D;
+    m[k] = ok ? s.vec[F_MEAN][base + k] : 0.0f;
+    sc[k] = ok ? ask_scale<ALGO>(s, rs, base + k) : 0.0f;
+  }
+  const int dir0 = s.rank * Ploc;
+  float* xr = x + (int64_t)r * s.Nloc * s.D + 4 * q;
+#pragma unroll 2
+  for (int il = i0; il < i1; ++il) {
+    const float4 z = normal4(ph, (uint32_t)q, (uint32_t)(dir0 + il), t);
+    const float zz[4] = {z.x, z.y, z.z, z.w};
+    float xp[4], xm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      xp[k] = __fmaf_rn(sc[k], zz[k], m[k]);
+      if (kAnti) xm[k] = __fmaf_rn(-sc[k], zz[k], m[k]);
+    }
+    const int64_t row = kAnti ? 2 * (int64_t)il : il;
+    float* p0 = xr + row * s.D;
+    if (V4) {
+      __stcs(reinterpret_cast<float4*>(p0), make_float4(xp[0], xp[1], xp[2], xp[3]));
+      if (kAnti)
+        __stcs(reinterpret_cast<float4*>(p0 + s.D), make_float4(xm[0], xm[1], xm[2], xm[3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (4 * q + k < s.D) {
+          p0[k] = xp[k];
+          if (kAnti) p0[s.D + k] = xm[k];
+        }
+      }
+    }
+  }
+}
+
+template <int ALGO>
+static cudaError_t launch_ask_t(const DevState& s, float* x, cudaStream_t st) {
+  constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+  const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
+  const int bpr = (int)((s.Q + kAskThreads - 1) / kAskThreads);
+  // Enough (thread, direction-chunk) items for ~4 waves of 16 warps/SM, ≥ 4 directions each.
+  const int64_t quads = (int64_t)s.R * bpr * kAskThreads;
+  const int64_t want = (int64_t)sm_count() * 2048 * 4;
+  int nchunk = (int)std::min<int64_t>(std::max<int64_t>(1, want / std::max<int64_t>(quads, 1)),
+                                      std::max(1, Ploc / 4));
+  nchunk = std::min(nchunk, 65535);
+  const int dpt = (Ploc + nchunk - 1) / nchunk;
+  nchunk = (Ploc + dpt - 1) / dpt;
+  dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
+  const bool v4 = (s.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if (v4) ask_kernel<ALGO, true><<<grid, kAskThreads, 0, st>>>(s, x, bpr, dpt);
+  else ask_kernel<ALGO, false><<<grid, kAskThreads, 0, st>>>(s, x, bpr, dpt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {
+  switch (s.algo) {
+    case OPENAI_ES: return launch_ask_t<OPENAI_ES>(s, x, st);
+    case PGPE: return launch_ask_t<PGPE>(s, x, st);
+    case SNES: return launch_ask_t<SNES>(s, x, st);
+    default: return launch_ask_t<SEP_CMA_ES>(s, x, st);
+  }
+}
+
+// N15: f_j = u_b(o_{j mod 4}) of counter (⌊j/4⌋, 0, t, 4), for this rank's members.
+__global__ void synth_kernel(DevState s, float* __restrict__ f) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)s.R * s.Nloc) return;
+  const int r = (int)(gid / s.Nloc);
+  const int jl = (int)(gid % s.Nloc);
+  const int j = s.rank * s.Nloc + jl;
+  const RunScal& rs = s.rs[r];
+  const Philox ph(rs.seed);
+  const uint4 o = ph((uint32_t)(j / 4), 0u, rs.t, TAG_SYNTH);
+  const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+  f[gid] = uni_b(ow[j % 4]);
+}
+
+cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st) {
+  const int64_t n = (int64_t)s.R * s.Nloc;
+  synth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, f);
+  return cudaGetLastError();
+}
+
+}  // namespace esb

@@ -1,0 +1,184 @@
+// k_rank.cu — K5: per-run ranking and fitness shaping (NUMERICS N9–N11), best tracking and the
+// per-generation scalars, one CTA per run.
+//
+// Keys: fp32 fitness → order-preserving u32 (NaN worst, ±0 equal) packed with the member index
+// into a u64, bitonic-sorted in shared memory (N ≤ 16384 → ≤ 128 KB). Tie groups [s, e] come from
+// two binary searches on the sorted high words. Shaping (P:213 centered rank; P:369 SNES
+// utilities; P:286 Sep-CMA elite weights) and the tell's per-direction coefficients are written
+// here so that the tell kernel only streams (direction, coefficient) pairs.
+#include <algorithm>
+
+#include "es_internal.h"
+
+namespace esb {
+
+__device__ __forceinline__ uint32_t rank_key(float f) {
+  if (f != f) return 0xFFFFFFFFu;
+  if (f == 0.0f) return 0x80000000u;
+  const uint32_t b = __float_as_uint(f);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < nw; ++k) t = __dadd_rn(t, red[k]);   // fixed order, every thread
+  return t;
+}
+
+// fsrc layout [W][R][Nloc] (for W == 1 simply [R][N]).
+__global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad) {
+  extern __shared__ uint64_t keys[];
+  __shared__ double red[32];
+  __shared__ int32_t sh_nw;
+  const int r = blockIdx.x;
+  const int N = s.N, T = blockDim.x;
+  float* fit = s.fit + (int64_t)r * N;
+  for (int p = threadIdx.x; p < npad; p += T) {
+    uint64_t v = ~0ull;
+    if (p < N) {
+      const int w = p / s.Nloc, jl = p % s.Nloc;
+      const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
+      fit[p] = f;
+      v = ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
+    }
+    keys[p] = v;
+  }
+  __syncthreads();
+  // bitonic sort, ascending
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (npad >> 1); i += T) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int hi = lo + j;
+        const uint64_t a = keys[lo], b = keys[hi];
+        const bool up = (lo & k) == 0;
+        if ((a > b) == up) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // tie groups and shaping
+  const RunScal& rs = s.rs[r];
+  int32_t* perm = s.perm + (int64_t)r * N;
+  int32_t* S = s.rs_s + (int64_t)r * N;
+  int32_t* E = s.rs_e + (int64_t)r * N;
+  float* shaped = s.shaped + (int64_t)r * N;
+  const float* wpos = s.wpos + (int64_t)r * N;
+  const bool anti = (s.algo == OPENAI_ES || s.algo == PGPE);
+  for (int p = threadIdx.x; p < N; p += T) {
+    const uint64_t v = keys[p];
+    const uint32_t key = (uint32_t)(v >> 32);
+    const int j = (int)(uint32_t)v;
+    int lo = 0, hi = p;                   // first position with key ≥ key
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint32_t)(keys[mid] >> 32) < key) lo = mid + 1; else hi = mid;
+    }
+    const int sj = lo;
+    lo = p; hi = N;                       // first position with key > key
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint32_t)(keys[mid] >> 32) <= key) lo = mid + 1; else hi = mid;
+    }
+    const int ej = lo - 1;
+    perm[p] = j;
+    S[j] = sj;
+    E[j] = ej;
+    float val;
+    if (anti) {
+      val = rs.shaping == 1 ? fit[j]
+                            : __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));  // N10
+    } else {
+      float acc = 0.0f;                                                                       // N11
+      for (int q = sj; q <= ej; ++q) acc = __fadd_rn(acc, wpos[q]);
+      val = __fdiv_rn(acc, (float)(ej - sj + 1));
+    }
+    shaped[j] = val;
+  }
+  __syncthreads();
+  // per-entry tell coefficients
+  uint32_t* dir = s.dir + (int64_t)r * N;
+  double* cA = s.coefA + (int64_t)r * N;
+  double* cB = s.coefB + (int64_t)r * N;
+  double bbar = 0.0;
+  if (s.algo == PGPE) {
+    double part = 0.0;
+    for (int j = threadIdx.x; j < N; j += T) part = __dadd_rn(part, (double)shaped[j]);
+    bbar = block_sum(part, red) / (double)N;
+  }
+  if (anti) {
+    for (int i = threadIdx.x; i < N / 2; i += T) {
+      const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
+      dir[i] = (uint32_t)i;
+      cA[i] = __dsub_rn(cp, cm);
+      if (s.algo == PGPE) cB[i] = __dsub_rn(__dmul_rn(__dadd_rn(cp, cm), 0.5), bbar);
+    }
+  } else if (s.algo == SNES) {
+    for (int j = threadIdx.x; j < N; j += T) {
+      dir[j] = (uint32_t)j;
+      cA[j] = (double)shaped[j];
+    }
+  } else {
+    if (threadIdx.x == 0) sh_nw = E[perm[rs.mu - 1]] + 1;   // end of the tie group at μ−1
+    __syncthreads();
+    for (int p = threadIdx.x; p < sh_nw; p += T) {
+      const int j = perm[p];
+      dir[p] = (uint32_t)j;
+      cA[p] = (double)shaped[j];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RunScal& w = s.rs[r];
+    GenScal g;
+    g.t = w.t;
+    g.jbest = perm[0];
+    const float fb = fit[g.jbest];
+    g.improved = fb < w.best_f;                 // strict; false for NaN
+    if (g.improved) w.best_f = fb;
+    g.lr = w.lr;
+    g.sigma = w.sigma;
+    g.nentries = anti ? N / 2 : (s.algo == SNES ? N : sh_nw);
+    g.bbar = bbar;
+    g.bc1 = g.bc2 = 1.0f;
+    g.sigma_new = w.sigma;
+    g.hsig = 0;
+    if (anti) {
+      const double b1 = __dmul_rn(w.b1pow, (double)w.beta1);
+      const double b2 = __dmul_rn(w.b2pow, (double)w.beta2);
+      g.bc1 = (float)__dsub_rn(1.0, b1);
+      g.bc2 = (float)__dsub_rn(1.0, b2);
+      w.b1pow = b1;
+      w.b2pow = b2;
+      w.lr = fmaxf(__fmul_rn(w.lr, w.lrate_decay), w.lrate_limit);
+      if (s.algo == OPENAI_ES) w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
+    }
+    w.t = g.t + 1;
+    s.gs[r] = g;
+  }
+}
+
+cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
+  int npad = 1;
+  while (npad < s.N) npad <<= 1;
+  const int T = std::min(1024, std::max(32, npad / 2));
+  const size_t smem = (size_t)npad * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  rank_kernel<<<s.R, T, smem, st>>>(s, fsrc, npad);
+  return cudaGetLastError();
+}
+
+}  // namespace esb

@@ -1,0 +1,359 @@
+// k_tell.cu — K6+K7: the fused tell. Regenerate z from the Philox counter (never stored, never
+// re-read), reduce the weighted direction sums of NUMERICS N12 in binary64, and apply the OpenAI-ES
+// + Adam, PGPE, SNES or Sep-CMA-ES update.
+//
+// Mapping: one thread owns (run r, quad q of 4 dims) and a contiguous range of tell entries
+// (directions, or Sep-CMA's weighted sorted positions); the (direction index, coefficients) of a
+// tile of entries are staged in shared memory and broadcast to all threads. Per entry: one Philox
+// call → 4 normals → k DFMAs per normal. When the entry range is split across several CTAs (grid.y
+// = nchunk, to fill 148 SMs), each CTA writes binary64 partials and the LAST CTA of its (run, quad
+// tile) — elected with a threadfence + atomic counter — sums the partials in chunk order (so the
+// result does not depend on scheduling) and runs the update epilogue in the same kernel.
+// Bound: Philox + Box–Muller issue rate (ALU); the state traffic (16–32 B/dim) is ~0.1 % of time.
+#include <algorithm>
+
+#include "es_internal.h"
+#include "noise.cuh"
+
+namespace esb {
+
+static constexpr int TT = kTellThreads;
+
+// s.G layout [2][R][D]: the first R·D doubles are the only ones OpenAI-ES all-reduces.
+__device__ __forceinline__ int64_t gidx(const DevState& s, int k, int r, int64_t d) {
+  return ((int64_t)k * s.R + r) * s.D + d;
+}
+static constexpr int kTile = 256;
+
+struct Acc {
+  double a[4], b[4];
+};
+
+template <int ALGO>
+__device__ __forceinline__ void accumulate(Acc& acc, const float4& z, double cA, double cB) {
+  const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double zd = (double)zz[k];
+    acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
+    if (ALGO == PGPE) acc.b[k] = __fma_rn(cB, __dsub_rn(__dmul_rn(zd, zd), 1.0), acc.b[k]);
+    if (ALGO == SNES) acc.b[k] = __fma_rn(cA, __dsub_rn(__dmul_rn(zd, zd), 1.0), acc.b[k]);
+    if (ALGO == SEP_CMA_ES) acc.b[k] = __fma_rn(cA, __dmul_rn(zd, zd), acc.b[k]);
+  }
+}
+
+__device__ __forceinline__ double block_sum_tt(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < TT / 32; ++k) t = __dadd_rn(t, red[k]);
+  return t;
+}
+
+__device__ __forceinline__ void adam_step(float& mean, float& am, float& av, float g,
+                                          const RunScal& rs, const GenScal& gs) {
+  const float b1 = rs.beta1, b2 = rs.beta2;
+  const float mn = __fmaf_rn(b1, am, __fmul_rn(__fsub_rn(1.0f, b1), g));
+  const float vn = __fmaf_rn(b2, av, __fmul_rn(__fsub_rn(1.0f, b2), __fmul_rn(g, g)));
+  const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vn, gs.bc2)), rs.eps);
+  mean = __fsub_rn(mean, __fmul_rn(gs.lr, __fdiv_rn(__fdiv_rn(mn, gs.bc1), den)));
+  am = mn;
+  av = vn;
+}
+
+// Update epilogue for the 4 dims of quad q of run r from the reduced sums G0, G1 (N12). Also
+// regenerates best_x from the pre-update state when this generation improved.
+// Sep-CMA: phase 1 only (mean, p_σ, Z/Q to s.G, ‖p_σ‖² partial of the block to normpart).
+template <int ALGO>
+__device__ void apply_update(const DevState& s, int r, int64_t q, bool active, const double* G0,
+                             const double* G1, int qb, int bpr, double* red) {
+  const RunScal& rs = s.rs[r];
+  const GenScal& gs = s.gs[r];
+  double norm2 = 0.0;
+  if (active) {
+    const Philox ph(rs.seed);
+    float4 zb = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sgn = 1.0f;
+    if (gs.improved) {
+      constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+      const int i = kAnti ? gs.jbest / 2 : gs.jbest;
+      sgn = (kAnti && (gs.jbest & 1)) ? -1.0f : 1.0f;
+      zb = normal4(ph, (uint32_t)q, (uint32_t)i, gs.t);
+    }
+    const float zbv[4] = {zb.x, zb.y, zb.z, zb.w};
+    float omcs = 0.f, ks = 0.f;
+    if (ALGO == SEP_CMA_ES) {
+      omcs = (float)__dsub_rn(1.0, rs.c_sigma);
+      ks = (float)sqrt(__dmul_rn(__dmul_rn(rs.c_sigma, __dsub_rn(2.0, rs.c_sigma)), rs.mueff));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t d = 4 * q + k;
+      if (d >= s.D) break;
+      const int64_t idx = (int64_t)r * s.D + d;
+      float mean = s.vec[F_MEAN][idx];
+      if (gs.improved) {
+        float sc;
+        if (ALGO == OPENAI_ES) sc = gs.sigma;
+        else if (ALGO == SEP_CMA_ES) sc = __fmul_rn(gs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
+        else sc = s.vec[F_SIGMA_D][idx];
+        s.vec[F_BEST_X][idx] = __fmaf_rn(sgn * sc, zbv[k], mean);
+      }
+      if (ALGO == OPENAI_ES) {
+        const float g = __fdiv_rn((float)G0[k], __fmul_rn((float)s.N, gs.sigma));
+        adam_step(mean, s.vec[F_ADAM_M][idx], s.vec[F_ADAM_V][idx], g, rs, gs);
+      } else if (ALGO == PGPE) {
+        const float sig = s.vec[F_SIGMA_D][idx];
+        const float gm = __fdiv_rn(__fmul_rn(sig, (float)G0[k]), (float)s.N);
+        const float gsg = __fdiv_rn(__fmul_rn(sig, (float)G1[k]), (float)(s.N / 2));
+        adam_step(mean, s.vec[F_ADAM_M][idx], s.vec[F_ADAM_V][idx], gm, rs, gs);
+        const float mc = rs.sigma_max_change;
+        float st = __fsub_rn(sig, __fmul_rn(rs.sigma_lrate, gsg));
+        const float lo = __fmul_rn(__fsub_rn(1.0f, mc), sig);
+        const float hi = __fmul_rn(__fadd_rn(1.0f, mc), sig);
+        st = fminf(fmaxf(st, lo), hi);
+        s.vec[F_SIGMA_D][idx] = fmaxf(__fmul_rn(st, rs.sigma_decay), rs.sigma_limit);
+      } else if (ALGO == SNES) {
+        const float sig = s.vec[F_SIGMA_D][idx];
+        mean = __fadd_rn(mean, __fmul_rn(sig, (float)G0[k]));
+        s.vec[F_SIGMA_D][idx] =
+            __fmul_rn(sig, (float)exp(__dmul_rn(__dmul_rn(rs.eta_sigma, 0.5), G1[k])));
+      } else {
+        const float Z = (float)G0[k];
+        const float y = __fmul_rn(__fsqrt_rn(s.vec[F_C][idx]), Z);
+        mean = __fadd_rn(mean, __fmul_rn(gs.sigma, y));
+        const float ps = __fadd_rn(__fmul_rn(omcs, s.vec[F_PSIGMA][idx]), __fmul_rn(ks, Z));
+        s.vec[F_PSIGMA][idx] = ps;
+        norm2 = __dadd_rn(norm2, __dmul_rn((double)ps, (double)ps));
+        s.G[gidx(s, 0, r, d)] = G0[k];
+        s.G[gidx(s, 1, r, d)] = G1[k];
+      }
+      s.vec[F_MEAN][idx] = mean;
+    }
+  }
+  if (ALGO == SEP_CMA_ES) {
+    const double tot = block_sum_tt(norm2, red);
+    if (threadIdx.x == 0) s.normpart[(int64_t)r * bpr + qb] = tot;
+  }
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(TT) tell_kernel(DevState s, int bpr, int nchunk, int fused) {
+  __shared__ uint32_t sdir[kTile];
+  __shared__ double sA[kTile];
+  __shared__ double sB[kTile];
+  __shared__ double red[TT / 32];
+  __shared__ int sh_last;
+  const int r = blockIdx.x / bpr;
+  const int qb = blockIdx.x % bpr;
+  const int64_t q = (int64_t)qb * TT + threadIdx.x;
+  const bool active = q < s.Q;
+  const int chunk = blockIdx.y;
+  const GenScal& gs = s.gs[r];
+  const int ne = gs.nentries;
+  const int per = (ne + s.W - 1) / s.W;
+  const int e0 = min(ne, s.rank * per), e1 = min(ne, e0 + per);
+  const int cper = (e1 - e0 + nchunk - 1) / nchunk;
+  const int c0 = min(e1, e0 + chunk * cper), c1 = min(e1, c0 + cper);
+  const Philox ph(s.rs[r].seed);
+  const uint32_t t = gs.t;
+  const uint32_t* dir = s.dir + (int64_t)r * s.N;
+  const double* cA = s.coefA + (int64_t)r * s.N;
+  const double* cB = s.coefB + (int64_t)r * s.N;
+  Acc acc;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc.a[k] = acc.b[k] = 0.0;
+  for (int b0 = c0; b0 < c1; b0 += kTile) {
+    const int nb = min(kTile, c1 - b0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb; e += TT) {
+      sdir[e] = dir[b0 + e];
+      sA[e] = cA[b0 + e];
+      if (ALGO == PGPE) sB[e] = cB[b0 + e];
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll 2
+      for (int e = 0; e < nb; ++e) {
+        const float4 z = normal4(ph, (uint32_t)q, sdir[e], t);
+        accumulate<ALGO>(acc, z, sA[e], ALGO == PGPE ? sB[e] : 0.0);
+      }
+    }
+  }
+  const int64_t D2 = 2 * s.D;
+  if (nchunk > 1) {
+    // publish partials, elect the last CTA of this (run, quad tile)
+    if (active) {
+      double* P = s.Gchunk + ((int64_t)chunk * s.R + r) * D2;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (4 * q + k < s.D) {
+          P[4 * q + k] = acc.a[k];
+          if (ALGO != OPENAI_ES) P[s.D + 4 * q + k] = acc.b[k];
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t prev = atomicAdd(&s.arrive[(int64_t)r * bpr + qb], 1u);
+      sh_last = (prev == (uint32_t)(nchunk - 1));
+      if (sh_last) s.arrive[(int64_t)r * bpr + qb] = 0u;
+    }
+    __syncthreads();
+    if (!sh_last) return;
+    __threadfence();
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc.a[k] = acc.b[k] = 0.0;
+      for (int c = 0; c < nchunk; ++c) {
+        const double* P = s.Gchunk + ((int64_t)c * s.R + r) * D2;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (4 * q + k < s.D) {
+            acc.a[k] = __dadd_rn(acc.a[k], __ldcg(P + 4 * q + k));
+            if (ALGO != OPENAI_ES) acc.b[k] = __dadd_rn(acc.b[k], __ldcg(P + s.D + 4 * q + k));
+          }
+        }
+      }
+    }
+  }
+  if (fused) {
+    apply_update<ALGO>(s, r, q, active, acc.a, acc.b, qb, bpr, red);
+  } else if (active) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (4 * q + k < s.D) {
+        s.G[gidx(s, 0, r, 4 * q + k)] = acc.a[k];
+        if (ALGO != OPENAI_ES) s.G[gidx(s, 1, r, 4 * q + k)] = acc.b[k];
+      }
+    }
+  }
+}
+
+// W > 1: after the all-reduce of s.G, apply the update.
+template <int ALGO>
+__global__ void __launch_bounds__(TT) update_kernel(DevState s, int bpr) {
+  __shared__ double red[TT / 32];
+  const int r = blockIdx.x / bpr;
+  const int qb = blockIdx.x % bpr;
+  const int64_t q = (int64_t)qb * TT + threadIdx.x;
+  const bool active = q < s.Q;
+  double G0[4] = {0, 0, 0, 0}, G1[4] = {0, 0, 0, 0};
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (4 * q + k < s.D) {
+        G0[k] = s.G[gidx(s, 0, r, 4 * q + k)];
+        if (ALGO != OPENAI_ES) G1[k] = s.G[gidx(s, 1, r, 4 * q + k)];
+      }
+    }
+  }
+  apply_update<ALGO>(s, r, q, active, G0, G1, qb, bpr, red);
+}
+
+// Sep-CMA-ES phase 2: global ‖p_σ'‖ (fixed-order sum of the block partials), σ', h_σ.
+__global__ void sepcma_norm_kernel(DevState s, int bpr) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < bpr; b += blockDim.x) v = __dadd_rn(v, s.normpart[(int64_t)r * bpr + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double n2 = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) n2 = __dadd_rn(n2, red[k]);
+    RunScal& rs = s.rs[r];
+    GenScal& gs = s.gs[r];
+    const double norm = sqrt(n2);
+    const double Dd = (double)s.D;
+    const float sig_new = __fmul_rn(
+        gs.sigma, (float)exp(__dmul_rn(__ddiv_rn(rs.c_sigma, rs.d_sigma),
+                                       __dsub_rn(__ddiv_rn(norm, rs.chi_d), 1.0))));
+    const double lhs = norm / sqrt(1.0 - pow(1.0 - rs.c_sigma, 2.0 * (double)(gs.t + 1)));
+    gs.hsig = lhs < (1.4 + 2.0 / (Dd + 1.0)) * rs.chi_d;
+    gs.sigma_new = sig_new;
+    rs.sigma = sig_new;
+  }
+}
+
+// Sep-CMA-ES phase 3: p_c and C from Z, Q (s.G) and h_σ.
+__global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)s.R * s.D) return;
+  const int r = (int)(gid / s.D);
+  const int64_t d = gid % s.D;
+  const RunScal& rs = s.rs[r];
+  const GenScal& gs = s.gs[r];
+  const double hs = gs.hsig ? 1.0 : 0.0;
+  const float omcc = (float)(1.0 - rs.c_c);
+  const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
+  const float aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
+  const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
+  const float Z = (float)s.G[gidx(s, 0, r, d)];
+  const float Qv = (float)s.G[gidx(s, 1, r, d)];
+  const int64_t idx = (int64_t)r * s.D + d;
+  const float C0 = s.vec[F_C][idx];
+  const float y = __fmul_rn(__fsqrt_rn(C0), Z);
+  const float pcn = __fadd_rn(__fmul_rn(omcc, s.vec[F_PC][idx]), __fmul_rn(kc, y));
+  s.vec[F_PC][idx] = pcn;
+  s.vec[F_C][idx] = __fadd_rn(__fadd_rn(__fmul_rn(aC, C0), __fmul_rn(c1f, __fmul_rn(pcn, pcn))),
+                              __fmul_rn(cmuf, __fmul_rn(C0, Qv)));
+}
+
+int tell_blocks_per_run(const DevState& s) { return (int)((s.Q + TT - 1) / TT); }
+
+int tell_pick_nchunk(const DevState& s) {
+  const int bpr = tell_blocks_per_run(s);
+  const int64_t blocks = (int64_t)s.R * bpr;
+  const int64_t want = (int64_t)sm_count() * (2048 / TT) * 2;   // ~2 waves at full occupancy
+  const int ent = std::max(1, (s.algo == OPENAI_ES || s.algo == PGPE ? s.N / 2 : s.N) / s.W);
+  int n = (int)std::max<int64_t>(1, (want + blocks - 1) / blocks);
+  n = std::min(n, std::max(1, ent / 16));   // ≥ 16 entries per chunk
+  return std::min(n, 64);
+}
+
+template <int ALGO>
+static void launch_tell_t(const DevState& s, bool fused, int nchunk, cudaStream_t st) {
+  const int bpr = tell_blocks_per_run(s);
+  dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
+  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, bpr, nchunk, fused ? 1 : 0);
+}
+
+cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st) {
+  switch (s.algo) {
+    case OPENAI_ES: launch_tell_t<OPENAI_ES>(s, fused, nchunk, st); break;
+    case PGPE: launch_tell_t<PGPE>(s, fused, nchunk, st); break;
+    case SNES: launch_tell_t<SNES>(s, fused, nchunk, st); break;
+    default: launch_tell_t<SEP_CMA_ES>(s, fused, nchunk, st); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tell_update(const DevState& s, cudaStream_t st) {
+  const int bpr = tell_blocks_per_run(s);
+  const unsigned g = (unsigned)(s.R * bpr);
+  switch (s.algo) {
+    case OPENAI_ES: update_kernel<OPENAI_ES><<<g, TT, 0, st>>>(s, bpr); break;
+    case PGPE: update_kernel<PGPE><<<g, TT, 0, st>>>(s, bpr); break;
+    case SNES: update_kernel<SNES><<<g, TT, 0, st>>>(s, bpr); break;
+    default: update_kernel<SEP_CMA_ES><<<g, TT, 0, st>>>(s, bpr); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk) {
+  const int bpr = tell_blocks_per_run(s);
+  sepcma_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr);
+  const int64_t n = (int64_t)s.R * s.D;
+  sepcma_pc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
+  if (nk) *nk = 2;
+  return cudaGetLastError();
+}
+
+}  // namespace esb

@@ -1,0 +1,138 @@
+"""Python mirror of Listing 1: Strategy(...).ask() → eval → .tell(fitness).
+
+Thin marshalling over include/es.h. torch is used for device memory and streams only; buffers are
+handed to the library by data_ptr(). Population sharding uses a torch.distributed process
+group to broadcast the ncclUniqueId; the collectives themselves run inside es_tell.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import FIELDS, RunParams, check, lib
+
+DEFAULT_PARAMS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=1.0,
+                      sigma_limit=0.0, lrate_init=0.01, lrate_decay=1.0, lrate_limit=0.0,
+                      beta1=0.9, beta2=0.999, eps=1e-8, sigma_lrate=0.2, sigma_max_change=0.2,
+                      temperature=12.0, elite_ratio=0.5, shaping=0)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def eval_bbob(fn, x, out=None, stream=None, ctx=None):
+    """Batched BBOB fitness of the rows of x (float32 [n, D], CUDA) → float32 [n]."""
+    assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+    n, D = x.shape
+    f = out if out is not None else torch.empty(n, dtype=torch.float32, device=x.device)
+    check(lib().es_eval_bbob(ctx, int(fn), _ptr(x), n, D, _ptr(f), _stream(stream)), ctx)
+    return f
+
+
+class Strategy:
+    """R independent runs of one algorithm (vmap over seeds / hyperparameters)."""
+
+    def __init__(self, algo, popsize, num_dims, params, device="cuda", group=None, stream=None):
+        """params: one dict per run (es_run_params_t fields; 'seed' required)."""
+        if isinstance(params, dict):
+            params = [params]
+        self.algo, self.popsize, self.num_dims = int(algo), int(popsize), int(num_dims)
+        self.R = len(params)
+        self.device = torch.device(device)
+        arr = (RunParams * self.R)()
+        for r, p in enumerate(params):
+            kw = dict(DEFAULT_PARAMS)
+            kw.update(p)
+            for k, v in kw.items():
+                setattr(arr[r], k, v)
+        self.world_size, self.rank, uid = 1, 0, None
+        if group is not None and torch.distributed.get_world_size(group) > 1:
+            self.world_size = torch.distributed.get_world_size(group)
+            self.rank = torch.distributed.get_rank(group)
+            n = lib().es_nccl_unique_id_size()
+            buf = torch.zeros(n, dtype=torch.uint8)
+            if self.rank == 0:
+                check(lib().es_nccl_get_unique_id(C.c_void_p(buf.data_ptr())))
+            bbuf = buf.to(self.device) if torch.distributed.get_backend(group) == "nccl" else buf
+            torch.distributed.broadcast(bbuf, src=torch.distributed.get_global_rank(group, 0),
+                                        group=group)
+            buf = bbuf.cpu()
+            self._uid = buf
+            uid = C.c_void_p(buf.data_ptr())
+        self.ctx = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().es_init(C.byref(self.ctx), self.algo, self.R, self.popsize, self.num_dims,
+                                arr, self.rank, self.world_size, uid, _stream(stream)))
+        self.local_popsize = self.popsize // self.world_size
+
+    # -- Listing 1 ------------------------------------------------------------------------------
+    def ask(self, out=None, stream=None):
+        x = out if out is not None else torch.empty(
+            (self.R, self.local_popsize, self.num_dims), dtype=torch.float32, device=self.device)
+        check(lib().es_ask(self.ctx, _ptr(x), _stream(stream)), self.ctx)
+        return x
+
+    def eval(self, fn, x, out=None, stream=None):
+        n = x.numel() // self.num_dims
+        f = out if out is not None else torch.empty(
+            (self.R, self.local_popsize), dtype=torch.float32, device=self.device)
+        check(lib().es_eval_bbob(self.ctx, int(fn), _ptr(x), n, self.num_dims, _ptr(f),
+                                 _stream(stream)), self.ctx)
+        return f
+
+    def tell(self, fitness, stream=None):
+        check(lib().es_tell(self.ctx, _ptr(fitness), _stream(stream)), self.ctx)
+
+    def synth_fitness(self, out=None, stream=None):
+        f = out if out is not None else torch.empty(
+            (self.R, self.local_popsize), dtype=torch.float32, device=self.device)
+        check(lib().es_synth_fitness(self.ctx, _ptr(f), _stream(stream)), self.ctx)
+        return f
+
+    def set_mlp_problem(self, widths, batch=128, data_seed=0, stream=None):
+        w = (C.c_int32 * len(widths))(*widths)
+        check(lib().es_set_mlp_problem(self.ctx, w, len(widths), batch, data_seed,
+                                       _stream(stream)), self.ctx)
+
+    # -- state ----------------------------------------------------------------------------------
+    def _shape(self, name):
+        R, N, D = self.R, self.popsize, self.num_dims
+        if name in ("best_f", "sigma", "lrate", "gen"):
+            return (R,)
+        if name in ("shaped", "rank_s", "rank_e", "perm", "fitness"):
+            return (R, N)
+        return (R, D)
+
+    def get(self, name, stream=None):
+        dt = {"gen": torch.int32, "rank_s": torch.int32, "rank_e": torch.int32,
+              "perm": torch.int32}.get(name, torch.float32)
+        out = torch.empty(self._shape(name), dtype=dt, device=self.device)
+        check(lib().es_get(self.ctx, FIELDS[name], _ptr(out), _stream(stream)), self.ctx)
+        return out
+
+    def set(self, name, value, stream=None):
+        v = value.to(self.device).contiguous()
+        check(lib().es_set(self.ctx, FIELDS[name], _ptr(v), _stream(stream)), self.ctx)
+
+    @property
+    def kernel_launches(self):
+        return lib().es_kernel_launches(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) and self.ctx.value:
+            lib().es_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,334 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): noise / populations and ranks bit-exact; fitness and state within
+1e-5 (Q24 metric) after one generation and 1e-3 after 100. Sizes span several tiles and ragged
+tails (D not a multiple of 4, D not a multiple of the 128-quad block, direction ranges split across
+CTAs); full BASELINE sizes are checked on sampled runs / dimensions."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import oracle as O
+from tests.gpu_helpers import KEPT, Pair, bits, q24
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = [W.OPENAI_ES, W.PGPE, W.SNES, W.SEP_CMA_ES]
+FNS = [W.SPHERE, W.ROSENBROCK, W.RASTRIGIN]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    O.build()
+
+
+def L():
+    from paper_2212_04180_b200 import _lib
+    return _lib.lib()
+
+
+def _prim(which, inp, out):
+    rc = L().es_debug_primitive(which, C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()),
+                                inp.shape[0], None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    return out
+
+
+# ------------------------------------------------------------------------ N1–N5 primitives
+def test_philox_kat_on_device():
+    import json, os
+    kat = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "philox_kat.json")))
+    rows = [[int(h, 16) for h in v["ctr"] + v["key"]] for v in kat["vectors"]]
+    inp = torch.tensor(np.array(rows, dtype=np.uint32).view(np.int32), device="cuda")
+    out = _prim(0, inp, torch.empty((len(rows), 4), dtype=torch.int32, device="cuda"))
+    got = out.cpu().numpy().view(np.uint32)
+    for g, v in zip(got, kat["vectors"]):
+        assert [f"{x:08x}" for x in g] == v["out"]
+
+
+def test_ln_exhaustive_bit_exact():
+    m = np.arange(2 ** 23, dtype=np.float64)
+    ua = (1.0 - m * 2.0 ** -23).astype(np.float32)
+    dev = _prim(1, torch.from_numpy(ua).cuda(), torch.empty(ua.size, device="cuda"))
+    assert np.array_equal(bits(dev.cpu().numpy()), bits(O.ln(ua)))
+
+
+def test_sincos_exhaustive_bit_exact():
+    ub = (np.arange(2 ** 23, dtype=np.float64) * 2.0 ** -23).astype(np.float32)
+    rng = np.random.default_rng(0)
+    extra = np.concatenate([rng.uniform(0, 0.5, 1 << 20), np.exp2(rng.uniform(-60, -1, 1 << 18))])
+    u = np.concatenate([ub, extra.astype(np.float32)])
+    dev = _prim(2, torch.from_numpy(u).cuda(), torch.empty((u.size, 2), device="cuda")).cpu().numpy()
+    c, s = O.sincos2pi(u)
+    assert np.array_equal(bits(dev[:, 0]), bits(c)) and np.array_equal(bits(dev[:, 1]), bits(s))
+
+
+@pytest.mark.parametrize("seed,i,t,tag", [(0, 0, 0, 0), (12345, 7, 3, 0), (2 ** 40 + 5, 99, 1000, 1),
+                                          (77, 0, 0, 4)])
+def test_normals_bit_exact(seed, i, t, tag):
+    n4 = 1 << 20
+    q = np.arange(n4, dtype=np.uint32)
+    rows = np.stack([q, np.full(n4, i), np.full(n4, t), np.full(n4, tag),
+                     np.full(n4, seed & 0xFFFFFFFF), np.full(n4, seed >> 32)], 1).astype(np.uint32)
+    dev = _prim(3, torch.from_numpy(rows.view(np.int32)).cuda(),
+                torch.empty((n4, 4), device="cuda")).cpu().numpy().reshape(-1)
+    assert np.array_equal(bits(dev), bits(O.normals(seed, i, t, tag, 4 * n4)))
+
+
+# ------------------------------------------------------------------------ ask
+def _params(algo, R, hyper=False, **over):
+    cfg = dict(algo=algo, init=(-2.0, 2.0))
+    out = []
+    for r in range(R):
+        p = W.config_params(cfg, r, seed_offset=1000 * algo + 17, hyper_vmap=hyper)
+        p.update(over)
+        out.append(p)
+    return out
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("N,D", [(16, 1), (16, 10), (64, 1000), (32, 4099), (8, 513)])
+def test_ask_bit_exact(algo, N, D):
+    pair = Pair(algo, N, D, _params(algo, 3, hyper=True))
+    x = pair.gpu.ask().cpu().numpy()
+    for r in range(pair.R):
+        assert np.array_equal(bits(x[r]), bits(pair.orc[r].ask())), r
+    pair.close()
+
+
+# ------------------------------------------------------------------------ fitness
+@pytest.mark.parametrize("fn", FNS)
+@pytest.mark.parametrize("n,D", [(7, 1), (33, 2), (64, 7), (64, 1000), (16, 4097), (4, 70001),
+                                 (3, 262144)])
+def test_eval_parity(fn, n, D):
+    from paper_2212_04180_b200 import strategy as S
+    rng = np.random.default_rng(n * 7 + D + fn)
+    x = W.random_population(rng, n, D, scale=2.5)
+    got = S.eval_bbob(fn, torch.from_numpy(x).cuda()).cpu().numpy()
+    ref = O.evaluate(fn, x)
+    ulp = np.abs(bits(got).astype(np.int64) - bits(ref).astype(np.int64))
+    assert ulp.max() <= 1 and (ulp > 0).sum() <= max(1, n // 1000), ulp
+
+
+def test_eval_empty_and_host_buffers():
+    n, D = 5, 37
+    x = W.random_population(np.random.default_rng(1), n, D)
+    f = np.zeros(n, np.float32)
+    rc = L().es_eval_bbob(None, W.RASTRIGIN, x.ctypes.data_as(C.c_void_p), n, D,
+                          f.ctypes.data_as(C.c_void_p), None)
+    assert rc == 0
+    assert np.array_equal(bits(f), bits(O.evaluate(W.RASTRIGIN, x)))
+    assert L().es_eval_bbob(None, 0, x.ctypes.data_as(C.c_void_p), 0, D,
+                            f.ctypes.data_as(C.c_void_p), None) == 0
+
+
+# ------------------------------------------------------------------------ ranks
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("N", [2, 16, 256, 1000, 4096, 16384])
+def test_rank_and_shaping_bit_exact(algo, N):
+    if algo == W.SEP_CMA_ES and N < 16:
+        pytest.skip("elite ratio 0.2 needs N >= 5")
+    R = 3
+    pair = Pair(algo, N, 6, _params(algo, R, hyper=True))
+    rng = np.random.default_rng(N + algo)
+    f = np.stack([W.random_fitness(rng, N, ties=N // 5 + 1, nans=min(3, N // 8), infs=min(2, N // 8))
+                  for _ in range(R)])
+    pair.gpu.ask()
+    pair.gpu.tell(torch.from_numpy(f).cuda())
+    S_, E_, P_, SH = (pair.gpu.get(k).cpu().numpy() for k in ("rank_s", "rank_e", "perm", "shaped"))
+    for r in range(R):
+        s, e, perm = O.rank(f[r])
+        assert np.array_equal(S_[r], s) and np.array_equal(E_[r], e) and np.array_equal(P_[r], perm)
+        if algo in (W.OPENAI_ES, W.PGPE):
+            ref = O.centered_rank(f[r])
+        else:
+            ref = O.member_weights(pair.orc[r].wpos, f[r])
+        assert np.array_equal(bits(SH[r]), bits(ref)), r
+    pair.close()
+
+
+# ------------------------------------------------------------------------ one generation
+SHAPES = [(3, 16, 10), (2, 64, 1003), (1, 256, 5000), (2, 32, 130), (1, 2, 1)]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("R,N,D", SHAPES)
+@pytest.mark.parametrize("fn", [W.SPHERE, W.RASTRIGIN])
+def test_one_generation(algo, R, N, D, fn):
+    if algo == W.SEP_CMA_ES and N < 4:
+        pytest.skip("elite needs N >= 4 at ratio 0.4")
+    pair = Pair(algo, N, D, _params(algo, R, hyper=True))
+    x = pair.gpu.ask()
+    f = pair.gpu.eval(fn, x)
+    pair.gpu.tell(f)
+    fh = f.cpu().numpy()
+    xh = x.cpu().numpy()
+    for r in range(R):
+        xo = pair.orc[r].ask()
+        assert np.array_equal(bits(xh[r]), bits(xo))
+        fo = O.evaluate(fn, xo)
+        assert q24(fh[r], fo) <= 1e-5
+        pair.orc[r].tell(fh[r])                  # teacher-forced on the GPU's fitness
+        pair.compare(r, 1e-5)
+    pair.close()
+
+
+# ------------------------------------------------------------------------ 100 generations
+@pytest.mark.parametrize("algo,fn,N,D,R", [
+    (W.OPENAI_ES, W.SPHERE, 16, 10, 1),          # config 1, full size
+    (W.PGPE, W.ROSENBROCK, 32, 200, 2),
+    (W.SNES, W.RASTRIGIN, 32, 100, 3),
+    (W.SEP_CMA_ES, W.RASTRIGIN, 32, 100, 3),
+])
+def test_hundred_generations(algo, fn, N, D, R):
+    """Both sides run free (each evaluates its own population): 1e-5 after 1, 1e-3 after 100."""
+    cfg = W.CONFIGS["c1"] if algo == W.OPENAI_ES else dict(algo=algo, init=(-5.12, 5.12))
+    params = [W.config_params(cfg, r, seed_offset=0) for r in range(R)]
+    pair = Pair(algo, N, D, params)
+    for g in range(100):
+        x = pair.gpu.ask()
+        f = pair.gpu.eval(fn, x)
+        pair.gpu.tell(f)
+        for r in range(R):
+            o = pair.orc[r]
+            o.tell(O.evaluate(fn, o.ask()))
+        if g == 0:
+            for r in range(R):
+                pair.compare(r, 1e-5)
+    for r in range(R):
+        pair.compare(r, 1e-3)
+    pair.close()
+
+
+# ------------------------------------------------------------------------ invariants
+@pytest.mark.parametrize("algo", ALGOS)
+def test_multirun_equals_solo(algo):
+    """vmap semantics: run r of an R-batch is bit-identical to the same run alone."""
+    from paper_2212_04180_b200 import strategy as S
+    params = _params(algo, 5, hyper=True)
+    batch = S.Strategy(algo, 32, 257, params)
+    solo = S.Strategy(algo, 32, 257, [params[3]])
+    for _ in range(5):
+        for es in (batch, solo):
+            es.tell(es.eval(W.RASTRIGIN, es.ask()))
+    for f in KEPT[algo]:
+        assert np.array_equal(bits(batch.get(f)[3].cpu().numpy()), bits(solo.get(f)[0].cpu().numpy()))
+    batch.close()
+    solo.close()
+
+
+def test_tell_without_ask_is_bad_state():
+    from paper_2212_04180_b200 import strategy as S
+    from paper_2212_04180_b200._lib import ESError
+    es = S.Strategy(W.SNES, 8, 4, _params(W.SNES, 1))
+    with pytest.raises(ESError) as ei:
+        es.tell(torch.zeros((1, 8), device="cuda"))
+    assert ei.value.code == 2
+    es.close()
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_checkpoint_resume(algo):
+    """es_get / es_set round trip: a resumed run continues bit-identically."""
+    from paper_2212_04180_b200 import strategy as S
+    params = _params(algo, 2)
+    a = S.Strategy(algo, 16, 50, params)
+    for _ in range(3):
+        a.tell(a.eval(W.SPHERE, a.ask()))
+    b = S.Strategy(algo, 16, 50, params)
+    names = KEPT[algo] + ["best_f", "gen"] + (["sigma"] if algo in (0, 3) else []) + \
+        (["lrate"] if algo in (0, 1) else [])
+    for nm in names:
+        b.set(nm, a.get(nm))
+    for es in (a, b):
+        es.tell(es.eval(W.SPHERE, es.ask()))
+    for nm in KEPT[algo]:
+        assert np.array_equal(bits(a.get(nm).cpu().numpy()), bits(b.get(nm).cpu().numpy())), nm
+    a.close()
+    b.close()
+
+
+def test_host_buffer_path_matches_device():
+    from paper_2212_04180_b200 import strategy as S
+    from paper_2212_04180_b200._lib import check
+    params = _params(W.PGPE, 2)
+    a = S.Strategy(W.PGPE, 16, 33, params)
+    b = S.Strategy(W.PGPE, 16, 33, params)
+    xa = a.ask()
+    xb = torch.empty((2, 16, 33), dtype=torch.float32).pin_memory()
+    check(L().es_ask(b.ctx, C.c_void_p(xb.data_ptr()), None), b.ctx)
+    assert torch.equal(xa.cpu(), xb)
+    fa = a.eval(W.SPHERE, xa)
+    fb = fa.cpu().numpy().copy()
+    a.tell(fa)
+    check(L().es_tell(b.ctx, fb.ctypes.data_as(C.c_void_p), None), b.ctx)
+    assert torch.equal(a.get("mean"), b.get("mean"))
+    a.close()
+    b.close()
+
+
+# ------------------------------------------------------------------------ full BASELINE sizes
+@pytest.mark.parametrize("key", ["c2_sepcma", "c2_snes"])
+def test_config2_full_size_sampled_runs(key):
+    cfg = W.CONFIGS[key]
+    R, N, D = cfg["R"], cfg["N"], cfg["D"]
+    params = [W.config_params(cfg, r, hyper_vmap=True) for r in range(R)]
+    from paper_2212_04180_b200 import strategy as S
+    es = S.Strategy(cfg["algo"], N, D, params)
+    x = es.ask()
+    f = es.eval(cfg["fn"], x)
+    es.tell(f)
+    xh, fh = x.cpu().numpy(), f.cpu().numpy()
+    for r in (0, 1, 255, R - 1):
+        o = O.Run(cfg["algo"], N, D, **params[r])
+        xo = o.ask()
+        assert np.array_equal(bits(xh[r]), bits(xo))
+        assert q24(fh[r], O.evaluate(cfg["fn"], xo)) <= 1e-5
+        o.tell(fh[r])
+        for fld in KEPT[cfg["algo"]]:
+            g = es.get(fld)[r].cpu().numpy()
+            assert q24(g, o.vec[["mean", "sigma_d", "adam_m", "adam_v", "p_sigma", "p_c", "C",
+                                 "best_x"].index(fld)]) <= 1e-5, fld
+    es.close()
+
+
+def test_config3_full_size():
+    cfg = W.CONFIGS["c3"]
+    params = [W.config_params(cfg, 0)]
+    pair = Pair(cfg["algo"], cfg["N"], cfg["D"], params)
+    x = pair.gpu.ask()
+    f = pair.gpu.eval(cfg["fn"], x)
+    pair.gpu.tell(f)
+    xo = pair.orc[0].ask()
+    assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo))
+    fo = O.evaluate(cfg["fn"], xo)
+    assert q24(f[0].cpu().numpy(), fo) <= 1e-5
+    pair.orc[0].tell(f[0].cpu().numpy())
+    pair.compare(0, 1e-5)
+    pair.close()
+
+
+@pytest.mark.parametrize("N,D", [(4096, 985_216), (16384, 100_000), (256, 10_000_000)])
+def test_tell_full_size_sampled_dims(N, D):
+    """Config 4 / sweep sizes: the tell on synthetic fitness (N15), checked on 64 sampled quads
+    (incl. the first and last) by an oracle run restricted to those dimensions."""
+    rng = np.random.default_rng(N)
+    quads = np.unique(np.concatenate([[0, (D - 1) // 4], rng.integers(0, (D + 3) // 4, 62)]))
+    dims = np.array([4 * q + k for q in quads for k in range(4) if 4 * q + k < D])
+    params = [W.run_params(W.OPENAI_ES, 5, init_min=-0.04, init_max=0.04)]
+    pair = Pair(W.OPENAI_ES, N, D, params, dims=dims)
+    f = pair.gpu.synth_fitness()          # stands in for ask + evaluate (x never materialised)
+    fo = O.synth_fitness(params[0]["seed"], 0, N)
+    assert np.array_equal(bits(f[0].cpu().numpy()), bits(fo))
+    pair.gpu.tell(f)
+    pair.orc[0].tell(fo)
+    pair.compare(0, 1e-5)
+    pair.close()
