@@ -12,7 +12,7 @@ import torch
 
 import workloads as W
 from oracle import oracle as O
-from tests.gpu_helpers import KEPT, Pair, bits, q24
+from gpu_helpers import KEPT, Pair, bits, q24
 
 pytestmark = pytest.mark.gpu
 
