@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ES hot path (BASELINE.json metric: ES generations/s and N·D samples/s per
+B200 at 1/2/4/8 GPUs, with the achieved fraction of the bounding roofline).
+
+Default workload = BASELINE.json configs[1] ("c2"): Sep-CMA-ES and SNES on Rastrigin, D=1000,
+N=256, 512 independent runs each (vmap over seeds). One step = one full generation
+(ask -> evaluate -> tell) of BOTH 512-run batches. Multi-GPU: every rank runs its own 512+512 runs
+(seeds offset by rank; "replicas only", no data-path collective) -> weak scaling.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c5] [--impl reference]
+
+Prints ONE JSON line (rank 0). See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+# NUMERICS.md N16: lane-ops of one normal (Philox ¼ + Box–Muller ½ pair), spec operation count.
+NORMAL_OPS = 37
+# consumer ops per normal: ask antithetic (2 FFMA), ask plain (1 FFMA); tell: F2F + DFMA(s)
+ASK_USE = {W.OPENAI_ES: 2, W.PGPE: 2, W.SNES: 1, W.SEP_CMA_ES: 1}
+TELL_USE = {W.OPENAI_ES: 2, W.PGPE: 5, W.SNES: 5, W.SEP_CMA_ES: 4}
+STATE_BYTES = {W.OPENAI_ES: 24, W.PGPE: 32, W.SNES: 16, W.SEP_CMA_ES: 40}   # r+w per dim per tell
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=d["hbm_gbs"], sm_max_mhz=d.get("sm_max_mhz", 1965.0), src="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
+
+
+def alu_peak(peaks, sms=148):
+    # 4 SMSPs x 1 warp-instruction/clk x 32 lanes per SM (guide: 148 SMs, 1965 MHz max clock)
+    return sms * 128 * peaks["sm_max_mhz"] * 1e6
+
+
+# ----------------------------------------------------------------------------- workloads
+def handles_for(cfg_key, rank):
+    """(label, cfg dict, params list) per ES handle of the workload."""
+    if cfg_key == "c2":
+        out = []
+        for key in ("c2_sepcma", "c2_snes"):
+            cfg = W.CONFIGS[key]
+            params = [W.config_params(cfg, r, seed_offset=rank * cfg["R"], hyper_vmap=True)
+                      for r in range(cfg["R"])]
+            out.append((key, cfg, params))
+        return out
+    if cfg_key in ("c1", "c3"):
+        cfg = W.CONFIGS[cfg_key]
+        return [(cfg_key, cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
+    raise SystemExit(f"unknown config {cfg_key}")
+
+
+def sweep_cfg(N, D):
+    return dict(name=f"openai_es-synthetic-D{D}-N{N}-R1", algo=W.OPENAI_ES, fn=None, D=D, N=N, R=1,
+                init=(-0.04, 0.04))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 7
+                          for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def _oracle_gen(args):
+    """One generation of one oracle run (ask, evaluate, tell); returns samples."""
+    algo, fn, N, D, params, gens = args
+    from oracle import oracle as O
+    run = O.Run(algo, N, D, **params)
+    t0 = time.perf_counter()
+    for _ in range(gens):
+        x = run.ask()
+        run.tell(O.evaluate(fn, x))
+    return N * D * gens, time.perf_counter() - t0
+
+
+def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
+    """The oracle as it stands, on the host cores, on a bounded sample of the same workload:
+    independent runs in parallel processes (one oracle run per process)."""
+    import multiprocessing as mp
+    from oracle import oracle as O
+    O.build()
+    hs = handles_for(cfg_key, 0)
+    procs = procs or min(os.cpu_count() or 1, 8)
+    # calibrate one generation of run 0 of each handle
+    per_gen = []
+    for _, cfg, params in hs:
+        s, t = _oracle_gen((cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[0], 1))
+        per_gen.append(t)
+    n_runs = min(procs, min(len(p) for _, _, p in hs))
+    gens = max(1, int(budget_s / (sum(per_gen) * math.ceil(n_runs / procs) + 1e-9)))
+    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r], gens)
+            for _, cfg, params in hs for r in range(n_runs)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_oracle_gen, jobs)
+    wall = time.perf_counter() - t0
+    samples = sum(s for s, _ in res)
+    return {"value": samples / wall, "unit": "samples/s", "cores": procs, "kind": "oracle",
+            "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} generations each "
+                      f"(ask+eval+tell), {procs} processes, {wall:.1f} s wall"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    O.build()
+    import multiprocessing as mp
+    hs = handles_for(args.config, 0)
+    procs = min(os.cpu_count() or 1, 8)
+    n_runs = min(procs, min(len(p) for _, _, p in hs))
+    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r], 1)
+            for _, cfg, params in hs for r in range(n_runs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        for _ in range(args.warmup):
+            pool.map(_oracle_gen, jobs)
+        t0 = time.perf_counter()
+        samples = 0
+        for _ in range(args.steps):
+            samples += sum(s for s, _ in pool.map(_oracle_gen, jobs))
+        wall = time.perf_counter() - t0
+    value = samples / wall
+    sample = (f"each step: 1 generation of {n_runs} runs of each of {[h[0] for h in hs]} "
+              f"({procs} processes)")
+    line = {"metric": metric_name(args.config), "value": value, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": config_block(args.config, 1),
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": procs, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def metric_name(cfg_key):
+    return ("ES samples/sec (R*N*D per generation, summed over GPUs; generations/s alongside) "
+            "and % of roofline")
+
+
+def config_block(cfg_key, world):
+    if cfg_key == "c2":
+        a, b = W.CONFIGS["c2_sepcma"], W.CONFIGS["c2_snes"]
+        return {"workload": "c2: Sep-CMA-ES and SNES on Rastrigin, D=1000, popsize=256, 512 "
+                            "independent seeds each (App. B columns vmapped), one generation of "
+                            "both per step",
+                "R": a["R"], "N": a["N"], "D": a["D"], "handles": [a["name"], b["name"]],
+                "parallelism": f"replicas x{world} (runs per GPU fixed, no collective)",
+                "l2": "inputs larger than L2: x is 1.05 GB per step (2 x 524 MB), state 2 MB/run "
+                      "array"}
+    cfg = W.CONFIGS.get(cfg_key, {})
+    return {"workload": f"{cfg_key}: {cfg.get('name', '')}", "R": cfg.get("R"), "N": cfg.get("N"),
+            "D": cfg.get("D"), "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
+            "l2": "state resident; x > L2 only for D*N*4 > 126 MB"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2212_04180_b200 import strategy as S
+
+    peaks = load_peaks()
+    stream = torch.cuda.current_stream()
+    sharded = world > 1 and args.config != "c2"       # population sharding
+    hs = []
+    for label, cfg, params in handles_for(args.config, 0 if sharded else rank):
+        es = S.Strategy(cfg["algo"], cfg["N"], cfg["D"], params,
+                        group=dist.group.WORLD if sharded else None)
+        nl = es.local_popsize
+        x = torch.empty((cfg["R"], nl, cfg["D"]), dtype=torch.float32, device="cuda")
+        f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
+        es.params = params
+        hs.append((label, cfg, es, x, f))
+
+    def step():
+        for _, cfg, es, x, f in hs:
+            es.ask(out=x)
+            es.eval(cfg["fn"], x, out=f)
+            es.tell(f)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = sum(h[2].kernel_launches for h in hs)
+    for h in hs:
+        h[2].profile(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = sum(h[2].kernel_launches for h in hs) - launches0
+    prof = {}
+    for label, cfg, es, _, _ in hs:
+        for k, (t, n) in es.profile_read().items():
+            prof.setdefault(k, []).append((label, cfg, t, n))
+        es.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    samples_per_step = sum(cfg["R"] * cfg["N"] * cfg["D"] for _, cfg, _, _, _ in hs) * \
+        (1 if sharded else world)
+    value = samples_per_step / (ms / 1e3)
+    W_ = world if sharded else 1      # the work model below is per rank
+
+    # --- roofline of the dominant kernel kind (algorithmic work / measured duration)
+    pk_alu, pk_hbm = alu_peak(peaks), peaks["hbm_gbs"] * 1e9
+    kinds = {}
+    elite = {label: sum(math.floor(float(p["elite_ratio"]) * cfg["N"]) for p in es.params) /
+             len(es.params) for label, cfg, es, _, _ in hs}
+    for k, lst in prof.items():
+        tot_ms = sum(t for _, _, t, _ in lst)
+        ops = byt = 0.0
+        for label, cfg, t, n in lst:
+            R, N, D, algo = cfg["R"], cfg["N"] // W_, cfg["D"], cfg["algo"]
+            P = N // 2 if algo in (W.OPENAI_ES, W.PGPE) else N          # this rank's directions
+            if k == "ask":
+                ops += n * R * P * D * (NORMAL_OPS + ASK_USE[algo])
+                byt += n * (4.0 * R * N * D + 8.0 * R * D)
+            elif k == "eval_bbob":
+                byt += n * (4.0 * R * N * D + 4.0 * R * N)
+            elif k in ("tell", "tell_reduce"):
+                # Sep-CMA regenerates only the mu weighted members (no ties in continuous fitness)
+                E = elite[label] / W_ if algo == W.SEP_CMA_ES else P
+                ops += n * R * E * D * (NORMAL_OPS + TELL_USE[algo])
+                byt += n * R * D * STATE_BYTES[algo]
+            elif k == "rank":
+                byt += n * R * cfg["N"] * 40.0
+        kinds[k] = dict(ms=tot_ms, ops=ops, bytes=byt,
+                        launches=sum(n for _, _, _, n in lst))
+    dom = max(kinds, key=lambda k: kinds[k]["ms"])
+    d = kinds[dom]
+    secs = d["ms"] / 1e3
+    t_alu, t_hbm = d["ops"] / pk_alu, d["bytes"] / pk_hbm
+    if t_alu >= t_hbm:
+        achieved = d["ops"] / secs / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": pk_alu / 1e12,
+                "unit": "Tlane-op/s", "frac": achieved / (pk_alu / 1e12)}
+    else:
+        achieved = d["bytes"] / secs / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof.update(kernel=dom, launches=d["launches"], peak_source=peaks["src"],
+                traffic=ncu_traffic(args.config, dom))
+    share = {k: round(v["ms"] / (ms * args.steps), 4) for k, v in kinds.items()}
+    kernels_ms = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in kinds.items()}
+
+    # --- end to end through the C ABI with HOST buffers (fitness read back and fed to tell)
+    e2e = e2e_run(hs, args, 1 if sharded else world)
+
+    line = {"metric": metric_name(args.config), "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_block(args.config, world),
+            "generations_per_s": 1e3 / ms, "roofline": roof, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk, "kernel_share": share,
+            "kernel_ms_per_launch": kernels_ms}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    for h in hs:
+        h[2].close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def ncu_traffic(cfg_key, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(cfg_key, {}).get(kernel)
+
+
+def e2e_run(hs, args, world):
+    """Same metric through the public API with host buffers: per step and handle, ask on the
+    device, evaluate into PINNED HOST fitness (D2H), tell from that host buffer (H2D), and read
+    best_fitness back (D2H)."""
+    import torch
+    fh = [torch.empty((cfg["R"], es.local_popsize), dtype=torch.float32).pin_memory()
+          for _, cfg, es, _, _ in hs]
+    bh = [torch.empty(cfg["R"], dtype=torch.float32).pin_memory() for _, cfg, _, _, _ in hs]
+    from paper_2212_04180_b200._lib import check, lib
+    import ctypes as C
+
+    def step():
+        for (label, cfg, es, x, _), f, b in zip(hs, fh, bh):
+            es.ask(out=x)
+            s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            n = cfg["R"] * es.local_popsize
+            check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n, cfg["D"],
+                                     C.c_void_p(f.data_ptr()), s), es.ctx)
+            check(lib().es_tell(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
+            check(lib().es_get(es.ctx, 8, C.c_void_p(b.data_ptr()), s), es.ctx)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    samples = sum(cfg["R"] * cfg["N"] * cfg["D"] for _, cfg, _, _, _ in hs) * world
+    return {"value": samples / dt, "unit": "samples/s", "ms_per_step": dt * 1e3,
+            "h2d_bytes_per_step": sum(4 * cfg["R"] * es.local_popsize for _, cfg, es, _, _ in hs),
+            "d2h_bytes_per_step": sum(4 * cfg["R"] * es.local_popsize + 4 * cfg["R"]
+                                      for _, cfg, es, _, _ in hs),
+            "timing": "host wall clock (host syncs are part of the API path)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -151,6 +151,15 @@ es_status_t es_shape(const es_ctx_t *ctx, int64_t out[7]);
 /* Number of kernels this library launched on behalf of the context since creation. */
 int64_t es_kernel_launches(const es_ctx_t *ctx);
 
+/* Kernel timing for the benchmark: while enabled, the library brackets every kernel it launches
+ * for this context with a CUDA event pair on the launching stream. es_profile_read synchronises
+ * on the last event, then writes up to max_kinds entries: names (NUL-terminated, 32 bytes each),
+ * total milliseconds and launch counts per kernel kind, clears the record and returns the number
+ * of kinds (or -1 on error). */
+es_status_t es_profile_enable(es_ctx_t *ctx, int32_t on);
+int32_t es_profile_read(es_ctx_t *ctx, char *names /* [max_kinds][32] */, double *ms,
+                        int64_t *counts, int32_t max_kinds);
+
 /* Diagnostics for the parity tests: evaluate one NUMERICS primitive elementwise on the device.
  *   which = 0  Philox4x32-10 (N1): in uint32 [n][6] = (c0, c1, c2, c3, k0, k1) → out uint32 [n][4]
  *   which = 1  LN (N4):            in float [n]                                 → out float [n]

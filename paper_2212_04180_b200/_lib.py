@@ -20,7 +20,7 @@ FIELDS = dict(mean=0, sigma_d=1, adam_m=2, adam_v=3, p_sigma=4, p_c=5, C=6, best
 EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "es_get", "es_set",
            "es_set_mlp_problem", "es_mlp_num_params", "es_shape", "es_kernel_launches",
            "es_destroy", "es_last_error", "es_status_string", "es_nccl_unique_id_size",
-           "es_nccl_get_unique_id", "es_debug_primitive"]
+           "es_nccl_get_unique_id", "es_debug_primitive", "es_profile_enable", "es_profile_read"]
 
 
 class RunParams(C.Structure):
@@ -70,6 +70,8 @@ def lib():
         "es_nccl_unique_id_size": (i32, []),
         "es_nccl_get_unique_id": (i32, [vp]),
         "es_debug_primitive": (i32, [i32, vp, vp, i64, vp]),
+        "es_profile_enable": (i32, [vp, i32]),
+        "es_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(i64), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

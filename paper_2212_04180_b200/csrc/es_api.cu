@@ -49,6 +49,10 @@ struct es_ctx {
   float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
   void* mlp = nullptr;
   int64_t launches = 0;
+  bool profiling = false;
+  struct Rec { const char* name; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
   std::vector<void*> allocs;
   std::string err;
 };
@@ -89,6 +93,34 @@ static cudaError_t dalloc(es_ctx* c, void** p, size_t bytes) {
   if (e == cudaSuccess) c->allocs.push_back(*p);
   return e;
 }
+
+// Profiling brackets (bench only): an event pair around each launch on the launching stream.
+static cudaEvent_t prof_event(es_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  es_ctx* c;
+  cudaStream_t st;
+  size_t idx = (size_t)-1;
+  ProfScope(es_ctx* c_, const char* name, cudaStream_t st_) : c(c_), st(st_) {
+    if (c && c->profiling) {
+      es_ctx::Rec r{name, prof_event(c), prof_event(c)};
+      cudaEventRecord(r.a, st);
+      c->recs.push_back(r);
+      idx = c->recs.size() - 1;
+    }
+  }
+  ~ProfScope() {
+    if (idx != (size_t)-1) cudaEventRecord(c->recs[idx].b, st);
+  }
+};
 
 static bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -178,6 +210,8 @@ es_status_t es_destroy(es_ctx_t* c) {
   if (!c) return ES_SUCCESS;
   cudaDeviceSynchronize();
   if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->pool) cudaEventDestroy(e);
   if (c->mlp) mlp_problem_destroy(c->mlp);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
@@ -313,7 +347,10 @@ es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
     if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, bytes));
     dst = c->xstage;
   }
-  CUDA_OR(c, launch_ask(s, dst, st));
+  {
+    ProfScope ps(c, "ask", st);
+    CUDA_OR(c, launch_ask(s, dst, st));
+  }
   c->launches += 1;
   if (host) {
     CUDA_OR(c, cudaMemcpyAsync(x, dst, bytes, cudaMemcpyDeviceToHost, st));
@@ -334,7 +371,10 @@ es_status_t es_synth_fitness(es_ctx_t* c, float* f, es_stream_t stream_) {
     if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, bytes));
     dst = c->fstage;
   }
-  CUDA_OR(c, launch_synth(s, dst, st));
+  {
+    ProfScope ps(c, "synth_fitness", st);
+    CUDA_OR(c, launch_synth(s, dst, st));
+  }
   c->launches += 1;
   if (host) {
     CUDA_OR(c, cudaMemcpyAsync(f, dst, bytes, cudaMemcpyDeviceToHost, st));
@@ -376,8 +416,12 @@ es_status_t es_eval_bbob(es_ctx_t* c, es_fitness_t fn, const float* x, int64_t n
       fd = (float*)tmpf;
     }
   }
-  cudaError_t e = fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, n, fd, st)
-                                   : launch_eval_bbob((int)fn, xd, n, D, fd, st);
+  cudaError_t e;
+  {
+    ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : "eval_bbob", st);
+    e = fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, n, fd, st)
+                         : launch_eval_bbob((int)fn, xd, n, D, fd, st);
+  }
   if (e != cudaSuccess) return fail(c, ES_ERR_CUDA, "eval launch: %s", cudaGetErrorString(e));
   if (c) c->launches += 1;
   if (fh) {
@@ -407,23 +451,38 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   }
   const float* fsrc = fl;
   if (s.W > 1) {   // a5: every rank obtains all N fitness values
+    ProfScope ps(c, "allgather", st);
     NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
     fsrc = c->fgather;
   }
-  CUDA_OR(c, launch_rank(s, fsrc, st));
+  {
+    ProfScope ps(c, "rank", st);
+    CUDA_OR(c, launch_rank(s, fsrc, st));
+  }
   c->launches += 1;
   if (s.W == 1) {
+    ProfScope ps(c, "tell", st);
     CUDA_OR(c, launch_tell_reduce(s, true, c->nchunk, st));
     c->launches += 1;
   } else {
-    CUDA_OR(c, launch_tell_reduce(s, false, c->nchunk, st));
+    {
+      ProfScope ps(c, "tell_reduce", st);
+      CUDA_OR(c, launch_tell_reduce(s, false, c->nchunk, st));
+    }
     const size_t cnt = (size_t)(s.algo == OPENAI_ES ? 1 : 2) * s.R * s.D;   // a8 (P:226 pmean)
-    NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
-    CUDA_OR(c, launch_tell_update(s, st));
+    {
+      ProfScope ps(c, "allreduce", st);
+      NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
+    }
+    {
+      ProfScope ps(c, "tell_update", st);
+      CUDA_OR(c, launch_tell_update(s, st));
+    }
     c->launches += 2;
   }
   if (s.algo == SEP_CMA_ES) {
     int nk = 0;
+    ProfScope ps(c, "sepcma_finish", st);
     CUDA_OR(c, launch_sepcma_finish(s, st, &nk));
     c->launches += nk;
   }
@@ -508,6 +567,40 @@ es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t s
   }
   CUDA_OR(c, cudaStreamSynchronize(st));
   return ES_SUCCESS;
+}
+
+es_status_t es_profile_enable(es_ctx_t* c, int32_t on) {
+  if (!c) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL context");
+  c->profiling = on != 0;
+  return ES_SUCCESS;
+}
+
+int32_t es_profile_read(es_ctx_t* c, char* names, double* ms, int64_t* counts, int32_t max_k) {
+  if (!c || !names || !ms || !counts || max_k < 1) return -1;
+  std::vector<std::string> kinds;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& r : c->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    size_t k = 0;
+    while (k < kinds.size() && kinds[k] != r.name) ++k;
+    if (k == kinds.size()) { kinds.push_back(r.name); tot.push_back(0.0); cnt.push_back(0); }
+    tot[k] += t;
+    cnt[k] += 1;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  const int n = std::min<int>((int)kinds.size(), max_k);
+  for (int k = 0; k < n; ++k) {
+    std::memset(names + 32 * k, 0, 32);
+    std::strncpy(names + 32 * k, kinds[k].c_str(), 31);
+    ms[k] = tot[k];
+    counts[k] = cnt[k];
+  }
+  return n;
 }
 
 es_status_t es_debug_primitive(int32_t which, const void* in, void* out, int64_t n,

@@ -122,6 +122,19 @@ class Strategy:
         v = value.to(self.device).contiguous()
         check(lib().es_set(self.ctx, FIELDS[name], _ptr(v), _stream(stream)), self.ctx)
 
+    def profile(self, on=True):
+        check(lib().es_profile_enable(self.ctx, 1 if on else 0), self.ctx)
+
+    def profile_read(self, max_kinds=16):
+        names = C.create_string_buffer(32 * max_kinds)
+        ms = (C.c_double * max_kinds)()
+        cnt = (C.c_int64 * max_kinds)()
+        n = lib().es_profile_read(self.ctx, names, ms, cnt, max_kinds)
+        if n < 0:
+            raise RuntimeError("es_profile_read failed")
+        raw = names.raw
+        return {raw[32 * k:32 * k + 32].split(b"\0")[0].decode(): (ms[k], cnt[k]) for k in range(n)}
+
     @property
     def kernel_launches(self):
         return lib().es_kernel_launches(self.ctx)
