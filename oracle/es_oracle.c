@@ -254,6 +254,21 @@ void orc_ask(const orc_run_t *r, float *x) {
 }
 
 /* ---------------- N7 fitness ---------------- */
+/* sin(pi b) for b in [0, 1/2]: b * P(b^2), P of degree 5 (NUMERICS N7, Rastrigin's S). */
+static const float R0 = 0x1.921fb6p+1f, R1 = -0x1.4abc12p+2f, R2 = 0x1.467bc4p+1f,
+                   R3 = -0x1.358390p-1f, R4 = 0x1.afe86cp-4f, R5 = -0x1.656ac0p-5f;
+
+float orc_sinpi_half(float b) {
+  float s = b * b;
+  float P = R5;
+  P = fmaf(P, s, R4);
+  P = fmaf(P, s, R3);
+  P = fmaf(P, s, R2);
+  P = fmaf(P, s, R1);
+  P = fmaf(P, s, R0);
+  return b * P;
+}
+
 float orc_eval_one(int32_t fn, const float *x, int64_t D) {
   double acc = 0.0;
   if (fn == ORC_SPHERE) {
@@ -269,9 +284,8 @@ float orc_eval_one(int32_t fn, const float *x, int64_t D) {
     for (int64_t d = 0; d < D; ++d) {
       float a = fabsf(x[d]);
       float fr = a - floorf(a);
-      float c, s;
-      orc_sincos2pi(fr * 0.5f, &c, &s);
-      double S = s;
+      float b = fminf(fr, 1.0f - fr);       /* sin(pi fr) = sin(pi min(fr, 1 - fr)), b exact */
+      double S = orc_sinpi_half(b);
       acc += (double)x[d] * (double)x[d] + 20.0 * (S * S);
     }
   }
@@ -487,6 +501,9 @@ void orc_synth_fitness(uint64_t seed, uint32_t t, int32_t N, float *f) {
 /* ---------------- batch helpers (tests) ---------------- */
 void orc_ln_n(const float *u, float *out, int64_t n) {
   for (int64_t k = 0; k < n; ++k) out[k] = orc_ln(u[k]);
+}
+void orc_sinpi_half_n(const float *b, float *out, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) out[k] = orc_sinpi_half(b[k]);
 }
 void orc_sincos2pi_n(const float *u, float *c, float *s, int64_t n) {
   for (int64_t k = 0; k < n; ++k) orc_sincos2pi(u[k], c + k, s + k);

@@ -80,6 +80,7 @@ void orc_member(const orc_run_t *r, int32_t j, float *x /* [D] */);
 /* N7 fitness */
 void orc_eval(int32_t fn, const float *x, int32_t n, int64_t D, float *f);
 float orc_eval_one(int32_t fn, const float *x, int64_t D);
+float orc_sinpi_half(float b);
 
 /* N9–N11 ranking and shaping */
 uint32_t orc_key(float f);
@@ -94,6 +95,7 @@ int orc_tell(orc_run_t *r, const float *f);
 /* batch helpers for exhaustive / statistical tests */
 void orc_ln_n(const float *u, float *out, int64_t n);
 void orc_sincos2pi_n(const float *u, float *c, float *s, int64_t n);
+void orc_sinpi_half_n(const float *b, float *out, int64_t n);
 void orc_normals_n(uint64_t seed, uint32_t i, uint32_t t, uint32_t tag, int64_t n, float *out);
 
 /* N15 synthetic fitness */

@@ -68,6 +68,7 @@ def lib():
             "orc_ln": (C.c_float, [C.c_float]),
             "orc_ln_n": (None, [fp, fp, C.c_int64]),
             "orc_sincos2pi_n": (None, [fp, fp, fp, C.c_int64]),
+            "orc_sinpi_half_n": (None, [fp, fp, C.c_int64]),
             "orc_normals_n": (None, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int64, fp]),
             "orc_direction": (None, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int64, fp]),
             "orc_init": (C.c_int, [C.POINTER(RunT)]),
@@ -113,6 +114,13 @@ def sincos2pi(u):
     c, s = np.empty_like(u), np.empty_like(u)
     lib().orc_sincos2pi_n(_p(u, C.c_float), _p(c, C.c_float), _p(s, C.c_float), u.size)
     return c, s
+
+
+def sinpi_half(b):
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    out = np.empty_like(b)
+    lib().orc_sinpi_half_n(_p(b, C.c_float), _p(out, C.c_float), b.size)
+    return out
 
 
 def normals(seed, i, t, tag, n):

@@ -19,6 +19,10 @@ __global__ void prim_kernel(int which, const void* __restrict__ in, void* __rest
     } else {
       reinterpret_cast<float4*>(out)[k] = box_muller4(o);
     }
+  } else if (which == 5) {
+    static_cast<float*>(out)[k] = sinpi_half(static_cast<const float*>(in)[k]);
+  } else if (which == 4) {
+    static_cast<float*>(out)[k] = rho_sqrt(static_cast<const float*>(in)[k]);
   } else if (which == 1) {
     static_cast<float*>(out)[k] = ln_poly(static_cast<const float*>(in)[k]);
   } else {

@@ -23,10 +23,18 @@ __device__ __forceinline__ double term(float a, float b, bool has_next) {
     const double t2 = __dsub_rn(1.0, da);
     return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
   }
+  return 0.0;   // Rastrigin accumulates two sums instead (rast_acc)
+}
+
+// Rastrigin (N7): Σx² and ΣS² accumulated separately with exact-product DFMAs, combined once;
+// S = sin(π·min(fr, 1 − fr)) by the degree-5 polynomial of N7.
+__device__ __forceinline__ void rast_acc(float a, double& ax, double& as) {
   const float ab = fabsf(a);
   const float fr = __fsub_rn(ab, floorf(ab));
-  const double S = (double)sin2pi_poly(__fmul_rn(fr, 0.5f));
-  return __dadd_rn(__dmul_rn((double)a, (double)a), __dmul_rn(20.0, __dmul_rn(S, S)));
+  const double S = (double)sinpi_half(fminf(fr, __fsub_rn(1.0f, fr)));
+  const double da = (double)a;
+  ax = __fma_rn(da, da, ax);
+  as = __fma_rn(S, S, as);
 }
 
 // Accumulate this thread's strided share of one row: quads q = lane0, lane0+stride, ...
@@ -34,6 +42,38 @@ template <int FN, bool V4>
 __device__ __forceinline__ double row_partial(const float* __restrict__ row, int64_t D,
                                               int64_t lane0, int64_t stride) {
   double acc = 0.0;
+  if (FN == FN_RASTRIGIN) {
+    double ax = 0.0, as = 0.0;
+    if (V4) {
+      for (int64_t q = lane0; q < D / 4; q += stride) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
+        rast_acc(v.x, ax, as);
+        rast_acc(v.y, ax, as);
+        rast_acc(v.z, ax, as);
+        rast_acc(v.w, ax, as);
+      }
+    } else {
+      for (int64_t d = lane0; d < D; d += stride) rast_acc(__ldg(row + d), ax, as);
+    }
+    return __fma_rn(20.0, as, ax);
+  }
+  if (FN == FN_SPHERE) {
+    if (V4) {
+      for (int64_t q = lane0; q < D / 4; q += stride) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
+        acc = __fma_rn((double)v.x, (double)v.x, acc);   // exact product: = mul-then-add
+        acc = __fma_rn((double)v.y, (double)v.y, acc);
+        acc = __fma_rn((double)v.z, (double)v.z, acc);
+        acc = __fma_rn((double)v.w, (double)v.w, acc);
+      }
+    } else {
+      for (int64_t d = lane0; d < D; d += stride) {
+        const double v = __ldg(row + d);
+        acc = __fma_rn(v, v, acc);
+      }
+    }
+    return acc;
+  }
   if (V4) {
     const int64_t Q = D / 4;
     for (int64_t q = lane0; q < Q; q += stride) {

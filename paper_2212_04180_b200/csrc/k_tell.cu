@@ -27,18 +27,30 @@ static constexpr int kTile = 256;
 
 struct Acc {
   double a[4], b[4];
+  double wsum;   // Σ of the z²-term coefficients (PGPE h_i, SNES ω_j): Σ c(z²−1) = Σ c z² − Σ c
 };
 
+// Per normal: F2F + 1 DFMA (OpenAI-ES); F2F + DFMA + DMUL + DFMA (PGPE); F2F + DMUL + DADD + DFMA
+// (SNES, Sep-CMA: u = ω z feeds both sums). The (z² − 1) of N12 is applied once per chunk through
+// wsum — the same real-number sum, reassociated (binary64, ~1e-16 relative).
 template <int ALGO>
 __device__ __forceinline__ void accumulate(Acc& acc, const float4& z, double cA, double cB) {
   const float zz[4] = {z.x, z.y, z.z, z.w};
+  if (ALGO == PGPE) acc.wsum = __dadd_rn(acc.wsum, cB);
+  if (ALGO == SNES) acc.wsum = __dadd_rn(acc.wsum, cA);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const double zd = (double)zz[k];
-    acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
-    if (ALGO == PGPE) acc.b[k] = __fma_rn(cB, __dsub_rn(__dmul_rn(zd, zd), 1.0), acc.b[k]);
-    if (ALGO == SNES) acc.b[k] = __fma_rn(cA, __dsub_rn(__dmul_rn(zd, zd), 1.0), acc.b[k]);
-    if (ALGO == SEP_CMA_ES) acc.b[k] = __fma_rn(cA, __dmul_rn(zd, zd), acc.b[k]);
+    if (ALGO == OPENAI_ES) {
+      acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
+    } else if (ALGO == PGPE) {
+      acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
+      acc.b[k] = __fma_rn(cB, __dmul_rn(zd, zd), acc.b[k]);
+    } else {
+      const double u = __dmul_rn(cA, zd);
+      acc.a[k] = __dadd_rn(acc.a[k], u);
+      acc.b[k] = __fma_rn(u, zd, acc.b[k]);
+    }
   }
 }
 
@@ -141,7 +153,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
 }
 
 template <int ALGO>
-__global__ void __launch_bounds__(TT) tell_kernel(DevState s, int bpr, int nchunk, int fused) {
+__global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nchunk, int fused) {
   __shared__ uint32_t sdir[kTile];
   __shared__ double sA[kTile];
   __shared__ double sB[kTile];
@@ -164,6 +176,7 @@ __global__ void __launch_bounds__(TT) tell_kernel(DevState s, int bpr, int nchun
   const double* cA = s.coefA + (int64_t)r * s.N;
   const double* cB = s.coefB + (int64_t)r * s.N;
   Acc acc;
+  acc.wsum = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) acc.a[k] = acc.b[k] = 0.0;
   for (int b0 = c0; b0 < c1; b0 += kTile) {
@@ -182,6 +195,10 @@ __global__ void __launch_bounds__(TT) tell_kernel(DevState s, int bpr, int nchun
         accumulate<ALGO>(acc, z, sA[e], ALGO == PGPE ? sB[e] : 0.0);
       }
     }
+  }
+  if (ALGO == PGPE || ALGO == SNES) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc.b[k] = __dsub_rn(acc.b[k], acc.wsum);
   }
   const int64_t D2 = 2 * s.D;
   if (nchunk > 1) {
@@ -308,14 +325,36 @@ __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
 
 int tell_blocks_per_run(const DevState& s) { return (int)((s.Q + TT - 1) / TT); }
 
+// Entry-range split: choose n minimising waves(n) · (entries/n + c0), waves(n) = ⌈blocks·n / slots⌉,
+// slots = resident CTAs of the kernel on all SMs, c0 ≈ the per-CTA fixed cost in entry-equivalents
+// (coefficient staging, partial write-back, last-CTA reduction).
+template <int ALGO>
+static int pick_nchunk_t(const DevState& s) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tell_kernel<ALGO>, TT, 0);
+  occ = std::max(occ, 1);
+  const int64_t slots = (int64_t)sm_count() * occ;
+  const int64_t blocks = (int64_t)s.R * tell_blocks_per_run(s);
+  int ent = (s.algo == OPENAI_ES || s.algo == PGPE ? s.N / 2 : s.N);
+  ent = std::max(1, (ent + s.W - 1) / s.W);
+  const double c0 = 8.0;
+  int best = 1;
+  double best_t = 1e300;
+  for (int n = 1; n <= std::min(64, ent); ++n) {
+    const double waves = (double)((blocks * n + slots - 1) / slots);
+    const double tn = waves * ((double)ent / n + c0);
+    if (tn < best_t * 0.999) { best_t = tn; best = n; }
+  }
+  return best;
+}
+
 int tell_pick_nchunk(const DevState& s) {
-  const int bpr = tell_blocks_per_run(s);
-  const int64_t blocks = (int64_t)s.R * bpr;
-  const int64_t want = (int64_t)sm_count() * (2048 / TT) * 2;   // ~2 waves at full occupancy
-  const int ent = std::max(1, (s.algo == OPENAI_ES || s.algo == PGPE ? s.N / 2 : s.N) / s.W);
-  int n = (int)std::max<int64_t>(1, (want + blocks - 1) / blocks);
-  n = std::min(n, std::max(1, ent / 16));   // ≥ 16 entries per chunk
-  return std::min(n, 64);
+  switch (s.algo) {
+    case OPENAI_ES: return pick_nchunk_t<OPENAI_ES>(s);
+    case PGPE: return pick_nchunk_t<PGPE>(s);
+    case SNES: return pick_nchunk_t<SNES>(s);
+    default: return pick_nchunk_t<SEP_CMA_ES>(s);
+  }
 }
 
 template <int ALGO>

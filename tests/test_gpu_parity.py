@@ -61,6 +61,23 @@ def test_ln_exhaustive_bit_exact():
     assert np.array_equal(bits(dev.cpu().numpy()), bits(O.ln(ua)))
 
 
+def test_rho_exhaustive_bit_exact():
+    """ρ = sqrt_rn(−2·LN(u_a)) on every one of the 2^23 values u_a can take: the branchless device
+    square root equals the oracle's IEEE sqrtf (numpy float32 sqrt) bit for bit."""
+    m = np.arange(2 ** 23, dtype=np.float64)
+    ua = (1.0 - m * 2.0 ** -23).astype(np.float32)
+    x = (np.float32(-2.0) * O.ln(ua)).astype(np.float32)
+    dev = _prim(4, torch.from_numpy(x).cuda(), torch.empty(x.size, device="cuda"))
+    assert np.array_equal(bits(dev.cpu().numpy()), bits(np.sqrt(x)))
+
+
+def test_sinpi_half_bit_exact():
+    b = np.concatenate([np.linspace(0, 0.5, 1 << 22), np.exp2(np.random.default_rng(5).uniform(-126, -1, 1 << 20))])
+    b = b.astype(np.float32)
+    dev = _prim(5, torch.from_numpy(b).cuda(), torch.empty(b.size, device="cuda"))
+    assert np.array_equal(bits(dev.cpu().numpy()), bits(O.sinpi_half(b)))
+
+
 def test_sincos_exhaustive_bit_exact():
     ub = (np.arange(2 ** 23, dtype=np.float64) * 2.0 ** -23).astype(np.float32)
     rng = np.random.default_rng(0)

@@ -105,3 +105,17 @@ def test_streams_independent(orc):
     z2 = orc.direction(9, 5, 3, 1000)[:37]
     assert np.array_equal(z1.view(np.uint32), z2.view(np.uint32))
     assert np.array_equal(z1.view(np.uint32), orc.normals(9, 5, 3, 0, 37).view(np.uint32))
+
+
+def test_sinpi_half_vs_libm(orc):
+    """NUMERICS N7 Rastrigin factor S = sin(pi b), b in [0, 1/2]: <= 3 ulp and 2e-7 absolute against
+    double libm over 4M points plus every float in [0, 2^-10)."""
+    b = np.concatenate([np.linspace(0, 0.5, 4_000_001),
+                        np.exp2(np.random.default_rng(3).uniform(-126, -10, 1_000_000))])
+    b = b.astype(np.float32)
+    got = orc.sinpi_half(b).astype(np.float64)
+    ref = np.sin(np.pi * b.astype(np.float64))
+    assert np.abs(got - ref).max() <= 2e-7
+    nz = ref > 0
+    assert (np.abs(got[nz] - ref[nz]) / np.spacing(ref[nz].astype(np.float32))).max() <= 3.0
+    assert orc.sinpi_half(np.array([0.0, 0.5], np.float32))[0] == 0.0

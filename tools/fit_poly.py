@@ -46,3 +46,16 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def fit_sinpi_half():
+    """N7 (revised): sin(pi b) = b * P(b^2) on b in [0, 1/2] (Rastrigin's S = sin(pi frac|x|))."""
+    xs = np.linspace(1e-5, 0.5, 40001)
+    for deg in (5, 6):
+        basis = [lambda x, k=k: x ** (2 * k + 1) for k in range(deg + 1)]
+        c, e = lawson(lambda x: np.sin(np.pi * x), basis, xs, np.sin(np.pi * xs))
+        print(f"SINPI deg {deg}: max rel err {e:.3e}", [float(np.float32(v)).hex() for v in c])
+
+
+if __name__ == "__main__" and "--sinpi" in __import__("sys").argv:
+    fit_sinpi_half()
