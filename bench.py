@@ -63,12 +63,19 @@ def handles_for(cfg_key, rank):
     if cfg_key in ("c1", "c3"):
         cfg = W.CONFIGS[cfg_key]
         return [(cfg_key, cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
+    if cfg_key == "c5":
+        cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
+        return [("c5", cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
     raise SystemExit(f"unknown config {cfg_key}")
 
 
+SWEEP = {"N": 4096, "D": 985_216}     # the north-star tell point (config 4's shape)
+
+
 def sweep_cfg(N, D):
-    return dict(name=f"openai_es-synthetic-D{D}-N{N}-R1", algo=W.OPENAI_ES, fn=None, D=D, N=N, R=1,
-                init=(-0.04, 0.04))
+    """Config 5 cell: OpenAI-ES tell on synthetic fitness (N15); x is never materialised."""
+    return dict(name=f"openai_es-tell-synthetic-D{D}-N{N}-R1", algo=W.OPENAI_ES, fn=None, D=D, N=N,
+                R=1, init=(-0.04, 0.04))
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -118,10 +125,21 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
+SWEEP_ORACLE_DIMS = 2048     # dimension subset of the oracle's tell-only sample (N15 sweeps)
+
+
 def _oracle_gen(args):
-    """One generation of one oracle run (ask, evaluate, tell); returns samples."""
+    """`gens` generations of one oracle run (ask, evaluate, tell); returns (samples, seconds).
+    Tell-only sweeps (fn None) run the oracle's tell on a subset of the dimensions."""
     algo, fn, N, D, params, gens = args
     from oracle import oracle as O
+    if fn is None:
+        dims = range(min(D, SWEEP_ORACLE_DIMS))
+        run = O.Run(algo, N, D, dims=dims, **params)
+        t0 = time.perf_counter()
+        for _ in range(gens):
+            run.tell(O.synth_fitness(params["seed"], run.t, N))
+        return N * len(dims) * gens, time.perf_counter() - t0
     run = O.Run(algo, N, D, **params)
     t0 = time.perf_counter()
     for _ in range(gens):
@@ -144,7 +162,7 @@ def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
         s, t = _oracle_gen((cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[0], 1))
         per_gen.append(t)
     n_runs = min(procs, min(len(p) for _, _, p in hs))
-    gens = max(1, int(budget_s / (sum(per_gen) * math.ceil(n_runs / procs) + 1e-9)))
+    gens = max(1, int(budget_s / (sum(per_gen) * math.ceil(len(hs) * n_runs / procs) + 1e-9)))
     jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r], gens)
             for _, cfg, params in hs for r in range(n_runs)]
     t0 = time.perf_counter()
@@ -152,9 +170,12 @@ def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
         res = pool.map(_oracle_gen, jobs)
     wall = time.perf_counter() - t0
     samples = sum(s for s, _ in res)
-    return {"value": samples / wall, "unit": "samples/s", "cores": procs, "kind": "oracle",
+    return {"value": samples / wall, "unit": "samples/s", "cores": min(procs, len(jobs)),
+            "kind": "oracle",
             "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} generations each "
-                      f"(ask+eval+tell), {procs} processes, {wall:.1f} s wall"}
+                      + ("(tell on synthetic fitness, first %d dims; samples = N x those dims)"
+                         % SWEEP_ORACLE_DIMS if hs[0][1]["fn"] is None else "(ask+eval+tell)")
+                      + f", {procs} processes, {wall:.1f} s wall"}
 
 
 def run_reference(args):
@@ -210,6 +231,12 @@ def config_block(cfg_key, world):
                 "l2": "inputs larger than L2: x is 1.05 GB per step (2 x 524 MB), state 2 MB/run "
                       "array"}
     cfg = W.CONFIGS.get(cfg_key, {})
+    if cfg_key == "c5":
+        cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
+        return {"workload": f"c5 cell: {cfg['name']} (tell only on synthetic fitness, the north-star "
+                            f"D~1e6 N=4096 point)", "R": 1, "N": cfg["N"], "D": cfg["D"],
+                "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
+                "l2": "x never materialised; state 12 MB resident in L2"}
     return {"workload": f"{cfg_key}: {cfg.get('name', '')}", "R": cfg.get("R"), "N": cfg.get("N"),
             "D": cfg.get("D"), "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
             "l2": "state resident; x > L2 only for D*N*4 > 126 MB"}
@@ -225,7 +252,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--N", type=int, default=SWEEP["N"], help="c5 popsize")
+    ap.add_argument("--D", type=int, default=SWEEP["D"], help="c5 dimensions")
     args = ap.parse_args()
+    SWEEP.update(N=args.N, D=args.D)
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
@@ -254,15 +284,19 @@ def main():
         es = S.Strategy(cfg["algo"], cfg["N"], cfg["D"], params,
                         group=dist.group.WORLD if sharded else None)
         nl = es.local_popsize
-        x = torch.empty((cfg["R"], nl, cfg["D"]), dtype=torch.float32, device="cuda")
+        x = (torch.empty((cfg["R"], nl, cfg["D"]), dtype=torch.float32, device="cuda")
+             if cfg["fn"] is not None else None)
         f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
         es.params = params
         hs.append((label, cfg, es, x, f))
 
     def step():
         for _, cfg, es, x, f in hs:
-            es.ask(out=x)
-            es.eval(cfg["fn"], x, out=f)
+            if cfg["fn"] is None:            # tell-only sweep: synthetic fitness stands in
+                es.synth_fitness(out=f)
+            else:
+                es.ask(out=x)
+                es.eval(cfg["fn"], x, out=f)
             es.tell(f)
 
     for _ in range(args.warmup):
@@ -388,11 +422,14 @@ def e2e_run(hs, args, world):
 
     def step():
         for (label, cfg, es, x, _), f, b in zip(hs, fh, bh):
-            es.ask(out=x)
             s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
             n = cfg["R"] * es.local_popsize
-            check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n, cfg["D"],
-                                     C.c_void_p(f.data_ptr()), s), es.ctx)
+            if cfg["fn"] is None:
+                check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
+            else:
+                es.ask(out=x)
+                check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n,
+                                         cfg["D"], C.c_void_p(f.data_ptr()), s), es.ctx)
             check(lib().es_tell(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
             check(lib().es_get(es.ctx, 8, C.c_void_p(b.data_ptr()), s), es.ctx)
 
