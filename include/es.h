@@ -87,7 +87,10 @@ typedef enum {
   ES_FIELD_RANK_E = 14,  /* int32 [R][N]  last tell's tie-group end e_j (N9)                 */
   ES_FIELD_PERM = 15,    /* int32 [R][N]  member at each sorted position (N9)                */
   ES_FIELD_FITNESS = 16, /* float [R][N]  last tell's full (gathered) fitness                 */
-  ES_NUM_FIELDS = 17
+  ES_FIELD_DIRSUM = 17,  /* double [2][R][D] this rank's (after es_tell_local) or the summed
+                            (before es_tell_apply) binary64 direction sums of N12; OpenAI-ES
+                            uses only the first R*D entries                                    */
+  ES_NUM_FIELDS = 18
 } es_field_t;
 
 typedef struct es_ctx es_ctx_t;
@@ -96,7 +99,8 @@ typedef struct es_ctx es_ctx_t;
  * (Listing 1 `strategy.initialize`; N6). popsize N is the GLOBAL population; each rank
  * owns N/W members (= N/(2W) antithetic pairs or N/W directions). For world_size > 1,
  * nccl_unique_id points at the 128-byte ncclUniqueId that rank 0 created and broadcast
- * (e.g. via torch.distributed); it must be NULL when world_size == 1.
+ * (e.g. via torch.distributed); it is ignored when world_size == 1.
+ * world_size > 1 with nccl_unique_id == NULL creates a communicator-less shard (split-phase tell only).
  * Errors: ES_ERR_INVALID_ARG if N < 2, D < 1, R < 1, N odd (OpenAI-ES/PGPE), N mod W != 0,
  * N/W odd (OpenAI-ES/PGPE), ⌊elite_ratio·N⌋ < 1 (Sep-CMA-ES), negative σ_init, non-positive
  * lrate_init (OpenAI-ES/PGPE), world_rank outside [0, W); ES_ERR_UNSUPPORTED if N > 16384;
@@ -126,6 +130,25 @@ es_status_t es_eval_bbob(es_ctx_t *ctx, es_fitness_t fn, const float *x, int64_t
  * t ← t+1. Errors: ES_ERR_BAD_STATE if no es_ask since the last tell; ES_ERR_INVALID_ARG for
  * NULL fitness. */
 es_status_t es_tell(es_ctx_t *ctx, const float *fitness, es_stream_t stream);
+
+/* Split-phase tell, for callers that manage the communication themselves (es_tell is exactly
+ * all-gather + es_tell_local + all-reduce(ES_FIELD_DIRSUM) + es_tell_apply):
+ *   es_tell_local  ranks/shapes the GATHERED fitness fitness_all (float [W][R][N/W], the rank-major
+ *                  result of all-gathering every rank's slice), tracks the best member and reduces
+ *                  this rank's share of the tell entries (es_shard_plan) into ES_FIELD_DIRSUM.
+ *   es_tell_apply  applies the update from ES_FIELD_DIRSUM, which the caller has replaced by its
+ *                  sum over ranks (es_get / es_set), and advances t.
+ * Contexts created with world_size > 1 and nccl_unique_id == NULL have no communicator and can
+ * only tell this way (es_tell then returns ES_ERR_BAD_STATE). Errors: ES_ERR_BAD_STATE when called
+ * out of order (ask → local → apply). */
+es_status_t es_tell_local(es_ctx_t *ctx, const float *fitness_all, es_stream_t stream);
+es_status_t es_tell_apply(es_ctx_t *ctx, es_stream_t stream);
+
+/* Population-sharding plan: for a population of `popsize` over world_size ranks and
+ * `entries` weighted tell entries (P directions, or Sep-CMA-ES's weighted positions), write
+ * out[0..4) = (first member, end member, first entry, end entry) owned by `rank`. Host-only. */
+es_status_t es_shard_plan(int32_t popsize, int32_t entries, int32_t world_size, int32_t rank,
+                          int32_t out[4]);
 
 /* Synthetic fitness for tell-only sweeps (N15): fitness[r][j], j over this rank's members. */
 es_status_t es_synth_fitness(es_ctx_t *ctx, float *fitness, es_stream_t stream);

@@ -350,10 +350,27 @@ void orc_member_weights(const float *wpos, const float *f, int32_t N, float *w) 
 }
 
 /* ---------------- N12 reductions ---------------- */
-void orc_reduce(const orc_run_t *r, const float *f, double *G) {
+/* Number of tell entries: P directions (antithetic), N members (SNES), or Sep-CMA's weighted
+ * sorted positions (through the end of the tie group containing position mu-1). */
+int orc_num_entries(const orc_run_t *r, const float *f) {
+  if (is_antithetic(r->algo)) return r->popsize / 2;
+  if (r->algo == ORC_SNES) return r->popsize;
+  int32_t N = r->popsize;
+  int32_t *s = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+  int32_t *e = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+  int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+  orc_rank(f, N, s, e, perm);
+  int ne = e[perm[r->mu - 1]] + 1;
+  free(s); free(e); free(perm);
+  return ne;
+}
+
+/* The direction sums of N12 restricted to tell entries [e0, e1): the share one rank of a
+ * population-sharded run reduces before the all-reduce ("batch evolutionary gradients ...
+ * aggregated via map-reduce"). orc_reduce is the full range. */
+void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1, double *G) {
   const int64_t D = r->num_dims;
   const int32_t N = r->popsize;
-  const int32_t P = orc_num_directions(r);
   double *G0 = G, *G1 = G + D;
   for (int64_t d = 0; d < 2 * D; ++d) G[d] = 0.0;
   float *sh = (float *)malloc(sizeof(float) * (size_t)N);
@@ -364,7 +381,7 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
     double bbar = 0.0;
     for (int32_t j = 0; j < N; ++j) bbar += (double)sh[j];
     bbar = bbar / N;
-    for (int32_t i = 0; i < P; ++i) {
+    for (int32_t i = e0; i < e1; ++i) {
       double a = (double)sh[2 * i] - (double)sh[2 * i + 1];
       double h = ((double)sh[2 * i] + (double)sh[2 * i + 1]) * 0.5 - bbar;
       run_direction(r, (uint32_t)i, r->t, z);
@@ -374,10 +391,16 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
       }
     }
   } else {
+    int32_t *s = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+    int32_t *e = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+    int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+    orc_rank(f, N, s, e, perm);
     orc_member_weights(r->wpos, f, N, sh);
-    for (int32_t j = 0; j < N; ++j) {
+    for (int32_t q = e0; q < e1; ++q) {
+      /* SNES entries are members in index order; Sep-CMA entries are sorted positions */
+      int32_t j = r->algo == ORC_SNES ? q : perm[q];
       double w = (double)sh[j];
-      if (sh[j] == 0.0f) continue; /* outside the elite (Sep-CMA); contributes exactly 0 */
+      if (sh[j] == 0.0f) continue; /* outside the elite: contributes exactly 0 */
       run_direction(r, (uint32_t)j, r->t, z);
       for (int64_t d = 0; d < D; ++d) {
         double zd = (double)z[d];
@@ -386,9 +409,14 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
         else G1[d] += w * (zd * zd);
       }
     }
+    free(s); free(e); free(perm);
   }
   free(sh);
   free(z);
+}
+
+void orc_reduce(const orc_run_t *r, const float *f, double *G) {
+  orc_reduce_range(r, f, 0, orc_num_entries(r, f), G);
 }
 
 static void adam(orc_run_t *r, int64_t d, float g, float bc1, float bc2) {

@@ -90,6 +90,8 @@ void orc_member_weights(const float *wpos, const float *f, int32_t N, float *w);
 
 /* N12 tell: reductions (double) G[k][D] from shaped values, then update. */
 void orc_reduce(const orc_run_t *r, const float *f, double *G /* [2][D] */);
+int orc_num_entries(const orc_run_t *r, const float *f);
+void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1, double *G);
 int orc_tell(orc_run_t *r, const float *f);
 
 /* batch helpers for exhaustive / statistical tests */

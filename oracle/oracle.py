@@ -81,6 +81,8 @@ def lib():
             "orc_centered_rank": (None, [fp, C.c_int32, fp]),
             "orc_member_weights": (None, [fp, fp, C.c_int32, fp]),
             "orc_reduce": (None, [C.POINTER(RunT), fp, dp]),
+            "orc_reduce_range": (None, [C.POINTER(RunT), fp, C.c_int32, C.c_int32, dp]),
+            "orc_num_entries": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_tell": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_synth_fitness": (None, [C.c_uint64, C.c_uint32, C.c_int32, fp]),
         }
@@ -242,6 +244,16 @@ class Run:
         G = np.empty((2, self.r.num_dims), dtype=np.float64)
         lib().orc_reduce(C.byref(self.r), _p(f, C.c_float), _p(G, C.c_double))
         return G
+
+    def reduce_range(self, f, e0, e1):
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        G = np.empty((2, self.r.num_dims), dtype=np.float64)
+        lib().orc_reduce_range(C.byref(self.r), _p(f, C.c_float), e0, e1, _p(G, C.c_double))
+        return G
+
+    def num_entries(self, f):
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        return lib().orc_num_entries(C.byref(self.r), _p(f, C.c_float))
 
     def tell(self, f):
         f = np.ascontiguousarray(f, dtype=np.float32)

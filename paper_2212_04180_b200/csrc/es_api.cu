@@ -42,10 +42,12 @@ struct es_ctx {
   std::vector<RunScal> host_rs;
   ncclComm_t comm = nullptr;
   bool asked = false;
+  bool told_local = false;
   bool broken = false;
   int nchunk = 1;
   float* fgather = nullptr;     // [W][R][Nloc]
   float* fstage = nullptr;      // [R][Nloc] staging of host fitness
+  float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
   float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
   void* mlp = nullptr;
   int64_t launches = 0;
@@ -231,8 +233,6 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   if (D < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be >= 1");
   if (D >= (int64_t(1) << 34)) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be < 2^34");
   if (W < 1 || rank < 0 || rank >= W) return fail(nullptr, ES_ERR_INVALID_ARG, "bad rank/world_size");
-  if ((W > 1) != (uid != nullptr))
-    return fail(nullptr, ES_ERR_INVALID_ARG, "nccl_unique_id must be given iff world_size > 1");
   if (N % W) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be divisible by world_size");
   if (antithetic(algo) && ((N % 2) || ((N / W) % 2)))
     return fail(nullptr, ES_ERR_INVALID_ARG, "antithetic strategies need an even popsize per rank");
@@ -321,7 +321,7 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   TRY(launch_init(s, st));
   c->launches += 1;
   TRY(cudaStreamSynchronize(st));   // host tables above are stack-owned
-  if (W > 1) {
+  if (W > 1 && uid) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     ncclResult_t nr = ncclCommInitRank(&c->comm, W, id, rank);
@@ -436,49 +436,27 @@ es_status_t es_eval_bbob(es_ctx_t* c, es_fitness_t fn, const float* x, int64_t n
   return ES_SUCCESS;
 }
 
-es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!c || !fitness) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
-  if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_tell without a preceding es_ask");
+// a6 + a7 (+ a10 bookkeeping): ranks of the gathered fitness, then this rank's entry reduction.
+static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cudaStream_t st) {
   const DevState& s = c->s;
-  const size_t nloc = (size_t)s.R * s.Nloc;
-  const float* fl = fitness;
-  if (!is_device_ptr(fitness)) {
-    if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
-    CUDA_OR(c, cudaMemcpyAsync(c->fstage, fitness, nloc * sizeof(float), cudaMemcpyHostToDevice, st));
-    fl = c->fstage;
-  }
-  const float* fsrc = fl;
-  if (s.W > 1) {   // a5: every rank obtains all N fitness values (P:226)
-    ProfScope ps(c, "allgather", st);
-    NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
-    fsrc = c->fgather;
-  }
   {
     ProfScope ps(c, "rank", st);
     CUDA_OR(c, launch_rank(s, fsrc, st));
   }
   c->launches += 1;
-  if (s.W == 1) {
-    ProfScope ps(c, "tell", st);
-    CUDA_OR(c, launch_tell_reduce(s, true, c->nchunk, st));
+  ProfScope ps(c, fused ? "tell" : "tell_reduce", st);
+  CUDA_OR(c, launch_tell_reduce(s, fused, c->nchunk, st));
+  c->launches += 1;
+  return ES_SUCCESS;
+}
+
+// a9 from the summed direction sums (update kernel), then Sep-CMA's global-norm phases.
+static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st) {
+  const DevState& s = c->s;
+  if (!fused) {
+    ProfScope ps(c, "tell_update", st);
+    CUDA_OR(c, launch_tell_update(s, st));
     c->launches += 1;
-  } else {
-    {
-      ProfScope ps(c, "tell_reduce", st);
-      CUDA_OR(c, launch_tell_reduce(s, false, c->nchunk, st));
-    }
-    const size_t cnt = (size_t)(s.algo == OPENAI_ES ? 1 : 2) * s.R * s.D;   // a8 (P:226 pmean)
-    {
-      ProfScope ps(c, "allreduce", st);
-      NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
-    }
-    {
-      ProfScope ps(c, "tell_update", st);
-      CUDA_OR(c, launch_tell_update(s, st));
-    }
-    c->launches += 2;
   }
   if (s.algo == SEP_CMA_ES) {
     int nk = 0;
@@ -486,7 +464,83 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     CUDA_OR(c, launch_sepcma_finish(s, st, &nk));
     c->launches += nk;
   }
+  return ES_SUCCESS;
+}
+
+static const float* stage_fitness(es_ctx* c, const float* f, size_t n, cudaStream_t st,
+                                  float** buf, es_status_t* err) {
+  *err = ES_SUCCESS;
+  if (is_device_ptr(f)) return f;
+  if (!*buf) {
+    cudaError_t e = dalloc(c, (void**)buf, n * sizeof(float));
+    if (e != cudaSuccess) { *err = fail(c, ES_ERR_OOM, "staging: %s", cudaGetErrorString(e)); return nullptr; }
+  }
+  cudaError_t e = cudaMemcpyAsync(*buf, f, n * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) { *err = fail(c, ES_ERR_CUDA, "H2D fitness: %s", cudaGetErrorString(e)); return nullptr; }
+  return *buf;
+}
+
+es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !fitness) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
+  if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_tell without a preceding es_ask");
+  const DevState& s = c->s;
+  if (s.W > 1 && !c->comm)
+    return fail(c, ES_ERR_BAD_STATE, "no communicator: use es_tell_local / es_tell_apply");
+  const size_t nloc = (size_t)s.R * s.Nloc;
+  es_status_t err;
+  const float* fl = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
+  if (!fl) return err;
+  const bool fused = s.W == 1;
+  const float* fsrc = fl;
+  if (s.W > 1) {   // a5: every rank obtains all N fitness values (P:226)
+    ProfScope ps(c, "allgather", st);
+    NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
+    fsrc = c->fgather;
+  }
+  if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
+  if (s.W > 1) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
+    const size_t cnt = (size_t)(s.algo == OPENAI_ES ? 1 : 2) * s.R * s.D;
+    ProfScope ps(c, "allreduce", st);
+    NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
+  }
+  if ((err = tell_apply_impl(c, fused, st)) != ES_SUCCESS) return err;
   c->asked = false;
+  return ES_SUCCESS;
+}
+
+es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !fitness_all) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->asked || c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_local out of order");
+  es_status_t err;
+  const float* fsrc = stage_fitness(c, fitness_all, (size_t)c->s.R * c->s.N, st, &c->fgather_stage, &err);
+  if (!fsrc) return err;
+  if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) return err;
+  c->told_local = true;
+  return ES_SUCCESS;
+}
+
+es_status_t es_tell_apply(es_ctx_t* c, es_stream_t stream_) {
+  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_apply without es_tell_local");
+  es_status_t err = tell_apply_impl(c, false, (cudaStream_t)stream_);
+  if (err != ES_SUCCESS) return err;
+  c->told_local = false;
+  c->asked = false;
+  return ES_SUCCESS;
+}
+
+es_status_t es_shard_plan(int32_t N, int32_t entries, int32_t W, int32_t rank, int32_t out[4]) {
+  if (!out || N < 1 || entries < 0 || W < 1 || rank < 0 || rank >= W || N % W)
+    return fail(nullptr, ES_ERR_INVALID_ARG, "bad shard plan arguments");
+  out[0] = rank * (N / W);
+  out[1] = (rank + 1) * (N / W);
+  int e0, e1;
+  shard_range(entries, W, rank, e0, e1);
+  out[2] = e0;
+  out[3] = e1;
   return ES_SUCCESS;
 }
 
@@ -511,6 +565,7 @@ static bool field_ok(const es_ctx* c, int f, void** base, size_t* elem, size_t* 
     case ES_FIELD_RANK_E: *base = s.rs_e; *count = RN; return true;
     case ES_FIELD_PERM: *base = s.perm; *count = RN; return true;
     case ES_FIELD_FITNESS: *base = s.fit; *count = RN; return true;
+    case ES_FIELD_DIRSUM: *base = s.G; *count = 2 * (size_t)s.R * s.D; *elem = 8; return true;
   }
   return false;
 }
@@ -535,7 +590,8 @@ es_status_t es_get(es_ctx_t* c, es_field_t field, void* dst, es_stream_t stream_
 es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !src) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (field >= ES_FIELD_SHAPED) return fail(c, ES_ERR_INVALID_ARG, "field %d is read-only", field);
+  if (field >= ES_FIELD_SHAPED && field != ES_FIELD_DIRSUM)
+    return fail(c, ES_ERR_INVALID_ARG, "field %d is read-only", field);
   void* base = nullptr;
   size_t elem, count = 0, off = 0;
   bool scal;

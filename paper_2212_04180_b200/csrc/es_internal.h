@@ -69,6 +69,14 @@ struct DevState {
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
 };
 
+// Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
+// tell kernel and es_shard_plan so that host plan and device split cannot disagree.
+__host__ __device__ __forceinline__ void shard_range(int ne, int W, int rank, int& e0, int& e1) {
+  const int per = (ne + W - 1) / W;
+  e0 = rank * per < ne ? rank * per : ne;
+  e1 = e0 + per < ne ? e0 + per : ne;
+}
+
 // Launch helpers (return cudaGetLastError()).
 cudaError_t launch_init(const DevState& s, cudaStream_t st);
 cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st);

@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
   const int chunk = blockIdx.y;
   const GenScal& gs = s.gs[r];
   const int ne = gs.nentries;
-  const int per = (ne + s.W - 1) / s.W;
-  const int e0 = min(ne, s.rank * per), e1 = min(ne, e0 + per);
+  int e0, e1;
+  shard_range(ne, s.W, s.rank, e0, e1);
   const int cper = (e1 - e0 + nchunk - 1) / nchunk;
   const int c0 = min(e1, e0 + chunk * cper), c1 = min(e1, c0 + cper);
   const Philox ph(s.rs[r].seed);

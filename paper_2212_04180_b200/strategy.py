@@ -40,8 +40,11 @@ def eval_bbob(fn, x, out=None, stream=None, ctx=None):
 class Strategy:
     """R independent runs of one algorithm (vmap over seeds / hyperparameters)."""
 
-    def __init__(self, algo, popsize, num_dims, params, device="cuda", group=None, stream=None):
-        """params: one dict per run (es_run_params_t fields; 'seed' required)."""
+    def __init__(self, algo, popsize, num_dims, params, device="cuda", group=None, stream=None,
+                 shard=None):
+        """params: one dict per run (es_run_params_t fields; 'seed' required).
+        group: torch.distributed group for population sharding with NCCL inside es_tell.
+        shard: (rank, world_size) for a communicator-less shard (split-phase tell only)."""
         if isinstance(params, dict):
             params = [params]
         self.algo, self.popsize, self.num_dims = int(algo), int(popsize), int(num_dims)
@@ -67,6 +70,8 @@ class Strategy:
             buf = bbuf.cpu()
             self._uid = buf
             uid = C.c_void_p(buf.data_ptr())
+        if shard is not None:
+            self.rank, self.world_size = int(shard[0]), int(shard[1])
         self.ctx = C.c_void_p()
         with torch.cuda.device(self.device):
             check(lib().es_init(C.byref(self.ctx), self.algo, self.R, self.popsize, self.num_dims,
@@ -91,6 +96,14 @@ class Strategy:
     def tell(self, fitness, stream=None):
         check(lib().es_tell(self.ctx, _ptr(fitness), _stream(stream)), self.ctx)
 
+    def tell_local(self, fitness_all, stream=None):
+        """Split phase 1: rank the gathered fitness [W, R, N/W] and reduce this rank's entries."""
+        check(lib().es_tell_local(self.ctx, _ptr(fitness_all), _stream(stream)), self.ctx)
+
+    def tell_apply(self, stream=None):
+        """Split phase 2: apply the update from the (summed) 'dirsum' field."""
+        check(lib().es_tell_apply(self.ctx, _stream(stream)), self.ctx)
+
     def synth_fitness(self, out=None, stream=None):
         f = out if out is not None else torch.empty(
             (self.R, self.local_popsize), dtype=torch.float32, device=self.device)
@@ -109,11 +122,13 @@ class Strategy:
             return (R,)
         if name in ("shaped", "rank_s", "rank_e", "perm", "fitness"):
             return (R, N)
+        if name == "dirsum":
+            return (2, R, D)
         return (R, D)
 
     def get(self, name, stream=None):
         dt = {"gen": torch.int32, "rank_s": torch.int32, "rank_e": torch.int32,
-              "perm": torch.int32}.get(name, torch.float32)
+              "perm": torch.int32, "dirsum": torch.float64}.get(name, torch.float32)
         out = torch.empty(self._shape(name), dtype=dt, device=self.device)
         check(lib().es_get(self.ctx, FIELDS[name], _ptr(out), _stream(stream)), self.ctx)
         return out

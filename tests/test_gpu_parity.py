@@ -349,3 +349,43 @@ def test_tell_full_size_sampled_dims(N, D):
     pair.orc[0].tell(fo)
     pair.compare(0, 1e-5)
     pair.close()
+
+
+# ------------------------------------------------------------------------ sharded population
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("Wn", [2, 4])
+def test_emulated_shards_match_single_gpu(algo, Wn):
+    """W communicator-less shards on one GPU, exchanging through the split-phase ABI exactly as
+    es_tell does through NCCL (all-gather of fitness, binary64 sum of the direction sums in rank
+    order): populations and ranks bit-identical to the unsharded run, state within 1e-6."""
+    from paper_2212_04180_b200 import strategy as S
+    N, D, R = 32, 301, 2
+    params = _params(algo, R, hyper=True)
+    ref = S.Strategy(algo, N, D, params)
+    shards = [S.Strategy(algo, N, D, params, shard=(w, Wn)) for w in range(Wn)]
+    nl = N // Wn
+    for gen in range(3):
+        x = ref.ask()
+        f = ref.eval(W.RASTRIGIN, x)
+        ref.tell(f)
+        locs = []
+        for w, sh in enumerate(shards):
+            xs = sh.ask()
+            assert torch.equal(xs, x[:, w * nl:(w + 1) * nl]), (gen, w)
+            locs.append(sh.eval(W.RASTRIGIN, xs))
+        gathered = torch.stack(locs).contiguous()                 # [W][R][N/W]
+        for sh in shards:
+            sh.tell_local(gathered)
+        total = shards[0].get("dirsum")
+        for sh in shards[1:]:
+            total = total + sh.get("dirsum")
+        for sh in shards:
+            sh.set("dirsum", total)
+            sh.tell_apply()
+        for sh in shards:
+            for k in ("perm", "shaped"):
+                assert torch.equal(sh.get(k), ref.get(k)), k
+            for fld in KEPT[algo]:
+                assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, fld
+    for es in shards + [ref]:
+        es.close()
