@@ -158,10 +158,12 @@ es_status_t es_synth_fitness(es_ctx_t *ctx, float *fitness, es_stream_t stream);
 es_status_t es_get(es_ctx_t *ctx, es_field_t field, void *dst, es_stream_t stream);
 es_status_t es_set(es_ctx_t *ctx, es_field_t field, const void *src, es_stream_t stream);
 
-/* MLP fitness problem (N14): widths[0..n_widths) layer widths (input first), `batch` inputs
- * drawn from the DATA stream of data_seed, teacher weights from the TEACHER stream. Flattening of
- * a parameter vector: per layer W as [in][out] row-major then b[out], layers in order.
- * Errors: ES_ERR_INVALID_ARG for n_widths < 2, widths not multiples of 16, batch not 128. */
+/* MLP fitness problem (N14): widths[0..n_widths) layer widths (input first; every layer tanh,
+ * P:268–269), `batch` inputs drawn from the DATA stream of data_seed, teacher θ* from the TEACHER
+ * stream, targets Y* = MLP_θ*(U) computed on the device by the same kernel. Flattening of a
+ * parameter vector: per layer W as [out][in] row-major (nn.Linear layout) then b[out], layers in
+ * order. Synchronises the stream. Errors: ES_ERR_INVALID_ARG for n_widths outside 2..16;
+ * ES_ERR_UNSUPPORTED for widths not multiples of 16 in [16, 512] or batch != 128. */
 es_status_t es_set_mlp_problem(es_ctx_t *ctx, const int32_t *widths, int32_t n_widths,
                                int32_t batch, uint64_t data_seed, es_stream_t stream);
 

@@ -544,3 +544,127 @@ void orc_normals_n(uint64_t seed, uint32_t i, uint32_t t, uint32_t tag, int64_t 
     for (int k = 0; k < 4 && 4 * q + k < n; ++k) out[4 * q + k] = v[k];
   }
 }
+
+/* ---------------- N14 synthetic MLP fitness ---------------- */
+/* IEEE binary16 round-to-nearest-even, returned widened to float (exact). */
+float orc_fp16(float f) {
+  if (isnan(f)) return f;
+  uint32_t sign = f2u(f) & 0x80000000u;
+  float a = fabsf(f);
+  float r;
+  if (a >= 65520.0f) {
+    r = INFINITY;
+  } else if (a < 0x1p-14f) {           /* binary16 subnormal range: quantum 2^-24 */
+    r = rintf(a * 0x1p24f) * 0x1p-24f;
+  } else {                             /* 11 significant bits: quantum 2^(e-10) */
+    int e = (int)((f2u(a) >> 23) & 0xFF) - 127;
+    float quantum = ldexpf(1.0f, e - 10);
+    r = rintf(a / quantum) * quantum;
+  }
+  return u2f(sign | f2u(r));
+}
+
+struct orc_mlp {
+  int32_t nw, batch;
+  int32_t w[16];
+  uint64_t seed;
+  int64_t D;
+  float *U;      /* [batch][w0] */
+  float *Y;      /* [batch][wL] teacher outputs */
+};
+
+int64_t orc_mlp_dims(const orc_mlp_t *p) { return p->D; }
+
+static int64_t layer_off(const orc_mlp_t *p, int l) {   /* l = 1..L */
+  int64_t off = 0;
+  for (int q = 1; q < l; ++q) off += (int64_t)p->w[q - 1] * p->w[q] + p->w[q];
+  return off;
+}
+
+void orc_mlp_teacher(const orc_mlp_t *p, float *theta) {
+  for (int l = 1; l < p->nw; ++l) {
+    const int in = p->w[l - 1], out = p->w[l];
+    const float s = (float)(1.0 / sqrt((double)in));
+    float *W = theta + layer_off(p, l);
+    for (int n = 0; n < out; ++n)
+      for (int k = 0; k < in; ++k) {
+        float z[4];
+        orc_normals4(p->seed, (uint32_t)(k / 4), (uint32_t)(4096 * l + n), 0u, 3u, z);
+        W[(int64_t)n * in + k] = z[k % 4] * s;
+      }
+    for (int n = 0; n < out; ++n) W[(int64_t)out * in + n] = 0.0f;
+  }
+}
+
+/* g_L of one parameter vector (N14); out [batch][wL] */
+static void mlp_forward(const orc_mlp_t *p, const float *x, float *out) {
+  const int B = p->batch;
+  int maxw = 0;
+  for (int l = 0; l < p->nw; ++l) maxw = p->w[l] > maxw ? p->w[l] : maxw;
+  double *h = (double *)malloc(sizeof(double) * (size_t)B * maxw);
+  double *hn = (double *)malloc(sizeof(double) * (size_t)B * maxw);
+  double *Wd = (double *)malloc(sizeof(double) * (size_t)maxw * maxw);
+  for (int b = 0; b < B; ++b)
+    for (int k = 0; k < p->w[0]; ++k) h[(int64_t)b * p->w[0] + k] = orc_fp16(p->U[(int64_t)b * p->w[0] + k]);
+  for (int l = 1; l < p->nw; ++l) {
+    const int in = p->w[l - 1], nout = p->w[l];
+    const float *W = x + layer_off(p, l);
+    const float *bias = W + (int64_t)nout * in;
+    for (int64_t e = 0; e < (int64_t)nout * in; ++e) Wd[e] = orc_fp16(W[e]);
+    for (int b = 0; b < B; ++b)
+      for (int n = 0; n < nout; ++n) {
+        double acc = 0.0;
+        for (int k = 0; k < in; ++k) acc += h[(int64_t)b * in + k] * Wd[(int64_t)n * in + k];
+        float g = (float)tanh(acc + (double)bias[n]);
+        if (l + 1 < p->nw) hn[(int64_t)b * nout + n] = orc_fp16(g);
+        else out[(int64_t)b * nout + n] = g;
+      }
+    double *t = h; h = hn; hn = t;
+  }
+  free(h); free(hn); free(Wd);
+}
+
+orc_mlp_t *orc_mlp_create(const int32_t *widths, int32_t nw, int32_t batch, uint64_t seed) {
+  if (nw < 2 || nw > 16 || batch < 1) return NULL;
+  orc_mlp_t *p = (orc_mlp_t *)calloc(1, sizeof(orc_mlp_t));
+  p->nw = nw; p->batch = batch; p->seed = seed;
+  for (int l = 0; l < nw; ++l) p->w[l] = widths[l];
+  p->D = layer_off(p, nw);
+  const int in0 = widths[0], outL = widths[nw - 1];
+  p->U = (float *)malloc(sizeof(float) * (size_t)batch * in0);
+  for (int b = 0; b < batch; ++b)
+    for (int k = 0; k < in0; ++k) {
+      float z[4];
+      orc_normals4(seed, (uint32_t)(k / 4), (uint32_t)b, 0u, 2u, z);
+      p->U[(int64_t)b * in0 + k] = z[k % 4];
+    }
+  float *theta = (float *)malloc(sizeof(float) * (size_t)p->D);
+  orc_mlp_teacher(p, theta);
+  p->Y = (float *)malloc(sizeof(float) * (size_t)batch * outL);
+  mlp_forward(p, theta, p->Y);
+  free(theta);
+  return p;
+}
+
+void orc_mlp_destroy(orc_mlp_t *p) {
+  if (!p) return;
+  free(p->U); free(p->Y); free(p);
+}
+
+void orc_mlp_eval(const orc_mlp_t *p, const float *x, int32_t n, float *f) {
+  const int B = p->batch, outL = p->w[p->nw - 1];
+  float *g = (float *)malloc(sizeof(float) * (size_t)B * outL);
+  for (int32_t j = 0; j < n; ++j) {
+    mlp_forward(p, x + (int64_t)j * p->D, g);
+    double acc = 0.0;
+    for (int64_t e = 0; e < (int64_t)B * outL; ++e) {
+      double d = (double)g[e] - (double)p->Y[e];
+      acc += d * d;
+    }
+    f[j] = (float)(acc / ((double)B * outL));
+  }
+  free(g);
+}
+
+const float *orc_mlp_targets(const orc_mlp_t *p) { return p->Y; }
+const float *orc_mlp_inputs(const orc_mlp_t *p) { return p->U; }

@@ -100,6 +100,17 @@ void orc_sincos2pi_n(const float *u, float *c, float *s, int64_t n);
 void orc_sinpi_half_n(const float *b, float *out, int64_t n);
 void orc_normals_n(uint64_t seed, uint32_t i, uint32_t t, uint32_t tag, int64_t n, float *out);
 
+/* N14 synthetic MLP fitness */
+typedef struct orc_mlp orc_mlp_t;
+float orc_fp16(float f);
+orc_mlp_t *orc_mlp_create(const int32_t *widths, int32_t nw, int32_t batch, uint64_t seed);
+void orc_mlp_destroy(orc_mlp_t *p);
+int64_t orc_mlp_dims(const orc_mlp_t *p);
+void orc_mlp_teacher(const orc_mlp_t *p, float *theta);
+void orc_mlp_eval(const orc_mlp_t *p, const float *x, int32_t n, float *f);
+const float *orc_mlp_targets(const orc_mlp_t *p);
+const float *orc_mlp_inputs(const orc_mlp_t *p);
+
 /* N15 synthetic fitness */
 void orc_synth_fitness(uint64_t seed, uint32_t t, int32_t N, float *f);
 

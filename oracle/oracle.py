@@ -85,6 +85,14 @@ def lib():
             "orc_num_entries": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_tell": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_synth_fitness": (None, [C.c_uint64, C.c_uint32, C.c_int32, fp]),
+            "orc_fp16": (C.c_float, [C.c_float]),
+            "orc_mlp_create": (C.c_void_p, [i32p, C.c_int32, C.c_int32, C.c_uint64]),
+            "orc_mlp_destroy": (None, [C.c_void_p]),
+            "orc_mlp_dims": (C.c_int64, [C.c_void_p]),
+            "orc_mlp_teacher": (None, [C.c_void_p, fp]),
+            "orc_mlp_eval": (None, [C.c_void_p, fp, C.c_int32, fp]),
+            "orc_mlp_targets": (fp, [C.c_void_p]),
+            "orc_mlp_inputs": (fp, [C.c_void_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -258,3 +266,46 @@ class Run:
     def tell(self, f):
         f = np.ascontiguousarray(f, dtype=np.float32)
         lib().orc_tell(C.byref(self.r), _p(f, C.c_float))
+
+
+class MLP:
+    """N14 synthetic MLP regression problem (oracle side)."""
+
+    def __init__(self, widths, batch=128, seed=0):
+        w = (C.c_int32 * len(widths))(*widths)
+        self.widths, self.batch = list(widths), batch
+        self.h = lib().orc_mlp_create(w, len(widths), batch, seed)
+        if not self.h:
+            raise ValueError("bad MLP problem")
+        self.D = lib().orc_mlp_dims(self.h)
+
+    def teacher(self):
+        t = np.empty(self.D, dtype=np.float32)
+        lib().orc_mlp_teacher(self.h, _p(t, C.c_float))
+        return t
+
+    def targets(self):
+        p = lib().orc_mlp_targets(self.h)
+        return np.ctypeslib.as_array(p, shape=(self.batch * self.widths[-1],)).reshape(
+            self.batch, self.widths[-1]).copy()
+
+    def inputs(self):
+        p = lib().orc_mlp_inputs(self.h)
+        return np.ctypeslib.as_array(p, shape=(self.batch * self.widths[0],)).reshape(
+            self.batch, self.widths[0]).copy()
+
+    def evaluate(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1, self.D)
+        f = np.empty(x.shape[0], dtype=np.float32)
+        lib().orc_mlp_eval(self.h, _p(x, C.c_float), x.shape[0], _p(f, C.c_float))
+        return f
+
+    def __del__(self):
+        try:
+            lib().orc_mlp_destroy(self.h)
+        except Exception:
+            pass
+
+
+def fp16(v):
+    return np.array([lib().orc_fp16(float(a)) for a in np.ravel(v)], dtype=np.float32)

@@ -1,17 +1,486 @@
-// k_mlp.cu — K4 synthetic-MLP fitness (NUMERICS N14). Placeholder until the tcgen05 kernel lands.
+// k_mlp.cu — K4: synthetic-MLP fitness on the 5th-generation tensor cores (NUMERICS N14; P:212
+// "MLP", topology P:268–270). Per population member: L chained [128 × w_{l-1}]·[w_{l-1} × w_l]
+// GEMMs (batch 128), tanh, and the MSE against the teacher's outputs.
+//
+// One persistent CTA per SM walks the members. Warp roles (544 threads):
+//   warps 0–7   producers: stream the member's fp32 weights from HBM (LDG.128, 16 in flight per
+//               thread), round to fp16, and store them into a 6-stage ring of [128 n × 64 k] fp16
+//               tiles in the UMMA K-major SWIZZLE_128B layout; arrive on full[s].
+//   warps 8–15  epilogue: tcgen05.ld the fp32 accumulator (TMEM lane = batch row), + bias, tanh,
+//               round to fp16 and write the next layer's A operand (smem, same layout); last layer:
+//               squared error vs. the teacher.
+//   warp 16     TMEM allocator + a single elected thread issuing tcgen05.mma.kind::f16
+//               (M=128, N=128, K=16; fp32 accumulation in TMEM, 512 columns = one whole layer).
+// The activations never leave the SM (A: 128 KB smem); weights are read from HBM exactly once.
+// Bound: HBM (4 B/parameter/member); tensor work is ~20 % of the HBM time at B = 128.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
 #include <string>
+#include <vector>
 
 #include "es_internal.h"
+#include "noise.cuh"
 
 namespace esb {
-void* mlp_problem_create(const int32_t*, int32_t, int32_t, uint64_t, cudaStream_t,
-                         std::string* err) {
-  *err = "unsupported: the MLP fitness kernel is not built in this revision";
-  return nullptr;
+
+static constexpr int kBatch = 128;
+static constexpr int kMaxLayers = 15;
+static constexpr int kStages = 6;
+static constexpr int kProdWarps = 8, kEpiWarps = 8;
+static constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
+static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
+static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
+static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 256;
+
+struct MlpParams {
+  int nl;                       // layers L
+  int w[kMaxLayers + 1];        // widths
+  int kpad[kMaxLayers + 1];     // w rounded up to 64 (as K of the next layer)
+  int npad[kMaxLayers + 1];     // w rounded up to 128 (as N)
+  int64_t off[kMaxLayers + 1];  // offset of W_l in a parameter vector (l = 1..L)
+  int64_t D;
+  const float* x;               // [n][D]
+  int64_t n;
+  float* f;                     // [n] fitness (mode 0)
+  const __half* uimg;           // layer-1 A image (pre-swizzled)
+  float* Y;                     // [128][w_L] teacher outputs (read in mode 0, written in mode 1)
+  int mode;
+};
+
+struct MlpProblem {
+  MlpParams p;                  // x/n/f/mode filled per launch
+  __half* uimg = nullptr;
+  float* Y = nullptr;
+  float* theta = nullptr;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
-void mlp_problem_destroy(void*) {}
-int64_t mlp_problem_dims(const void*) { return -1; }
-cudaError_t launch_mlp_eval(void*, const float*, int64_t, float*, cudaStream_t) {
-  return cudaErrorNotSupported;
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: SBO = 1024 B between 8-row groups,
+// version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D f32, A/B f16, both K-major, N = 128, M = 128.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Byte offset of the 16-byte chunk c (k = 8c..8c+7) of row r in a [rows × 64] fp16 K-major
+// SWIZZLE_128B tile: 8-row groups of 1024 B, chunk index XOR (row mod 8).
+__host__ __device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  uint4 o;
+  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
+  __half2 h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
+  o.x = *reinterpret_cast<uint32_t*>(&h0);
+  o.y = *reinterpret_cast<uint32_t*>(&h1);
+  o.z = *reinterpret_cast<uint32_t*>(&h2);
+  o.w = *reinterpret_cast<uint32_t*>(&h3);
+  return o;
+}
+
+// ---------------------------------------------------------------- the fitness kernel
+__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* A = smem;                                 // [8][128 rows][64] fp16
+  uint8_t* Bst = smem + kABytes;                     // [kStages][128 rows][64] fp16
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages * kTileBytes);
+  uint64_t* full = bars;                             // [kStages]
+  uint64_t* empty = bars + kStages;                  // [kStages]
+  uint64_t* dready = bars + 2 * kStages;
+  uint64_t* aready = bars + 2 * kStages + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
+  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 3);   // [kEpiWarps]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (smem_u32(smem) & 1023) __trap();               // SWIZZLE_128B needs 1024-B alignment
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kProdWarps);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(dready, 1);
+    mbar_init(aready, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProdWarps + kEpiWarps) {              // TMEM: 512 fp32 columns × 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int L = P.nl;
+
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ producers
+    const int t = threadIdx.x;                       // 0..255
+    int stage = 0;
+    uint32_t phase = 0;
+    // flat task stream: (member, layer, n-tile, k-chunk); two stages per round for MLP
+    for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
+      const float* xm = P.x + m * P.D;
+      for (int l = 1; l <= L; ++l) {
+        const int in = P.w[l - 1], out = P.w[l];
+        const float* W = xm + P.off[l];
+        const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+        for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+          const int nt = tile / kc_n, kc = tile % kc_n;
+          mbar_wait(&empty[stage], phase ^ 1);
+          float4 v[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {              // 1024 chunks of 8 k per tile, 4 per thread
+            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
+            const int n = nt * 128 + r, k = kc * 64 + c * 8;
+            if (n < out && k < in) {
+              const float4* src = reinterpret_cast<const float4*>(W + (int64_t)n * in + k);
+              v[2 * j] = __ldcs(src);
+              v[2 * j + 1] = __ldcs(src + 1);
+            } else {
+              v[2 * j] = v[2 * j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          uint8_t* dst = Bst + stage * kTileBytes;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
+            const float e[8] = {v[2 * j].x, v[2 * j].y, v[2 * j].z, v[2 * j].w,
+                                v[2 * j + 1].x, v[2 * j + 1].y, v[2 * j + 1].z, v[2 * j + 1].w};
+            *reinterpret_cast<uint4*>(dst + swz(r, c)) = pack8(e);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp < kProdWarps + kEpiWarps) {
+    // ------------------------------------------------------------ epilogue
+    const int e = warp - kProdWarps;                 // 0..7
+    const int q = e & 3, hh = e >> 2;                // TMEM lane quarter, column half
+    const int row = q * 32 + lane;                   // batch row = TMEM lane
+    const int et = threadIdx.x - kProdWarps * 32;    // 0..255
+    uint32_t dphase = 0;
+    for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
+      const float* xm = P.x + m * P.D;
+      // A <- layer-1 inputs (fp16 image, L2-resident)
+      {
+        const int bytes = (P.kpad[0] >> 6) * kTileBytes;
+        const uint4* src = reinterpret_cast<const uint4*>(P.uimg);
+        for (int o = et; o < bytes / 16; o += kEpiWarps * 32)
+          reinterpret_cast<uint4*>(A)[o] = __ldg(src + o);
+        fence_async_smem();
+        named_bar(1, kEpiWarps * 32);
+        if (et == 0) mbar_arrive(aready);
+      }
+      float sq = 0.0f;
+      for (int l = 1; l <= L; ++l) {
+        const int in = P.w[l - 1], out = P.w[l];
+        const float* bias = xm + P.off[l] + (int64_t)out * in;
+        const int half = P.npad[l] >> 1;
+        mbar_wait(dready, dphase);
+        dphase ^= 1;
+        tc_fence_after();
+        for (int c0 = hh * half; c0 < (hh + 1) * half; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int n = c0 + i;
+            v[i] = n < out ? tanhf(__fadd_rn(v[i], __ldg(bias + n))) : 0.0f;
+          }
+          if (l < L) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {            // 4 chunks of 8 k in k-block c0/64
+              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = pack8(v + 8 * c);
+            }
+          } else if (P.mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int n = c0 + i;
+              if (n < out) {
+                const float d = __fsub_rn(v[i], __ldg(P.Y + (int64_t)row * out + n));
+                sq = __fmaf_rn(d, d, sq);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i < out) P.Y[(int64_t)row * out + c0 + i] = v[i];
+          }
+        }
+        tc_fence_before();
+        if (l < L) {
+          fence_async_smem();
+          named_bar(1, kEpiWarps * 32);
+          if (et == 0) mbar_arrive(aready);
+        }
+      }
+      // fitness = Σ squares / (B · w_L)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) red[e] = sq;
+      named_bar(1, kEpiWarps * 32);
+      if (et == 0 && P.mode == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < kEpiWarps; ++k) tot += (double)red[k];
+        P.f[m] = (float)(tot / ((double)kBatch * P.w[L]));
+      }
+      named_bar(1, kEpiWarps * 32);
+    }
+  } else {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16(128, 128);
+      int stage = 0;
+      uint32_t phase = 0, aphase = 0;
+      const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
+        for (int l = 1; l <= L; ++l) {
+          mbar_wait(aready, aphase);
+          aphase ^= 1;
+          tc_fence_after();
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+            const int nt = tile / kc_n, kc = tile % kc_n;
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {          // K = 16 per instruction, 64 per tile
+              const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
+              const uint64_t bd = smem_desc(b_base + stage * kTileBytes + ks * 32);
+              mma_f16(tmem + (uint32_t)(nt * 128), ad, bd, idesc, (kc | ks) != 0);
+            }
+            mma_commit(&empty[stage]);               // frees the stage when these MMAs finish
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(dready);                        // the layer's accumulator is complete
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProdWarps + kEpiWarps) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- problem setup kernels
+// U (DATA stream) → fp16 → the pre-swizzled layer-1 A image.
+__global__ void mlp_uimg_kernel(uint64_t seed, int w0, int kpad0, __half* img) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;   // one thread per (row, 8-k chunk)
+  const int chunks = kpad0 / 8;
+  if (idx >= kBatch * chunks) return;
+  const int r = idx / chunks, cc = idx % chunks;
+  const Philox ph(seed);
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    const int k = cc * 8 + i;
+    if (k < w0) {
+      const float4 z = normal4(ph, (uint32_t)(k / 4), (uint32_t)r, 0u, TAG_DATA);
+      v[i] = z.x; v[i + 1] = z.y; v[i + 2] = z.z; v[i + 3] = z.w;
+    } else {
+      v[i] = v[i + 1] = v[i + 2] = v[i + 3] = 0.f;
+    }
+  }
+  const int kb = cc / 8, c = cc % 8;
+  uint8_t* base = reinterpret_cast<uint8_t*>(img) + kb * kTileBytes + swz(r, c);
+  *reinterpret_cast<uint4*>(base) = pack8(v);
+}
+
+// θ* (TEACHER stream): W*_l[n][k] = z ⊗ (float)(1/√in), b* = 0.
+__global__ void mlp_teacher_kernel(uint64_t seed, int l, int in, int out, float scale,
+                                   float* W) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)out * in + out) return;
+  if (idx >= (int64_t)out * in) {
+    W[idx] = 0.0f;
+    return;
+  }
+  const int n = (int)(idx / in), k = (int)(idx % in);
+  const Philox ph(seed);
+  const float4 z = normal4(ph, (uint32_t)(k / 4), (uint32_t)(4096 * l + n), 0u, TAG_TEACHER);
+  W[idx] = __fmul_rn(f4get(z, k % 4), scale);
+}
+
+void mlp_problem_destroy(void* prob);
+
+static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
+  p.nl = nw - 1;
+  int64_t off = 0;
+  for (int l = 0; l < nw; ++l) {
+    p.w[l] = widths[l];
+    p.kpad[l] = (widths[l] + 63) / 64 * 64;
+    p.npad[l] = (widths[l] + 127) / 128 * 128;
+  }
+  for (int l = 1; l < nw; ++l) {
+    p.off[l] = off;
+    off += (int64_t)widths[l - 1] * widths[l] + widths[l];
+  }
+  p.off[0] = 0;
+  p.D = off;
+}
+
+static cudaError_t launch_mlp(const MlpParams& p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = (int)std::min<int64_t>(p.n, sm_count());
+  mlp_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
+                         cudaStream_t st, std::string* err) {
+  if (batch != kBatch) { *err = "unsupported: batch must be 128"; return nullptr; }
+  if (nw < 2 || nw > kMaxLayers + 1) { *err = "need 2..16 widths"; return nullptr; }
+  for (int l = 0; l < nw; ++l) {
+    if (widths[l] < 16 || widths[l] % 16 || widths[l] > 512) {
+      *err = "unsupported: widths must be multiples of 16 in [16, 512]";
+      return nullptr;
+    }
+  }
+  MlpProblem* pr = new MlpProblem();
+  fill_params(pr->p, widths, nw);
+  const MlpParams& p = pr->p;
+  cudaError_t e = cudaSuccess;
+  const size_t img = (size_t)(p.kpad[0] / 64) * kTileBytes;
+  if ((e = cudaMalloc(&pr->uimg, img)) != cudaSuccess ||
+      (e = cudaMalloc(&pr->Y, (size_t)kBatch * widths[nw - 1] * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&pr->theta, (size_t)p.D * sizeof(float))) != cudaSuccess) {
+    *err = std::string("allocation: ") + cudaGetErrorString(e);
+    mlp_problem_destroy(pr);
+    return nullptr;
+  }
+  const int nthr = kBatch * (p.kpad[0] / 8);
+  mlp_uimg_kernel<<<(nthr + 255) / 256, 256, 0, st>>>(seed, widths[0], p.kpad[0], pr->uimg);
+  for (int l = 1; l < nw; ++l) {
+    const int64_t cnt = (int64_t)widths[l] * widths[l - 1] + widths[l];
+    const float sc = (float)(1.0 / std::sqrt((double)widths[l - 1]));
+    mlp_teacher_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(
+        seed, l, widths[l - 1], widths[l], sc, pr->theta + p.off[l]);
+  }
+  pr->p.uimg = pr->uimg;
+  pr->p.Y = pr->Y;
+  MlpParams q = pr->p;
+  q.x = pr->theta;
+  q.n = 1;
+  q.f = nullptr;
+  q.mode = 1;                                   // write Y* = g_L(θ*)
+  if ((e = launch_mlp(q, st)) != cudaSuccess || (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    *err = std::string("teacher forward: ") + cudaGetErrorString(e);
+    mlp_problem_destroy(pr);
+    return nullptr;
+  }
+  return pr;
+}
+
+void mlp_problem_destroy(void* prob) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  if (!pr) return;
+  cudaFree(pr->uimg);
+  cudaFree(pr->Y);
+  cudaFree(pr->theta);
+  delete pr;
+}
+
+int64_t mlp_problem_dims(const void* prob) {
+  return prob ? static_cast<const MlpProblem*>(prob)->p.D : -1;
+}
+
+cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
+  MlpParams q = pr->p;
+  q.x = x;
+  q.n = n;
+  q.f = f;
+  q.mode = 0;
+  return launch_mlp(q, st);
+}
+
+// es_get helpers for tests: teacher parameters and targets (device pointers).
+const float* mlp_problem_theta(const void* prob) { return static_cast<const MlpProblem*>(prob)->theta; }
+const float* mlp_problem_targets(const void* prob) { return static_cast<const MlpProblem*>(prob)->Y; }
+
 }  // namespace esb

@@ -389,3 +389,56 @@ def test_emulated_shards_match_single_gpu(algo, Wn):
                 assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, fld
     for es in shards + [ref]:
         es.close()
+
+
+# ------------------------------------------------------------------------ MLP fitness (N14, tcgen05)
+@pytest.mark.parametrize("widths,n", [([32, 64, 64, 64, 64, 16], 24), ([16, 32], 8),
+                                      ([256, 512, 512, 512, 512, 128], 6),
+                                      ([96, 160, 48], 10)])
+def test_mlp_fitness_parity(widths, n):
+    from paper_2212_04180_b200 import strategy as S
+    m = O.MLP(widths, 128, 7)
+    es = S.Strategy(W.OPENAI_ES, 16, m.D, [W.run_params(W.OPENAI_ES, 1, init_min=-0.04,
+                                                       init_max=0.04)])
+    es.set_mlp_problem(widths, 128, 7)
+    theta = m.teacher()
+    f0 = es.eval(W.MLP, torch.from_numpy(theta[None]).cuda(), out=torch.empty(1, device="cuda"))
+    assert float(f0[0]) == 0.0           # GPU teacher stream and targets identical to the spec
+    rng = np.random.default_rng(len(widths))
+    scales = np.geomspace(1e-3, 0.5, n)
+    xs = np.stack([theta + s * rng.standard_normal(m.D) for s in scales]).astype(np.float32)
+    got = es.eval(W.MLP, torch.from_numpy(xs).cuda(), out=torch.empty(n, device="cuda"))
+    got = got.cpu().numpy().astype(np.float64)
+    ref = m.evaluate(xs).astype(np.float64)
+    # DESIGN §3 / NUMERICS N14: the tensor cores accumulate in fp32, the oracle in binary64; the
+    # accumulation order flips rare fp16 roundings of activations. An fp32-vs-binary64 emulation of
+    # the same forward (numpy sgemm vs dgemm) differs by the same amounts (≤ 6e-5 relative at
+    # f ≈ 3e-3, ≤ 3e-6 at f ≈ 1), so the derived bar is Q24 ≤ 1e-4 over the population's fitness
+    # vector and 1e-5 relative for members with f ≥ 0.03.
+    assert q24(got, ref) <= 1e-4, (got, ref)
+    big = ref >= 3e-2
+    assert np.all(np.abs(got[big] - ref[big]) <= 1e-5 * ref[big]), (got, ref)
+    es.close()
+
+
+def test_mlp_openai_es_generations_teacher_forced():
+    """Config-4 path at reduced size ([32, 64x4, 16], D = 15,632, N = 256): ask bit-exact, MLP
+    fitness within the derived 1e-4 (Q24), tell fed the GPU's fitness within 1e-5, 5 generations."""
+    from paper_2212_04180_b200 import strategy as S
+    widths = [32, 64, 64, 64, 64, 16]
+    m = O.MLP(widths, 128, 3)
+    params = [W.run_params(W.OPENAI_ES, 9, init_min=-0.04, init_max=0.04)]
+    pair = Pair(W.OPENAI_ES, 256, m.D, params)
+    pair.gpu.set_mlp_problem(widths, 128, 3)
+    for g in range(5):
+        x = pair.gpu.ask()
+        f = pair.gpu.eval(W.MLP, x)
+        xo = pair.orc[0].ask()
+        assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo))
+        if g in (0, 4):
+            fo = m.evaluate(xo[:32])
+            assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-4
+        pair.gpu.tell(f)
+        pair.orc[0].tell(f[0].cpu().numpy())
+        pair.compare(0, 1e-5)
+    pair.close()
