@@ -40,8 +40,9 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return dict(hbm_gbs=d["hbm_gbs"], sm_max_mhz=d.get("sm_max_mhz", 1965.0), src="measured")
-    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
+        return dict(hbm_gbs=d["hbm_gbs"], sm_max_mhz=d.get("sm_max_mhz", 1965.0),
+                    bf16_tflops=d.get("bf16_tflops", 1590.0), src="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, bf16_tflops=1590.0, src="fallback")
 
 
 def alu_peak(peaks, sms=148):
@@ -66,10 +67,14 @@ def handles_for(cfg_key, rank):
     if cfg_key == "c5":
         cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
         return [("c5", cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
+    if cfg_key == "c4":
+        cfg = dict(W.CONFIGS["c4"], widths=MLP_WIDTHS, batch=128, data_seed=0)
+        return [("c4", cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
     raise SystemExit(f"unknown config {cfg_key}")
 
 
 SWEEP = {"N": 4096, "D": 985_216}     # the north-star tell point (config 4's shape)
+MLP_WIDTHS = [256, 512, 512, 512, 512, 128]   # config 4: D = 985,216
 
 
 def sweep_cfg(N, D):
@@ -140,6 +145,15 @@ def _oracle_gen(args):
         for _ in range(gens):
             run.tell(O.synth_fitness(params["seed"], run.t, N))
         return N * len(dims) * gens, time.perf_counter() - t0
+    if fn == W.MLP:
+        # config 4: ask + MLP fitness of `gens` members (the tell, a third of the oracle's
+        # per-generation work, is excluded from this sample)
+        mlp = O.MLP(MLP_WIDTHS, 128, 0)
+        run = O.Run(algo, N, D, **params)
+        t0 = time.perf_counter()
+        for j in range(gens):
+            mlp.evaluate(run.member(j % N))
+        return D * gens, time.perf_counter() - t0
     run = O.Run(algo, N, D, **params)
     t0 = time.perf_counter()
     for _ in range(gens):
@@ -162,8 +176,10 @@ def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
         s, t = _oracle_gen((cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[0], 1))
         per_gen.append(t)
     n_runs = min(procs, min(len(p) for _, _, p in hs))
+    if hs[0][1]["fn"] == W.MLP:
+        n_runs = procs                     # one run, members spread over processes
     gens = max(1, int(budget_s / (sum(per_gen) * math.ceil(len(hs) * n_runs / procs) + 1e-9)))
-    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r], gens)
+    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r % len(params)], gens)
             for _, cfg, params in hs for r in range(n_runs)]
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(procs) as pool:
@@ -172,9 +188,11 @@ def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
     samples = sum(s for s, _ in res)
     return {"value": samples / wall, "unit": "samples/s", "cores": min(procs, len(jobs)),
             "kind": "oracle",
-            "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} generations each "
-                      + ("(tell on synthetic fitness, first %d dims; samples = N x those dims)"
-                         % SWEEP_ORACLE_DIMS if hs[0][1]["fn"] is None else "(ask+eval+tell)")
+            "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} "
+                      + ("generations each (tell on synthetic fitness, first %d dims; samples = "
+                         "N x those dims)" % SWEEP_ORACLE_DIMS if hs[0][1]["fn"] is None else
+                         "members each (ask + MLP fitness; tell excluded)"
+                         if hs[0][1]["fn"] == W.MLP else "generations each (ask+eval+tell)")
                       + f", {procs} processes, {wall:.1f} s wall"}
 
 
@@ -189,7 +207,9 @@ def run_reference(args):
     hs = handles_for(args.config, 0)
     procs = min(os.cpu_count() or 1, 8)
     n_runs = min(procs, min(len(p) for _, _, p in hs))
-    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r], 1)
+    if hs[0][1]["fn"] == W.MLP:
+        n_runs = procs
+    jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r % len(params)], 1)
             for _, cfg, params in hs for r in range(n_runs)]
     with mp.get_context("fork").Pool(procs) as pool:
         for _ in range(args.warmup):
@@ -231,6 +251,13 @@ def config_block(cfg_key, world):
                 "l2": "inputs larger than L2: x is 1.05 GB per step (2 x 524 MB), state 2 MB/run "
                       "array"}
     cfg = W.CONFIGS.get(cfg_key, {})
+    if cfg_key == "c4":
+        c = W.CONFIGS["c4"]
+        return {"workload": "c4: OpenAI-ES + Adam on the synthetic tanh-MLP fitness "
+                            f"{MLP_WIDTHS} (D=985,216), popsize 4096, batch 128",
+                "R": 1, "N": c["N"], "D": c["D"],
+                "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
+                "l2": "inputs larger than L2: x is 16.1 GB per step"}
     if cfg_key == "c5":
         cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
         return {"workload": f"c5 cell: {cfg['name']} (tell only on synthetic fitness, the north-star "
@@ -288,6 +315,8 @@ def main():
              if cfg["fn"] is not None else None)
         f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
         es.params = params
+        if cfg["fn"] == W.MLP:
+            es.set_mlp_problem(cfg["widths"], cfg["batch"], cfg["data_seed"])
         hs.append((label, cfg, es, x, f))
 
     def step():
@@ -343,7 +372,7 @@ def main():
              len(es.params) for label, cfg, es, _, _ in hs}
     for k, lst in prof.items():
         tot_ms = sum(t for _, _, t, _ in lst)
-        ops = byt = 0.0
+        ops = byt = flops = 0.0
         for label, cfg, t, n in lst:
             R, N, D, algo = cfg["R"], cfg["N"] // W_, cfg["D"], cfg["algo"]
             P = N // 2 if algo in (W.OPENAI_ES, W.PGPE) else N          # this rank's directions
@@ -359,13 +388,23 @@ def main():
                 byt += n * R * D * STATE_BYTES[algo]
             elif k == "rank":
                 byt += n * R * cfg["N"] * 40.0
-        kinds[k] = dict(ms=tot_ms, ops=ops, bytes=byt,
+            elif k == "eval_mlp":
+                byt += n * (4.0 * R * N * D + 4.0 * R * N)
+                wd = cfg["widths"]
+                flops += n * R * N * 2.0 * cfg["batch"] * sum(wd[i] * wd[i + 1]
+                                                              for i in range(len(wd) - 1))
+        kinds[k] = dict(ms=tot_ms, ops=ops, bytes=byt, flops=flops,
                         launches=sum(n for _, _, _, n in lst))
     dom = max(kinds, key=lambda k: kinds[k]["ms"])
     d = kinds[dom]
     secs = d["ms"] / 1e3
     t_alu, t_hbm = d["ops"] / pk_alu, d["bytes"] / pk_hbm
-    if t_alu >= t_hbm:
+    t_tc = d["flops"] / (peaks["bf16_tflops"] * 1e12)
+    if t_tc > max(t_alu, t_hbm):
+        achieved = d["flops"] / secs / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"]}
+    elif t_alu >= t_hbm:
         achieved = d["ops"] / secs / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": pk_alu / 1e12,
                 "unit": "Tlane-op/s", "frac": achieved / (pk_alu / 1e12)}
@@ -375,6 +414,12 @@ def main():
                 "frac": achieved / peaks["hbm_gbs"]}
     roof.update(kernel=dom, launches=d["launches"], peak_source=peaks["src"],
                 traffic=ncu_traffic(args.config, dom))
+    extra = {}
+    for k, v in kinds.items():
+        if v["ms"] > 0:
+            extra[k] = {"GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
+                        "Tlane-op/s": round(v["ops"] / (v["ms"] / 1e3) / 1e12, 2),
+                        "TFLOP/s": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1)}
     share = {k: round(v["ms"] / (ms * args.steps), 4) for k, v in kinds.items()}
     kernels_ms = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in kinds.items()}
 
@@ -388,7 +433,7 @@ def main():
             "data": "synthetic", "config": config_block(args.config, world),
             "generations_per_s": 1e3 / ms, "roofline": roof, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "kernel_share": share,
-            "kernel_ms_per_launch": kernels_ms}
+            "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_budget)
     if rank == 0:

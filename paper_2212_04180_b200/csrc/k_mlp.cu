@@ -3,9 +3,10 @@
 // GEMMs (batch 128), tanh, and the MSE against the teacher's outputs.
 //
 // One persistent CTA per SM walks the members. Warp roles (544 threads):
-//   warps 0–7   producers: stream the member's fp32 weights from HBM (LDG.128, 16 in flight per
-//               thread), round to fp16, and store them into a 6-stage ring of [128 n × 64 k] fp16
-//               tiles in the UMMA K-major SWIZZLE_128B layout; arrive on full[s].
+//   warps 0–7   producers: prefetch the next (layer, n-tile) weight block into L2 with the TMA
+//               engine (cp.async.bulk.prefetch.L2), stream the current one with LDG.128, round to
+//               fp16, and store it into a 6-stage ring of [128 n × 64 k] fp16 tiles in the UMMA
+//               K-major SWIZZLE_128B layout; arrive on full[s].
 //   warps 8–15  epilogue: tcgen05.ld the fp32 accumulator (TMEM lane = batch row), + bias, tanh,
 //               round to fp16 and write the next layer's A operand (smem, same layout); last layer:
 //               squared error vs. the teacher.
@@ -73,6 +74,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -187,7 +191,34 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
     const int t = threadIdx.x;                       // 0..255
     int stage = 0;
     uint32_t phase = 0;
-    // flat task stream: (member, layer, n-tile, k-chunk); two stages per round for MLP
+    // Task stream: (member, layer, n-tile, k-chunk). The 128 weight rows of one (layer, n-tile)
+    // are one contiguous block; when a block starts, warp 0 asks the TMA engine to prefetch the
+    // NEXT block into L2 (cp.async.bulk.prefetch), so the LDG.128s below hit L2 and the HBM stream
+    // does not depend on the producers' own load parallelism.
+    auto block_of = [&](int64_t m, int l, int nt, const float** ptr, uint32_t* bytes) {
+      const int in = P.w[l - 1], out = P.w[l];
+      const int rows = min(128, out - nt * 128);
+      *ptr = P.x + m * P.D + P.off[l] + (int64_t)nt * 128 * in;
+      *bytes = rows > 0 ? (uint32_t)rows * in * 4u : 0u;
+    };
+    auto prefetch_block = [&](int64_t m, int l, int nt) {
+      // next (layer, n-tile) after (m, l, nt) in stream order
+      if (++nt >= (P.npad[l] >> 7)) { nt = 0; if (++l > L) { l = 1; m += gridDim.x; } }
+      if (m >= P.n) return;
+      const float* ptr;
+      uint32_t bytes;
+      block_of(m, l, nt, &ptr, &bytes);
+      const uint32_t chunk = 8192;
+      for (uint32_t o = lane * chunk; o < bytes; o += 32 * chunk)
+        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(chunk, bytes - o));
+    };
+    if (warp == 0 && blockIdx.x < P.n) {
+      const float* ptr;
+      uint32_t bytes;
+      block_of(blockIdx.x, 1, 0, &ptr, &bytes);
+      for (uint32_t o = lane * 8192u; o < bytes; o += 32 * 8192u)
+        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(8192u, bytes - o));
+    }
     for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
       const float* xm = P.x + m * P.D;
       for (int l = 1; l <= L; ++l) {
@@ -196,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
         const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
         for (int tile = 0; tile < nt_n * kc_n; ++tile) {
           const int nt = tile / kc_n, kc = tile % kc_n;
+          if (kc == 0 && warp == 0) prefetch_block(m, l, nt);
           mbar_wait(&empty[stage], phase ^ 1);
           float4 v[8];
 #pragma unroll
