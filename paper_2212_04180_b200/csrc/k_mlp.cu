@@ -29,11 +29,11 @@ namespace esb {
 static constexpr int kBatch = 128;
 static constexpr int kMaxLayers = 15;
 static constexpr int kStages = 6;
-static constexpr int kProdWarps = 8, kEpiWarps = 8;
+static constexpr int kProdWarps = 8, kEpiWarps = 16;
 static constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
-static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 256;
+static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 512;
 
 struct MlpParams {
   int nl;                       // layers L
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
   uint64_t* dready = bars + 2 * kStages;
   uint64_t* aready = bars + 2 * kStages + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
-  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 3);   // [kEpiWarps]
+  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 3);   // [kEpiWarps] (64 B)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (smem_u32(smem) & 1023) __trap();               // SWIZZLE_128B needs 1024-B alignment
@@ -259,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
     }
   } else if (warp < kProdWarps + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - kProdWarps;                 // 0..7
-    const int q = e & 3, hh = e >> 2;                // TMEM lane quarter, column half
+    const int e = warp - kProdWarps;                 // 0..15
+    const int q = e & 3, part = e >> 2;              // TMEM lane quarter, column quarter
     const int row = q * 32 + lane;                   // batch row = TMEM lane
-    const int et = threadIdx.x - kProdWarps * 32;    // 0..255
+    const int et = threadIdx.x - kProdWarps * 32;    // 0..511
     uint32_t dphase = 0;
     for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
       const float* xm = P.x + m * P.D;
@@ -280,17 +280,39 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
       for (int l = 1; l <= L; ++l) {
         const int in = P.w[l - 1], out = P.w[l];
         const float* bias = xm + P.off[l] + (int64_t)out * in;
-        const int half = P.npad[l] >> 1;
+        const int quarter = P.npad[l] >> 2;          // columns per part (multiple of 32)
         mbar_wait(dready, dphase);
         dphase ^= 1;
         tc_fence_after();
-        for (int c0 = hh * half; c0 < (hh + 1) * half; c0 += 32) {
+        // hidden layers also zero-fill the padded K columns [out, kpad) of the next A
+        const int cend = min((part + 1) * quarter, l < L ? P.kpad[l] : out);
+        for (int c0 = part * quarter; c0 < cend; c0 += 32) {
+          if (c0 >= out) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = make_uint4(0, 0, 0, 0);
+            }
+            continue;
+          }
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+          if (c0 + 32 <= out) {
+            // bias: 32 uniform values, eight broadcast float4 loads
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int n = c0 + i;
-            v[i] = n < out ? tanhf(__fadd_rn(v[i], __ldg(bias + n))) : 0.0f;
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
+              v[i] = tanhf(__fadd_rn(v[i], b4.x));
+              v[i + 1] = tanhf(__fadd_rn(v[i + 1], b4.y));
+              v[i + 2] = tanhf(__fadd_rn(v[i + 2], b4.z));
+              v[i + 3] = tanhf(__fadd_rn(v[i + 3], b4.w));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int n = c0 + i;
+              v[i] = n < out ? tanhf(__fadd_rn(v[i], __ldg(bias + n))) : 0.0f;
+            }
           }
           if (l < L) {
 #pragma unroll
@@ -299,11 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
               *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = pack8(v + 8 * c);
             }
           } else if (P.mode == 0) {
+            const float* yr = P.Y + (int64_t)row * out;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int n = c0 + i;
               if (n < out) {
-                const float d = __fsub_rn(v[i], __ldg(P.Y + (int64_t)row * out + n));
+                const float d = __fsub_rn(v[i], __ldg(yr + n));
                 sq = __fmaf_rn(d, d, sq);
               }
             }
