@@ -278,6 +278,9 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="1: time replays of one generation captured as a CUDA graph "
+                         "(default on for the launch-bound c1/c3)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--N", type=int, default=SWEEP["N"], help="c5 popsize")
     ap.add_argument("--D", type=int, default=SWEEP["D"], help="c5 dimensions")
@@ -331,6 +334,22 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    use_graph = args.graph if args.graph is not None else (args.config in ("c1", "c3")
+                                                           and world == 1)
+    graph = None
+    if use_graph:
+        # one generation captured once and replayed: the per-run scalars live on the device, so
+        # replays advance t, lr, sigma exactly like eager calls (NCCL calls would be capturable too)
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs):
+            step()
+        torch.cuda.current_stream().wait_stream(cs)
+        with torch.cuda.graph(graph, stream=cs, capture_error_mode="thread_local"):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
     launches0 = sum(h[2].kernel_launches for h in hs)
     for h in hs:
         h[2].profile(True)
@@ -342,14 +361,24 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        step()          # eager pass: per-kernel CUDA-event timing (es_profile)
     e1.record(stream)
     torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = sum(h[2].kernel_launches for h in hs) - launches0
+    if graph is not None:
+        for h in hs:
+            h[2].profile(False)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        ms = g0.elapsed_time(g1) / args.steps
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    launches = sum(h[2].kernel_launches for h in hs) - launches0
     prof = {}
     for label, cfg, es, _, _ in hs:
         for k, (t, n) in es.profile_read().items():
@@ -433,7 +462,9 @@ def main():
             "data": "synthetic", "config": config_block(args.config, world),
             "generations_per_s": 1e3 / ms, "roofline": roof, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "kernel_share": share,
-            "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra}
+            "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra,
+            "timing": "CUDA-graph replays of one generation" if graph is not None else
+                      "eager C-ABI calls, CUDA events on the stream"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_budget)
     if rank == 0:
