@@ -34,6 +34,9 @@ NORMAL_OPS = 37
 ASK_USE = {W.OPENAI_ES: 2, W.PGPE: 2, W.SNES: 1, W.SEP_CMA_ES: 1}
 TELL_USE = {W.OPENAI_ES: 2, W.PGPE: 5, W.SNES: 5, W.SEP_CMA_ES: 4}
 STATE_BYTES = {W.OPENAI_ES: 24, W.PGPE: 32, W.SNES: 16, W.SEP_CMA_ES: 40}   # r+w per dim per tell
+# N7 operations per evaluated element (fused ask+eval): conversions + binary64 accumulation (+ the
+# Rastrigin sin(pi b) polynomial, Rosenbrock's double pair term)
+EVAL_OPS = {W.SPHERE: 2, W.ROSENBROCK: 12, W.RASTRIGIN: 15}
 
 
 def load_peaks():
@@ -278,6 +281,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", type=int, default=0,
+                    help="1: BBOB configs use the fused ask+evaluate kernel (x still written)")
     ap.add_argument("--graph", type=int, default=None,
                     help="1: time replays of one generation captured as a CUDA graph "
                          "(default on for the launch-bound c1/c3)")
@@ -322,10 +327,14 @@ def main():
             es.set_mlp_problem(cfg["widths"], cfg["batch"], cfg["data_seed"])
         hs.append((label, cfg, es, x, f))
 
+    fused = bool(args.fused)
+
     def step():
         for _, cfg, es, x, f in hs:
             if cfg["fn"] is None:            # tell-only sweep: synthetic fitness stands in
                 es.synth_fitness(out=f)
+            elif fused and cfg["fn"] != W.MLP:
+                es.ask_eval(cfg["fn"], out_x=x, out_f=f)     # x is still materialised
             else:
                 es.ask(out=x)
                 es.eval(cfg["fn"], x, out=f)
@@ -408,6 +417,10 @@ def main():
             if k == "ask":
                 ops += n * R * P * D * (NORMAL_OPS + ASK_USE[algo])
                 byt += n * (4.0 * R * N * D + 8.0 * R * D)
+            elif k == "ask_eval":
+                ops += n * (R * P * D * (NORMAL_OPS + ASK_USE[algo]) +
+                            R * N * D * EVAL_OPS[cfg["fn"]])
+                byt += n * (4.0 * R * N * D + 8.0 * R * D)
             elif k == "eval_bbob":
                 byt += n * (4.0 * R * N * D + 4.0 * R * N)
             elif k in ("tell", "tell_reduce"):
@@ -453,13 +466,16 @@ def main():
     kernels_ms = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in kinds.items()}
 
     # --- end to end through the C ABI with HOST buffers (fitness read back and fed to tell)
-    e2e = e2e_run(hs, args, 1 if sharded else world)
+    e2e = e2e_run(hs, args, 1 if sharded else world, fused)
 
+    cb = config_block(args.config, world)
+    cb["path"] = ("fused ask+evaluate kernel (x written), then tell" if fused and
+                  hs[0][1]["fn"] not in (None, W.MLP) else "ask, evaluate, tell kernels")
     line = {"metric": metric_name(args.config), "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config_block(args.config, world),
+            "data": "synthetic", "config": cb,
             "generations_per_s": 1e3 / ms, "roofline": roof, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "kernel_share": share,
             "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra,
@@ -485,7 +501,7 @@ def ncu_traffic(cfg_key, kernel):
     return d.get(cfg_key, {}).get(kernel)
 
 
-def e2e_run(hs, args, world):
+def e2e_run(hs, args, world, fused=False):
     """Same metric through the public API with host buffers: per step and handle, ask on the
     device, evaluate into PINNED HOST fitness (D2H), tell from that host buffer (H2D), and read
     best_fitness back (D2H)."""
@@ -502,6 +518,9 @@ def e2e_run(hs, args, world):
             n = cfg["R"] * es.local_popsize
             if cfg["fn"] is None:
                 check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
+            elif fused and cfg["fn"] != W.MLP:
+                check(lib().es_ask_eval(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()),
+                                        C.c_void_p(f.data_ptr()), s), es.ctx)
             else:
                 es.ask(out=x)
                 check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n,

@@ -115,6 +115,14 @@ es_status_t es_init(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t po
  * a generation. Errors: ES_ERR_INVALID_ARG for NULL x. */
 es_status_t es_ask(es_ctx_t *ctx, float *x, es_stream_t stream);
 
+/* Fused ask + evaluate ("sampling ... can become a burden", P:225
+ * memory): one pass that forms this rank's population exactly as es_ask (bit-identical x, written
+ * to x [R][N/W][D] unless x is NULL — then it is never materialised) and writes its BBOB fitness
+ * (as es_eval_bbob, fn ∈ {SPHERE, ROSENBROCK, RASTRIGIN}) to fitness [R][N/W]. Counts as the
+ * generation's ask. Errors: ES_ERR_INVALID_ARG for NULL fitness or fn = ES_FIT_MLP. */
+es_status_t es_ask_eval(es_ctx_t *ctx, es_fitness_t fn, float *x, float *fitness,
+                        es_stream_t stream);
+
 /* evaluate: fitness[n] = f(x[n]) for n rows of length D (N7; MLP: N14).
  * Context-free for the BBOB functions (ctx may be NULL); ES_FIT_MLP needs a context on which
  * es_set_mlp_problem was called and D equal to its parameter count. x float [n][D], fitness

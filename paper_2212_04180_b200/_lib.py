@@ -22,7 +22,7 @@ EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "
            "es_set_mlp_problem", "es_mlp_num_params", "es_shape", "es_kernel_launches",
            "es_destroy", "es_last_error", "es_status_string", "es_nccl_unique_id_size",
            "es_nccl_get_unique_id", "es_debug_primitive", "es_profile_enable", "es_profile_read",
-           "es_tell_local", "es_tell_apply", "es_shard_plan"]
+           "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval"]
 
 
 class RunParams(C.Structure):
@@ -74,6 +74,7 @@ def lib():
         "es_debug_primitive": (i32, [i32, vp, vp, i64, vp]),
         "es_profile_enable": (i32, [vp, i32]),
         "es_tell_local": (i32, [vp, vp, vp]),
+        "es_ask_eval": (i32, [vp, i32, vp, vp, vp]),
         "es_tell_apply": (i32, [vp, vp]),
         "es_shard_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
         "es_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(i64), i32]),

@@ -33,6 +33,9 @@ void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint6
 void mlp_problem_destroy(void* prob);
 int64_t mlp_problem_dims(const void* prob);
 cudaError_t launch_primitive(int which, const void* in, void* out, int64_t n, cudaStream_t st);
+cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
+                            cudaStream_t st);
+int ask_eval_blocks_per_run(const DevState& s);
 }  // namespace esb
 
 using namespace esb;
@@ -49,6 +52,7 @@ struct es_ctx {
   float* fstage = nullptr;      // [R][Nloc] staging of host fitness
   float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
   float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
+  double* aepart = nullptr;     // [R][Nloc][blocks] fused ask+eval partial sums
   void* mlp = nullptr;
   int64_t launches = 0;
   bool profiling = false;
@@ -356,6 +360,39 @@ es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
     CUDA_OR(c, cudaMemcpyAsync(x, dst, bytes, cudaMemcpyDeviceToHost, st));
     CUDA_OR(c, cudaStreamSynchronize(st));
   }
+  c->asked = true;
+  return ES_SUCCESS;
+}
+
+es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if ((int)fn < 0 || (int)fn > 2) return fail(c, ES_ERR_INVALID_ARG, "fn must be a BBOB function");
+  if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
+  const DevState& s = c->s;
+  const size_t nloc = (size_t)s.R * s.Nloc;
+  if (!c->aepart)
+    CUDA_OR(c, dalloc(c, (void**)&c->aepart, nloc * ask_eval_blocks_per_run(s) * sizeof(double)));
+  float* xd = x;
+  const bool xh = x && !is_device_ptr(x);
+  if (xh) {
+    if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.D * sizeof(float)));
+    xd = c->xstage;
+  }
+  float* fd = f;
+  const bool fh = !is_device_ptr(f);
+  if (fh) {
+    if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
+    fd = c->fstage;
+  }
+  {
+    ProfScope ps(c, "ask_eval", st);
+    CUDA_OR(c, launch_ask_eval(s, (int)fn, xd, c->aepart, fd, st));
+  }
+  c->launches += 2;
+  if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.D * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (fh) CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (xh || fh) CUDA_OR(c, cudaStreamSynchronize(st));
   c->asked = true;
   return ES_SUCCESS;
 }

@@ -1,0 +1,53 @@
+// fitness.cuh — per-element BBOB fitness accumulation (NUMERICS N7), shared by the standalone
+// evaluation kernel (k_eval.cu) and the fused ask+evaluate kernel (k_ask_eval.cu).
+// Binary64 accumulation; Sphere uses exact-product DFMAs (= the oracle's mul-then-add), Rastrigin
+// accumulates Σx² and ΣS² separately and combines them once as Σx² + 20·ΣS² (N7).
+#pragma once
+#include "noise.cuh"
+
+namespace esb {
+
+enum { FN_SPHERE = 0, FN_ROSENBROCK = 1, FN_RASTRIGIN = 2 };
+
+struct FitAcc {
+  double a = 0.0, b = 0.0;
+};
+
+// Rosenbrock term of the pair (x_d, x_{d+1}), every operation in double as the oracle.
+__device__ __forceinline__ double rosen_term(float a, float b) {
+  const double da = a, db = b;
+  const double t1 = __dsub_rn(db, __dmul_rn(da, da));
+  const double t2 = __dsub_rn(1.0, da);
+  return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
+}
+
+// Add element x (and, for Rosenbrock, the pair term with its successor xn when has_next).
+template <int FN>
+__device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has_next) {
+  if (FN == FN_SPHERE) {
+    const double d = (double)x;
+    acc.a = __fma_rn(d, d, acc.a);
+  } else if (FN == FN_ROSENBROCK) {
+    if (has_next) acc.a = __dadd_rn(acc.a, rosen_term(x, xn));
+  } else {
+    const float ab = fabsf(x);
+    const float fr = __fsub_rn(ab, floorf(ab));
+    const double S = (double)sinpi_half(fminf(fr, __fsub_rn(1.0f, fr)));
+    const double d = (double)x;
+    acc.a = __fma_rn(d, d, acc.a);
+    acc.b = __fma_rn(S, S, acc.b);
+  }
+}
+
+template <int FN>
+__device__ __forceinline__ double fit_total(const FitAcc& acc) {
+  return FN == FN_RASTRIGIN ? __fma_rn(20.0, acc.b, acc.a) : acc.a;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace esb

@@ -7,100 +7,37 @@
 #include <algorithm>
 
 #include "es_internal.h"
-#include "noise.cuh"
+#include "fitness.cuh"
 
 namespace esb {
-
-enum { FN_SPHERE = 0, FN_ROSENBROCK = 1, FN_RASTRIGIN = 2 };
-
-template <int FN>
-__device__ __forceinline__ double term(float a, float b, bool has_next) {
-  if (FN == FN_SPHERE) return __dmul_rn((double)a, (double)a);
-  if (FN == FN_ROSENBROCK) {
-    if (!has_next) return 0.0;
-    const double da = a, db = b;
-    const double t1 = __dsub_rn(db, __dmul_rn(da, da));
-    const double t2 = __dsub_rn(1.0, da);
-    return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
-  }
-  return 0.0;   // Rastrigin accumulates two sums instead (rast_acc)
-}
-
-// Rastrigin (N7): Σx² and ΣS² accumulated separately with exact-product DFMAs, combined once;
-// S = sin(π·min(fr, 1 − fr)) by the degree-5 polynomial of N7.
-__device__ __forceinline__ void rast_acc(float a, double& ax, double& as) {
-  const float ab = fabsf(a);
-  const float fr = __fsub_rn(ab, floorf(ab));
-  const double S = (double)sinpi_half(fminf(fr, __fsub_rn(1.0f, fr)));
-  const double da = (double)a;
-  ax = __fma_rn(da, da, ax);
-  as = __fma_rn(S, S, as);
-}
 
 // Accumulate this thread's strided share of one row: quads q = lane0, lane0+stride, ...
 template <int FN, bool V4>
 __device__ __forceinline__ double row_partial(const float* __restrict__ row, int64_t D,
                                               int64_t lane0, int64_t stride) {
-  double acc = 0.0;
-  if (FN == FN_RASTRIGIN) {
-    double ax = 0.0, as = 0.0;
-    if (V4) {
-      for (int64_t q = lane0; q < D / 4; q += stride) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
-        rast_acc(v.x, ax, as);
-        rast_acc(v.y, ax, as);
-        rast_acc(v.z, ax, as);
-        rast_acc(v.w, ax, as);
-      }
-    } else {
-      for (int64_t d = lane0; d < D; d += stride) rast_acc(__ldg(row + d), ax, as);
-    }
-    return __fma_rn(20.0, as, ax);
-  }
-  if (FN == FN_SPHERE) {
-    if (V4) {
-      for (int64_t q = lane0; q < D / 4; q += stride) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
-        acc = __fma_rn((double)v.x, (double)v.x, acc);   // exact product: = mul-then-add
-        acc = __fma_rn((double)v.y, (double)v.y, acc);
-        acc = __fma_rn((double)v.z, (double)v.z, acc);
-        acc = __fma_rn((double)v.w, (double)v.w, acc);
-      }
-    } else {
-      for (int64_t d = lane0; d < D; d += stride) {
-        const double v = __ldg(row + d);
-        acc = __fma_rn(v, v, acc);
-      }
-    }
-    return acc;
-  }
+  FitAcc acc;
   if (V4) {
     const int64_t Q = D / 4;
     for (int64_t q = lane0; q < Q; q += stride) {
       const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
-      float nx = 0.0f;
       const bool nn = (FN == FN_ROSENBROCK) && (4 * q + 4 < D);
-      if (FN == FN_ROSENBROCK && nn) nx = __ldg(row + 4 * q + 4);
-      acc = __dadd_rn(acc, term<FN>(v.x, v.y, true));
-      acc = __dadd_rn(acc, term<FN>(v.y, v.z, true));
-      acc = __dadd_rn(acc, term<FN>(v.z, v.w, true));
-      acc = __dadd_rn(acc, term<FN>(v.w, nx, nn));
+      const float nx = (FN == FN_ROSENBROCK && nn) ? __ldg(row + 4 * q + 4) : 0.0f;
+      fit_add<FN>(acc, v.x, v.y, true);
+      fit_add<FN>(acc, v.y, v.z, true);
+      fit_add<FN>(acc, v.z, v.w, true);
+      fit_add<FN>(acc, v.w, nx, nn);
     }
   } else {
     for (int64_t d = lane0; d < D; d += stride) {
       const bool nn = d + 1 < D;
       const float b = (FN == FN_ROSENBROCK && nn) ? __ldg(row + d + 1) : 0.0f;
-      acc = __dadd_rn(acc, term<FN>(__ldg(row + d), b, nn));
+      fit_add<FN>(acc, __ldg(row + d), b, nn);
     }
   }
-  return acc;
+  return fit_total<FN>(acc);
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
+__device__ __forceinline__ double warp_sum(double v) { return warp_sum_d(v); }
 
 template <int FN, bool V4>
 __global__ void __launch_bounds__(256) eval_warp_kernel(const float* __restrict__ x, int64_t n,

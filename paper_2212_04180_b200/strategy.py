@@ -85,6 +85,19 @@ class Strategy:
         check(lib().es_ask(self.ctx, _ptr(x), _stream(stream)), self.ctx)
         return x
 
+    def ask_eval(self, fn, out_x=None, out_f=None, write_x=True, stream=None):
+        """Fused ask + BBOB evaluate (§8(f) f1). write_x=False never materialises x."""
+        x = None
+        if write_x:
+            x = out_x if out_x is not None else torch.empty(
+                (self.R, self.local_popsize, self.num_dims), dtype=torch.float32,
+                device=self.device)
+        f = out_f if out_f is not None else torch.empty(
+            (self.R, self.local_popsize), dtype=torch.float32, device=self.device)
+        check(lib().es_ask_eval(self.ctx, int(fn), _ptr(x) if x is not None else None, _ptr(f),
+                                _stream(stream)), self.ctx)
+        return x, f
+
     def eval(self, fn, x, out=None, stream=None):
         n = x.numel() // self.num_dims
         f = out if out is not None else torch.empty(

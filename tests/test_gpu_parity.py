@@ -442,3 +442,27 @@ def test_mlp_openai_es_generations_teacher_forced():
         pair.orc[0].tell(f[0].cpu().numpy())
         pair.compare(0, 1e-5)
     pair.close()
+
+
+# ------------------------------------------------------------------------ fused ask + evaluate (f1)
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("fn", FNS)
+@pytest.mark.parametrize("N,D", [(16, 1), (16, 10), (64, 1000), (32, 4099), (8, 513), (256, 1000)])
+def test_ask_eval_fused(algo, fn, N, D):
+    """x bit-identical to es_ask, fitness within 1 ulp of the oracle (and bit-identical whether or
+    not x is materialised), and the generation tells normally afterwards."""
+    from paper_2212_04180_b200 import strategy as S
+    params = _params(algo, 3, hyper=True)
+    es = S.Strategy(algo, N, D, params)
+    x1, f1 = es.ask_eval(fn)
+    _, f2 = es.ask_eval(fn, write_x=False)
+    x0 = es.ask()
+    assert torch.equal(x1, x0)
+    assert np.array_equal(bits(f1.cpu().numpy()), bits(f2.cpu().numpy()))
+    xh, fh = x0.cpu().numpy(), f1.cpu().numpy()
+    for r in range(3):
+        ref = O.evaluate(fn, xh[r])
+        ulp = np.abs(bits(fh[r]).astype(np.int64) - bits(ref).astype(np.int64))
+        assert ulp.max() <= 1 and (ulp > 0).sum() <= max(1, N // 64), ulp
+    es.tell(f1)
+    es.close()

@@ -10,7 +10,7 @@ python bench.py --impl reference --steps 5 --warmup 3 "$@" > $OUT/bench_ref_$TAG
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline $@"
 if $CMD > $OUT/plain_$TAG.log 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
-  KRE=${KRE:-"tell_kernel|ask_kernel|eval_warp|rank_kernel|mlp_kernel"}
+  KRE=${KRE:-"tell_kernel|ask_kernel|eval_warp|rank_kernel|mlp_kernel|ask_eval_kernel"}
   KCNT=${KCNT:-8}
   ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s 8 -c $KCNT -o $OUT/prof_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 else
