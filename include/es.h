@@ -103,7 +103,7 @@ typedef struct es_ctx es_ctx_t;
  * world_size > 1 with nccl_unique_id == NULL creates a communicator-less shard (split-phase tell only).
  * Errors: ES_ERR_INVALID_ARG if N < 2, D < 1, R < 1, N odd (OpenAI-ES/PGPE), N mod W != 0,
  * N/W odd (OpenAI-ES/PGPE), ⌊elite_ratio·N⌋ < 1 (Sep-CMA-ES), negative σ_init, non-positive
- * lrate_init (OpenAI-ES/PGPE), world_rank outside [0, W); ES_ERR_UNSUPPORTED if N > 16384;
+ * lrate_init (OpenAI-ES/PGPE), world_rank outside [0, W); ES_ERR_UNSUPPORTED if N > 2^20;
  * ES_ERR_OOM / ES_ERR_CUDA / ES_ERR_NCCL on allocation / runtime failure. *out is NULL on error.
  * Ownership: the context owns every state buffer and the NCCL communicator. */
 es_status_t es_init(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t popsize,

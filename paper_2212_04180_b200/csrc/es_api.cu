@@ -240,7 +240,7 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   if (N % W) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be divisible by world_size");
   if (antithetic(algo) && ((N % 2) || ((N / W) % 2)))
     return fail(nullptr, ES_ERR_INVALID_ARG, "antithetic strategies need an even popsize per rank");
-  if (N > 16384) return fail(nullptr, ES_ERR_UNSUPPORTED, "popsize > 16384 is not implemented");
+  if (N > (1 << 20)) return fail(nullptr, ES_ERR_UNSUPPORTED, "popsize > 2^20 is not implemented");
   for (int r = 0; r < R; ++r) {
     const es_run_params_t& p = params[r];
     if (!(p.sigma_init >= 0.0f)) return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: sigma_init < 0", r);
@@ -294,6 +294,12 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   if (c->nchunk > 1) TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->nchunk * 2 * RD * sizeof(double)));
   TRY(dalloc(c, (void**)&s.arrive, (size_t)R * bpr * sizeof(uint32_t)));
   TRY(dalloc(c, (void**)&s.normpart, (size_t)R * bpr * sizeof(double)));
+  {
+    int npad = 1;
+    while (npad < N) npad <<= 1;
+    s.gkeys = nullptr;
+    if (npad > 16384) TRY(dalloc(c, (void**)&s.gkeys, (size_t)R * npad * sizeof(uint64_t)));
+  }
   if (W > 1) TRY(dalloc(c, (void**)&c->fgather, RN * sizeof(float)));
   // per-run scalars and weight tables, computed on the host in binary64
   c->host_rs.assign(R, RunScal{});
@@ -480,7 +486,7 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
     ProfScope ps(c, "rank", st);
     CUDA_OR(c, launch_rank(s, fsrc, st));
   }
-  c->launches += 1;
+  c->launches += rank_launches(s);
   ProfScope ps(c, fused ? "tell" : "tell_reduce", st);
   CUDA_OR(c, launch_tell_reduce(s, fused, c->nchunk, st));
   c->launches += 1;

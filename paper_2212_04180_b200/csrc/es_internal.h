@@ -67,6 +67,7 @@ struct DevState {
   double* Gchunk;      // [nchunk][R][2][D] partials when the direction range is split
   uint32_t* arrive;    // [R][blocks_per_run] last-block counters
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
+  uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
 };
 
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
@@ -83,6 +84,7 @@ cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st);
 cudaError_t launch_eval_bbob(int fn, const float* x, int64_t n, int64_t D, float* f,
                              cudaStream_t st);
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st);
+int rank_launches(const DevState& s);
 cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
 // Tell: regenerate-and-reduce over this rank's entries. fused=true (W == 1) applies the update in
 // the same kernel; otherwise the sums land in s.G for the all-reduce and launch_tell_update

@@ -31,41 +31,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
-// fsrc layout [W][R][Nloc] (for W == 1 simply [R][N]).
-__global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad) {
-  extern __shared__ uint64_t keys[];
-  __shared__ double red[32];
-  __shared__ int32_t sh_nw;
-  const int r = blockIdx.x;
+// Sorted (key, index) pairs → tie groups, shaping, tell coefficients and the generation's
+// scalars (N9–N12 bookkeeping). `keys` is the run's sorted array (shared or global memory).
+__device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, double* red,
+                            int32_t* sh_nw_p) {
   const int N = s.N, T = blockDim.x;
   float* fit = s.fit + (int64_t)r * N;
-  for (int p = threadIdx.x; p < npad; p += T) {
-    uint64_t v = ~0ull;
-    if (p < N) {
-      const int w = p / s.Nloc, jl = p % s.Nloc;
-      const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
-      fit[p] = f;
-      v = ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
-    }
-    keys[p] = v;
-  }
-  __syncthreads();
-  // bitonic sort, ascending
-  for (int k = 2; k <= npad; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (npad >> 1); i += T) {
-        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        const int hi = lo + j;
-        const uint64_t a = keys[lo], b = keys[hi];
-        const bool up = (lo & k) == 0;
-        if ((a > b) == up) {
-          keys[lo] = b;
-          keys[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  int32_t& sh_nw = *sh_nw_p;
   // tie groups and shaping
   const RunScal& rs = s.rs[r];
   int32_t* perm = s.perm + (int64_t)r * N;
@@ -167,18 +139,141 @@ __global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad
   }
 }
 
+// fsrc layout [W][R][Nloc] (for W == 1 simply [R][N]).
+__device__ __forceinline__ uint64_t load_key(const DevState& s, const float* __restrict__ fsrc,
+                                             int r, int p) {
+  if (p >= s.N) return ~0ull;
+  const int w = p / s.Nloc, jl = p % s.Nloc;
+  const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
+  s.fit[(int64_t)r * s.N + p] = f;
+  return ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
+}
+
+// In-shared-memory bitonic steps k ∈ [k0, k1], all j < k (indices global: direction (g & k)).
+__device__ __forceinline__ void bitonic_smem(uint64_t* keys, int n, int64_t gbase, int k0,
+                                             int k1, int jmax) {
+  const int T = blockDim.x;
+  for (int k = k0; k <= k1; k <<= 1) {
+    for (int j = min(k >> 1, jmax); j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (n >> 1); i += T) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int hi = lo + j;
+        const uint64_t a = keys[lo], b = keys[hi];
+        const bool up = ((gbase + lo) & k) == 0;
+        if ((a > b) == up) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// N ≤ 16384: one CTA per run, the whole sort in shared memory.
+__global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad) {
+  extern __shared__ uint64_t keys[];
+  __shared__ double red[32];
+  __shared__ int32_t sh_nw;
+  const int r = blockIdx.x;
+  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p);
+  __syncthreads();
+  bitonic_smem(keys, npad, 0, 2, npad, npad);
+  rank_finish(s, r, keys, red, &sh_nw);
+}
+
+// N > 16384: hybrid bitonic sort over global memory. Chunks of kChunk keys are sorted and merged
+// in shared memory; only the strides j ≥ kChunk go through global memory, one launch each.
+static constexpr int kChunk = 16384;
+
+__global__ void rank_chunk_sort_kernel(DevState s, const float* __restrict__ fsrc,
+                                       uint64_t* __restrict__ gkeys, int npad) {
+  extern __shared__ uint64_t keys[];
+  const int nch = npad / kChunk;
+  const int r = blockIdx.x / nch, c = blockIdx.x % nch;
+  const int64_t g0 = (int64_t)c * kChunk;
+  for (int p = threadIdx.x; p < kChunk; p += blockDim.x)
+    keys[p] = load_key(s, fsrc, r, (int)(g0 + p));
+  __syncthreads();
+  bitonic_smem(keys, kChunk, g0, 2, kChunk, kChunk);
+  uint64_t* out = gkeys + (int64_t)r * npad + g0;
+  for (int p = threadIdx.x; p < kChunk; p += blockDim.x) out[p] = keys[p];
+}
+
+__global__ void rank_global_step_kernel(uint64_t* __restrict__ gkeys, int npad, int k, int j,
+                                        int R) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t half = npad >> 1;
+  if (i >= (int64_t)R * half) return;
+  const int r = (int)(i / half);
+  const int ii = (int)(i % half);
+  const int lo = ((ii & ~(j - 1)) << 1) | (ii & (j - 1));
+  uint64_t* kr = gkeys + (int64_t)r * npad;
+  const uint64_t a = kr[lo], b = kr[lo + j];
+  const bool up = (lo & k) == 0;
+  if ((a > b) == up) {
+    kr[lo] = b;
+    kr[lo + j] = a;
+  }
+}
+
+__global__ void rank_chunk_merge_kernel(uint64_t* __restrict__ gkeys, int npad, int k) {
+  extern __shared__ uint64_t keys[];
+  const int nch = npad / kChunk;
+  const int r = blockIdx.x / nch, c = blockIdx.x % nch;
+  const int64_t g0 = (int64_t)c * kChunk;
+  uint64_t* io = gkeys + (int64_t)r * npad + g0;
+  for (int p = threadIdx.x; p < kChunk; p += blockDim.x) keys[p] = io[p];
+  __syncthreads();
+  bitonic_smem(keys, kChunk, g0, k, k, kChunk >> 1);
+  for (int p = threadIdx.x; p < kChunk; p += blockDim.x) io[p] = keys[p];
+}
+
+__global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkeys, int npad) {
+  __shared__ double red[32];
+  __shared__ int32_t sh_nw;
+  rank_finish(s, blockIdx.x, gkeys + (int64_t)blockIdx.x * npad, red, &sh_nw);
+}
+
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
   int npad = 1;
   while (npad < s.N) npad <<= 1;
-  const int T = std::min(1024, std::max(32, npad / 2));
-  const size_t smem = (size_t)npad * sizeof(uint64_t);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (const void* f : {(const void*)rank_kernel, (const void*)rank_chunk_sort_kernel,
+                          (const void*)rank_chunk_merge_kernel})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  rank_kernel<<<s.R, T, smem, st>>>(s, fsrc, npad);
+  if (npad <= kChunk) {
+    const int T = std::min(1024, std::max(32, npad / 2));
+    rank_kernel<<<s.R, T, (size_t)npad * sizeof(uint64_t), st>>>(s, fsrc, npad);
+    return cudaGetLastError();
+  }
+  const int nch = npad / kChunk;
+  const size_t smem = (size_t)kChunk * sizeof(uint64_t);
+  rank_chunk_sort_kernel<<<s.R * nch, 1024, smem, st>>>(s, fsrc, s.gkeys, npad);
+  const int64_t pairs = (int64_t)s.R * (npad >> 1);
+  for (int k = 2 * kChunk; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j >= kChunk; j >>= 1)
+      rank_global_step_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(s.gkeys, npad, k,
+                                                                            j, s.R);
+    rank_chunk_merge_kernel<<<s.R * nch, 1024, smem, st>>>(s.gkeys, npad, k);
+  }
+  rank_finish_kernel<<<s.R, 1024, 0, st>>>(s, s.gkeys, npad);
   return cudaGetLastError();
+}
+
+int rank_launches(const DevState& s) {
+  int npad = 1, n = 1;
+  while (npad < s.N) npad <<= 1;
+  if (npad <= kChunk) return 1;
+  n = 2;
+  for (int k = 2 * kChunk; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j >= kChunk; j >>= 1) ++n;
+    ++n;
+  }
+  return n;
 }
 
 }  // namespace esb

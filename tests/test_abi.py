@@ -74,7 +74,7 @@ def test_invalid_arguments_rejected(L, kw):
 
 
 def test_unsupported_popsize(L):
-    rc, _ = _init(L, N=32768)
+    rc, _ = _init(L, N=1 << 21)
     assert rc == 6
 
 

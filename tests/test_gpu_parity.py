@@ -149,7 +149,7 @@ def test_eval_empty_and_host_buffers():
 
 # ------------------------------------------------------------------------ ranks
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("N", [2, 16, 256, 1000, 4096, 16384])
+@pytest.mark.parametrize("N", [2, 16, 256, 1000, 4096, 16384, 16386, 40000, 65536])
 def test_rank_and_shaping_bit_exact(algo, N):
     if algo == W.SEP_CMA_ES and N < 16:
         pytest.skip("elite ratio 0.2 needs N >= 5")
@@ -333,7 +333,8 @@ def test_config3_full_size():
     pair.close()
 
 
-@pytest.mark.parametrize("N,D", [(4096, 985_216), (16384, 100_000), (256, 10_000_000)])
+@pytest.mark.parametrize("N,D", [(4096, 985_216), (16384, 100_000), (256, 10_000_000),
+                                 (65536, 1000), (32768, 10_000)])
 def test_tell_full_size_sampled_dims(N, D):
     """Config 4 / sweep sizes: the tell on synthetic fitness (N15), checked on 64 sampled quads
     (incl. the first and last) by an oracle run restricted to those dimensions."""
