@@ -281,8 +281,11 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fused", type=int, default=0,
-                    help="1: BBOB configs use the fused ask+evaluate kernel (x still written)")
+    ap.add_argument("--fused", type=int, default=None,
+                    help="1: es_ask_eval (BBOB: one fused kernel; MLP: ask writes the fp16 image "
+                         "the TMA-fed tcgen05 kernel reads). Default: on for c4, off otherwise")
+    ap.add_argument("--write-x", type=int, default=1,
+                    help="with --fused 1: also materialise the fp32 population x (default 1)")
     ap.add_argument("--graph", type=int, default=None,
                     help="1: time replays of one generation captured as a CUDA graph "
                          "(default on for the launch-bound c1/c3)")
@@ -327,14 +330,15 @@ def main():
             es.set_mlp_problem(cfg["widths"], cfg["batch"], cfg["data_seed"])
         hs.append((label, cfg, es, x, f))
 
-    fused = bool(args.fused)
+    fused = bool(args.fused) if args.fused is not None else args.config == "c4"
+    write_x = bool(args.write_x)
 
     def step():
         for _, cfg, es, x, f in hs:
             if cfg["fn"] is None:            # tell-only sweep: synthetic fitness stands in
                 es.synth_fitness(out=f)
-            elif fused and cfg["fn"] != W.MLP:
-                es.ask_eval(cfg["fn"], out_x=x, out_f=f)     # x is still materialised
+            elif fused:
+                es.ask_eval(cfg["fn"], out_x=x if write_x else None, out_f=f, write_x=write_x)
             else:
                 es.ask(out=x)
                 es.eval(cfg["fn"], x, out=f)
@@ -417,6 +421,9 @@ def main():
             if k == "ask":
                 ops += n * R * P * D * (NORMAL_OPS + ASK_USE[algo])
                 byt += n * (4.0 * R * N * D + 8.0 * R * D)
+            elif k == "ask16":                 # ask + fp16 parameter image (N14′)
+                ops += n * R * P * D * (NORMAL_OPS + ASK_USE[algo])
+                byt += n * ((4.0 if write_x else 0.0) * R * N * D + 2.0 * R * N * D + 8.0 * R * D)
             elif k == "ask_eval":
                 ops += n * (R * P * D * (NORMAL_OPS + ASK_USE[algo]) +
                             R * N * D * EVAL_OPS[cfg["fn"]])
@@ -431,7 +438,7 @@ def main():
             elif k == "rank":
                 byt += n * R * cfg["N"] * 40.0
             elif k == "eval_mlp":
-                byt += n * (4.0 * R * N * D + 4.0 * R * N)
+                byt += n * ((2.0 if fused else 4.0) * R * N * D + 4.0 * R * N)
                 wd = cfg["widths"]
                 flops += n * R * N * 2.0 * cfg["batch"] * sum(wd[i] * wd[i + 1]
                                                               for i in range(len(wd) - 1))
@@ -469,8 +476,15 @@ def main():
     e2e = e2e_run(hs, args, 1 if sharded else world, fused)
 
     cb = config_block(args.config, world)
-    cb["path"] = ("fused ask+evaluate kernel (x written), then tell" if fused and
-                  hs[0][1]["fn"] not in (None, W.MLP) else "ask, evaluate, tell kernels")
+    if hs[0][1]["fn"] is None:
+        cb["path"] = "synthetic fitness, tell"
+    elif fused and hs[0][1]["fn"] == W.MLP:
+        cb["path"] = ("es_ask_eval: ask writes " + ("x and " if write_x else "") +
+                      "the fp16 parameter image (N14'), TMA-fed tcgen05 MLP fitness, then tell")
+    elif fused:
+        cb["path"] = "fused ask+evaluate kernel" + (" (x written)" if write_x else "") + ", tell"
+    else:
+        cb["path"] = "ask, evaluate, tell kernels"
     line = {"metric": metric_name(args.config), "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
@@ -518,7 +532,7 @@ def e2e_run(hs, args, world, fused=False):
             n = cfg["R"] * es.local_popsize
             if cfg["fn"] is None:
                 check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
-            elif fused and cfg["fn"] != W.MLP:
+            elif fused:
                 check(lib().es_ask_eval(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()),
                                         C.c_void_p(f.data_ptr()), s), es.ctx)
             else:

@@ -116,10 +116,13 @@ es_status_t es_init(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t po
 es_status_t es_ask(es_ctx_t *ctx, float *x, es_stream_t stream);
 
 /* Fused ask + evaluate ("sampling ... can become a burden", P:225
- * memory): one pass that forms this rank's population exactly as es_ask (bit-identical x, written
- * to x [R][N/W][D] unless x is NULL — then it is never materialised) and writes its BBOB fitness
- * (as es_eval_bbob, fn ∈ {SPHERE, ROSENBROCK, RASTRIGIN}) to fitness [R][N/W]. Counts as the
- * generation's ask. Errors: ES_ERR_INVALID_ARG for NULL fitness or fn = ES_FIT_MLP. */
+ * memory): forms this rank's population exactly as es_ask (bit-identical x, written to x
+ * [R][N/W][D] unless x is NULL — then it is never materialised in fp32) and writes its fitness (as
+ * es_eval_bbob) to fitness [R][N/W]. BBOB: one kernel that evaluates while sampling. ES_FIT_MLP
+ * (N14′): the ask kernel writes the fp16 parameter image the fitness uses, which the tcgen05 MLP
+ * kernel streams with TMA (x, if given, must be device memory; D % 4 == 0). Counts as the
+ * generation's ask. Errors: ES_ERR_INVALID_ARG for NULL fitness; ES_ERR_BAD_STATE for ES_FIT_MLP
+ * without es_set_mlp_problem. */
 es_status_t es_ask_eval(es_ctx_t *ctx, es_fitness_t fn, float *x, float *fitness,
                         es_stream_t stream);
 

@@ -615,7 +615,7 @@ static void mlp_forward(const orc_mlp_t *p, const float *x, float *out) {
       for (int n = 0; n < nout; ++n) {
         double acc = 0.0;
         for (int k = 0; k < in; ++k) acc += h[(int64_t)b * in + k] * Wd[(int64_t)n * in + k];
-        float g = (float)tanh(acc + (double)bias[n]);
+        float g = (float)tanh(acc + (double)orc_fp16(bias[n]));
         if (l + 1 < p->nw) hn[(int64_t)b * nout + n] = orc_fp16(g);
         else out[(int64_t)b * nout + n] = g;
       }

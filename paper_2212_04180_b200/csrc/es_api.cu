@@ -1,6 +1,7 @@
 // es_api.cu — the C ABI (include/es.h): context lifetime, argument validation, host-side constant
 // tables (binary64, NUMERICS N11/N12), host↔device staging, NCCL plumbing and the launch sequence
 // of one generation. No exception crosses the ABI; every CUDA/NCCL failure becomes a status code.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -35,6 +36,9 @@ int64_t mlp_problem_dims(const void* prob);
 cudaError_t launch_primitive(int which, const void* in, void* out, int64_t n, cudaStream_t st);
 cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
                             cudaStream_t st);
+cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st);
+cudaError_t launch_mlp_eval16(void* prob, const __half* x16, int64_t n, float* f,
+                              cudaStream_t st);
 int ask_eval_blocks_per_run(const DevState& s);
 }  // namespace esb
 
@@ -53,6 +57,7 @@ struct es_ctx {
   float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
   float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
   double* aepart = nullptr;     // [R][Nloc][blocks] fused ask+eval partial sums
+  __half* x16 = nullptr;        // [R][Nloc][D] fp16 parameter image (MLP fused path, N14′)
   void* mlp = nullptr;
   int64_t launches = 0;
   bool profiling = false;
@@ -373,10 +378,38 @@ es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
 es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if ((int)fn < 0 || (int)fn > 2) return fail(c, ES_ERR_INVALID_ARG, "fn must be a BBOB function");
+  if ((int)fn < 0 || (int)fn > 3) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   const DevState& s = c->s;
   const size_t nloc = (size_t)s.R * s.Nloc;
+  if (fn == ES_FIT_MLP) {
+    // N14′: the ask writes fp16(x) (and x unless NULL); the MLP streams that image with TMA
+    if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
+    if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
+    if (x && !is_device_ptr(x)) return fail(c, ES_ERR_INVALID_ARG, "x must be device memory");
+    if (!c->x16) CUDA_OR(c, dalloc(c, (void**)&c->x16, nloc * s.D * sizeof(__half)));
+    float* fd = f;
+    const bool fh = !is_device_ptr(f);
+    if (fh) {
+      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
+      fd = c->fstage;
+    }
+    {
+      ProfScope ps(c, "ask16", st);
+      CUDA_OR(c, launch_ask16(s, x, c->x16, st));
+    }
+    {
+      ProfScope ps(c, "eval_mlp", st);
+      CUDA_OR(c, launch_mlp_eval16(c->mlp, c->x16, (int64_t)nloc, fd, st));
+    }
+    c->launches += 2;
+    if (fh) {
+      CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+      CUDA_OR(c, cudaStreamSynchronize(st));
+    }
+    c->asked = true;
+    return ES_SUCCESS;
+  }
   if (!c->aepart)
     CUDA_OR(c, dalloc(c, (void**)&c->aepart, nloc * ask_eval_blocks_per_run(s) * sizeof(double)));
   float* xd = x;

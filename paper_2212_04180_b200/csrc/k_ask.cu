@@ -7,6 +7,8 @@
 // threads own consecutive quads, so each warp store is a 512-B contiguous segment of one row.
 // Bound: the HBM write of x (4·N·D bytes) for antithetic strategies; the Philox/Box–Muller issue
 // rate for SNES / Sep-CMA (one direction per member). See DESIGN.md §Kernels.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 
 #include "es_internal.h"
@@ -58,9 +60,11 @@ __device__ __forceinline__ float ask_scale(const DevState& s, const RunScal& rs,
   return __fmul_rn(rs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
 }
 
-template <int ALGO, bool V4>
+// W16: also write fp16(x) into x16 (N14′, the MLP fitness's parameter image); x may be NULL then.
+template <int ALGO, bool V4, bool W16>
 __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
-                                                           int bpr, int dpt) {
+                                                           __half* __restrict__ x16, int bpr,
+                                                           int dpt) {
   constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
   const int r = blockIdx.x / bpr;
   const int64_t q = (int64_t)(blockIdx.x % bpr) * kAskThreads + threadIdx.x;
@@ -81,7 +85,8 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
     sc[k] = ok ? ask_scale<ALGO>(s, rs, base + k) : 0.0f;
   }
   const int dir0 = s.rank * Ploc;
-  float* xr = x + (int64_t)r * s.Nloc * s.D + 4 * q;
+  float* xr = x ? x + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
+  __half* hr = W16 ? x16 + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
 #pragma unroll 2
   for (int il = i0; il < i1; ++il) {
     const float4 z = normal4(ph, (uint32_t)q, (uint32_t)(dir0 + il), t);
@@ -93,6 +98,21 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
       if (kAnti) xm[k] = __fmaf_rn(-sc[k], zz[k], m[k]);
     }
     const int64_t row = kAnti ? 2 * (int64_t)il : il;
+    if (W16) {            // D % 4 == 0 is required for this path (8-byte stores)
+      __half* h0 = hr + row * s.D;
+      __half2 a0 = __floats2half2_rn(xp[0], xp[1]), a1 = __floats2half2_rn(xp[2], xp[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&a0);
+      u.y = *reinterpret_cast<uint32_t*>(&a1);
+      __stcs(reinterpret_cast<uint2*>(h0), u);
+      if (kAnti) {
+        __half2 b0 = __floats2half2_rn(xm[0], xm[1]), b1 = __floats2half2_rn(xm[2], xm[3]);
+        u.x = *reinterpret_cast<uint32_t*>(&b0);
+        u.y = *reinterpret_cast<uint32_t*>(&b1);
+        __stcs(reinterpret_cast<uint2*>(h0 + s.D), u);
+      }
+      if (!xr) continue;
+    }
     float* p0 = xr + row * s.D;
     if (V4) {
       __stcs(reinterpret_cast<float4*>(p0), make_float4(xp[0], xp[1], xp[2], xp[3]));
@@ -111,7 +131,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
 }
 
 template <int ALGO>
-static cudaError_t launch_ask_t(const DevState& s, float* x, cudaStream_t st) {
+static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaStream_t st) {
   constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
   const int bpr = (int)((s.Q + kAskThreads - 1) / kAskThreads);
@@ -124,19 +144,27 @@ static cudaError_t launch_ask_t(const DevState& s, float* x, cudaStream_t st) {
   const int dpt = (Ploc + nchunk - 1) / nchunk;
   nchunk = (Ploc + dpt - 1) / dpt;
   dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
+  if (x16) {
+    ask_kernel<ALGO, true, true><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
+    return cudaGetLastError();
+  }
   const bool v4 = (s.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if (v4) ask_kernel<ALGO, true><<<grid, kAskThreads, 0, st>>>(s, x, bpr, dpt);
-  else ask_kernel<ALGO, false><<<grid, kAskThreads, 0, st>>>(s, x, bpr, dpt);
+  if (v4) ask_kernel<ALGO, true, false><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
+  else ask_kernel<ALGO, false, false><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
   return cudaGetLastError();
 }
 
-cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {
+cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st) {
   switch (s.algo) {
-    case OPENAI_ES: return launch_ask_t<OPENAI_ES>(s, x, st);
-    case PGPE: return launch_ask_t<PGPE>(s, x, st);
-    case SNES: return launch_ask_t<SNES>(s, x, st);
-    default: return launch_ask_t<SEP_CMA_ES>(s, x, st);
+    case OPENAI_ES: return launch_ask_t<OPENAI_ES>(s, x, x16, st);
+    case PGPE: return launch_ask_t<PGPE>(s, x, x16, st);
+    case SNES: return launch_ask_t<SNES>(s, x, x16, st);
+    default: return launch_ask_t<SEP_CMA_ES>(s, x, x16, st);
   }
+}
+
+cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {
+  return launch_ask16(s, x, nullptr, st);
 }
 
 // N15: f_j = u_b(o_{j mod 4}) of counter (⌊j/4⌋, 0, t, 4), for this rank's members.

@@ -14,6 +14,7 @@
 //               (M=128, N=128, K=16; fp32 accumulation in TMEM, 512 columns = one whole layer).
 // The activations never leave the SM (A: 128 KB smem); weights are read from HBM exactly once.
 // Bound: HBM (4 B/parameter/member); tensor work is ~20 % of the HBM time at B = 128.
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -31,6 +32,8 @@ static constexpr int kMaxLayers = 15;
 static constexpr int kStages = 6;
 static constexpr int kProdWarps = 8, kEpiWarps = 16;
 static constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
+// TMA mode: one producer warp (a single thread issues the tile copies) instead of eight.
+static constexpr int kThreadsTma = (1 + kEpiWarps + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
 static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 512;
@@ -48,6 +51,8 @@ struct MlpParams {
   const __half* uimg;           // layer-1 A image (pre-swizzled)
   float* Y;                     // [128][w_L] teacher outputs (read in mode 0, written in mode 1)
   int mode;
+  const __half* x16;            // TMA mode: the fp16 parameter image [n][D] (N14′)
+  CUtensorMap tmap[kMaxLayers + 1];   // TMA mode: per layer, 3-D (in, out, member) fp16 tiles
 };
 
 struct MlpProblem {
@@ -77,6 +82,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -151,7 +169,10 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 }
 
 // ---------------------------------------------------------------- the fitness kernel
-__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
+template <bool TMA>
+__global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
+    mlp_kernel(const __grid_constant__ MlpParams P) {
+  constexpr int kProd = TMA ? 1 : kProdWarps;          // producer warps
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                 // [8][128 rows][64] fp16
   uint8_t* Bst = smem + kABytes;                     // [kStages][128 rows][64] fp16
@@ -168,14 +189,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kProdWarps);
+      mbar_init(&full[s], TMA ? 1 : kProdWarps);
       mbar_init(&empty[s], 1);
     }
     mbar_init(dready, 1);
     mbar_init(aready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProdWarps + kEpiWarps) {              // TMEM: 512 fp32 columns × 128 lanes
+  if (warp == kProd + kEpiWarps) {                   // TMEM: 512 fp32 columns × 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -186,7 +207,29 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
   const uint32_t tmem = *tmem_slot;
   const int L = P.nl;
 
-  if (warp < kProdWarps) {
+  if (TMA && warp == 0) {
+    // ------------------------------------------------------------ TMA producer (fp16 image)
+    if (lane == 0) {
+      for (int l = 1; l <= L; ++l)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap[l])));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
+        for (int l = 1; l <= L; ++l) {
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+            const int nt = tile / kc_n, kc = tile % kc_n;
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], kTileBytes);
+            tma_load_3d(Bst + stage * kTileBytes, &P.tmap[l], kc * 64, nt * 128, (int)m,
+                        &full[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (!TMA && warp < kProdWarps) {
     // ------------------------------------------------------------ producers
     const int t = threadIdx.x;                       // 0..255
     int stage = 0;
@@ -257,12 +300,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
         }
       }
     }
-  } else if (warp < kProdWarps + kEpiWarps) {
+  } else if (warp < kProd + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - kProdWarps;                 // 0..15
-    const int q = e & 3, part = e >> 2;              // TMEM lane quarter, column quarter
+    const int e = warp - kProd;                      // 0..15
+    // a warp may only tcgen05.ld the TMEM lane quarter (warp id mod 4); part = column quarter
+    const int q = warp & 3, part = e >> 2;
     const int row = q * 32 + lane;                   // batch row = TMEM lane
-    const int et = threadIdx.x - kProdWarps * 32;    // 0..511
+    const int et = threadIdx.x - kProd * 32;         // 0..511
     uint32_t dphase = 0;
     for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
       const float* xm = P.x + m * P.D;
@@ -279,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
       float sq = 0.0f;
       for (int l = 1; l <= L; ++l) {
         const int in = P.w[l - 1], out = P.w[l];
-        const float* bias = xm + P.off[l] + (int64_t)out * in;
+        const float* bias = TMA ? nullptr : xm + P.off[l] + (int64_t)out * in;
+        const __half* bias16 = TMA ? P.x16 + m * P.D + P.off[l] + (int64_t)out * in : nullptr;
         const int quarter = P.npad[l] >> 2;          // columns per part (multiple of 32)
         mbar_wait(dready, dphase);
         dphase ^= 1;
@@ -297,21 +342,36 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
           }
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-          if (c0 + 32 <= out) {
-            // bias: 32 uniform values, eight broadcast float4 loads
+          // bias (N14: fp16(b), uniform across the warp → broadcast loads)
+          if (TMA) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              const int n = c0 + i;
+              if (n < out) {
+                const uint4 hb = __ldg(reinterpret_cast<const uint4*>(bias16 + n));
+                const __half* hh = reinterpret_cast<const __half*>(&hb);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[i + u] = tanhf(__fadd_rn(v[i + u], __half2float(hh[u])));
+              } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[i + u] = 0.0f;
+              }
+            }
+          } else if (c0 + 32 <= out) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
-              v[i] = tanhf(__fadd_rn(v[i], b4.x));
-              v[i + 1] = tanhf(__fadd_rn(v[i + 1], b4.y));
-              v[i + 2] = tanhf(__fadd_rn(v[i + 2], b4.z));
-              v[i + 3] = tanhf(__fadd_rn(v[i + 3], b4.w));
+              v[i] = tanhf(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
+              v[i + 1] = tanhf(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
+              v[i + 2] = tanhf(__fadd_rn(v[i + 2], __half2float(__float2half_rn(b4.z))));
+              v[i + 3] = tanhf(__fadd_rn(v[i + 3], __half2float(__float2half_rn(b4.w))));
             }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int n = c0 + i;
-              v[i] = n < out ? tanhf(__fadd_rn(v[i], __ldg(bias + n))) : 0.0f;
+              v[i] = n < out ? tanhf(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
+                             : 0.0f;
             }
           }
           if (l < L) {
@@ -389,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const MlpParams P) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kProdWarps + kEpiWarps) {
+  if (warp == kProd + kEpiWarps) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -455,14 +515,55 @@ static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
 static cudaError_t launch_mlp(const MlpParams& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(mlp_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mlp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = (int)std::min<int64_t>(p.n, sm_count());
-  mlp_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  if (p.x16) mlp_kernel<true><<<grid, kThreadsTma, kSmemBytes, st>>>(p);
+  else mlp_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);
   return cudaGetLastError();
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+// Per layer: the fp16 image viewed as a 3-D tensor (k = in, n = out, member) with strides
+// (2 B, in·2 B, D·2 B); a box of 64 k × 128 n × 1 member lands in smem in exactly the UMMA
+// K-major SWIZZLE_128B layout of a B stage (rows past `out` / columns past `in` are zero-filled).
+static cudaError_t encode_maps(MlpParams& q, const __half* x16, int64_t n) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  for (int l = 1; l <= q.nl; ++l) {
+    const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};
+    const cuuint64_t strides[2] = {(cuuint64_t)q.w[l - 1] * 2, (cuuint64_t)q.D * 2};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&q.tmap[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                     const_cast<__half*>(x16 + q.off[l]), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
 }
 
 void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
@@ -497,6 +598,7 @@ void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint6
   }
   pr->p.uimg = pr->uimg;
   pr->p.Y = pr->Y;
+  pr->p.x16 = nullptr;
   MlpParams q = pr->p;
   q.x = pr->theta;
   q.n = 1;
@@ -528,9 +630,26 @@ cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cud
   if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
   MlpParams q = pr->p;
   q.x = x;
+  q.x16 = nullptr;
   q.n = n;
   q.f = f;
   q.mode = 0;
+  return launch_mlp(q, st);
+}
+
+// N14′: fitness of the fp16 parameter image written by the ask kernel (TMA producer).
+cudaError_t launch_mlp_eval16(void* prob, const __half* x16, int64_t n, float* f,
+                              cudaStream_t st) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  if (reinterpret_cast<uintptr_t>(x16) & 15) return cudaErrorMisalignedAddress;
+  MlpParams q = pr->p;
+  q.x = nullptr;
+  q.x16 = x16;
+  q.n = n;
+  q.f = f;
+  q.mode = 0;
+  cudaError_t e = encode_maps(q, x16, n);
+  if (e != cudaSuccess) return e;
   return launch_mlp(q, st);
 }
 

@@ -27,7 +27,7 @@ def _numpy_forward(widths, U, x):
     for l in range(1, len(widths)):
         i, o = widths[l - 1], widths[l]
         W = x[off:off + o * i].reshape(o, i).astype(np.float16).astype(np.float64)
-        b = x[off + o * i: off + o * i + o].astype(np.float64)
+        b = x[off + o * i: off + o * i + o].astype(np.float16).astype(np.float64)
         off += o * i + o
         g = np.tanh(h @ W.T + b).astype(np.float32)
         h = g.astype(np.float16).astype(np.float64) if l + 1 < len(widths) else g
