@@ -140,7 +140,9 @@ static void run_direction(const orc_run_t *r, uint32_t i, uint32_t t, float *z) 
 static int64_t gdim(const orc_run_t *r, int64_t d) { return r->dims ? r->dims[d] : d; }
 
 /* ---------------- N6 init / ask ---------------- */
-static int is_antithetic(int algo) { return algo == ORC_OPENAI_ES || algo == ORC_PGPE; }
+static int is_antithetic(int algo) {
+  return algo == ORC_OPENAI_ES || algo == ORC_PGPE || algo == ORC_ARS;
+}
 
 int orc_num_directions(const orc_run_t *r) {
   return is_antithetic(r->algo) ? r->popsize / 2 : r->popsize;
@@ -153,7 +155,7 @@ int orc_init(orc_run_t *r) {
   const int32_t N = r->popsize;
   if (N < 2 || D < 1) return 1;
   if (is_antithetic(r->algo) && (N % 2) != 0) return 1;
-  if (r->algo < 0 || r->algo > 3) return 1;
+  if (r->algo < 0 || r->algo > 4) return 1;
   const orc_params_t *p = &r->p;
   uint32_t key[2] = {(uint32_t)p->seed, (uint32_t)(p->seed >> 32)};
   float *mean = vf(r, ORC_V_MEAN);
@@ -239,6 +241,7 @@ void orc_member(const orc_run_t *r, int32_t j, float *x) {
     float s;
     switch (r->algo) {
       case ORC_OPENAI_ES: s = r->sigma; break;
+      case ORC_ARS: s = r->sigma; break;
       case ORC_PGPE: s = sd[d]; break;
       case ORC_SNES: s = sd[d]; break;
       default: s = r->sigma * sqrtf(Cd[d]); break;
@@ -349,10 +352,53 @@ void orc_member_weights(const float *wpos, const float *f, int32_t N, float *w) 
   free(e);
 }
 
+/* z-score shaping: (f - mean) / (std + 1e-8), population std, in double. */
+void orc_zscore(const float *f, int32_t N, float *out) {
+  double mu = 0.0, var = 0.0;
+  for (int32_t j = 0; j < N; ++j) mu += (double)f[j];
+  mu = mu / N;
+  for (int32_t j = 0; j < N; ++j) var += ((double)f[j] - mu) * ((double)f[j] - mu);
+  double sd = sqrt(var / N) + 1e-8;
+  for (int32_t j = 0; j < N; ++j) out[j] = (float)(((double)f[j] - mu) / sd);
+}
+
 /* ---------------- N12 reductions ---------------- */
 /* Number of tell entries: P directions (antithetic), N members (SNES), or Sep-CMA's weighted
  * sorted positions (through the end of the tie group containing position mu-1). */
+/* ARS (Mania et al. 2018): k = max(1, round(elite_ratio * P)) directions with
+ * the best min(f+, f-), ordered by (key(min), index). */
+static int ars_k(const orc_run_t *r) {
+  int P = r->popsize / 2;
+  int k = (int)floor((double)r->p.elite_ratio * (double)P + 0.5);
+  return k < 1 ? 1 : (k > P ? P : k);
+}
+
+static void ars_select(const orc_run_t *r, const float *f, int32_t *sel /* [k] */) {
+  int P = r->popsize / 2;
+  float *mn = (float *)malloc(sizeof(float) * (size_t)P);
+  int32_t *s = (int32_t *)malloc(sizeof(int32_t) * (size_t)P);
+  int32_t *e = (int32_t *)malloc(sizeof(int32_t) * (size_t)P);
+  int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)P);
+  for (int i = 0; i < P; ++i) mn[i] = fminf(f[2 * i], f[2 * i + 1]);
+  orc_rank(mn, P, s, e, perm);
+  for (int q = 0; q < ars_k(r); ++q) sel[q] = perm[q];
+  free(mn); free(s); free(e); free(perm);
+}
+
+/* population std of the 2k fitness values of the selected pairs (double) */
+static double ars_sigma_r(const orc_run_t *r, const float *f, const int32_t *sel, int k) {
+  double m = 0.0, v = 0.0;
+  for (int q = 0; q < k; ++q) m += (double)f[2 * sel[q]] + (double)f[2 * sel[q] + 1];
+  m = m / (2.0 * k);
+  for (int q = 0; q < k; ++q) {
+    double a = (double)f[2 * sel[q]] - m, b = (double)f[2 * sel[q] + 1] - m;
+    v += a * a + b * b;
+  }
+  return sqrt(v / (2.0 * k));
+}
+
 int orc_num_entries(const orc_run_t *r, const float *f) {
+  if (r->algo == ORC_ARS) return ars_k(r);
   if (is_antithetic(r->algo)) return r->popsize / 2;
   if (r->algo == ORC_SNES) return r->popsize;
   int32_t N = r->popsize;
@@ -375,9 +421,26 @@ void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1
   for (int64_t d = 0; d < 2 * D; ++d) G[d] = 0.0;
   float *sh = (float *)malloc(sizeof(float) * (size_t)N);
   float *z = (float *)malloc(sizeof(float) * (size_t)D);
-  if (is_antithetic(r->algo)) {
-    if (r->p.shaping == 1) memcpy(sh, f, sizeof(float) * (size_t)N);
-    else orc_centered_rank(f, N, sh);
+  if (r->algo == ORC_ARS) {
+    /* entries are the selected directions in selection order; coefficient f+ - f- (raw) */
+    int k = ars_k(r);
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
+    ars_select(r, f, sel);
+    for (int32_t q = e0; q < e1; ++q) {
+      int i = sel[q];
+      double a = (double)f[2 * i] - (double)f[2 * i + 1];
+      run_direction(r, (uint32_t)i, r->t, z);
+      for (int64_t d = 0; d < D; ++d) G0[d] += a * (double)z[d];
+    }
+    free(sel);
+  } else if (is_antithetic(r->algo)) {
+    if (r->p.shaping == 1) {
+      memcpy(sh, f, sizeof(float) * (size_t)N);
+    } else if (r->p.shaping == 2) {
+      orc_zscore(f, N, sh);
+    } else {
+      orc_centered_rank(f, N, sh);
+    }
     double bbar = 0.0;
     for (int32_t j = 0; j < N; ++j) bbar += (double)sh[j];
     bbar = bbar / N;
@@ -419,6 +482,14 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G) {
   orc_reduce_range(r, f, 0, orc_num_entries(r, f), G);
 }
 
+/* SGD with momentum: v' = fma(mu, v, g); mean' = mean - lr * v'. State in ADAM_M. */
+static void sgd(orc_run_t *r, int64_t d, float g) {
+  float *mean = vf(r, ORC_V_MEAN), *v = vf(r, ORC_V_ADAM_M);
+  float vn = fmaf(r->p.momentum, v[d], g);
+  v[d] = vn;
+  mean[d] = mean[d] - r->lr * vn;
+}
+
 static void adam(orc_run_t *r, int64_t d, float g, float bc1, float bc2) {
   float *mean = vf(r, ORC_V_MEAN), *am = vf(r, ORC_V_ADAM_M), *av = vf(r, ORC_V_ADAM_V);
   const float b1 = r->p.beta1, b2 = r->p.beta2;
@@ -452,19 +523,33 @@ int orc_tell(orc_run_t *r, const float *f) {
   const double *G0 = G, *G1 = G + D;
   float *mean = vf(r, ORC_V_MEAN), *sd = vf(r, ORC_V_SIGMA);
 
-  if (r->algo == ORC_OPENAI_ES || r->algo == ORC_PGPE) {
+  if (r->algo == ORC_ARS) {
+    /* ARS V1 update for minimisation: mean -= alpha / (k sigma_R) * sum (f+ - f-) z_i */
+    int k = ars_k(r);
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
+    ars_select(r, f, sel);
+    double sr = ars_sigma_r(r, f, sel, k);
+    free(sel);
+    if (sr > 0.0) {
+      float scale = (float)((double)r->lr / ((double)k * sr));
+      for (int64_t d = 0; d < D; ++d) mean[d] = mean[d] - scale * (float)G0[d];
+    }
+    r->lr = fmaxf(r->lr * r->p.lrate_decay, r->p.lrate_limit);
+    r->sigma = fmaxf(r->sigma * r->p.sigma_decay, r->p.sigma_limit);
+  } else if (r->algo == ORC_OPENAI_ES || r->algo == ORC_PGPE) {
     r->b1pow = r->b1pow * (double)r->p.beta1;
     r->b2pow = r->b2pow * (double)r->p.beta2;
     float bc1 = (float)(1.0 - r->b1pow), bc2 = (float)(1.0 - r->b2pow);
+    /* gradients of the mean (and PGPE's sigma step) first, so that ClipUp's global norms can be
+     * formed before any mean moves */
+    float *gm = (float *)malloc(sizeof(float) * (size_t)D);
     for (int64_t d = 0; d < D; ++d) {
       if (r->algo == ORC_OPENAI_ES) {
-        float g = (float)G0[d] / ((float)N * r->sigma);
-        adam(r, d, g, bc1, bc2);
+        gm[d] = (float)G0[d] / ((float)N * r->sigma);
       } else {
         float sig = sd[d];
-        float gm = (sig * (float)G0[d]) / (float)N;
+        gm[d] = (sig * (float)G0[d]) / (float)N;
         float gs = (sig * (float)G1[d]) / (float)P;
-        adam(r, d, gm, bc1, bc2);
         float mc = r->p.sigma_max_change;
         float st = sig - r->p.sigma_lrate * gs;
         float lo = (1.0f - mc) * sig, hi = (1.0f + mc) * sig;
@@ -472,6 +557,31 @@ int orc_tell(orc_run_t *r, const float *f) {
         sd[d] = fmaxf(st * r->p.sigma_decay, r->p.sigma_limit);
       }
     }
+    if (r->p.optimizer == ORC_ADAM) {
+      for (int64_t d = 0; d < D; ++d) adam(r, d, gm[d], bc1, bc2);
+    } else if (r->p.optimizer == ORC_SGD) {
+      for (int64_t d = 0; d < D; ++d) sgd(r, d, gm[d]);
+    } else {
+      /* ClipUp (Toklu et al. 2020): g_hat = g / ||g||, v' = mu v + lr g_hat,
+       * v' clipped to norm max_speed, mean' = mean - v'. Norms in double. */
+      float *v = vf(r, ORC_V_ADAM_M);
+      double n2 = 0.0;
+      for (int64_t d = 0; d < D; ++d) n2 += (double)gm[d] * (double)gm[d];
+      double gn = sqrt(n2);
+      float inv = gn > 0.0 ? (float)(1.0 / gn) : 0.0f;
+      double v2 = 0.0;
+      for (int64_t d = 0; d < D; ++d) {
+        v[d] = fmaf(r->p.momentum, v[d], r->lr * (gm[d] * inv));
+        v2 += (double)v[d] * (double)v[d];
+      }
+      double vn = sqrt(v2);
+      float clip = vn > (double)r->p.max_speed ? (float)((double)r->p.max_speed / vn) : 1.0f;
+      for (int64_t d = 0; d < D; ++d) {
+        v[d] = v[d] * clip;
+        mean[d] = mean[d] - v[d];
+      }
+    }
+    free(gm);
     r->lr = fmaxf(r->lr * r->p.lrate_decay, r->p.lrate_limit);
     if (r->algo == ORC_OPENAI_ES) r->sigma = fmaxf(r->sigma * r->p.sigma_decay, r->p.sigma_limit);
   } else if (r->algo == ORC_SNES) {

@@ -17,7 +17,8 @@
 extern "C" {
 #endif
 
-enum { ORC_OPENAI_ES = 0, ORC_PGPE = 1, ORC_SNES = 2, ORC_SEP_CMA_ES = 3 };
+enum { ORC_OPENAI_ES = 0, ORC_PGPE = 1, ORC_SNES = 2, ORC_SEP_CMA_ES = 3, ORC_ARS = 4 };
+enum { ORC_ADAM = 0, ORC_SGD = 1, ORC_CLIPUP = 2 };
 enum { ORC_SPHERE = 0, ORC_ROSENBROCK = 1, ORC_RASTRIGIN = 2 };
 
 /* Per-run vector fields inside orc_run_t.vec, each [D] floats. */
@@ -33,7 +34,10 @@ typedef struct {
   float sigma_lrate, sigma_max_change;
   float temperature;
   float elite_ratio;
-  int32_t shaping; /* 0 centered rank, 1 raw fitness (OpenAI-ES/PGPE tests only) */
+  int32_t shaping; /* 0 centered rank, 1 raw fitness, 2 z-score (OpenAI-ES/PGPE) */
+  int32_t optimizer;   /* 0 Adam, 1 SGD with momentum, 2 ClipUp (OpenAI-ES/PGPE) */
+  float momentum;      /* SGD / ClipUp momentum */
+  float max_speed;     /* ClipUp velocity clip */
 } orc_params_t;
 
 typedef struct {
@@ -87,6 +91,7 @@ uint32_t orc_key(float f);
 void orc_rank(const float *f, int32_t N, int32_t *s, int32_t *e, int32_t *perm);
 void orc_centered_rank(const float *f, int32_t N, float *c);
 void orc_member_weights(const float *wpos, const float *f, int32_t N, float *w);
+void orc_zscore(const float *f, int32_t N, float *out);
 
 /* N12 tell: reductions (double) G[k][D] from shaped values, then update. */
 void orc_reduce(const orc_run_t *r, const float *f, double *G /* [2][D] */);

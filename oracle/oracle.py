@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(HERE, "libes_oracle.so")
 SRC = os.path.join(HERE, "es_oracle.c")
 HDR = os.path.join(HERE, "es_oracle.h")
 
-OPENAI_ES, PGPE, SNES, SEP_CMA_ES = 0, 1, 2, 3
+OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS = 0, 1, 2, 3, 4
+ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN = 0, 1, 2
 V_MEAN, V_SIGMA, V_ADAM_M, V_ADAM_V, V_PSIGMA, V_PC, V_C, V_BEST_X, NV = range(9)
 
@@ -38,7 +39,8 @@ class Params(C.Structure):
                 ("lrate_init", C.c_float), ("lrate_decay", C.c_float), ("lrate_limit", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("sigma_lrate", C.c_float), ("sigma_max_change", C.c_float),
-                ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32)]
+                ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32),
+                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float)]
 
 
 class RunT(C.Structure):
@@ -80,6 +82,7 @@ def lib():
             "orc_rank": (None, [fp, C.c_int32, i32p, i32p, i32p]),
             "orc_centered_rank": (None, [fp, C.c_int32, fp]),
             "orc_member_weights": (None, [fp, fp, C.c_int32, fp]),
+            "orc_zscore": (None, [fp, C.c_int32, fp]),
             "orc_reduce": (None, [C.POINTER(RunT), fp, dp]),
             "orc_reduce_range": (None, [C.POINTER(RunT), fp, C.c_int32, C.c_int32, dp]),
             "orc_num_entries": (C.c_int, [C.POINTER(RunT), fp]),
@@ -164,6 +167,13 @@ def centered_rank(f):
     return c
 
 
+def zscore(f):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    out = np.empty_like(f)
+    lib().orc_zscore(_p(f, C.c_float), f.size, _p(out, C.c_float))
+    return out
+
+
 def member_weights(wpos, f):
     f = np.ascontiguousarray(f, dtype=np.float32)
     wpos = np.ascontiguousarray(wpos, dtype=np.float32)
@@ -191,7 +201,7 @@ def synth_fitness(seed, t, N):
 DEFAULTS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=0.999, sigma_limit=0.01,
                 lrate_init=0.01, lrate_decay=0.999, lrate_limit=0.001, beta1=0.9, beta2=0.999,
                 eps=1e-8, sigma_lrate=0.2, sigma_max_change=0.2, temperature=12.0,
-                elite_ratio=0.5, shaping=0)
+                elite_ratio=0.5, shaping=0, optimizer=0, momentum=0.9, max_speed=0.02)
 
 
 class Run:

@@ -8,8 +8,10 @@ from __future__ import annotations
 
 import numpy as np
 
-OPENAI_ES, PGPE, SNES, SEP_CMA_ES = 0, 1, 2, 3
-ALGO_NAMES = {OPENAI_ES: "openai_es", PGPE: "pgpe", SNES: "snes", SEP_CMA_ES: "sep_cma_es"}
+OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS = 0, 1, 2, 3, 4
+ALGO_NAMES = {OPENAI_ES: "openai_es", PGPE: "pgpe", SNES: "snes", SEP_CMA_ES: "sep_cma_es",
+              ARS: "ars"}
+ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
 FN_NAMES = {SPHERE: "sphere", ROSENBROCK: "rosenbrock", RASTRIGIN: "rastrigin", MLP: "mlp"}
 
@@ -22,6 +24,9 @@ ANT = {
                sigma_lrate=0.2, sigma_max_change=0.2),
     SNES: dict(sigma_init=0.05, temperature=12.0),
     SEP_CMA_ES: dict(sigma_init=0.05, elite_ratio=0.4),
+    # ARS has no App. B column (Table 1 row only): OpenAI-ES-like schedules, top-50 % pairs
+    ARS: dict(sigma_init=0.05, sigma_decay=0.999, sigma_limit=0.01, lrate_init=0.01,
+              lrate_decay=0.999, lrate_limit=0.001, elite_ratio=0.5),
 }
 # The four App. B columns (Ant, Fetch, HalfCheetah, Humanoid) for the hyperparameter-vmap variant.
 SEP_CMA_COLUMNS = [(0.05, 0.4), (0.125, 0.2), (0.05, 0.5), (0.1, 0.2)]
@@ -29,7 +34,8 @@ SNES_COLUMNS = [(0.05, 12.0), (0.075, 12.0), (0.05, 16.0), (0.075, 32.0)]   # P:
 
 BASE = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=1.0, sigma_limit=0.0,
             lrate_init=0.01, lrate_decay=1.0, lrate_limit=0.0, beta1=0.9, beta2=0.999, eps=1e-8,
-            sigma_lrate=0.2, sigma_max_change=0.2, temperature=12.0, elite_ratio=0.5, shaping=0)
+            sigma_lrate=0.2, sigma_max_change=0.2, temperature=12.0, elite_ratio=0.5, shaping=0,
+            optimizer=0, momentum=0.9, max_speed=0.02)
 
 
 def run_params(algo, seed, **over):
