@@ -32,7 +32,15 @@ extern "C" {
 
 typedef struct CUstream_st *es_stream_t; /* == cudaStream_t */
 
-typedef enum { ES_OPENAI_ES = 0, ES_PGPE = 1, ES_SNES = 2, ES_SEP_CMA_ES = 3 } es_algo_t;
+typedef enum {
+  ES_OPENAI_ES = 0,
+  ES_PGPE = 1,
+  ES_SNES = 2,
+  ES_SEP_CMA_ES = 3,/* P:179 */
+  ES_ARS = 4        /* antithetic, top-k directions, sigma_R normalised */
+} es_algo_t;
+
+typedef enum { ES_OPT_ADAM = 0, ES_OPT_SGD = 1, ES_OPT_CLIPUP = 2 } es_optimizer_t;
 
 typedef enum {
   ES_FIT_SPHERE = 0,     /* Σ x_d²                                  (P:212 BBOB)      */
@@ -64,15 +72,19 @@ typedef struct {
   float sigma_max_change;     /* PGPE relative σ clip: 0.2                              */
   float temperature;          /* SNES β                                          */
   float elite_ratio;          /* Sep-CMA-ES μ = ⌊elite_ratio·N⌋                         */
-  int32_t shaping;            /* 0 = centered rank; 1 = raw fitness (OpenAI-ES,
-                                 PGPE only; for gradient tests)                                 */
+  int32_t shaping;            /* 0 = centered rank; 1 = raw fitness; 2 = z-score
+                                 (P:213). OpenAI-ES / PGPE only (ARS always uses raw fitness)    */
+  int32_t optimizer;          /* es_optimizer_t for the mean of OpenAI-ES / PGPE: Adam,
+                                 SGD with momentum, ClipUp                               */
+  float momentum;             /* SGD / ClipUp momentum (0.9)                                     */
+  float max_speed;            /* ClipUp velocity norm limit (2·lrate)                            */
 } es_run_params_t;
 
 /* Fields readable with es_get / writable with es_set (checkpoint / resume). Shapes per context. */
 typedef enum {
   ES_FIELD_MEAN = 0,     /* float [R][D]                                                     */
   ES_FIELD_SIGMA_D = 1,  /* float [R][D]  per-dimension σ (PGPE, SNES)                       */
-  ES_FIELD_ADAM_M = 2,   /* float [R][D]  (OpenAI-ES, PGPE)                                   */
+  ES_FIELD_ADAM_M = 2,   /* float [R][D]  Adam m / SGD / ClipUp velocity (OpenAI-ES, PGPE)    */
   ES_FIELD_ADAM_V = 3,   /* float [R][D]                                                     */
   ES_FIELD_P_SIGMA = 4,  /* float [R][D]  Sep-CMA-ES evolution path p_σ                      */
   ES_FIELD_P_C = 5,      /* float [R][D]  Sep-CMA-ES evolution path p_c                       */

@@ -12,7 +12,8 @@ ES_SUCCESS = 0
 STATUS = {0: "success", 1: "invalid argument", 2: "bad state", 3: "CUDA error", 4: "NCCL error",
           5: "out of device memory", 6: "unsupported"}
 
-OPENAI_ES, PGPE, SNES, SEP_CMA_ES = 0, 1, 2, 3
+OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS = 0, 1, 2, 3, 4
+ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
 FIELDS = dict(mean=0, sigma_d=1, adam_m=2, adam_v=3, p_sigma=4, p_c=5, C=6, best_x=7, best_f=8,
               sigma=9, lrate=10, gen=11, shaped=12, rank_s=13, rank_e=14, perm=15, fitness=16,
@@ -32,7 +33,8 @@ class RunParams(C.Structure):
                 ("lrate_init", C.c_float), ("lrate_decay", C.c_float), ("lrate_limit", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("sigma_lrate", C.c_float), ("sigma_max_change", C.c_float),
-                ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32)]
+                ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32),
+                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float)]
 
 
 class ESError(RuntimeError):

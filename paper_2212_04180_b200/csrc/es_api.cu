@@ -47,6 +47,7 @@ using namespace esb;
 struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
+  bool any_clipup = false;
   ncclComm_t comm = nullptr;
   bool asked = false;
   bool told_local = false;
@@ -142,7 +143,7 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-static bool antithetic(int algo) { return algo == OPENAI_ES || algo == PGPE; }
+static bool antithetic(int algo) { return is_anti(algo); }
 
 // ---- host constant tables (binary64; NUMERICS N11, N12) ------------------------------------
 static void snes_weights(int N, double beta, std::vector<float>& out) {
@@ -235,7 +236,7 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   cudaStream_t st = (cudaStream_t)stream_;
   if (!out) return fail(nullptr, ES_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  if ((int)algo < 0 || (int)algo > 3) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
+  if ((int)algo < 0 || (int)algo > 4) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
   if (!params) return fail(nullptr, ES_ERR_INVALID_ARG, "params is NULL");
   if (R < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_runs must be >= 1");
   if (N < 2) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be >= 2");
@@ -255,8 +256,15 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: floor(elite_ratio*N) < 1", r);
     if (algo == ES_SEP_CMA_ES && !(p.elite_ratio <= 1.0f))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: elite_ratio > 1", r);
-    if (p.shaping != 0 && !(p.shaping == 1 && antithetic(algo)))
-      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: raw shaping only for OpenAI-ES/PGPE", r);
+    const bool adamish = algo == ES_OPENAI_ES || algo == ES_PGPE;
+    if (p.shaping != 0 && !((p.shaping == 1 || p.shaping == 2) && adamish))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: raw/z-score shaping only for OpenAI-ES/PGPE", r);
+    if (p.optimizer != ES_OPT_ADAM && !(adamish && (p.optimizer == ES_OPT_SGD || p.optimizer == ES_OPT_CLIPUP)))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: SGD/ClipUp only for OpenAI-ES/PGPE", r);
+    if (p.optimizer == ES_OPT_CLIPUP && !(p.max_speed > 0.0f))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: ClipUp needs max_speed > 0", r);
+    if (algo == ES_ARS && !(p.elite_ratio > 0.0f && p.elite_ratio <= 1.0f))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: ARS elite_ratio must be in (0, 1]", r);
   }
   es_ctx* c = new (std::nothrow) es_ctx();
   if (!c) return fail(nullptr, ES_ERR_OOM, "host allocation failed");
@@ -290,6 +298,7 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   TRY(dalloc(c, (void**)&s.rs_s, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.rs_e, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.perm, RN * sizeof(int32_t)));
+  TRY(dalloc(c, (void**)&s.pos, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.dir, RN * sizeof(uint32_t)));
   TRY(dalloc(c, (void**)&s.coefA, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.coefB, RN * sizeof(double)));
@@ -319,6 +328,12 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
     rs.lrate_decay = p.lrate_decay; rs.lrate_limit = p.lrate_limit;
     rs.beta1 = p.beta1; rs.beta2 = p.beta2; rs.eps = p.eps;
     rs.sigma_lrate = p.sigma_lrate; rs.sigma_max_change = p.sigma_max_change;
+    rs.optimizer = p.optimizer; rs.momentum = p.momentum; rs.max_speed = p.max_speed;
+    if (algo == ES_ARS) {   // k = max(1, round(elite_ratio · P)), P = N/2
+      const int P = N / 2;
+      rs.ars_k = std::max(1, std::min(P, (int)std::floor((double)p.elite_ratio * (double)P + 0.5)));
+    }
+    if (p.optimizer == ES_OPT_CLIPUP) c->any_clipup = true;
     std::fill(wr.begin(), wr.end(), 0.0f);
     if (algo == ES_SNES) {
       snes_weights(N, (double)p.temperature, wr);
@@ -540,6 +555,12 @@ static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st) {
     CUDA_OR(c, launch_sepcma_finish(s, st, &nk));
     c->launches += nk;
   }
+  if (c->any_clipup) {
+    int nk = 0;
+    ProfScope ps(c, "clipup_finish", st);
+    CUDA_OR(c, launch_clipup_finish(s, st, &nk));
+    c->launches += nk;
+  }
   return ES_SUCCESS;
 }
 
@@ -577,7 +598,7 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   }
   if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
   if (s.W > 1) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
-    const size_t cnt = (size_t)(s.algo == OPENAI_ES ? 1 : 2) * s.R * s.D;
+    const size_t cnt = (size_t)(s.algo == OPENAI_ES || s.algo == ARS ? 1 : 2) * s.R * s.D;
     ProfScope ps(c, "allreduce", st);
     NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));
   }

@@ -17,7 +17,9 @@
 
 namespace esb {
 
-enum Algo : int { OPENAI_ES = 0, PGPE = 1, SNES = 2, SEP_CMA_ES = 3 };
+enum Algo : int { OPENAI_ES = 0, PGPE = 1, SNES = 2, SEP_CMA_ES = 3, ARS = 4 };
+enum Optim : int { OPT_ADAM = 0, OPT_SGD = 1, OPT_CLIPUP = 2 };
+__host__ __device__ constexpr bool is_anti(int a) { return a == OPENAI_ES || a == PGPE || a == ARS; }
 enum Field : int {
   F_MEAN = 0, F_SIGMA_D = 1, F_ADAM_M = 2, F_ADAM_V = 3, F_PSIGMA = 4, F_PC = 5, F_C = 6,
   F_BEST_X = 7, NVEC = 8
@@ -33,6 +35,8 @@ struct alignas(16) RunScal {
   float init_min, init_max, sigma_init, sigma_decay, sigma_limit, lrate_decay, lrate_limit;
   float beta1, beta2, eps, sigma_lrate, sigma_max_change;
   double c_sigma, d_sigma, c_c, c_1, c_mu, chi_d, mueff, eta_sigma;
+  int32_t optimizer, ars_k;
+  float momentum, max_speed;
 };
 
 struct alignas(16) GenScal {
@@ -45,6 +49,8 @@ struct alignas(16) GenScal {
   double bbar;         // PGPE baseline
   float sigma_new;     // Sep-CMA σ' (written by the norm kernel)
   int32_t hsig;        // Sep-CMA h_σ
+  float ars_scale;     // ARS: α / (k·σ_R), or 0 when σ_R = 0
+  float clip_inv;      // ClipUp: 1/‖g‖ (0 if ‖g‖ = 0), then the velocity clip factor
 };
 
 struct DevState {
@@ -68,6 +74,7 @@ struct DevState {
   uint32_t* arrive;    // [R][blocks_per_run] last-block counters
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
   uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
+  int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
 };
 
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
@@ -93,6 +100,7 @@ cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
 cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st);
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
+cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 int tell_blocks_per_run(const DevState& s);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;

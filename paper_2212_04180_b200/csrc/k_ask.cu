@@ -55,7 +55,7 @@ cudaError_t launch_init(const DevState& s, cudaStream_t st) {
 // Per-dimension scale of the sample for this algorithm (N6): x = fma(±scale, z, m).
 template <int ALGO>
 __device__ __forceinline__ float ask_scale(const DevState& s, const RunScal& rs, int64_t idx) {
-  if (ALGO == OPENAI_ES) return rs.sigma;
+  if (ALGO == OPENAI_ES || ALGO == ARS) return rs.sigma;
   if (ALGO == PGPE || ALGO == SNES) return s.vec[F_SIGMA_D][idx];
   return __fmul_rn(rs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
 }
@@ -65,7 +65,7 @@ template <int ALGO, bool V4, bool W16>
 __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
                                                            __half* __restrict__ x16, int bpr,
                                                            int dpt) {
-  constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+  constexpr bool kAnti = is_anti(ALGO);
   const int r = blockIdx.x / bpr;
   const int64_t q = (int64_t)(blockIdx.x % bpr) * kAskThreads + threadIdx.x;
   if (q >= s.Q) return;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
 
 template <int ALGO>
 static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaStream_t st) {
-  constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+  constexpr bool kAnti = is_anti(ALGO);
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
   const int bpr = (int)((s.Q + kAskThreads - 1) / kAskThreads);
   // Enough (thread, direction-chunk) items for ~4 waves of 16 warps/SM, ≥ 4 directions each.
@@ -159,6 +159,7 @@ cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t 
     case OPENAI_ES: return launch_ask_t<OPENAI_ES>(s, x, x16, st);
     case PGPE: return launch_ask_t<PGPE>(s, x, x16, st);
     case SNES: return launch_ask_t<SNES>(s, x, x16, st);
+    case ARS: return launch_ask_t<ARS>(s, x, x16, st);
     default: return launch_ask_t<SEP_CMA_ES>(s, x, x16, st);
   }
 }

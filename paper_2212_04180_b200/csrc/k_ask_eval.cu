@@ -20,7 +20,7 @@ static constexpr int kMaxDpt = 32;   // directions per thread-chunk (red buffer 
 
 template <int ALGO>
 __device__ __forceinline__ float ae_scale(const DevState& s, const RunScal& rs, int64_t idx) {
-  if (ALGO == OPENAI_ES) return rs.sigma;
+  if (ALGO == OPENAI_ES || ALGO == ARS) return rs.sigma;
   if (ALGO == PGPE || ALGO == SNES) return s.vec[F_SIGMA_D][idx];
   return __fmul_rn(rs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
 }
@@ -29,7 +29,7 @@ template <int ALGO, int FN, bool WX, bool V4>
 __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __restrict__ x,
                                                        double* __restrict__ part, int bpr,
                                                        int dpt) {
-  constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+  constexpr bool kAnti = is_anti(ALGO);
   constexpr int M = kAnti ? 2 : 1;
   __shared__ double red[4][kMaxDpt * 2];
   const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
@@ -151,7 +151,7 @@ static void launch_ae_a(int fn, const DevState& s, float* x, double* part, dim3 
 // Two kernels: the fused ask+evaluate and the per-member block sum.
 cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
                             cudaStream_t st) {
-  const bool anti = (s.algo == OPENAI_ES || s.algo == PGPE);
+  const bool anti = is_anti(s.algo);
   const int Ploc = anti ? s.Nloc / 2 : s.Nloc;
   const int bpr = ask_eval_blocks_per_run(s);
   const int64_t quads = (int64_t)s.R * bpr * kAE;
@@ -166,6 +166,7 @@ cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, f
     case OPENAI_ES: launch_ae_a<OPENAI_ES>(fn, s, x, part, grid, bpr, dpt, st); break;
     case PGPE: launch_ae_a<PGPE>(fn, s, x, part, grid, bpr, dpt, st); break;
     case SNES: launch_ae_a<SNES>(fn, s, x, part, grid, bpr, dpt, st); break;
+    case ARS: launch_ae_a<ARS>(fn, s, x, part, grid, bpr, dpt, st); break;
     default: launch_ae_a<SEP_CMA_ES>(fn, s, x, part, grid, bpr, dpt, st); break;
   }
   const int64_t rows = (int64_t)s.R * s.Nloc;

@@ -45,7 +45,21 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
   int32_t* E = s.rs_e + (int64_t)r * N;
   float* shaped = s.shaped + (int64_t)r * N;
   const float* wpos = s.wpos + (int64_t)r * N;
-  const bool anti = (s.algo == OPENAI_ES || s.algo == PGPE);
+  const bool anti = is_anti(s.algo);
+  // z-score shaping: population mean and std of the fitness, binary64
+  double zmu = 0.0, zsd = 1.0;
+  const bool zscore = anti && s.algo != ARS && rs.shaping == 2;
+  if (zscore) {
+    double part = 0.0;
+    for (int j = threadIdx.x; j < N; j += T) part = __dadd_rn(part, (double)fit[j]);
+    zmu = block_sum(part, red) / (double)N;
+    part = 0.0;
+    for (int j = threadIdx.x; j < N; j += T) {
+      const double d = __dsub_rn((double)fit[j], zmu);
+      part = __dadd_rn(part, __dmul_rn(d, d));
+    }
+    zsd = __dadd_rn(sqrt(block_sum(part, red) / (double)N), 1e-8);
+  }
   for (int p = threadIdx.x; p < N; p += T) {
     const uint64_t v = keys[p];
     const uint32_t key = (uint32_t)(v >> 32);
@@ -65,10 +79,14 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     perm[p] = j;
     S[j] = sj;
     E[j] = ej;
+    s.pos[(int64_t)r * N + j] = p;
     float val;
-    if (anti) {
-      val = rs.shaping == 1 ? fit[j]
-                            : __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));  // N10
+    if (s.algo == ARS || (anti && rs.shaping == 1)) {
+      val = fit[j];                                                      // raw fitness
+    } else if (zscore) {
+      val = (float)__ddiv_rn(__dsub_rn((double)fit[j], zmu), zsd);
+    } else if (anti) {
+      val = __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));  // N10
     } else {
       float acc = 0.0f;                                                                       // N11
       for (int q = sj; q <= ej; ++q) acc = __fadd_rn(acc, wpos[q]);
@@ -87,7 +105,53 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     for (int j = threadIdx.x; j < N; j += T) part = __dadd_rn(part, (double)shaped[j]);
     bbar = block_sum(part, red) / (double)N;
   }
-  if (anti) {
+  float ars_scale = 0.0f;
+  if (s.algo == ARS) {
+    // ARS: pairs ordered by (key(min(f+, f−)), pair index) = by the position of
+    // their better member; pair i is "first seen" at p = min(pos(2i), pos(2i+1)). A block scan over
+    // positions gives each first-seen pair its order; the first k are the elite directions.
+    const int32_t* pos = s.pos + (int64_t)r * N;
+    const int k = rs.ars_k;
+    const int per = (N + T - 1) / T, p0 = threadIdx.x * per, p1 = min(N, p0 + per);
+    int cnt = 0;
+    for (int p = p0; p < p1; ++p) cnt += pos[perm[p] ^ 1] > p;
+    // exclusive scan of cnt over the block (fixed order)
+    int* scan = reinterpret_cast<int*>(red);          // ≤ 32 warps: warp totals
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) >= o) v += u;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 31) scan[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) wbase += scan[w];
+    int idx = wbase + v - cnt;
+    double psum = 0.0;
+    for (int p = p0; p < p1; ++p) {
+      if (pos[perm[p] ^ 1] > p) {
+        if (idx < k) {
+          const int i = perm[p] >> 1;
+          dir[idx] = (uint32_t)i;
+          cA[idx] = __dsub_rn((double)fit[2 * i], (double)fit[2 * i + 1]);
+          psum = __dadd_rn(psum, __dadd_rn((double)fit[2 * i], (double)fit[2 * i + 1]));
+        }
+        ++idx;
+      }
+    }
+    __syncthreads();
+    const double mu = block_sum(psum, red) / (2.0 * k);
+    double pv = 0.0;
+    for (int e = threadIdx.x; e < k; e += T) {
+      const int i = (int)dir[e];
+      const double a = __dsub_rn((double)fit[2 * i], mu), b = __dsub_rn((double)fit[2 * i + 1], mu);
+      pv = __dadd_rn(pv, __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+    }
+    const double sr = sqrt(block_sum(pv, red) / (2.0 * k));
+    if (sr > 0.0) ars_scale = (float)((double)rs.lr / ((double)k * sr));
+  } else if (anti) {
     for (int i = threadIdx.x; i < N / 2; i += T) {
       const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
       dir[i] = (uint32_t)i;
@@ -119,7 +183,9 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     if (g.improved) w.best_f = fb;
     g.lr = w.lr;
     g.sigma = w.sigma;
-    g.nentries = anti ? N / 2 : (s.algo == SNES ? N : sh_nw);
+    g.nentries = s.algo == ARS ? w.ars_k : (anti ? N / 2 : (s.algo == SNES ? N : sh_nw));
+    g.ars_scale = ars_scale;
+    g.clip_inv = 0.0f;
     g.bbar = bbar;
     g.bc1 = g.bc2 = 1.0f;
     g.sigma_new = w.sigma;
@@ -132,7 +198,8 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
       w.b1pow = b1;
       w.b2pow = b2;
       w.lr = fmaxf(__fmul_rn(w.lr, w.lrate_decay), w.lrate_limit);
-      if (s.algo == OPENAI_ES) w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
+      if (s.algo == OPENAI_ES || s.algo == ARS)
+        w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
     }
     w.t = g.t + 1;
     s.gs[r] = g;

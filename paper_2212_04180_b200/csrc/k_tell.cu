@@ -41,7 +41,7 @@ __device__ __forceinline__ void accumulate(Acc& acc, const float4& z, double cA,
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const double zd = (double)zz[k];
-    if (ALGO == OPENAI_ES) {
+    if (ALGO == OPENAI_ES || ALGO == ARS) {
       acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
     } else if (ALGO == PGPE) {
       acc.a[k] = __fma_rn(cA, zd, acc.a[k]);
@@ -76,6 +76,24 @@ __device__ __forceinline__ void adam_step(float& mean, float& am, float& av, flo
   av = vn;
 }
 
+// The optimizer step of OpenAI-ES / PGPE for one dim. Adam and momentum SGD
+// update in place; ClipUp needs two global norms, so here it only parks g (binary64 slot of s.G)
+// and adds g² to the block's norm partial; launch_clipup_finish completes the step.
+__device__ __forceinline__ void opt_step(const DevState& s, int r, int64_t d, int64_t idx,
+                                         float& mean, float g, const RunScal& rs,
+                                         const GenScal& gs, double& norm2) {
+  if (rs.optimizer == OPT_ADAM) {
+    adam_step(mean, s.vec[F_ADAM_M][idx], s.vec[F_ADAM_V][idx], g, rs, gs);
+  } else if (rs.optimizer == OPT_SGD) {
+    const float vn = __fmaf_rn(rs.momentum, s.vec[F_ADAM_M][idx], g);
+    s.vec[F_ADAM_M][idx] = vn;
+    mean = __fsub_rn(mean, __fmul_rn(gs.lr, vn));
+  } else {
+    s.G[gidx(s, 0, r, d)] = (double)g;
+    norm2 = __dadd_rn(norm2, __dmul_rn((double)g, (double)g));
+  }
+}
+
 // Update epilogue for the 4 dims of quad q of run r from the reduced sums G0, G1 (N12). Also
 // regenerates best_x from the pre-update state when this generation improved.
 // Sep-CMA: phase 1 only (mean, p_σ, Z/Q to s.G, ‖p_σ‖² partial of the block to normpart).
@@ -90,7 +108,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
     float4 zb = make_float4(0.f, 0.f, 0.f, 0.f);
     float sgn = 1.0f;
     if (gs.improved) {
-      constexpr bool kAnti = (ALGO == OPENAI_ES || ALGO == PGPE);
+      constexpr bool kAnti = is_anti(ALGO);
       const int i = kAnti ? gs.jbest / 2 : gs.jbest;
       sgn = (kAnti && (gs.jbest & 1)) ? -1.0f : 1.0f;
       zb = normal4(ph, (uint32_t)q, (uint32_t)i, gs.t);
@@ -109,19 +127,22 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
       float mean = s.vec[F_MEAN][idx];
       if (gs.improved) {
         float sc;
-        if (ALGO == OPENAI_ES) sc = gs.sigma;
+        if (ALGO == OPENAI_ES || ALGO == ARS) sc = gs.sigma;
         else if (ALGO == SEP_CMA_ES) sc = __fmul_rn(gs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
         else sc = s.vec[F_SIGMA_D][idx];
         s.vec[F_BEST_X][idx] = __fmaf_rn(sgn * sc, zbv[k], mean);
       }
-      if (ALGO == OPENAI_ES) {
+      if (ALGO == ARS) {
+        // ARS V1: mean −= α/(k σ_R) · Σ_sel (f+ − f−) z; no step when σ_R = 0
+        if (gs.ars_scale != 0.0f) mean = __fsub_rn(mean, __fmul_rn(gs.ars_scale, (float)G0[k]));
+      } else if (ALGO == OPENAI_ES) {
         const float g = __fdiv_rn((float)G0[k], __fmul_rn((float)s.N, gs.sigma));
-        adam_step(mean, s.vec[F_ADAM_M][idx], s.vec[F_ADAM_V][idx], g, rs, gs);
+        opt_step(s, r, d, idx, mean, g, rs, gs, norm2);
       } else if (ALGO == PGPE) {
         const float sig = s.vec[F_SIGMA_D][idx];
         const float gm = __fdiv_rn(__fmul_rn(sig, (float)G0[k]), (float)s.N);
         const float gsg = __fdiv_rn(__fmul_rn(sig, (float)G1[k]), (float)(s.N / 2));
-        adam_step(mean, s.vec[F_ADAM_M][idx], s.vec[F_ADAM_V][idx], gm, rs, gs);
+        opt_step(s, r, d, idx, mean, gm, rs, gs, norm2);
         const float mc = rs.sigma_max_change;
         float st = __fsub_rn(sig, __fmul_rn(rs.sigma_lrate, gsg));
         const float lo = __fmul_rn(__fsub_rn(1.0f, mc), sig);
@@ -146,7 +167,8 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
       s.vec[F_MEAN][idx] = mean;
     }
   }
-  if (ALGO == SEP_CMA_ES) {
+  // block-uniform: one run per block
+  if (ALGO == SEP_CMA_ES || ((ALGO == OPENAI_ES || ALGO == PGPE) && rs.optimizer == OPT_CLIPUP)) {
     const double tot = block_sum_tt(norm2, red);
     if (threadIdx.x == 0) s.normpart[(int64_t)r * bpr + qb] = tot;
   }
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
       for (int k = 0; k < 4; ++k) {
         if (4 * q + k < s.D) {
           P[4 * q + k] = acc.a[k];
-          if (ALGO != OPENAI_ES) P[s.D + 4 * q + k] = acc.b[k];
+          if (ALGO != OPENAI_ES && ALGO != ARS) P[s.D + 4 * q + k] = acc.b[k];
         }
       }
     }
@@ -232,7 +254,8 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
         for (int k = 0; k < 4; ++k) {
           if (4 * q + k < s.D) {
             acc.a[k] = __dadd_rn(acc.a[k], __ldcg(P + 4 * q + k));
-            if (ALGO != OPENAI_ES) acc.b[k] = __dadd_rn(acc.b[k], __ldcg(P + s.D + 4 * q + k));
+            if (ALGO != OPENAI_ES && ALGO != ARS)
+              acc.b[k] = __dadd_rn(acc.b[k], __ldcg(P + s.D + 4 * q + k));
           }
         }
       }
@@ -245,7 +268,7 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
     for (int k = 0; k < 4; ++k) {
       if (4 * q + k < s.D) {
         s.G[gidx(s, 0, r, 4 * q + k)] = acc.a[k];
-        if (ALGO != OPENAI_ES) s.G[gidx(s, 1, r, 4 * q + k)] = acc.b[k];
+        if (ALGO != OPENAI_ES && ALGO != ARS) s.G[gidx(s, 1, r, 4 * q + k)] = acc.b[k];
       }
     }
   }
@@ -265,26 +288,33 @@ __global__ void __launch_bounds__(TT) update_kernel(DevState s, int bpr) {
     for (int k = 0; k < 4; ++k) {
       if (4 * q + k < s.D) {
         G0[k] = s.G[gidx(s, 0, r, 4 * q + k)];
-        if (ALGO != OPENAI_ES) G1[k] = s.G[gidx(s, 1, r, 4 * q + k)];
+        if (ALGO != OPENAI_ES && ALGO != ARS) G1[k] = s.G[gidx(s, 1, r, 4 * q + k)];
       }
     }
   }
   apply_update<ALGO>(s, r, q, active, G0, G1, qb, bpr, red);
 }
 
-// Sep-CMA-ES phase 2: global ‖p_σ'‖ (fixed-order sum of the block partials), σ', h_σ.
-__global__ void sepcma_norm_kernel(DevState s, int bpr) {
-  __shared__ double red[32];
-  const int r = blockIdx.x;
+// Fixed-order sum of run r's per-block norm partials (valid in thread 0).
+__device__ __forceinline__ double normpart_total(const DevState& s, int r, int bpr, double* red) {
   double v = 0.0;
   for (int b = threadIdx.x; b < bpr; b += blockDim.x) v = __dadd_rn(v, s.normpart[(int64_t)r * bpr + b]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double n2 = 0.0;
+  double n2 = 0.0;
+  if (threadIdx.x == 0)
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) n2 = __dadd_rn(n2, red[k]);
+  return n2;
+}
+
+// Sep-CMA-ES phase 2: global ‖p_σ'‖ (fixed-order sum of the block partials), σ', h_σ.
+__global__ void sepcma_norm_kernel(DevState s, int bpr) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  const double n2 = normpart_total(s, r, bpr, red);
+  if (threadIdx.x == 0) {
     RunScal& rs = s.rs[r];
     GenScal& gs = s.gs[r];
     const double norm = sqrt(n2);
@@ -323,6 +353,62 @@ __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
                               __fmul_rn(cmuf, __fmul_rn(C0, Qv)));
 }
 
+// ClipUp (Toklu et al. 2020), phases after the gradient g is parked in s.G:
+//   norm(0): inv = 1/‖g‖ (0 if ‖g‖ = 0)      vel: v' = μ v + lr (g · inv), ‖v'‖² partials
+//   norm(1): clip = max_speed/‖v'‖ if ‖v'‖ > max_speed else 1      apply: v = v' clip, m −= v.
+// Runs using another optimizer skip every phase.
+__global__ void clipup_norm_kernel(DevState s, int bpr, int phase) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  if (s.rs[r].optimizer != OPT_CLIPUP) return;
+  const double n2 = normpart_total(s, r, bpr, red);
+  if (threadIdx.x == 0) {
+    const double n = sqrt(n2);
+    GenScal& gs = s.gs[r];
+    if (phase == 0) {
+      gs.clip_inv = n > 0.0 ? (float)(1.0 / n) : 0.0f;
+    } else {
+      const double ms = (double)s.rs[r].max_speed;
+      gs.clip_inv = n > ms ? (float)(ms / n) : 1.0f;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TT) clipup_vel_kernel(DevState s, int bpr) {
+  __shared__ double red[TT / 32];
+  const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
+  const RunScal& rs = s.rs[r];
+  if (rs.optimizer != OPT_CLIPUP) return;              // block-uniform
+  const GenScal& gs = s.gs[r];
+  const int64_t q = (int64_t)qb * TT + threadIdx.x;
+  double v2 = 0.0;
+  if (q < s.Q) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t d = 4 * q + k;
+      if (d >= s.D) break;
+      const int64_t idx = (int64_t)r * s.D + d;
+      const float g = (float)s.G[gidx(s, 0, r, d)];
+      const float vn = __fmaf_rn(rs.momentum, s.vec[F_ADAM_M][idx],
+                                 __fmul_rn(gs.lr, __fmul_rn(g, gs.clip_inv)));
+      s.vec[F_ADAM_M][idx] = vn;
+      v2 = __dadd_rn(v2, __dmul_rn((double)vn, (double)vn));
+    }
+  }
+  const double tot = block_sum_tt(v2, red);
+  if (threadIdx.x == 0) s.normpart[(int64_t)r * bpr + qb] = tot;
+}
+
+__global__ void __launch_bounds__(256) clipup_apply_kernel(DevState s) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)s.R * s.D) return;
+  const int r = (int)(gid / s.D);
+  if (s.rs[r].optimizer != OPT_CLIPUP) return;
+  const float v = __fmul_rn(s.vec[F_ADAM_M][gid], s.gs[r].clip_inv);
+  s.vec[F_ADAM_M][gid] = v;
+  s.vec[F_MEAN][gid] = __fsub_rn(s.vec[F_MEAN][gid], v);
+}
+
 int tell_blocks_per_run(const DevState& s) { return (int)((s.Q + TT - 1) / TT); }
 
 // Entry-range split: choose n minimising waves(n) · (entries/n + c0), waves(n) = ⌈blocks·n / slots⌉,
@@ -335,7 +421,7 @@ static int pick_nchunk_t(const DevState& s) {
   occ = std::max(occ, 1);
   const int64_t slots = (int64_t)sm_count() * occ;
   const int64_t blocks = (int64_t)s.R * tell_blocks_per_run(s);
-  int ent = (s.algo == OPENAI_ES || s.algo == PGPE ? s.N / 2 : s.N);
+  int ent = (is_anti(s.algo) ? s.N / 2 : s.N);
   ent = std::max(1, (ent + s.W - 1) / s.W);
   const double c0 = 8.0;
   int best = 1;
@@ -353,6 +439,7 @@ int tell_pick_nchunk(const DevState& s) {
     case OPENAI_ES: return pick_nchunk_t<OPENAI_ES>(s);
     case PGPE: return pick_nchunk_t<PGPE>(s);
     case SNES: return pick_nchunk_t<SNES>(s);
+    case ARS: return pick_nchunk_t<ARS>(s);
     default: return pick_nchunk_t<SEP_CMA_ES>(s);
   }
 }
@@ -369,6 +456,7 @@ cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaSt
     case OPENAI_ES: launch_tell_t<OPENAI_ES>(s, fused, nchunk, st); break;
     case PGPE: launch_tell_t<PGPE>(s, fused, nchunk, st); break;
     case SNES: launch_tell_t<SNES>(s, fused, nchunk, st); break;
+    case ARS: launch_tell_t<ARS>(s, fused, nchunk, st); break;
     default: launch_tell_t<SEP_CMA_ES>(s, fused, nchunk, st); break;
   }
   return cudaGetLastError();
@@ -381,6 +469,7 @@ cudaError_t launch_tell_update(const DevState& s, cudaStream_t st) {
     case OPENAI_ES: update_kernel<OPENAI_ES><<<g, TT, 0, st>>>(s, bpr); break;
     case PGPE: update_kernel<PGPE><<<g, TT, 0, st>>>(s, bpr); break;
     case SNES: update_kernel<SNES><<<g, TT, 0, st>>>(s, bpr); break;
+    case ARS: update_kernel<ARS><<<g, TT, 0, st>>>(s, bpr); break;
     default: update_kernel<SEP_CMA_ES><<<g, TT, 0, st>>>(s, bpr); break;
   }
   return cudaGetLastError();
@@ -392,6 +481,17 @@ cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk) {
   const int64_t n = (int64_t)s.R * s.D;
   sepcma_pc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
   if (nk) *nk = 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk) {
+  const int bpr = tell_blocks_per_run(s);
+  const int64_t n = (int64_t)s.R * s.D;
+  clipup_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr, 0);
+  clipup_vel_kernel<<<(unsigned)(s.R * bpr), TT, 0, st>>>(s, bpr);
+  clipup_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr, 1);
+  clipup_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
+  if (nk) *nk = 4;
   return cudaGetLastError();
 }
 

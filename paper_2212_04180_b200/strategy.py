@@ -16,7 +16,8 @@ from ._lib import FIELDS, RunParams, check, lib
 DEFAULT_PARAMS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=1.0,
                       sigma_limit=0.0, lrate_init=0.01, lrate_decay=1.0, lrate_limit=0.0,
                       beta1=0.9, beta2=0.999, eps=1e-8, sigma_lrate=0.2, sigma_max_change=0.2,
-                      temperature=12.0, elite_ratio=0.5, shaping=0)
+                      temperature=12.0, elite_ratio=0.5, shaping=0, optimizer=0,
+                      momentum=0.9, max_speed=0.02)
 
 
 def _ptr(t):

@@ -14,7 +14,10 @@ KEPT = {
     W.PGPE: ["mean", "sigma_d", "adam_m", "adam_v", "best_x"],
     W.SNES: ["mean", "sigma_d", "best_x"],
     W.SEP_CMA_ES: ["mean", "p_sigma", "p_c", "C", "best_x"],
+    W.ARS: ["mean", "best_x"],
 }
+HAS_SIGMA = (W.OPENAI_ES, W.SEP_CMA_ES, W.ARS)
+HAS_LRATE = (W.OPENAI_ES, W.PGPE, W.ARS)
 
 
 def q24(a, b):
@@ -45,9 +48,9 @@ class Pair:
     def gpu_state(self, r):
         st = {f: self.gpu.get(f)[r].cpu().numpy() for f in KEPT[self.algo]}
         st["best_f"] = float(self.gpu.get("best_f")[r])
-        if self.algo in (W.OPENAI_ES, W.SEP_CMA_ES):
+        if self.algo in HAS_SIGMA:
             st["sigma"] = float(self.gpu.get("sigma")[r])
-        if self.algo in (W.OPENAI_ES, W.PGPE):
+        if self.algo in HAS_LRATE:
             st["lrate"] = float(self.gpu.get("lrate")[r])
         st["gen"] = int(self.gpu.get("gen")[r])
         if self.dims is not None:
@@ -59,9 +62,9 @@ class Pair:
         o = self.orc[r]
         st = {f: o.vec[VEC_FIELDS.index(f)].copy() for f in KEPT[self.algo]}
         st["best_f"] = float(o.best_f)
-        if self.algo in (W.OPENAI_ES, W.SEP_CMA_ES):
+        if self.algo in HAS_SIGMA:
             st["sigma"] = float(o.sigma)
-        if self.algo in (W.OPENAI_ES, W.PGPE):
+        if self.algo in HAS_LRATE:
             st["lrate"] = float(o.lr)
         st["gen"] = int(o.t)
         return st
