@@ -248,12 +248,34 @@ void orc_member(const orc_run_t *r, int32_t j, float *x) {
     }
     if (neg) s = -s;
     x[d] = fmaf(s, z[d], mean[d]);
+    /* box bounds: only the asked member is clipped, the distribution is not truncated */
+    x[d] = fminf(fmaxf(x[d], r->p.clip_min), r->p.clip_max);
   }
   free(z);
 }
 
 void orc_ask(const orc_run_t *r, float *x) {
   for (int32_t j = 0; j < r->popsize; ++j) orc_member(r, j, x + (int64_t)j * r->num_dims);
+}
+
+/* Weight-decay regularisation ("weight decay regularization"): the penalty
+ * coef * ||x_j||_2^2 is added to the minimised fitness, ||x||^2 summed in binary64 in d order. */
+void orc_weight_decay(const float *f, const float *x, int32_t n, int64_t D, float coef, float *out) {
+  for (int32_t j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int64_t d = 0; d < D; ++d) s += (double)x[j * D + d] * (double)x[j * D + d];
+    out[j] = (float)((double)f[j] + (double)coef * s);
+  }
+}
+
+void orc_run_weight_decay(const orc_run_t *r, const float *f, float *out) {
+  const int64_t D = r->num_dims;
+  float *x = (float *)malloc(sizeof(float) * (size_t)D);
+  for (int32_t j = 0; j < r->popsize; ++j) {
+    orc_member(r, j, x);
+    orc_weight_decay(f + j, x, 1, D, r->p.weight_decay, out + j);
+  }
+  free(x);
 }
 
 /* ---------------- N7 fitness ---------------- */
@@ -367,6 +389,7 @@ void orc_zscore(const float *f, int32_t N, float *out) {
  * sorted positions (through the end of the tie group containing position mu-1). */
 /* ARS (Mania et al. 2018): k = max(1, round(elite_ratio * P)) directions with
  * the best min(f+, f-), ordered by (key(min), index). */
+/* PGPE uses the same rule for its elite pairs (Q13: elite_ratio 1.0 keeps every pair). */
 static int ars_k(const orc_run_t *r) {
   int P = r->popsize / 2;
   int k = (int)floor((double)r->p.elite_ratio * (double)P + 0.5);
@@ -398,7 +421,7 @@ static double ars_sigma_r(const orc_run_t *r, const float *f, const int32_t *sel
 }
 
 int orc_num_entries(const orc_run_t *r, const float *f) {
-  if (r->algo == ORC_ARS) return ars_k(r);
+  if (r->algo == ORC_ARS || r->algo == ORC_PGPE) return ars_k(r);
   if (is_antithetic(r->algo)) return r->popsize / 2;
   if (r->algo == ORC_SNES) return r->popsize;
   int32_t N = r->popsize;
@@ -444,7 +467,16 @@ void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1
     double bbar = 0.0;
     for (int32_t j = 0; j < N; ++j) bbar += (double)sh[j];
     bbar = bbar / N;
-    for (int32_t i = e0; i < e1; ++i) {
+    /* PGPE elite pairs (reading Q13b): with k = round(elite_ratio P) < P the entries are the k
+     * pairs ARS would select (by key(min(f+, f-)), then pair index), in that order; k = P keeps
+     * every pair in index order. The shaping and the baseline use the whole population. */
+    int32_t *sel = NULL;
+    if (r->algo == ORC_PGPE && ars_k(r) < N / 2) {
+      sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)ars_k(r));
+      ars_select(r, f, sel);
+    }
+    for (int32_t q = e0; q < e1; ++q) {
+      int32_t i = sel ? sel[q] : q;
       double a = (double)sh[2 * i] - (double)sh[2 * i + 1];
       double h = ((double)sh[2 * i] + (double)sh[2 * i + 1]) * 0.5 - bbar;
       run_direction(r, (uint32_t)i, r->t, z);
@@ -453,6 +485,7 @@ void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1
         if (r->algo == ORC_PGPE) G1[d] += h * ((double)z[d] * (double)z[d] - 1.0);
       }
     }
+    free(sel);
   } else {
     int32_t *s = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
     int32_t *e = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
@@ -500,7 +533,20 @@ static void adam(orc_run_t *r, int64_t d, float g, float bc1, float bc2) {
   mean[d] = mean[d] - r->lr * ((mn / bc1) / (sqrtf(vn / bc2) + r->p.eps));
 }
 
+static int tell_impl(orc_run_t *r, const float *f);
+
+/* Weight decay (when set) is the first step of tell: every later step — best tracking included
+ * (reading R-WD) — sees f_j + weight_decay ||x_j||^2. */
 int orc_tell(orc_run_t *r, const float *f) {
+  if (r->p.weight_decay == 0.0f) return tell_impl(r, f);
+  float *fw = (float *)malloc(sizeof(float) * (size_t)r->popsize);
+  orc_run_weight_decay(r, f, fw);
+  int rc = tell_impl(r, fw);
+  free(fw);
+  return rc;
+}
+
+static int tell_impl(orc_run_t *r, const float *f) {
   const int64_t D = r->num_dims;
   const int32_t N = r->popsize;
   const int32_t P = orc_num_directions(r);
@@ -547,9 +593,10 @@ int orc_tell(orc_run_t *r, const float *f) {
       if (r->algo == ORC_OPENAI_ES) {
         gm[d] = (float)G0[d] / ((float)N * r->sigma);
       } else {
+        /* PGPE normalises by the 2k members / k pairs it used (k = P: N and P) */
         float sig = sd[d];
-        gm[d] = (sig * (float)G0[d]) / (float)N;
-        float gs = (sig * (float)G1[d]) / (float)P;
+        gm[d] = (sig * (float)G0[d]) / (float)(2 * ars_k(r));
+        float gs = (sig * (float)G1[d]) / (float)ars_k(r);
         float mc = r->p.sigma_max_change;
         float st = sig - r->p.sigma_lrate * gs;
         float lo = (1.0f - mc) * sig, hi = (1.0f + mc) * sig;

@@ -33,11 +33,13 @@ typedef struct {
   float beta1, beta2, eps;
   float sigma_lrate, sigma_max_change;
   float temperature;
-  float elite_ratio;
+  float elite_ratio;   /* Sep-CMA elite; ARS / PGPE fraction of pairs kept (PGPE 1.0 = all) */
   int32_t shaping; /* 0 centered rank, 1 raw fitness, 2 z-score (OpenAI-ES/PGPE) */
   int32_t optimizer;   /* 0 Adam, 1 SGD with momentum, 2 ClipUp (OpenAI-ES/PGPE) */
   float momentum;      /* SGD / ClipUp momentum */
   float max_speed;     /* ClipUp velocity clip */
+  float weight_decay;  /* fitness += weight_decay * ||x_j||^2 at tell */
+  float clip_min, clip_max; /* box bounds applied to the asked members */
 } orc_params_t;
 
 typedef struct {
@@ -80,6 +82,10 @@ int orc_init(orc_run_t *r);
 int orc_num_directions(const orc_run_t *r);
 void orc_ask(const orc_run_t *r, float *x /* [N][D] */);
 void orc_member(const orc_run_t *r, int32_t j, float *x /* [D] */);
+/* weight-decay regularisation: out_j = f_j + coef ||x_j||^2 for n rows x */
+void orc_weight_decay(const float *f, const float *x, int32_t n, int64_t D, float coef, float *out);
+/* the same for the run's current members (regenerated); out may alias f */
+void orc_run_weight_decay(const orc_run_t *r, const float *f, float *out);
 
 /* N7 fitness */
 void orc_eval(int32_t fn, const float *x, int32_t n, int64_t D, float *f);

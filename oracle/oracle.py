@@ -40,7 +40,8 @@ class Params(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("sigma_lrate", C.c_float), ("sigma_max_change", C.c_float),
                 ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32),
-                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float)]
+                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float),
+                ("weight_decay", C.c_float), ("clip_min", C.c_float), ("clip_max", C.c_float)]
 
 
 class RunT(C.Structure):
@@ -87,6 +88,8 @@ def lib():
             "orc_reduce_range": (None, [C.POINTER(RunT), fp, C.c_int32, C.c_int32, dp]),
             "orc_num_entries": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_tell": (C.c_int, [C.POINTER(RunT), fp]),
+            "orc_weight_decay": (None, [fp, fp, C.c_int32, C.c_int64, C.c_float, fp]),
+            "orc_run_weight_decay": (None, [C.POINTER(RunT), fp, fp]),
             "orc_synth_fitness": (None, [C.c_uint64, C.c_uint32, C.c_int32, fp]),
             "orc_fp16": (C.c_float, [C.c_float]),
             "orc_mlp_create": (C.c_void_p, [i32p, C.c_int32, C.c_int32, C.c_uint64]),
@@ -167,6 +170,15 @@ def centered_rank(f):
     return c
 
 
+def weight_decay(f, x, coef):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(f.size, -1)
+    out = np.empty_like(f)
+    lib().orc_weight_decay(_p(f, C.c_float), _p(x, C.c_float), f.size, x.shape[1], coef,
+                           _p(out, C.c_float))
+    return out
+
+
 def zscore(f):
     f = np.ascontiguousarray(f, dtype=np.float32)
     out = np.empty_like(f)
@@ -201,7 +213,9 @@ def synth_fitness(seed, t, N):
 DEFAULTS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=0.999, sigma_limit=0.01,
                 lrate_init=0.01, lrate_decay=0.999, lrate_limit=0.001, beta1=0.9, beta2=0.999,
                 eps=1e-8, sigma_lrate=0.2, sigma_max_change=0.2, temperature=12.0,
-                elite_ratio=0.5, shaping=0, optimizer=0, momentum=0.9, max_speed=0.02)
+                elite_ratio=0.5, shaping=0, optimizer=0, momentum=0.9, max_speed=0.02,
+                weight_decay=0.0, clip_min=-np.inf, clip_max=np.inf)
+PGPE_ELITE_DEFAULT = 1.0     # Q13: App. B has no PGPE elite ratio; every pair is kept
 
 
 class Run:
@@ -210,6 +224,8 @@ class Run:
     def __init__(self, algo, popsize, num_dims, seed=0, dims=None, **params):
         """dims: optional sorted global dimension indices (num_dims is then the full D)."""
         kw = dict(DEFAULTS)
+        if algo == PGPE:
+            kw["elite_ratio"] = PGPE_ELITE_DEFAULT
         kw.update(params)
         full = num_dims
         if dims is not None:
@@ -276,6 +292,13 @@ class Run:
     def tell(self, f):
         f = np.ascontiguousarray(f, dtype=np.float32)
         lib().orc_tell(C.byref(self.r), _p(f, C.c_float))
+
+    def weight_decay(self, f):
+        """f_j + weight_decay ||x_j||^2 for the current members (what tell ranks)."""
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        out = np.empty_like(f)
+        lib().orc_run_weight_decay(C.byref(self.r), _p(f, C.c_float), _p(out, C.c_float))
+        return out
 
 
 class MLP:

@@ -21,7 +21,7 @@ ANT = {
                     lrate_init=0.01, lrate_decay=0.999, lrate_limit=0.001),
     PGPE: dict(sigma_init=0.025, sigma_decay=0.999, sigma_limit=0.01,
                lrate_init=0.01, lrate_decay=0.999, lrate_limit=0.001,
-               sigma_lrate=0.2, sigma_max_change=0.2),
+               sigma_lrate=0.2, sigma_max_change=0.2, elite_ratio=1.0),   # Q13: every pair
     SNES: dict(sigma_init=0.05, temperature=12.0),
     SEP_CMA_ES: dict(sigma_init=0.05, elite_ratio=0.4),
     # ARS has no App. B column (Table 1 row only): OpenAI-ES-like schedules, top-50 % pairs
@@ -35,7 +35,8 @@ SNES_COLUMNS = [(0.05, 12.0), (0.075, 12.0), (0.05, 16.0), (0.075, 32.0)]   # P:
 BASE = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=1.0, sigma_limit=0.0,
             lrate_init=0.01, lrate_decay=1.0, lrate_limit=0.0, beta1=0.9, beta2=0.999, eps=1e-8,
             sigma_lrate=0.2, sigma_max_change=0.2, temperature=12.0, elite_ratio=0.5, shaping=0,
-            optimizer=0, momentum=0.9, max_speed=0.02)
+            optimizer=0, momentum=0.9, max_speed=0.02, weight_decay=0.0, clip_min=-np.inf,
+            clip_max=np.inf)
 
 
 def run_params(algo, seed, **over):
