@@ -71,13 +71,20 @@ typedef struct {
   float sigma_lrate;          /* PGPE σ learning rate: 0.2                              */
   float sigma_max_change;     /* PGPE relative σ clip: 0.2                              */
   float temperature;          /* SNES β                                          */
-  float elite_ratio;          /* Sep-CMA-ES μ = ⌊elite_ratio·N⌋                         */
+  float elite_ratio;          /* Sep-CMA-ES μ = ⌊elite_ratio·N⌋; ARS / PGPE keep
+                                 k = max(1, round(elite_ratio·N/2)) pairs of best min(f+, f−)
+                                 (PGPE 1.0 = every pair, DESIGN reading Q13b), in (0, 1] */
   int32_t shaping;            /* 0 = centered rank; 1 = raw fitness; 2 = z-score
                                  (P:213). OpenAI-ES / PGPE only (ARS always uses raw fitness)    */
   int32_t optimizer;          /* es_optimizer_t for the mean of OpenAI-ES / PGPE: Adam,
                                  SGD with momentum, ClipUp                               */
   float momentum;             /* SGD / ClipUp momentum (0.9)                                     */
   float max_speed;            /* ClipUp velocity norm limit (2·lrate)                            */
+  float weight_decay;         /* ≥ 0: tell ranks f_j + weight_decay·‖x_j‖² ("weight decay
+                                 regularization"; every algorithm; best tracking included)      */
+  float clip_min, clip_max;   /* box bounds: asked members are clipped into
+                                 [clip_min, clip_max]; the distribution is not truncated (the
+                                 tell regenerates the unclipped z). ±INFINITY = unbounded        */
 } es_run_params_t;
 
 /* Fields readable with es_get / writable with es_set (checkpoint / resume). Shapes per context. */
@@ -166,6 +173,15 @@ es_status_t es_tell(es_ctx_t *ctx, const float *fitness, es_stream_t stream);
  * out of order (ask → local → apply). */
 es_status_t es_tell_local(es_ctx_t *ctx, const float *fitness_all, es_stream_t stream);
 es_status_t es_tell_apply(es_ctx_t *ctx, es_stream_t stream);
+
+/* Weight-decay regularisation of this rank's fitness slice:
+ * out[r][j] = (float)((double)fitness[r][j] + (double)weight_decay_r · Σ_d (double)x_jd²) for the
+ * members x_j of the current (asked, not yet told) generation, regenerated from the noise counter
+ * (x is not an input); out = fitness where weight_decay_r = 0. es_tell applies it itself; callers
+ * of the split-phase tell apply it to their slice BEFORE gathering. fitness / out: float [R][N/W],
+ * host or device, may alias. Errors: ES_ERR_BAD_STATE outside ask → tell; ES_ERR_INVALID_ARG for
+ * NULL pointers. */
+es_status_t es_weight_decay(es_ctx_t *ctx, const float *fitness, float *out, es_stream_t stream);
 
 /* Population-sharding plan: for a population of `popsize` over world_size ranks and
  * `entries` weighted tell entries (P directions, or Sep-CMA-ES's weighted positions), write

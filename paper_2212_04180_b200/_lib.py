@@ -23,7 +23,7 @@ EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "
            "es_set_mlp_problem", "es_mlp_num_params", "es_shape", "es_kernel_launches",
            "es_destroy", "es_last_error", "es_status_string", "es_nccl_unique_id_size",
            "es_nccl_get_unique_id", "es_debug_primitive", "es_profile_enable", "es_profile_read",
-           "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval"]
+           "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay"]
 
 
 class RunParams(C.Structure):
@@ -34,7 +34,8 @@ class RunParams(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("sigma_lrate", C.c_float), ("sigma_max_change", C.c_float),
                 ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32),
-                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float)]
+                ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float),
+                ("weight_decay", C.c_float), ("clip_min", C.c_float), ("clip_max", C.c_float)]
 
 
 class ESError(RuntimeError):
@@ -78,6 +79,7 @@ def lib():
         "es_tell_local": (i32, [vp, vp, vp]),
         "es_ask_eval": (i32, [vp, i32, vp, vp, vp]),
         "es_tell_apply": (i32, [vp, vp]),
+        "es_weight_decay": (i32, [vp, vp, vp, vp]),
         "es_shard_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
         "es_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(i64), i32]),
     }

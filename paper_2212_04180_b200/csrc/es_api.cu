@@ -48,6 +48,8 @@ struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
   bool any_clipup = false;
+  bool any_wd = false;
+  float* wdbuf = nullptr;       // [R][Nloc] weight-decayed fitness
   ncclComm_t comm = nullptr;
   bool asked = false;
   bool told_local = false;
@@ -263,13 +265,18 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: SGD/ClipUp only for OpenAI-ES/PGPE", r);
     if (p.optimizer == ES_OPT_CLIPUP && !(p.max_speed > 0.0f))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: ClipUp needs max_speed > 0", r);
-    if (algo == ES_ARS && !(p.elite_ratio > 0.0f && p.elite_ratio <= 1.0f))
-      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: ARS elite_ratio must be in (0, 1]", r);
+    if ((algo == ES_ARS || algo == ES_PGPE) && !(p.elite_ratio > 0.0f && p.elite_ratio <= 1.0f))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: ARS/PGPE elite_ratio must be in (0, 1]", r);
+    if (!(p.weight_decay >= 0.0f) || std::isinf(p.weight_decay))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: weight_decay must be finite and >= 0", r);
+    if (!(p.clip_min <= p.clip_max))
+      return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: need clip_min <= clip_max", r);
   }
   es_ctx* c = new (std::nothrow) es_ctx();
   if (!c) return fail(nullptr, ES_ERR_OOM, "host allocation failed");
   DevState& s = c->s;
   s.algo = algo; s.R = R; s.N = N; s.W = W; s.rank = rank; s.Nloc = N / W; s.D = D;
+  s.any_clip = 0;
   s.Q = (D + 3) / 4;
   s.P = antithetic(algo) ? N / 2 : N;
   auto bail = [&](es_status_t e) { std::string m = c->err; es_destroy(c); g_err = m; return e; };
@@ -329,7 +336,11 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
     rs.beta1 = p.beta1; rs.beta2 = p.beta2; rs.eps = p.eps;
     rs.sigma_lrate = p.sigma_lrate; rs.sigma_max_change = p.sigma_max_change;
     rs.optimizer = p.optimizer; rs.momentum = p.momentum; rs.max_speed = p.max_speed;
-    if (algo == ES_ARS) {   // k = max(1, round(elite_ratio · P)), P = N/2
+    rs.weight_decay = p.weight_decay; rs.clip_lo = p.clip_min; rs.clip_hi = p.clip_max;
+    rs.clip = std::isfinite(p.clip_min) || std::isfinite(p.clip_max);
+    if (rs.clip) s.any_clip = 1;
+    if (p.weight_decay != 0.0f) c->any_wd = true;
+    if (algo == ES_ARS || algo == ES_PGPE) {   // k = max(1, round(elite_ratio · P)), P = N/2
       const int P = N / 2;
       rs.ars_k = std::max(1, std::min(P, (int)std::floor((double)p.elite_ratio * (double)P + 0.5)));
     }
@@ -577,6 +588,8 @@ static const float* stage_fitness(es_ctx* c, const float* f, size_t n, cudaStrea
   return *buf;
 }
 
+static es_status_t weight_decay_impl(es_ctx* c, const float* fd, float* out, cudaStream_t st);
+
 es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !fitness) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
@@ -589,6 +602,10 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   es_status_t err;
   const float* fl = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
   if (!fl) return err;
+  if (c->any_wd) {   // weight decay on this rank's slice before anything sees it
+    if ((err = weight_decay_impl(c, fl, nullptr, st)) != ES_SUCCESS) return err;
+    fl = c->wdbuf;
+  }
   const bool fused = s.W == 1;
   const float* fsrc = fl;
   if (s.W > 1) {   // a5: every rank obtains all N fitness values
@@ -604,6 +621,39 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   }
   if ((err = tell_apply_impl(c, fused, st)) != ES_SUCCESS) return err;
   c->asked = false;
+  return ES_SUCCESS;
+}
+
+// out == nullptr: into c->wdbuf.
+static es_status_t weight_decay_impl(es_ctx* c, const float* fd, float* out, cudaStream_t st) {
+  const DevState& s = c->s;
+  const size_t nloc = (size_t)s.R * s.Nloc;
+  if (!c->aepart)
+    CUDA_OR(c, dalloc(c, (void**)&c->aepart, nloc * ask_eval_blocks_per_run(s) * sizeof(double)));
+  if (!out) {
+    if (!c->wdbuf) CUDA_OR(c, dalloc(c, (void**)&c->wdbuf, nloc * sizeof(float)));
+    out = c->wdbuf;
+  }
+  ProfScope ps(c, "weight_decay", st);
+  CUDA_OR(c, launch_weight_decay(s, c->aepart, fd, out, st));
+  c->launches += 2;
+  return ES_SUCCESS;
+}
+
+es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c || !fitness || !out) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_weight_decay needs an asked generation");
+  const size_t nloc = (size_t)c->s.R * c->s.Nloc;
+  es_status_t err;
+  const float* fd = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
+  if (!fd) return err;
+  const bool oh = !is_device_ptr(out);
+  if ((err = weight_decay_impl(c, fd, oh ? nullptr : out, st)) != ES_SUCCESS) return err;
+  if (oh) {
+    CUDA_OR(c, cudaMemcpyAsync(out, c->wdbuf, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CUDA_OR(c, cudaStreamSynchronize(st));
+  }
   return ES_SUCCESS;
 }
 

@@ -35,8 +35,10 @@ struct alignas(16) RunScal {
   float init_min, init_max, sigma_init, sigma_decay, sigma_limit, lrate_decay, lrate_limit;
   float beta1, beta2, eps, sigma_lrate, sigma_max_change;
   double c_sigma, d_sigma, c_c, c_1, c_mu, chi_d, mueff, eta_sigma;
-  int32_t optimizer, ars_k;
+  int32_t optimizer, ars_k;      // ars_k: elite pairs k of ARS / PGPE (P when every pair is kept)
   float momentum, max_speed;
+  float weight_decay, clip_lo, clip_hi;
+  int32_t clip;                   // clip_lo or clip_hi finite
 };
 
 struct alignas(16) GenScal {
@@ -55,6 +57,7 @@ struct alignas(16) GenScal {
 
 struct DevState {
   int algo, R, N, Nloc, W, rank;
+  int any_clip;        // some run has box bounds (selects the clipping ask instances)
   int64_t D, Q;        // Q = ceil(D/4) quads
   int P;               // global directions
   float* vec[NVEC];
@@ -101,6 +104,9 @@ cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaSt
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
 cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
+// f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)
+cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,
+                                cudaStream_t st);
 int tell_blocks_per_run(const DevState& s);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;

@@ -61,7 +61,9 @@ __device__ __forceinline__ float ask_scale(const DevState& s, const RunScal& rs,
 }
 
 // W16: also write fp16(x) into x16 (N14′, the MLP fitness's parameter image); x may be NULL then.
-template <int ALGO, bool V4, bool W16>
+// CLIP: clamp the members into the run's box [clip_lo, clip_hi] (the z the tell regenerates
+// is unclipped). Instantiated only when some run has bounds.
+template <int ALGO, bool V4, bool W16, bool CLIP>
 __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
                                                            __half* __restrict__ x16, int bpr,
                                                            int dpt) {
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
     sc[k] = ok ? ask_scale<ALGO>(s, rs, base + k) : 0.0f;
   }
   const int dir0 = s.rank * Ploc;
+  const float lo = CLIP ? rs.clip_lo : 0.0f, hi = CLIP ? rs.clip_hi : 0.0f;
   float* xr = x ? x + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
   __half* hr = W16 ? x16 + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
 #pragma unroll 2
@@ -96,6 +99,10 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
     for (int k = 0; k < 4; ++k) {
       xp[k] = __fmaf_rn(sc[k], zz[k], m[k]);
       if (kAnti) xm[k] = __fmaf_rn(-sc[k], zz[k], m[k]);
+      if (CLIP) {
+        xp[k] = fminf(fmaxf(xp[k], lo), hi);
+        if (kAnti) xm[k] = fminf(fmaxf(xm[k], lo), hi);
+      }
     }
     const int64_t row = kAnti ? 2 * (int64_t)il : il;
     if (W16) {            // D % 4 == 0 is required for this path (8-byte stores)
@@ -130,7 +137,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   }
 }
 
-template <int ALGO>
+template <int ALGO, bool CLIP>
 static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaStream_t st) {
   constexpr bool kAnti = is_anti(ALGO);
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
@@ -145,23 +152,28 @@ static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaSt
   nchunk = (Ploc + dpt - 1) / dpt;
   dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
   if (x16) {
-    ask_kernel<ALGO, true, true><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
+    ask_kernel<ALGO, true, true, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
     return cudaGetLastError();
   }
   const bool v4 = (s.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if (v4) ask_kernel<ALGO, true, false><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
-  else ask_kernel<ALGO, false, false><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
+  if (v4) ask_kernel<ALGO, true, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
+  else ask_kernel<ALGO, false, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
   return cudaGetLastError();
 }
 
-cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st) {
+template <bool CLIP>
+static cudaError_t launch_ask_c(const DevState& s, float* x, __half* x16, cudaStream_t st) {
   switch (s.algo) {
-    case OPENAI_ES: return launch_ask_t<OPENAI_ES>(s, x, x16, st);
-    case PGPE: return launch_ask_t<PGPE>(s, x, x16, st);
-    case SNES: return launch_ask_t<SNES>(s, x, x16, st);
-    case ARS: return launch_ask_t<ARS>(s, x, x16, st);
-    default: return launch_ask_t<SEP_CMA_ES>(s, x, x16, st);
+    case OPENAI_ES: return launch_ask_t<OPENAI_ES, CLIP>(s, x, x16, st);
+    case PGPE: return launch_ask_t<PGPE, CLIP>(s, x, x16, st);
+    case SNES: return launch_ask_t<SNES, CLIP>(s, x, x16, st);
+    case ARS: return launch_ask_t<ARS, CLIP>(s, x, x16, st);
+    default: return launch_ask_t<SEP_CMA_ES, CLIP>(s, x, x16, st);
   }
+}
+
+cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st) {
+  return s.any_clip ? launch_ask_c<true>(s, x, x16, st) : launch_ask_c<false>(s, x, x16, st);
 }
 
 cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {

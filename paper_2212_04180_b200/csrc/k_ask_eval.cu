@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
     scN = ae_scale<ALGO>(s, rs, base + 4);
   }
   const int dir0 = s.rank * Ploc;
+  const bool clip = rs.clip != 0;                     // box bounds, block-uniform
+  const float lo = rs.clip_lo, hi = rs.clip_hi;
   float* xr = x ? x + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
   for (int il = i0; il < i1; ++il) {
     const uint32_t dir = (uint32_t)(dir0 + il);
@@ -68,6 +70,10 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
     for (int k = 0; k < 4; ++k) {
       xv[0][k] = __fmaf_rn(sc[k], zz[k], m[k]);
       if (kAnti) xv[M - 1][k] = __fmaf_rn(-sc[k], zz[k], m[k]);
+      if (clip) {
+#pragma unroll
+        for (int h = 0; h < M; ++h) xv[h][k] = fminf(fmaxf(xv[h][k], lo), hi);
+      }
     }
     if (WX && active) {
       const int64_t row = kAnti ? 2 * (int64_t)il : il;
@@ -93,6 +99,10 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
         const float zN = normal4(ph, (uint32_t)(q + 1), dir, t).x;
         nx[0] = __fmaf_rn(scN, zN, mN);
         if (kAnti) nx[M - 1] = __fmaf_rn(-scN, zN, mN);
+        if (clip) {
+#pragma unroll
+          for (int h = 0; h < M; ++h) nx[h] = fminf(fmaxf(nx[h], lo), hi);
+        }
       }
     }
 #pragma unroll
@@ -129,6 +139,19 @@ __global__ void ae_finalize_kernel(const double* __restrict__ part, int64_t rows
   f[j] = (float)v;
 }
 
+// Weight decay: out_j = f_j + λ_r Σ_b part[j][b] (the member's ‖x_j‖², binary64).
+__global__ void wd_finalize_kernel(DevState s, const double* __restrict__ part, int bpr,
+                                   const float* f, float* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= (int64_t)s.R * s.Nloc) return;
+  const float wd = s.rs[j / s.Nloc].weight_decay;
+  const float fj = f[j];
+  if (wd == 0.0f) { out[j] = fj; return; }
+  double v = 0.0;
+  for (int b = 0; b < bpr; ++b) v = __dadd_rn(v, part[j * bpr + b]);
+  out[j] = (float)__dadd_rn((double)fj, __dmul_rn((double)wd, v));
+}
+
 int ask_eval_blocks_per_run(const DevState& s) { return (int)((s.Q + kAE - 1) / kAE); }
 
 template <int ALGO, int FN>
@@ -148,20 +171,43 @@ static void launch_ae_a(int fn, const DevState& s, float* x, double* part, dim3 
   else launch_ae_t<ALGO, FN_RASTRIGIN>(s, x, part, grid, bpr, dpt, st);
 }
 
-// Two kernels: the fused ask+evaluate and the per-member block sum.
-cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
-                            cudaStream_t st) {
+static dim3 ae_grid(const DevState& s, int& bpr, int& dpt) {
   const bool anti = is_anti(s.algo);
   const int Ploc = anti ? s.Nloc / 2 : s.Nloc;
-  const int bpr = ask_eval_blocks_per_run(s);
+  bpr = ask_eval_blocks_per_run(s);
   const int64_t quads = (int64_t)s.R * bpr * kAE;
   const int64_t want = (int64_t)sm_count() * 2048 * 4;
   int nchunk = (int)std::max<int64_t>(1, want / std::max<int64_t>(quads, 1));
   nchunk = std::max(nchunk, (Ploc + kMaxDpt - 1) / kMaxDpt);
   nchunk = std::min(nchunk, std::max(1, Ploc));
-  const int dpt = (Ploc + nchunk - 1) / nchunk;
+  dpt = (Ploc + nchunk - 1) / nchunk;
   nchunk = (Ploc + dpt - 1) / dpt;
-  const dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
+  return dim3((unsigned)(s.R * bpr), (unsigned)nchunk);
+}
+
+// ‖x_j‖² of the regenerated (clipped) members = the Sphere pass of the fused kernel without the
+// x write, then the weight-decay finalize.
+cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,
+                                cudaStream_t st) {
+  int bpr, dpt;
+  const dim3 grid = ae_grid(s, bpr, dpt);
+  switch (s.algo) {
+    case OPENAI_ES: launch_ae_t<OPENAI_ES, FN_SPHERE>(s, nullptr, part, grid, bpr, dpt, st); break;
+    case PGPE: launch_ae_t<PGPE, FN_SPHERE>(s, nullptr, part, grid, bpr, dpt, st); break;
+    case SNES: launch_ae_t<SNES, FN_SPHERE>(s, nullptr, part, grid, bpr, dpt, st); break;
+    case ARS: launch_ae_t<ARS, FN_SPHERE>(s, nullptr, part, grid, bpr, dpt, st); break;
+    default: launch_ae_t<SEP_CMA_ES, FN_SPHERE>(s, nullptr, part, grid, bpr, dpt, st); break;
+  }
+  const int64_t rows = (int64_t)s.R * s.Nloc;
+  wd_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(s, part, bpr, f, out);
+  return cudaGetLastError();
+}
+
+// Two kernels: the fused ask+evaluate and the per-member block sum.
+cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
+                            cudaStream_t st) {
+  int bpr, dpt;
+  const dim3 grid = ae_grid(s, bpr, dpt);
   switch (s.algo) {
     case OPENAI_ES: launch_ae_a<OPENAI_ES>(fn, s, x, part, grid, bpr, dpt, st); break;
     case PGPE: launch_ae_a<PGPE>(fn, s, x, part, grid, bpr, dpt, st); break;

@@ -106,7 +106,9 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     bbar = block_sum(part, red) / (double)N;
   }
   float ars_scale = 0.0f;
-  if (s.algo == ARS) {
+  // PGPE with elite pairs (k < N/2, reading Q13b) selects its entries with ARS's rule
+  const bool elite_sel = s.algo == ARS || (s.algo == PGPE && rs.ars_k < N / 2);
+  if (elite_sel) {
     // ARS: pairs ordered by (key(min(f+, f−)), pair index) = by the position of
     // their better member; pair i is "first seen" at p = min(pos(2i), pos(2i+1)). A block scan over
     // positions gives each first-seen pair its order; the first k are the elite directions.
@@ -135,22 +137,30 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
         if (idx < k) {
           const int i = perm[p] >> 1;
           dir[idx] = (uint32_t)i;
-          cA[idx] = __dsub_rn((double)fit[2 * i], (double)fit[2 * i + 1]);
-          psum = __dadd_rn(psum, __dadd_rn((double)fit[2 * i], (double)fit[2 * i + 1]));
+          if (s.algo == ARS) {         // raw differences; σ_R below
+            cA[idx] = __dsub_rn((double)fit[2 * i], (double)fit[2 * i + 1]);
+            psum = __dadd_rn(psum, __dadd_rn((double)fit[2 * i], (double)fit[2 * i + 1]));
+          } else {                     // PGPE: shaped coefficients, whole-population baseline
+            const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
+            cA[idx] = __dsub_rn(cp, cm);
+            cB[idx] = __dsub_rn(__dmul_rn(__dadd_rn(cp, cm), 0.5), bbar);
+          }
         }
         ++idx;
       }
     }
     __syncthreads();
-    const double mu = block_sum(psum, red) / (2.0 * k);
-    double pv = 0.0;
-    for (int e = threadIdx.x; e < k; e += T) {
-      const int i = (int)dir[e];
-      const double a = __dsub_rn((double)fit[2 * i], mu), b = __dsub_rn((double)fit[2 * i + 1], mu);
-      pv = __dadd_rn(pv, __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+    if (s.algo == ARS) {               // block-uniform
+      const double mu = block_sum(psum, red) / (2.0 * k);
+      double pv = 0.0;
+      for (int e = threadIdx.x; e < k; e += T) {
+        const int i = (int)dir[e];
+        const double a = __dsub_rn((double)fit[2 * i], mu), b = __dsub_rn((double)fit[2 * i + 1], mu);
+        pv = __dadd_rn(pv, __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+      }
+      const double sr = sqrt(block_sum(pv, red) / (2.0 * k));
+      if (sr > 0.0) ars_scale = (float)((double)rs.lr / ((double)k * sr));
     }
-    const double sr = sqrt(block_sum(pv, red) / (2.0 * k));
-    if (sr > 0.0) ars_scale = (float)((double)rs.lr / ((double)k * sr));
   } else if (anti) {
     for (int i = threadIdx.x; i < N / 2; i += T) {
       const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
@@ -183,7 +193,8 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     if (g.improved) w.best_f = fb;
     g.lr = w.lr;
     g.sigma = w.sigma;
-    g.nentries = s.algo == ARS ? w.ars_k : (anti ? N / 2 : (s.algo == SNES ? N : sh_nw));
+    g.nentries = (s.algo == ARS || s.algo == PGPE) ? w.ars_k
+                                                   : (anti ? N / 2 : (s.algo == SNES ? N : sh_nw));
     g.ars_scale = ars_scale;
     g.clip_inv = 0.0f;
     g.bbar = bbar;

@@ -130,7 +130,9 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
         if (ALGO == OPENAI_ES || ALGO == ARS) sc = gs.sigma;
         else if (ALGO == SEP_CMA_ES) sc = __fmul_rn(gs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
         else sc = s.vec[F_SIGMA_D][idx];
-        s.vec[F_BEST_X][idx] = __fmaf_rn(sgn * sc, zbv[k], mean);
+        float xb = __fmaf_rn(sgn * sc, zbv[k], mean);
+        if (rs.clip) xb = fminf(fmaxf(xb, rs.clip_lo), rs.clip_hi);   // the member as asked
+        s.vec[F_BEST_X][idx] = xb;
       }
       if (ALGO == ARS) {
         // ARS V1: mean −= α/(k σ_R) · Σ_sel (f+ − f−) z; no step when σ_R = 0
@@ -140,8 +142,9 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
         opt_step(s, r, d, idx, mean, g, rs, gs, norm2);
       } else if (ALGO == PGPE) {
         const float sig = s.vec[F_SIGMA_D][idx];
-        const float gm = __fdiv_rn(__fmul_rn(sig, (float)G0[k]), (float)s.N);
-        const float gsg = __fdiv_rn(__fmul_rn(sig, (float)G1[k]), (float)(s.N / 2));
+        // normalised by the 2k members / k pairs used (k = N/2 unless elite pairs, Q13b)
+        const float gm = __fdiv_rn(__fmul_rn(sig, (float)G0[k]), (float)(2 * gs.nentries));
+        const float gsg = __fdiv_rn(__fmul_rn(sig, (float)G1[k]), (float)gs.nentries);
         opt_step(s, r, d, idx, mean, gm, rs, gs, norm2);
         const float mc = rs.sigma_max_change;
         float st = __fsub_rn(sig, __fmul_rn(rs.sigma_lrate, gsg));

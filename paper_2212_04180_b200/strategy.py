@@ -7,6 +7,7 @@ group to broadcast the ncclUniqueId; the collectives themselves run inside es_te
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import torch
 
@@ -17,7 +18,9 @@ DEFAULT_PARAMS = dict(init_min=-1.0, init_max=1.0, sigma_init=0.05, sigma_decay=
                       sigma_limit=0.0, lrate_init=0.01, lrate_decay=1.0, lrate_limit=0.0,
                       beta1=0.9, beta2=0.999, eps=1e-8, sigma_lrate=0.2, sigma_max_change=0.2,
                       temperature=12.0, elite_ratio=0.5, shaping=0, optimizer=0,
-                      momentum=0.9, max_speed=0.02)
+                      momentum=0.9, max_speed=0.02, weight_decay=0.0, clip_min=-math.inf,
+                      clip_max=math.inf)
+PGPE_ELITE_DEFAULT = 1.0    # DESIGN Q13: every pair unless elite_ratio is given
 
 
 def _ptr(t):
@@ -54,6 +57,8 @@ class Strategy:
         arr = (RunParams * self.R)()
         for r, p in enumerate(params):
             kw = dict(DEFAULT_PARAMS)
+            if self.algo == 1:                                   # PGPE
+                kw["elite_ratio"] = PGPE_ELITE_DEFAULT
             kw.update(p)
             for k, v in kw.items():
                 setattr(arr[r], k, v)
@@ -113,6 +118,13 @@ class Strategy:
     def tell_local(self, fitness_all, stream=None):
         """Split phase 1: rank the gathered fitness [W, R, N/W] and reduce this rank's entries."""
         check(lib().es_tell_local(self.ctx, _ptr(fitness_all), _stream(stream)), self.ctx)
+
+    def weight_decay(self, fitness, out=None, stream=None):
+        """f + weight_decay·‖x_j‖² for this rank's members of the asked generation (es_tell does
+        this itself; split-phase callers apply it to their slice before gathering)."""
+        o = out if out is not None else torch.empty_like(fitness)
+        check(lib().es_weight_decay(self.ctx, _ptr(fitness), _ptr(o), _stream(stream)), self.ctx)
+        return o
 
     def tell_apply(self, stream=None):
         """Split phase 2: apply the update from the (summed) 'dirsum' field."""

@@ -213,6 +213,9 @@ def test_variants_emulated_shards(algo, per, Wn):
     (W.ARS, dict(optimizer=W.SGD)), (W.OPENAI_ES, dict(optimizer=3)),
     (W.OPENAI_ES, dict(optimizer=W.CLIPUP, max_speed=0.0)), (W.ARS, dict(shaping=2)),
     (W.SNES, dict(shaping=2)), (W.ARS, dict(elite_ratio=0.0)), (W.PGPE, dict(shaping=3)),
+    (W.PGPE, dict(elite_ratio=0.0)), (W.PGPE, dict(elite_ratio=1.5)),
+    (W.SNES, dict(weight_decay=-0.1)), (W.OPENAI_ES, dict(clip_min=1.0, clip_max=0.0)),
+    (W.SEP_CMA_ES, dict(clip_min=float("nan"))),
 ])
 def test_variant_argument_errors(algo, over):
     from paper_2212_04180_b200 import strategy as S
@@ -226,3 +229,135 @@ def test_ars_odd_popsize_rejected():
     from paper_2212_04180_b200._lib import ESError
     with pytest.raises(ESError):
         S.Strategy(W.ARS, 15, 8, _params(W.ARS, 1))
+
+
+# ------------------------------------------------------------------------ PGPE elite pairs (Q13b)
+PGPE_ELITES = [dict(elite_ratio=0.25), dict(elite_ratio=1.0), dict(elite_ratio=0.1),
+               dict(elite_ratio=0.6)]
+
+
+@pytest.mark.parametrize("R,N,D", [(4, 16, 10), (4, 64, 1003), (1, 256, 5000), (4, 2, 1),
+                                   (2, 40000, 9)])
+def test_pgpe_elite_one_generation(R, N, D):
+    pair = Pair(W.PGPE, N, D, _params(W.PGPE, R, PGPE_ELITES))
+    _one_gen(pair, W.RASTRIGIN)
+    pair.close()
+
+
+# ------------------------------------------------------------------------ weight decay
+WDS = [dict(weight_decay=0.05), dict(weight_decay=0.0), dict(weight_decay=0.7)]
+
+
+@pytest.mark.parametrize("algo", [W.OPENAI_ES, W.PGPE, W.SNES, W.SEP_CMA_ES, W.ARS])
+@pytest.mark.parametrize("R,N,D", [(3, 16, 10), (3, 64, 1003), (1, 32, 70001)])
+def test_weight_decay_one_generation(algo, R, N, D):
+    pair = Pair(algo, N, D, _params(algo, R, WDS))
+    x = pair.gpu.ask()
+    f = pair.gpu.eval(W.RASTRIGIN, x)
+    fw = pair.gpu.weight_decay(f).cpu().numpy()
+    pair.gpu.tell(f)
+    fh = f.cpu().numpy()
+    for r in range(R):
+        o = pair.orc[r]
+        o.ask()
+        ref = o.weight_decay(fh[r])
+        assert np.all(np.abs(fw[r].astype(np.float64) - ref) <= np.spacing(np.abs(ref))), r
+        if WDS[r % 3]["weight_decay"] == 0.0:
+            assert np.array_equal(bits(fw[r]), bits(fh[r]))
+        o.tell(fh[r])
+        pair.compare(r, 1e-5)
+    pair.close()
+
+
+def test_weight_decay_host_buffers():
+    pair = Pair(W.OPENAI_ES, 16, 33, _params(W.OPENAI_ES, 2, WDS))
+    x = pair.gpu.ask()
+    f = pair.gpu.eval(W.SPHERE, x)
+    dev = pair.gpu.weight_decay(f).cpu()
+    host = pair.gpu.weight_decay(f.cpu())
+    assert torch.equal(dev, host)
+    pair.gpu.tell(f)
+    pair.close()
+
+
+# ------------------------------------------------------------------------ box bounds
+BOXES = [dict(clip_min=-0.5, clip_max=0.3), dict(), dict(clip_min=0.0),
+         dict(clip_max=-0.25)]
+
+
+@pytest.mark.parametrize("algo", [W.OPENAI_ES, W.PGPE, W.SNES, W.SEP_CMA_ES, W.ARS])
+@pytest.mark.parametrize("R,N,D", [(4, 16, 10), (4, 64, 1003), (1, 32, 4099)])
+def test_box_bounds_one_generation(algo, R, N, D):
+    pair = Pair(algo, N, D, _params(algo, R, BOXES))
+    _one_gen(pair, W.SPHERE)                      # x bit-exact (clipped) and state incl. best_x
+    pair.close()
+
+
+@pytest.mark.parametrize("algo", [W.OPENAI_ES, W.SNES])
+@pytest.mark.parametrize("fn", [W.SPHERE, W.ROSENBROCK, W.RASTRIGIN])
+def test_box_bounds_fused_ask_eval(algo, fn):
+    """The fused ask+eval kernel evaluates the clipped members (Rosenbrock's cross-quad successor
+    included)."""
+    N, D, R = 16, 1003, 4
+    pair = Pair(algo, N, D, _params(algo, R, BOXES))
+    x, f = pair.gpu.ask_eval(fn, write_x=True)
+    xh, fh = x.cpu().numpy(), f.cpu().numpy()
+    for r in range(R):
+        xo = pair.orc[r].ask()
+        assert np.array_equal(bits(xh[r]), bits(xo))
+        assert q24(fh[r], O.evaluate(fn, xo)) <= 1e-5
+    pair.close()
+
+
+# ------------------------------------------------------------------------ combined, 100 generations
+@pytest.mark.parametrize("algo,per", [
+    (W.PGPE, [dict(elite_ratio=0.25, weight_decay=0.01, clip_min=-1.0, clip_max=1.5),
+              dict(elite_ratio=1.0, optimizer=W.CLIPUP, max_speed=0.05)]),
+    (W.ARS, [dict(weight_decay=0.02, clip_min=-1.0), dict(elite_ratio=0.3)]),
+    (W.SEP_CMA_ES, [dict(weight_decay=0.1, clip_max=1.0), dict()]),
+])
+def test_f3_combined_hundred_generations(algo, per):
+    N, D, R = 32, 100, 2
+    pair = Pair(algo, N, D, _params(algo, R, per))
+    for g in range(100):
+        pair.gpu.tell(pair.gpu.eval(W.RASTRIGIN, pair.gpu.ask()))
+        for r in range(R):
+            o = pair.orc[r]
+            o.tell(O.evaluate(W.RASTRIGIN, o.ask()))
+        if g == 0:
+            for r in range(R):
+                pair.compare(r, 1e-5)
+    for r in range(R):
+        pair.compare(r, 1e-3)
+    pair.close()
+
+
+@pytest.mark.parametrize("algo", [W.PGPE, W.SNES])
+def test_weight_decay_emulated_shards(algo):
+    """Split-phase tell with weight decay: each shard decays its own slice before the gather."""
+    from paper_2212_04180_b200 import strategy as S
+    N, D, R, Wn = 32, 301, 3, 2
+    per = [dict(weight_decay=0.05, elite_ratio=0.5), dict(weight_decay=0.0),
+           dict(weight_decay=0.3, clip_min=-0.5)]
+    params = _params(algo, R, per)
+    ref = S.Strategy(algo, N, D, params)
+    shards = [S.Strategy(algo, N, D, params, shard=(w, Wn)) for w in range(Wn)]
+    for gen in range(3):
+        ref.tell(ref.eval(W.RASTRIGIN, ref.ask()))
+        locs = []
+        for sh in shards:
+            xs = sh.ask()
+            locs.append(sh.weight_decay(sh.eval(W.RASTRIGIN, xs)))
+        gathered = torch.stack(locs).contiguous()
+        for sh in shards:
+            sh.tell_local(gathered)
+        total = shards[0].get("dirsum") + shards[1].get("dirsum")
+        for sh in shards:
+            sh.set("dirsum", total)
+            sh.tell_apply()
+        for sh in shards:
+            assert torch.equal(sh.get("perm"), ref.get("perm"))
+            for fld in KEPT[algo]:
+                assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, fld
+    for es in shards + [ref]:
+        es.close()
