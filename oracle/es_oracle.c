@@ -570,7 +570,8 @@ static int tell_impl(orc_run_t *r, const float *f) {
   float *mean = vf(r, ORC_V_MEAN), *sd = vf(r, ORC_V_SIGMA);
 
   if (r->algo == ORC_ARS) {
-    /* ARS V1 update for minimisation: mean -= alpha / (k sigma_R) * sum (f+ - f-) z_i */
+    /* ARS update for minimisation (elite directions, sigma_R; no state normalisation):
+     * mean -= alpha / (k sigma_R) * sum (f+ - f-) z_i */
     int k = ars_k(r);
     int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
     ars_select(r, f, sel);

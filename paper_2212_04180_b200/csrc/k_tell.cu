@@ -135,7 +135,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
         s.vec[F_BEST_X][idx] = xb;
       }
       if (ALGO == ARS) {
-        // ARS V1: mean −= α/(k σ_R) · Σ_sel (f+ − f−) z; no step when σ_R = 0
+        // ARS: mean −= α/(k σ_R) · Σ_sel (f+ − f−) z; no step when σ_R = 0
         if (gs.ars_scale != 0.0f) mean = __fsub_rn(mean, __fmul_rn(gs.ars_scale, (float)G0[k]));
       } else if (ALGO == OPENAI_ES) {
         const float g = __fdiv_rn((float)G0[k], __fmul_rn((float)s.N, gs.sigma));
