@@ -109,7 +109,9 @@ typedef enum {
   ES_FIELD_DIRSUM = 17,  /* double [2][R][D] this rank's (after es_tell_local) or the summed
                             (before es_tell_apply) binary64 direction sums of N12; OpenAI-ES
                             uses only the first R*D entries                                    */
-  ES_NUM_FIELDS = 18
+  ES_FIELD_NORM2 = 18,   /* double [R] Sep-CMA-ES: a D-shard's share of ‖p_σ'‖² after
+                            es_tell_local; the caller sets the rank sum before es_tell_apply     */
+  ES_NUM_FIELDS = 19
 } es_field_t;
 
 typedef struct es_ctx es_ctx_t;
@@ -173,6 +175,38 @@ es_status_t es_tell(es_ctx_t *ctx, const float *fitness, es_stream_t stream);
  * out of order (ask → local → apply). */
 es_status_t es_tell_local(es_ctx_t *ctx, const float *fitness_all, es_stream_t stream);
 es_status_t es_tell_apply(es_ctx_t *ctx, es_stream_t stream);
+
+/* D-sharded contexts ("D-sharded multi-GPU mode for separable fitness"):
+ * instead of splitting the population, each of W ranks owns a quad-aligned range of
+ * dimensions [d_begin, d_end) of every member (es_dshard_plan) for all N members and R runs. The
+ * noise counter is the global quad index, so every rank's members are column slices of the
+ * unsharded population, bit for bit. A separable BBOB fitness (Sphere, Rosenbrock,
+ * Rastrigin) is a sum over dims, so the only data-path collective of a generation is an
+ * all-reduce of R·N binary64 partial fitness values inside es_ask_eval (plus R doubles of
+ * ‖p_σ'‖² for Sep-CMA-ES inside es_tell); the tell needs no gradient all-reduce at all because
+ * each rank updates only its own dims. Rosenbrock's pair term across a boundary uses a halo dim
+ * d_end whose state each rank updates redundantly (identical arithmetic, identical bits).
+ *   es_init_dshard     as es_init, W = world size of the dimension split; nccl_unique_id as there
+ *                      (NULL: a communicator-less shard, split phase only). Weight decay and
+ *                      ClipUp (global norms) are ES_ERR_UNSUPPORTED when W > 1.
+ *   es_dshard_plan     out = (d_begin, d_end, state end = min(d_end + 1, D)); ES_ERR_INVALID_ARG
+ *                      if ceil(D/4) < W (a rank would own no dims).
+ *   es_dshard_info     out = (d_begin, d_end, state end, D) of a context.
+ *   es_ask_eval        with a communicator: fitness [R][N] of the WHOLE problem on every rank
+ *                      (x, if given, is this rank's column slice [R][N][d_end − d_begin]).
+ *   es_ask_eval_partial  this rank's binary64 partial fitness [R][N] (host or device) for callers
+ *                      that sum over ranks themselves; fitness = (float)(Σ_ranks partial).
+ *   es_tell            fitness [R][N] (the full population's); no gradient collective.
+ *   es_tell_local / es_tell_apply  (no communicator) as es_tell, with Sep-CMA-ES's ES_FIELD_NORM2
+ *                      share summed by the caller in between.
+ * State fields (es_get / es_set) have the context's state dims (d_end − d_begin + halo). */
+es_status_t es_init_dshard(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t popsize,
+                           int64_t num_dims, const es_run_params_t *params, int32_t world_rank,
+                           int32_t world_size, const void *nccl_unique_id, es_stream_t stream);
+es_status_t es_dshard_plan(int64_t num_dims, int32_t world_size, int32_t rank, int64_t out[3]);
+es_status_t es_dshard_info(const es_ctx_t *ctx, int64_t out[4]);
+es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double *partial,
+                                es_stream_t stream);
 
 /* Weight-decay regularisation of this rank's fitness slice:
  * out[r][j] = (float)((double)fitness[r][j] + (double)weight_decay_r · Σ_d (double)x_jd²) for the

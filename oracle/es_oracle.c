@@ -549,7 +549,6 @@ int orc_tell(orc_run_t *r, const float *f) {
 static int tell_impl(orc_run_t *r, const float *f) {
   const int64_t D = r->num_dims;
   const int32_t N = r->popsize;
-  const int32_t P = orc_num_directions(r);
   /* best tracking with the pre-update state */
   int32_t *s = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
   int32_t *e = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);

@@ -17,13 +17,14 @@ ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
 FIELDS = dict(mean=0, sigma_d=1, adam_m=2, adam_v=3, p_sigma=4, p_c=5, C=6, best_x=7, best_f=8,
               sigma=9, lrate=10, gen=11, shaped=12, rank_s=13, rank_e=14, perm=15, fitness=16,
-              dirsum=17)
+              dirsum=17, norm2=18)
 
 EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "es_get", "es_set",
            "es_set_mlp_problem", "es_mlp_num_params", "es_shape", "es_kernel_launches",
            "es_destroy", "es_last_error", "es_status_string", "es_nccl_unique_id_size",
            "es_nccl_get_unique_id", "es_debug_primitive", "es_profile_enable", "es_profile_read",
-           "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay"]
+           "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay",
+           "es_init_dshard", "es_dshard_plan", "es_dshard_info", "es_ask_eval_partial"]
 
 
 class RunParams(C.Structure):
@@ -80,6 +81,11 @@ def lib():
         "es_ask_eval": (i32, [vp, i32, vp, vp, vp]),
         "es_tell_apply": (i32, [vp, vp]),
         "es_weight_decay": (i32, [vp, vp, vp, vp]),
+        "es_init_dshard": (i32, [C.POINTER(vp), i32, i32, i32, i64, C.POINTER(RunParams), i32, i32,
+                                 vp, vp]),
+        "es_dshard_plan": (i32, [i64, i32, i32, C.POINTER(i64)]),
+        "es_dshard_info": (i32, [vp, C.POINTER(i64)]),
+        "es_ask_eval_partial": (i32, [vp, i32, vp, vp, vp]),
         "es_shard_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
         "es_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(i64), i32]),
     }

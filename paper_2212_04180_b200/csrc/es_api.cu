@@ -47,6 +47,9 @@ using namespace esb;
 struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
+  int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
+  int64_t d0 = 0;               // first owned global dim
+  double* fpart = nullptr;      // [R][N] D-shard binary64 partial fitness
   bool any_clipup = false;
   bool any_wd = false;
   float* wdbuf = nullptr;       // [R][Nloc] weight-decayed fitness
@@ -232,10 +235,28 @@ es_status_t es_destroy(es_ctx_t* c) {
   return ES_SUCCESS;
 }
 
-es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_t D,
-                    const es_run_params_t* params, int32_t rank, int32_t W, const void* uid,
-                    es_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
+// f1 D-sharding: quad-aligned contiguous dimension ranges (the Philox counter is the global quad).
+static bool dshard_range(int64_t D, int32_t W, int32_t rank, int64_t& d0, int64_t& d1) {
+  const int64_t Qg = (D + 3) / 4;                         // balanced: sizes differ by ≤ 1 quad
+  const int64_t q0 = Qg * rank / W, q1 = Qg * (rank + 1) / W;
+  d0 = 4 * q0;
+  d1 = std::min<int64_t>(4 * q1, D);
+  return d1 > d0;
+}
+
+es_status_t es_dshard_plan(int64_t D, int32_t W, int32_t rank, int64_t out[3]) {
+  if (!out || D < 1 || W < 1 || rank < 0 || rank >= W)
+    return fail(nullptr, ES_ERR_INVALID_ARG, "bad D-shard plan arguments");
+  int64_t d0, d1;
+  if (!dshard_range(D, W, rank, d0, d1))
+    return fail(nullptr, ES_ERR_INVALID_ARG, "ceil(D/4) < world_size: rank %d owns no dims", rank);
+  out[0] = d0; out[1] = d1; out[2] = std::min<int64_t>(d1 + 1, D);
+  return ES_SUCCESS;
+}
+
+static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_t D,
+                             const es_run_params_t* params, int32_t rank, int32_t W,
+                             const void* uid, cudaStream_t st, bool dsh) {
   if (!out) return fail(nullptr, ES_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if ((int)algo < 0 || (int)algo > 4) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
@@ -245,8 +266,12 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   if (D < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be >= 1");
   if (D >= (int64_t(1) << 34)) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be < 2^34");
   if (W < 1 || rank < 0 || rank >= W) return fail(nullptr, ES_ERR_INVALID_ARG, "bad rank/world_size");
-  if (N % W) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be divisible by world_size");
-  if (antithetic(algo) && ((N % 2) || ((N / W) % 2)))
+  const int32_t pW = dsh ? 1 : W, prank = dsh ? 0 : rank;   // population sharding
+  int64_t d0 = 0, d1 = D;
+  if (dsh && !dshard_range(D, W, rank, d0, d1))
+    return fail(nullptr, ES_ERR_INVALID_ARG, "ceil(D/4) < world_size: rank %d owns no dims", rank);
+  if (N % pW) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be divisible by world_size");
+  if (antithetic(algo) && ((N % 2) || ((N / pW) % 2)))
     return fail(nullptr, ES_ERR_INVALID_ARG, "antithetic strategies need an even popsize per rank");
   if (N > (1 << 20)) return fail(nullptr, ES_ERR_UNSUPPORTED, "popsize > 2^20 is not implemented");
   for (int r = 0; r < R; ++r) {
@@ -271,13 +296,27 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: weight_decay must be finite and >= 0", r);
     if (!(p.clip_min <= p.clip_max))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: need clip_min <= clip_max", r);
+    if (dsh && W > 1 && (p.weight_decay != 0.0f || p.optimizer == ES_OPT_CLIPUP))
+      return fail(nullptr, ES_ERR_UNSUPPORTED, "run %d: weight decay / ClipUp need global norms, "
+                  "not implemented for D-sharded contexts", r);
   }
   es_ctx* c = new (std::nothrow) es_ctx();
   if (!c) return fail(nullptr, ES_ERR_OOM, "host allocation failed");
   DevState& s = c->s;
-  s.algo = algo; s.R = R; s.N = N; s.W = W; s.rank = rank; s.Nloc = N / W; s.D = D;
+  s.algo = algo; s.R = R; s.N = N; s.W = pW; s.rank = prank; s.Nloc = N / pW;
   s.any_clip = 0;
-  s.Q = (D + 3) / 4;
+  // state dims: the owned [d0, d1) plus, for a D-shard that is not the last, the halo dim d1
+  // (updated redundantly, bit-identically to its owner) that Rosenbrock's last pair term needs
+  s.Dg = D;
+  s.dshard = dsh ? 1 : 0;
+  s.q0 = d0 / 4;
+  s.Dx = d1 - d0;
+  s.D = std::min<int64_t>(d1 + 1, D) - d0;
+  s.Q = (s.D + 3) / 4;
+  s.Qx = (s.Dx + 3) / 4;
+  c->dW = dsh ? W : 1;
+  c->drank = dsh ? rank : 0;
+  c->d0 = d0;
   s.P = antithetic(algo) ? N / 2 : N;
   auto bail = [&](es_status_t e) { std::string m = c->err; es_destroy(c); g_err = m; return e; };
 #define TRY(expr)                                                                              \
@@ -289,7 +328,7 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
       return bail(_e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA);               \
     }                                                                                         \
   } while (0)
-  const size_t RD = (size_t)R * D, RN = (size_t)R * N;
+  const size_t RD = (size_t)R * s.D, RN = (size_t)R * N;
   const int a = (int)algo;
   bool need[NVEC] = {true, a == PGPE || a == SNES, antithetic(a), antithetic(a),
                      a == SEP_CMA_ES, a == SEP_CMA_ES, a == SEP_CMA_ES, true};
@@ -306,6 +345,8 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   TRY(dalloc(c, (void**)&s.rs_e, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.perm, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.pos, RN * sizeof(int32_t)));
+  TRY(dalloc(c, (void**)&s.n2, R * sizeof(double)));
+  if (dsh) TRY(dalloc(c, (void**)&c->fpart, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.dir, RN * sizeof(uint32_t)));
   TRY(dalloc(c, (void**)&s.coefA, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.coefB, RN * sizeof(double)));
@@ -376,12 +417,30 @@ es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_
   return ES_SUCCESS;
 }
 
+es_status_t es_init(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_t D,
+                    const es_run_params_t* params, int32_t rank, int32_t W, const void* uid,
+                    es_stream_t stream) {
+  return init_impl(out, algo, R, N, D, params, rank, W, uid, (cudaStream_t)stream, false);
+}
+
+es_status_t es_init_dshard(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t N, int64_t D,
+                           const es_run_params_t* params, int32_t rank, int32_t W,
+                           const void* uid, es_stream_t stream) {
+  return init_impl(out, algo, R, N, D, params, rank, W, uid, (cudaStream_t)stream, true);
+}
+
+es_status_t es_dshard_info(const es_ctx_t* c, int64_t out[4]) {
+  if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  out[0] = c->d0; out[1] = c->d0 + c->s.Dx; out[2] = c->d0 + c->s.D; out[3] = c->s.Dg;
+  return ES_SUCCESS;
+}
+
 es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !x) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   const DevState& s = c->s;
-  const size_t bytes = (size_t)s.R * s.Nloc * s.D * sizeof(float);
+  const size_t bytes = (size_t)s.R * s.Nloc * s.Dx * sizeof(float);
   float* dst = x;
   const bool host = !is_device_ptr(x);
   if (host) {
@@ -401,6 +460,9 @@ es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
   return ES_SUCCESS;
 }
 
+static es_status_t ask_eval_bbob(es_ctx* c, es_fitness_t fn, float* x, float* f, double* fpo,
+                                 cudaStream_t st);
+
 es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
@@ -408,8 +470,11 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   const DevState& s = c->s;
   const size_t nloc = (size_t)s.R * s.Nloc;
+  if (s.dshard && c->dW > 1 && !c->comm)
+    return fail(c, ES_ERR_BAD_STATE, "D-shard without communicator: use es_ask_eval_partial");
   if (fn == ES_FIT_MLP) {
     // N14′: the ask writes fp16(x) (and x unless NULL); the MLP streams that image with TMA
+    if (s.dshard) return fail(c, ES_ERR_UNSUPPORTED, "the MLP fitness is not separable over dims");
     if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
     if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
     if (x && !is_device_ptr(x)) return fail(c, ES_ERR_INVALID_ARG, "x must be device memory");
@@ -436,30 +501,64 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
     c->asked = true;
     return ES_SUCCESS;
   }
+  return ask_eval_bbob(c, fn, x, f, nullptr, st);
+}
+
+// BBOB fused ask + evaluate. f: fitness out (a D-shard sums the ranks' binary64 partials with
+// NCCL first); fpo: a D-shard's own partials out instead (es_ask_eval_partial).
+static es_status_t ask_eval_bbob(es_ctx* c, es_fitness_t fn, float* x, float* f, double* fpo,
+                                 cudaStream_t st) {
+  const DevState& s = c->s;
+  const size_t nloc = (size_t)s.R * s.Nloc;
   if (!c->aepart)
     CUDA_OR(c, dalloc(c, (void**)&c->aepart, nloc * ask_eval_blocks_per_run(s) * sizeof(double)));
   float* xd = x;
   const bool xh = x && !is_device_ptr(x);
   if (xh) {
-    if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.D * sizeof(float)));
+    if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.Dx * sizeof(float)));
     xd = c->xstage;
   }
+  void* out = f ? (void*)f : (void*)fpo;
+  const bool oh = !is_device_ptr(out);
   float* fd = f;
-  const bool fh = !is_device_ptr(f);
-  if (fh) {
+  if (f && oh) {
     if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
     fd = c->fstage;
   }
-  {
+  if (!s.dshard) {
     ProfScope ps(c, "ask_eval", st);
     CUDA_OR(c, launch_ask_eval(s, (int)fn, xd, c->aepart, fd, st));
+    c->launches += 2;
+  } else {
+    {
+      ProfScope ps(c, "ask_eval", st);
+      CUDA_OR(c, launch_ask_eval_partial(s, (int)fn, xd, c->aepart, c->fpart, st));
+      c->launches += 2;
+    }
+    if (f) {
+      if (c->dW > 1) {     // the only data-path collective of a D-sharded generation: R·N doubles
+        ProfScope ps(c, "allreduce", st);
+        NCCL_OR(c, ncclAllReduce(c->fpart, c->fpart, nloc, ncclFloat64, ncclSum, c->comm, st));
+      }
+      CUDA_OR(c, launch_partial_to_fitness(c->fpart, (int64_t)nloc, fd, st));
+      c->launches += 1;
+    } else {
+      CUDA_OR(c, cudaMemcpyAsync(fpo, c->fpart, nloc * sizeof(double), cudaMemcpyDefault, st));
+    }
   }
-  c->launches += 2;
-  if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.D * sizeof(float), cudaMemcpyDeviceToHost, st));
-  if (fh) CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
-  if (xh || fh) CUDA_OR(c, cudaStreamSynchronize(st));
+  if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.Dx * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (f && oh) CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (xh || oh) CUDA_OR(c, cudaStreamSynchronize(st));
   c->asked = true;
   return ES_SUCCESS;
+}
+
+es_status_t es_ask_eval_partial(es_ctx_t* c, es_fitness_t fn, float* x, double* fpart,
+                                es_stream_t stream_) {
+  if (!c || !fpart) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->s.dshard) return fail(c, ES_ERR_BAD_STATE, "es_ask_eval_partial needs a D-sharded context");
+  if ((int)fn < 0 || (int)fn > 2) return fail(c, ES_ERR_INVALID_ARG, "separable BBOB fitness only");
+  return ask_eval_bbob(c, fn, x, nullptr, fpart, (cudaStream_t)stream_);
 }
 
 es_status_t es_synth_fitness(es_ctx_t* c, float* f, es_stream_t stream_) {
@@ -553,7 +652,8 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
 }
 
 // a9 from the summed direction sums (update kernel), then Sep-CMA's global-norm phases.
-static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st) {
+// n2_summed: a D-shard's ‖p_σ'‖² share was already summed over ranks by the caller (split phase).
+static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st, bool n2_summed = false) {
   const DevState& s = c->s;
   if (!fused) {
     ProfScope ps(c, "tell_update", st);
@@ -561,6 +661,14 @@ static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st) {
     c->launches += 1;
   }
   if (s.algo == SEP_CMA_ES) {
+    if (s.dshard && !n2_summed) {
+      CUDA_OR(c, launch_sepcma_n2(s, st));
+      c->launches += 1;
+      if (c->dW > 1) {   // R doubles: the D-shard's second (tiny) collective
+        ProfScope ps(c, "allreduce", st);
+        NCCL_OR(c, ncclAllReduce(s.n2, s.n2, (size_t)s.R, ncclFloat64, ncclSum, c->comm, st));
+      }
+    }
     int nk = 0;
     ProfScope ps(c, "sepcma_finish", st);
     CUDA_OR(c, launch_sepcma_finish(s, st, &nk));
@@ -596,7 +704,7 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_tell without a preceding es_ask");
   const DevState& s = c->s;
-  if (s.W > 1 && !c->comm)
+  if ((s.W > 1 || (c->dW > 1 && s.algo == SEP_CMA_ES)) && !c->comm)
     return fail(c, ES_ERR_BAD_STATE, "no communicator: use es_tell_local / es_tell_apply");
   const size_t nloc = (size_t)s.R * s.Nloc;
   es_status_t err;
@@ -664,7 +772,17 @@ es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t str
   es_status_t err;
   const float* fsrc = stage_fitness(c, fitness_all, (size_t)c->s.R * c->s.N, st, &c->fgather_stage, &err);
   if (!fsrc) return err;
-  if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) return err;
+  if (c->s.dshard) {
+    // D-shard: every rank ranks the full fitness and updates its own dims in place; only
+    // Sep-CMA-ES leaves a share (ES_FIELD_NORM2) for the caller to sum before es_tell_apply
+    if ((err = tell_local_impl(c, fsrc, true, st)) != ES_SUCCESS) return err;
+    if (c->s.algo == SEP_CMA_ES) {
+      CUDA_OR(c, launch_sepcma_n2(c->s, st));
+      c->launches += 1;
+    }
+  } else if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) {
+    return err;
+  }
   c->told_local = true;
   return ES_SUCCESS;
 }
@@ -672,7 +790,7 @@ es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t str
 es_status_t es_tell_apply(es_ctx_t* c, es_stream_t stream_) {
   if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_apply without es_tell_local");
-  es_status_t err = tell_apply_impl(c, false, (cudaStream_t)stream_);
+  es_status_t err = tell_apply_impl(c, c->s.dshard != 0, (cudaStream_t)stream_, true);
   if (err != ES_SUCCESS) return err;
   c->told_local = false;
   c->asked = false;
@@ -713,6 +831,7 @@ static bool field_ok(const es_ctx* c, int f, void** base, size_t* elem, size_t* 
     case ES_FIELD_PERM: *base = s.perm; *count = RN; return true;
     case ES_FIELD_FITNESS: *base = s.fit; *count = RN; return true;
     case ES_FIELD_DIRSUM: *base = s.G; *count = 2 * (size_t)s.R * s.D; *elem = 8; return true;
+    case ES_FIELD_NORM2: *base = s.n2; *count = (size_t)s.R; *elem = 8; return s.algo == SEP_CMA_ES;
   }
   return false;
 }
@@ -737,7 +856,7 @@ es_status_t es_get(es_ctx_t* c, es_field_t field, void* dst, es_stream_t stream_
 es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !src) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (field >= ES_FIELD_SHAPED && field != ES_FIELD_DIRSUM)
+  if (field >= ES_FIELD_SHAPED && field != ES_FIELD_DIRSUM && field != ES_FIELD_NORM2)
     return fail(c, ES_ERR_INVALID_ARG, "field %d is read-only", field);
   void* base = nullptr;
   size_t elem, count = 0, off = 0;

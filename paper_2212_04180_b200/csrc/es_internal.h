@@ -58,7 +58,11 @@ struct alignas(16) GenScal {
 struct DevState {
   int algo, R, N, Nloc, W, rank;
   int any_clip;        // some run has box bounds (selects the clipping ask instances)
-  int64_t D, Q;        // Q = ceil(D/4) quads
+  int64_t D, Q;        // state dims of this context (incl. a D-shard's halo dim), Q = ceil(D/4)
+  int64_t Dx, Qx;      // member row length written to x (= D unless D-sharded), Qx = ceil(Dx/4)
+  int64_t q0;          // global quad of local dim 0 (D-shard: d_begin/4) — the noise counter
+  int64_t Dg;          // global problem dimension (constants, Sep-CMA h_σ)
+  int dshard;          // dimension-sharded context (f1): fitness partials are summed over ranks
   int P;               // global directions
   float* vec[NVEC];
   RunScal* rs;
@@ -78,6 +82,7 @@ struct DevState {
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
   uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
   int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
+  double* n2;          // [R] D-shard Sep-CMA ‖p_σ'‖² share, summed over ranks before the finish
 };
 
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
@@ -103,6 +108,12 @@ cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
 cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st);
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
+cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st);
+// D-shard: per-member binary64 partial fitness of the owned dims (fused ask + evaluate), and the
+// conversion of the rank-summed partials to fp32 fitness
+cudaError_t launch_ask_eval_partial(const DevState& s, int fn, float* x, double* part,
+                                    double* fpart, cudaStream_t st);
+cudaError_t launch_partial_to_fitness(const double* fsum, int64_t n, float* f, cudaStream_t st);
 cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 // f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)
 cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,

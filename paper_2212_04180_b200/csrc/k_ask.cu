@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) init_kernel(DevState s) {
   const uint32_t q = (uint32_t)(gid % s.Q);
   const RunScal& rs = s.rs[r];
   const Philox ph(rs.seed);
-  const uint4 o = ph(q, 0u, 0u, TAG_INIT);
+  const uint4 o = ph((uint32_t)(q + s.q0), 0u, 0u, TAG_INIT);
   const float span = __fsub_rn(rs.init_max, rs.init_min);
   const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   constexpr bool kAnti = is_anti(ALGO);
   const int r = blockIdx.x / bpr;
   const int64_t q = (int64_t)(blockIdx.x % bpr) * kAskThreads + threadIdx.x;
-  if (q >= s.Q) return;
+  if (q >= s.Qx) return;
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
   const int i0 = blockIdx.y * dpt;
   const int i1 = min(Ploc, i0 + dpt);
@@ -88,11 +88,11 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   }
   const int dir0 = s.rank * Ploc;
   const float lo = CLIP ? rs.clip_lo : 0.0f, hi = CLIP ? rs.clip_hi : 0.0f;
-  float* xr = x ? x + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
-  __half* hr = W16 ? x16 + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
+  float* xr = x ? x + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
+  __half* hr = W16 ? x16 + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
 #pragma unroll 2
   for (int il = i0; il < i1; ++il) {
-    const float4 z = normal4(ph, (uint32_t)q, (uint32_t)(dir0 + il), t);
+    const float4 z = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)(dir0 + il), t);
     const float zz[4] = {z.x, z.y, z.z, z.w};
     float xp[4], xm[4];
 #pragma unroll
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
     }
     const int64_t row = kAnti ? 2 * (int64_t)il : il;
     if (W16) {            // D % 4 == 0 is required for this path (8-byte stores)
-      __half* h0 = hr + row * s.D;
+      __half* h0 = hr + row * s.Dx;
       __half2 a0 = __floats2half2_rn(xp[0], xp[1]), a1 = __floats2half2_rn(xp[2], xp[3]);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&a0);
@@ -116,21 +116,21 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
         __half2 b0 = __floats2half2_rn(xm[0], xm[1]), b1 = __floats2half2_rn(xm[2], xm[3]);
         u.x = *reinterpret_cast<uint32_t*>(&b0);
         u.y = *reinterpret_cast<uint32_t*>(&b1);
-        __stcs(reinterpret_cast<uint2*>(h0 + s.D), u);
+        __stcs(reinterpret_cast<uint2*>(h0 + s.Dx), u);
       }
       if (!xr) continue;
     }
-    float* p0 = xr + row * s.D;
+    float* p0 = xr + row * s.Dx;
     if (V4) {
       __stcs(reinterpret_cast<float4*>(p0), make_float4(xp[0], xp[1], xp[2], xp[3]));
       if (kAnti)
-        __stcs(reinterpret_cast<float4*>(p0 + s.D), make_float4(xm[0], xm[1], xm[2], xm[3]));
+        __stcs(reinterpret_cast<float4*>(p0 + s.Dx), make_float4(xm[0], xm[1], xm[2], xm[3]));
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (4 * q + k < s.D) {
+        if (4 * q + k < s.Dx) {
           p0[k] = xp[k];
-          if (kAnti) p0[s.D + k] = xm[k];
+          if (kAnti) p0[s.Dx + k] = xm[k];
         }
       }
     }
@@ -141,7 +141,7 @@ template <int ALGO, bool CLIP>
 static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaStream_t st) {
   constexpr bool kAnti = is_anti(ALGO);
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
-  const int bpr = (int)((s.Q + kAskThreads - 1) / kAskThreads);
+  const int bpr = (int)((s.Qx + kAskThreads - 1) / kAskThreads);
   // Enough (thread, direction-chunk) items for ~4 waves of 16 warps/SM, ≥ 4 directions each.
   const int64_t quads = (int64_t)s.R * bpr * kAskThreads;
   const int64_t want = (int64_t)sm_count() * 2048 * 4;
@@ -155,7 +155,7 @@ static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaSt
     ask_kernel<ALGO, true, true, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
     return cudaGetLastError();
   }
-  const bool v4 = (s.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool v4 = (s.Dx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   if (v4) ask_kernel<ALGO, true, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
   else ask_kernel<ALGO, false, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
   return cudaGetLastError();

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
   const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = (int64_t)qb * kAE + threadIdx.x;
-  const bool active = q < s.Q;
+  const bool active = q < s.Q;    // state quads: a D-shard's halo quad feeds the shuffled xn
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
   const int i0 = blockIdx.y * dpt, i1 = min(Ploc, i0 + dpt);
   if (i0 >= i1) return;                               // block-uniform
@@ -60,10 +60,10 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
   const int dir0 = s.rank * Ploc;
   const bool clip = rs.clip != 0;                     // box bounds, block-uniform
   const float lo = rs.clip_lo, hi = rs.clip_hi;
-  float* xr = x ? x + (int64_t)r * s.Nloc * s.D + 4 * q : nullptr;
+  float* xr = x ? x + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
   for (int il = i0; il < i1; ++il) {
     const uint32_t dir = (uint32_t)(dir0 + il);
-    const float4 z = normal4(ph, (uint32_t)q, dir, t);
+    const float4 z = normal4(ph, (uint32_t)(q + s.q0), dir, t);
     const float zz[4] = {z.x, z.y, z.z, z.w};
     float xv[M][4];
 #pragma unroll
@@ -75,17 +75,17 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
         for (int h = 0; h < M; ++h) xv[h][k] = fminf(fmaxf(xv[h][k], lo), hi);
       }
     }
-    if (WX && active) {
+    if (WX && q < s.Qx) {                             // owned quads only
       const int64_t row = kAnti ? 2 * (int64_t)il : il;
 #pragma unroll
       for (int h = 0; h < M; ++h) {
-        float* p0 = xr + (row + h) * s.D;
+        float* p0 = xr + (row + h) * s.Dx;
         if (V4) {
           __stcs(reinterpret_cast<float4*>(p0), make_float4(xv[h][0], xv[h][1], xv[h][2], xv[h][3]));
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (4 * q + k < s.D) p0[k] = xv[h][k];
+            if (4 * q + k < s.Dx) p0[k] = xv[h][k];
         }
       }
     }
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
 #pragma unroll
       for (int h = 0; h < M; ++h) nx[h] = __shfl_down_sync(0xffffffffu, xv[h][0], 1);
       if (lane == 31 && has_next) {
-        const float zN = normal4(ph, (uint32_t)(q + 1), dir, t).x;
+        const float zN = normal4(ph, (uint32_t)(q + 1 + s.q0), dir, t).x;
         nx[0] = __fmaf_rn(scN, zN, mN);
         if (kAnti) nx[M - 1] = __fmaf_rn(-scN, zN, mN);
         if (clip) {
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int64_t d = 4 * q + k;
-        if (active && d < s.D) {
+        if (active && d < s.Dx) {                    // a D-shard's halo dim only feeds xn
           const float xn = k < 3 ? xv[h][k + 1] : nx[h];
           fit_add<FN>(acc, xv[h][k], xn, d + 1 < s.D);
         }
@@ -130,13 +130,26 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
   }
 }
 
+// f (fp32) or, for a D-shard, the member's binary64 partial over the owned dims (fpart).
 __global__ void ae_finalize_kernel(const double* __restrict__ part, int64_t rows, int bpr,
-                                   float* __restrict__ f) {
+                                   float* __restrict__ f, double* __restrict__ fpart) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= rows) return;
   double v = 0.0;
   for (int b = 0; b < bpr; ++b) v = __dadd_rn(v, part[j * bpr + b]);
-  f[j] = (float)v;
+  if (fpart) fpart[j] = v;
+  else f[j] = (float)v;
+}
+
+__global__ void partial_to_fitness_kernel(const double* __restrict__ fsum, int64_t n,
+                                          float* __restrict__ f) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) f[j] = (float)fsum[j];
+}
+
+cudaError_t launch_partial_to_fitness(const double* fsum, int64_t n, float* f, cudaStream_t st) {
+  partial_to_fitness_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fsum, n, f);
+  return cudaGetLastError();
 }
 
 // Weight decay: out_j = f_j + λ_r Σ_b part[j][b] (the member's ‖x_j‖², binary64).
@@ -157,7 +170,7 @@ int ask_eval_blocks_per_run(const DevState& s) { return (int)((s.Q + kAE - 1) / 
 template <int ALGO, int FN>
 static void launch_ae_t(const DevState& s, float* x, double* part, dim3 grid, int bpr, int dpt,
                         cudaStream_t st) {
-  const bool v4 = x && (s.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool v4 = x && (s.Dx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   if (!x) ask_eval_kernel<ALGO, FN, false, false><<<grid, kAE, 0, st>>>(s, x, part, bpr, dpt);
   else if (v4) ask_eval_kernel<ALGO, FN, true, true><<<grid, kAE, 0, st>>>(s, x, part, bpr, dpt);
   else ask_eval_kernel<ALGO, FN, true, false><<<grid, kAE, 0, st>>>(s, x, part, bpr, dpt);
@@ -203,9 +216,22 @@ cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f,
   return cudaGetLastError();
 }
 
-// Two kernels: the fused ask+evaluate and the per-member block sum.
+static cudaError_t ask_eval_impl(const DevState& s, int fn, float* x, double* part, float* f,
+                                 double* fpart, cudaStream_t st);
+
 cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
                             cudaStream_t st) {
+  return ask_eval_impl(s, fn, x, part, f, nullptr, st);
+}
+
+cudaError_t launch_ask_eval_partial(const DevState& s, int fn, float* x, double* part,
+                                    double* fpart, cudaStream_t st) {
+  return ask_eval_impl(s, fn, x, part, nullptr, fpart, st);
+}
+
+// Two kernels: the fused ask+evaluate and the per-member block sum.
+static cudaError_t ask_eval_impl(const DevState& s, int fn, float* x, double* part, float* f,
+                                 double* fpart, cudaStream_t st) {
   int bpr, dpt;
   const dim3 grid = ae_grid(s, bpr, dpt);
   switch (s.algo) {
@@ -216,7 +242,7 @@ cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, f
     default: launch_ae_a<SEP_CMA_ES>(fn, s, x, part, grid, bpr, dpt, st); break;
   }
   const int64_t rows = (int64_t)s.R * s.Nloc;
-  ae_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(part, rows, bpr, f);
+  ae_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(part, rows, bpr, f, fpart);
   return cudaGetLastError();
 }
 

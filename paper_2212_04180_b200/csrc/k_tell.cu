@@ -90,7 +90,7 @@ __device__ __forceinline__ void opt_step(const DevState& s, int r, int64_t d, in
     mean = __fsub_rn(mean, __fmul_rn(gs.lr, vn));
   } else {
     s.G[gidx(s, 0, r, d)] = (double)g;
-    norm2 = __dadd_rn(norm2, __dmul_rn((double)g, (double)g));
+    if (d < s.Dx) norm2 = __dadd_rn(norm2, __dmul_rn((double)g, (double)g));
   }
 }
 
@@ -111,7 +111,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
       constexpr bool kAnti = is_anti(ALGO);
       const int i = kAnti ? gs.jbest / 2 : gs.jbest;
       sgn = (kAnti && (gs.jbest & 1)) ? -1.0f : 1.0f;
-      zb = normal4(ph, (uint32_t)q, (uint32_t)i, gs.t);
+      zb = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)i, gs.t);
     }
     const float zbv[4] = {zb.x, zb.y, zb.z, zb.w};
     float omcs = 0.f, ks = 0.f;
@@ -163,7 +163,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
         mean = __fadd_rn(mean, __fmul_rn(gs.sigma, y));
         const float ps = __fadd_rn(__fmul_rn(omcs, s.vec[F_PSIGMA][idx]), __fmul_rn(ks, Z));
         s.vec[F_PSIGMA][idx] = ps;
-        norm2 = __dadd_rn(norm2, __dmul_rn((double)ps, (double)ps));
+        if (d < s.Dx) norm2 = __dadd_rn(norm2, __dmul_rn((double)ps, (double)ps));   // not the halo
         s.G[gidx(s, 0, r, d)] = G0[k];
         s.G[gidx(s, 1, r, d)] = G1[k];
       }
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
     if (active) {
 #pragma unroll 2
       for (int e = 0; e < nb; ++e) {
-        const float4 z = normal4(ph, (uint32_t)q, sdir[e], t);
+        const float4 z = normal4(ph, (uint32_t)(q + s.q0), sdir[e], t);
         accumulate<ALGO>(acc, z, sA[e], ALGO == PGPE ? sB[e] : 0.0);
       }
     }
@@ -313,15 +313,23 @@ __device__ __forceinline__ double normpart_total(const DevState& s, int r, int b
 }
 
 // Sep-CMA-ES phase 2: global ‖p_σ'‖ (fixed-order sum of the block partials), σ', h_σ.
+// D-sharded contexts split it: sepcma_n2_kernel writes this rank's ‖p_σ'‖² share to s.n2, the
+// shares are summed over ranks (NCCL or the caller), then sepcma_norm_kernel reads s.n2.
+__global__ void sepcma_n2_kernel(DevState s, int bpr) {
+  __shared__ double red[32];
+  const double n2 = normpart_total(s, blockIdx.x, bpr, red);
+  if (threadIdx.x == 0) s.n2[blockIdx.x] = n2;
+}
+
 __global__ void sepcma_norm_kernel(DevState s, int bpr) {
   __shared__ double red[32];
   const int r = blockIdx.x;
-  const double n2 = normpart_total(s, r, bpr, red);
+  const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
   if (threadIdx.x == 0) {
     RunScal& rs = s.rs[r];
     GenScal& gs = s.gs[r];
     const double norm = sqrt(n2);
-    const double Dd = (double)s.D;
+    const double Dd = (double)s.Dg;
     const float sig_new = __fmul_rn(
         gs.sigma, (float)exp(__dmul_rn(__ddiv_rn(rs.c_sigma, rs.d_sigma),
                                        __dsub_rn(__ddiv_rn(norm, rs.chi_d), 1.0))));
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(TT) clipup_vel_kernel(DevState s, int bpr) {
       const float vn = __fmaf_rn(rs.momentum, s.vec[F_ADAM_M][idx],
                                  __fmul_rn(gs.lr, __fmul_rn(g, gs.clip_inv)));
       s.vec[F_ADAM_M][idx] = vn;
-      v2 = __dadd_rn(v2, __dmul_rn((double)vn, (double)vn));
+      if (d < s.Dx) v2 = __dadd_rn(v2, __dmul_rn((double)vn, (double)vn));
     }
   }
   const double tot = block_sum_tt(v2, red);
@@ -475,6 +483,11 @@ cudaError_t launch_tell_update(const DevState& s, cudaStream_t st) {
     case ARS: update_kernel<ARS><<<g, TT, 0, st>>>(s, bpr); break;
     default: update_kernel<SEP_CMA_ES><<<g, TT, 0, st>>>(s, bpr); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st) {
+  sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, tell_blocks_per_run(s));
   return cudaGetLastError();
 }
 

@@ -45,10 +45,11 @@ class Strategy:
     """R independent runs of one algorithm (vmap over seeds / hyperparameters)."""
 
     def __init__(self, algo, popsize, num_dims, params, device="cuda", group=None, stream=None,
-                 shard=None):
+                 shard=None, split="population"):
         """params: one dict per run (es_run_params_t fields; 'seed' required).
-        group: torch.distributed group for population sharding with NCCL inside es_tell.
-        shard: (rank, world_size) for a communicator-less shard (split-phase tell only)."""
+        group: torch.distributed group for sharding with NCCL inside the library.
+        shard: (rank, world_size) for a communicator-less shard (split-phase exchange).
+        split: "population" (es_init) or "dims" (f1 D-sharding, es_init_dshard)."""
         if isinstance(params, dict):
             params = [params]
         self.algo, self.popsize, self.num_dims = int(algo), int(popsize), int(num_dims)
@@ -78,16 +79,26 @@ class Strategy:
             uid = C.c_void_p(buf.data_ptr())
         if shard is not None:
             self.rank, self.world_size = int(shard[0]), int(shard[1])
+        self.split = split
         self.ctx = C.c_void_p()
+        init = lib().es_init_dshard if split == "dims" else lib().es_init
         with torch.cuda.device(self.device):
-            check(lib().es_init(C.byref(self.ctx), self.algo, self.R, self.popsize, self.num_dims,
-                                arr, self.rank, self.world_size, uid, _stream(stream)))
+            check(init(C.byref(self.ctx), self.algo, self.R, self.popsize, self.num_dims,
+                       arr, self.rank, self.world_size, uid, _stream(stream)))
         self.local_popsize = self.popsize // self.world_size
+        self.x_dims = self.state_dims = self.num_dims
+        self.d_begin = 0
+        if split == "dims":
+            info = (C.c_int64 * 4)()
+            check(lib().es_dshard_info(self.ctx, info), self.ctx)
+            self.d_begin, d_end, s_end = info[0], info[1], info[2]
+            self.x_dims, self.state_dims = d_end - self.d_begin, s_end - self.d_begin
+            self.local_popsize = self.popsize
 
     # -- Listing 1 ------------------------------------------------------------------------------
     def ask(self, out=None, stream=None):
         x = out if out is not None else torch.empty(
-            (self.R, self.local_popsize, self.num_dims), dtype=torch.float32, device=self.device)
+            (self.R, self.local_popsize, self.x_dims), dtype=torch.float32, device=self.device)
         check(lib().es_ask(self.ctx, _ptr(x), _stream(stream)), self.ctx)
         return x
 
@@ -96,7 +107,7 @@ class Strategy:
         x = None
         if write_x:
             x = out_x if out_x is not None else torch.empty(
-                (self.R, self.local_popsize, self.num_dims), dtype=torch.float32,
+                (self.R, self.local_popsize, self.x_dims), dtype=torch.float32,
                 device=self.device)
         f = out_f if out_f is not None else torch.empty(
             (self.R, self.local_popsize), dtype=torch.float32, device=self.device)
@@ -142,9 +153,20 @@ class Strategy:
                                        _stream(stream)), self.ctx)
 
     # -- state ----------------------------------------------------------------------------------
+    def ask_eval_partial(self, fn, out_x=None, write_x=False, stream=None):
+        """D-shard: this rank's binary64 partial fitness [R, N] (fused ask + evaluate)."""
+        x = None
+        if write_x:
+            x = out_x if out_x is not None else torch.empty(
+                (self.R, self.popsize, self.x_dims), dtype=torch.float32, device=self.device)
+        p = torch.empty((self.R, self.popsize), dtype=torch.float64, device=self.device)
+        check(lib().es_ask_eval_partial(self.ctx, int(fn), _ptr(x) if x is not None else None,
+                                        _ptr(p), _stream(stream)), self.ctx)
+        return x, p
+
     def _shape(self, name):
-        R, N, D = self.R, self.popsize, self.num_dims
-        if name in ("best_f", "sigma", "lrate", "gen"):
+        R, N, D = self.R, self.popsize, self.state_dims
+        if name in ("best_f", "sigma", "lrate", "gen", "norm2"):
             return (R,)
         if name in ("shaped", "rank_s", "rank_e", "perm", "fitness"):
             return (R, N)
@@ -154,7 +176,8 @@ class Strategy:
 
     def get(self, name, stream=None):
         dt = {"gen": torch.int32, "rank_s": torch.int32, "rank_e": torch.int32,
-              "perm": torch.int32, "dirsum": torch.float64}.get(name, torch.float32)
+              "perm": torch.int32, "dirsum": torch.float64,
+              "norm2": torch.float64}.get(name, torch.float32)
         out = torch.empty(self._shape(name), dtype=dt, device=self.device)
         check(lib().es_get(self.ctx, FIELDS[name], _ptr(out), _stream(stream)), self.ctx)
         return out

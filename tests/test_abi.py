@@ -96,3 +96,24 @@ def test_product_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not bad.search(txt), f
+
+
+def test_dshard_plan_tiles_quad_aligned():
+    """f1 D-sharding plan (host-only): ranges tile [0, D), start on quads, halo = next dim."""
+    import ctypes as C
+    from paper_2212_04180_b200 import _lib
+    L = _lib.lib()
+    for D in (1, 4, 5, 37, 1000, 1003, 100_000, 985_216):
+        for W in (1, 2, 3, 4, 8):
+            if (D + 3) // 4 < W:                      # some rank would own no dims
+                out = (C.c_int64 * 3)()
+                assert any(L.es_dshard_plan(D, W, r, out) != 0 for r in range(W))
+                continue
+            prev = 0
+            for r in range(W):
+                out = (C.c_int64 * 3)()
+                assert L.es_dshard_plan(D, W, r, out) == 0
+                d0, d1, s1 = out[0], out[1], out[2]
+                assert d0 == prev and d0 % 4 == 0 and d1 > d0 and s1 == min(d1 + 1, D)
+                prev = d1
+            assert prev == D
