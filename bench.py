@@ -289,6 +289,9 @@ def main():
     ap.add_argument("--graph", type=int, default=None,
                     help="1: time replays of one generation captured as a CUDA graph "
                          "(default on for the launch-bound c1/c3)")
+    ap.add_argument("--split", default="population", choices=["population", "dims"],
+                    help="multi-GPU c1/c3: shard the population (P:226) or the dimensions "
+                         "(f1 D-sharding: only R*N partial fitness doubles are all-reduced)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--N", type=int, default=SWEEP["N"], help="c5 popsize")
     ap.add_argument("--D", type=int, default=SWEEP["D"], help="c5 dimensions")
@@ -317,12 +320,16 @@ def main():
     peaks = load_peaks()
     stream = torch.cuda.current_stream()
     sharded = world > 1 and args.config != "c2"       # population sharding
+    dsplit = sharded and args.split == "dims"
+    if dsplit and args.config not in ("c1", "c3"):
+        raise SystemExit("--split dims needs a separable BBOB config (c1, c3)")
     hs = []
     for label, cfg, params in handles_for(args.config, 0 if sharded else rank):
         es = S.Strategy(cfg["algo"], cfg["N"], cfg["D"], params,
-                        group=dist.group.WORLD if sharded else None)
+                        group=dist.group.WORLD if sharded else None,
+                        split="dims" if dsplit else "population")
         nl = es.local_popsize
-        x = (torch.empty((cfg["R"], nl, cfg["D"]), dtype=torch.float32, device="cuda")
+        x = (torch.empty((cfg["R"], nl, es.x_dims), dtype=torch.float32, device="cuda")
              if cfg["fn"] is not None else None)
         f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
         es.params = params
@@ -331,6 +338,7 @@ def main():
         hs.append((label, cfg, es, x, f))
 
     fused = bool(args.fused) if args.fused is not None else args.config == "c4"
+    fused = fused or dsplit                       # a D-shard evaluates inside es_ask_eval
     write_x = bool(args.write_x)
 
     def step():
@@ -417,6 +425,8 @@ def main():
         ops = byt = flops = 0.0
         for label, cfg, t, n in lst:
             R, N, D, algo = cfg["R"], cfg["N"] // W_, cfg["D"], cfg["algo"]
+            if dsplit:                                   # all members, this rank's dims
+                N, D = cfg["N"], hs[0][2].x_dims
             P = N // 2 if algo in (W.OPENAI_ES, W.PGPE) else N          # this rank's directions
             if k == "ask":
                 ops += n * R * P * D * (NORMAL_OPS + ASK_USE[algo])
@@ -432,7 +442,7 @@ def main():
                 byt += n * (4.0 * R * N * D + 4.0 * R * N)
             elif k in ("tell", "tell_reduce"):
                 # Sep-CMA regenerates only the mu weighted members (no ties in continuous fitness)
-                E = elite[label] / W_ if algo == W.SEP_CMA_ES else P
+                E = elite[label] / (1 if dsplit else W_) if algo == W.SEP_CMA_ES else P
                 ops += n * R * E * D * (NORMAL_OPS + TELL_USE[algo])
                 byt += n * R * D * STATE_BYTES[algo]
             elif k == "rank":
@@ -476,6 +486,8 @@ def main():
     e2e = e2e_run(hs, args, 1 if sharded else world, fused)
 
     cb = config_block(args.config, world)
+    if dsplit:
+        cb["parallelism"] = f"dimensions sharded x{world} (R*N partial-fitness all-reduce only)"
     if hs[0][1]["fn"] is None:
         cb["path"] = "synthetic fitness, tell"
     elif fused and hs[0][1]["fn"] == W.MLP:

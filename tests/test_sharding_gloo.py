@@ -100,3 +100,61 @@ def test_shard_plan_partitions():
                 covered += list(range(out[2], out[3]))
             assert mem == list(range(N)) and covered == list(range(ne))
     assert L.es_shard_plan(10, 4, 3, 0, out) == 1     # N not divisible by W
+
+
+# ------------------------------------------------------------------ f1 D-sharding over gloo
+def _dshard_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workloads as W
+        from oracle import oracle as O
+        from paper_2212_04180_b200._lib import lib
+        L = lib()
+        N, D = 16, 41
+        plan = (C.c_int64 * 3)()
+        assert L.es_dshard_plan(D, world, rank, plan) == 0
+        d0, d1, s1 = plan[0], plan[1], plan[2]
+        for algo in (0, 1, 2):                                   # dims-subset-exact algorithms
+            for fn in (W.SPHERE, W.ROSENBROCK):
+                p = W.run_params(algo, 90 + algo, init_min=-2, init_max=2)
+                full = O.Run(algo, N, D, **p)
+                mine = O.Run(algo, N, D, dims=np.arange(d0, s1), **p)   # owned dims + halo
+                for _ in range(2):
+                    xf, xm = full.ask(), mine.ask()
+                    assert np.array_equal(xm.view(np.uint32), xf[:, d0:s1].view(np.uint32))
+                    x = xm.astype(np.float64)
+                    if fn == W.SPHERE:                           # this rank's terms, binary64
+                        part = (x[:, :d1 - d0] ** 2).sum(1)
+                    else:
+                        a, b = x[:, :-1], x[:, 1:]
+                        part = (100 * (b - a * a) ** 2 + (1 - a) ** 2)[:, :min(d1, D - 1) - d0].sum(1)
+                    t = torch.from_numpy(np.ascontiguousarray(part))
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM)      # the one collective (R·N doubles)
+                    f = O.evaluate(fn, xf)
+                    assert np.allclose(t.numpy(), f, rtol=1e-6, atol=1e-6)
+                    full.tell(f)
+                    mine.tell(f)
+                    for v in range(mine.vec.shape[0]):           # state slice, bit for bit
+                        assert np.array_equal(mine.vec[v].view(np.uint32),
+                                              full.vec[v][d0:s1].view(np.uint32)), (algo, v)
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_dshard_matches_unsharded():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dshard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(0, "ok"), (1, "ok")], res
