@@ -37,7 +37,10 @@ typedef enum {
   ES_PGPE = 1,      /* P:165 */
   ES_SNES = 2,      /* P:172 */
   ES_SEP_CMA_ES = 3,/* P:179 */
-  ES_ARS = 4        /* P:166, SURVEY 8(f) f3: antithetic, top-k directions, sigma_R normalised */
+  ES_ARS = 4,       /* P:166, SURVEY 8(f) f3: antithetic, top-k directions, sigma_R normalised */
+  ES_CMA_ES = 5     /* P:177, SURVEY 8(f) f4: full covariance, x = m + σ·A·z with A = chol(C)
+                       (P:106), refreshed every k = max(1, ⌊1/(10·D·(c₁+c_μ))⌋) tells; D ≤ 4096,
+                       world_size 1; es_ask / es_ask_eval (BBOB) / es_tell as the others        */
 } es_algo_t;
 
 typedef enum { ES_OPT_ADAM = 0, ES_OPT_SGD = 1, ES_OPT_CLIPUP = 2 } es_optimizer_t;
@@ -111,7 +114,9 @@ typedef enum {
                             uses only the first R*D entries                                    */
   ES_FIELD_NORM2 = 18,   /* double [R] Sep-CMA-ES: a D-shard's share of ‖p_σ'‖² after
                             es_tell_local; the caller sets the rank sum before es_tell_apply     */
-  ES_NUM_FIELDS = 19
+  ES_FIELD_COV = 19,     /* float [R][D][D] CMA-ES covariance C (symmetric, both triangles)   */
+  ES_FIELD_CHOL = 20,    /* float [R][D][D] CMA-ES sampling factor A (lower; upper = 0)       */
+  ES_NUM_FIELDS = 21
 } es_field_t;
 
 typedef struct es_ctx es_ctx_t;

@@ -12,12 +12,12 @@ ES_SUCCESS = 0
 STATUS = {0: "success", 1: "invalid argument", 2: "bad state", 3: "CUDA error", 4: "NCCL error",
           5: "out of device memory", 6: "unsupported"}
 
-OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS = 0, 1, 2, 3, 4
+OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS, CMA_ES = 0, 1, 2, 3, 4, 5
 ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
 FIELDS = dict(mean=0, sigma_d=1, adam_m=2, adam_v=3, p_sigma=4, p_c=5, C=6, best_x=7, best_f=8,
               sigma=9, lrate=10, gen=11, shaped=12, rank_s=13, rank_e=14, perm=15, fitness=16,
-              dirsum=17, norm2=18)
+              dirsum=17, norm2=18, cov=19, chol=20)
 
 EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "es_get", "es_set",
            "es_set_mlp_problem", "es_mlp_num_params", "es_shape", "es_kernel_launches",

@@ -48,6 +48,7 @@ struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
   int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
+  std::vector<uint32_t> host_t; // completed tells per run (CMA-ES Cholesky refresh schedule)
   int64_t d0 = 0;               // first owned global dim
   double* fpart = nullptr;      // [R][N] D-shard binary64 partial fitness
   bool any_clipup = false;
@@ -259,7 +260,7 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
                              const void* uid, cudaStream_t st, bool dsh) {
   if (!out) return fail(nullptr, ES_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  if ((int)algo < 0 || (int)algo > 4) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
+  if ((int)algo < 0 || (int)algo > 5) return fail(nullptr, ES_ERR_INVALID_ARG, "unknown algo %d", algo);
   if (!params) return fail(nullptr, ES_ERR_INVALID_ARG, "params is NULL");
   if (R < 1) return fail(nullptr, ES_ERR_INVALID_ARG, "num_runs must be >= 1");
   if (N < 2) return fail(nullptr, ES_ERR_INVALID_ARG, "popsize must be >= 2");
@@ -267,6 +268,13 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   if (D >= (int64_t(1) << 34)) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be < 2^34");
   if (W < 1 || rank < 0 || rank >= W) return fail(nullptr, ES_ERR_INVALID_ARG, "bad rank/world_size");
   const int32_t pW = dsh ? 1 : W, prank = dsh ? 0 : rank;   // population sharding
+  if (algo == ES_CMA_ES && (W > 1 || dsh))
+    return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: sharding is not implemented");
+  for (int r = 0; r < R && algo == ES_CMA_ES; ++r)
+    if (params && params[r].weight_decay != 0.0f)
+      return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: weight decay is not implemented");
+  if (algo == ES_CMA_ES && D > kCmaMaxDims)
+    return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: num_dims > %d is not implemented", kCmaMaxDims);
   int64_t d0 = 0, d1 = D;
   if (dsh && !dshard_range(D, W, rank, d0, d1))
     return fail(nullptr, ES_ERR_INVALID_ARG, "ceil(D/4) < world_size: rank %d owns no dims", rank);
@@ -279,9 +287,10 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     if (!(p.sigma_init >= 0.0f)) return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: sigma_init < 0", r);
     if (antithetic(algo) && !(p.lrate_init > 0.0f))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: lrate_init must be > 0", r);
-    if (algo == ES_SEP_CMA_ES && (int)std::floor((double)p.elite_ratio * N) < 1)
+    const bool cmaish = algo == ES_SEP_CMA_ES || algo == ES_CMA_ES;
+    if (cmaish && (int)std::floor((double)p.elite_ratio * N) < 1)
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: floor(elite_ratio*N) < 1", r);
-    if (algo == ES_SEP_CMA_ES && !(p.elite_ratio <= 1.0f))
+    if (cmaish && !(p.elite_ratio <= 1.0f))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: elite_ratio > 1", r);
     const bool adamish = algo == ES_OPENAI_ES || algo == ES_PGPE;
     if (p.shaping != 0 && !((p.shaping == 1 || p.shaping == 2) && adamish))
@@ -330,8 +339,9 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   } while (0)
   const size_t RD = (size_t)R * s.D, RN = (size_t)R * N;
   const int a = (int)algo;
+  const bool cma = a == CMA_ES;
   bool need[NVEC] = {true, a == PGPE || a == SNES, antithetic(a), antithetic(a),
-                     a == SEP_CMA_ES, a == SEP_CMA_ES, a == SEP_CMA_ES, true};
+                     a == SEP_CMA_ES || cma, a == SEP_CMA_ES || cma, a == SEP_CMA_ES, true};
   for (int f = 0; f < NVEC; ++f) {
     s.vec[f] = nullptr;
     if (need[f]) TRY(dalloc(c, (void**)&s.vec[f], RD * sizeof(float)));
@@ -346,6 +356,17 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   TRY(dalloc(c, (void**)&s.perm, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.pos, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.n2, R * sizeof(double)));
+  s.cov = s.chol = s.cw = s.zbuf = s.ybuf = nullptr;
+  s.chol_fail = nullptr;
+  if (cma) {
+    const size_t RDD = (size_t)R * s.D * s.D, RND = (size_t)R * N * s.D;
+    TRY(dalloc(c, (void**)&s.cov, RDD * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.chol, RDD * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.cw, RDD * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.zbuf, RND * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.ybuf, RND * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.chol_fail, R * sizeof(int32_t)));
+  }
   if (dsh) TRY(dalloc(c, (void**)&c->fpart, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.dir, RN * sizeof(uint32_t)));
   TRY(dalloc(c, (void**)&s.coefA, RN * sizeof(double)));
@@ -392,6 +413,14 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
       rs.eta_sigma = (3.0 + std::log((double)D)) / (5.0 * std::sqrt((double)D));
     } else if (algo == ES_SEP_CMA_ES) {
       sepcma_setup(N, D, p.elite_ratio, rs, wr);
+    } else if (algo == ES_CMA_ES) {
+      sepcma_setup(N, D, p.elite_ratio, rs, wr);
+      // full CMA-ES: the tutorial rates without the separable (D+2)/3 boost, and the refresh
+      // period k = max(1, ⌊1/(10·D·(c₁ + c_μ))⌋) of the Cholesky factor (R-CMA)
+      const double Dd = (double)D, me = rs.mueff;
+      rs.c_1 = 2.0 / ((Dd + 1.3) * (Dd + 1.3) + me);
+      rs.c_mu = std::min(1.0 - rs.c_1, 2.0 * (me - 2.0 + 1.0 / me) / ((Dd + 2.0) * (Dd + 2.0) + me));
+      rs.k_refresh = std::max(1, (int)std::floor(1.0 / (10.0 * Dd * (rs.c_1 + rs.c_mu))));
     }
     std::copy(wr.begin(), wr.end(), wpos.begin() + (size_t)r * N);
   }
@@ -402,6 +431,11 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   TRY(cudaMemsetAsync(s.coefB, 0, RN * sizeof(double), st));
   TRY(launch_init(s, st));
   c->launches += 1;
+  if (cma) {
+    TRY(launch_cma_init(s, st));
+    c->launches += 1;
+  }
+  c->host_t.assign(R, 0u);
   TRY(cudaStreamSynchronize(st));   // host tables above are stack-owned
   if (W > 1 && uid) {
     ncclUniqueId id;
@@ -447,11 +481,16 @@ es_status_t es_ask(es_ctx_t* c, float* x, es_stream_t stream_) {
     if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, bytes));
     dst = c->xstage;
   }
-  {
+  if (s.algo == CMA_ES) {
+    int nk = 0;
+    ProfScope ps(c, "cma_ask", st);
+    CUDA_OR(c, launch_cma_ask(s, dst, st, &nk));
+    c->launches += nk;
+  } else {
     ProfScope ps(c, "ask", st);
     CUDA_OR(c, launch_ask(s, dst, st));
+    c->launches += 1;
   }
-  c->launches += 1;
   if (host) {
     CUDA_OR(c, cudaMemcpyAsync(x, dst, bytes, cudaMemcpyDeviceToHost, st));
     CUDA_OR(c, cudaStreamSynchronize(st));
@@ -472,6 +511,35 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
   const size_t nloc = (size_t)s.R * s.Nloc;
   if (s.dshard && c->dW > 1 && !c->comm)
     return fail(c, ES_ERR_BAD_STATE, "D-shard without communicator: use es_ask_eval_partial");
+  if (s.algo == CMA_ES) {     // sample (tiled contraction) then evaluate
+    if (fn == ES_FIT_MLP) return fail(c, ES_ERR_UNSUPPORTED, "CMA-ES with the MLP fitness");
+    const bool xh = x && !is_device_ptr(x), fh = !is_device_ptr(f);
+    float* xd = x;
+    if (!x || xh) {
+      if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.Dx * sizeof(float)));
+      xd = c->xstage;
+    }
+    float* fd = f;
+    if (fh) {
+      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
+      fd = c->fstage;
+    }
+    int nk = 0;
+    {
+      ProfScope ps(c, "cma_ask", st);
+      CUDA_OR(c, launch_cma_ask(s, xd, st, &nk));
+    }
+    {
+      ProfScope ps(c, "eval_bbob", st);
+      CUDA_OR(c, launch_eval_bbob((int)fn, xd, (int64_t)nloc, s.D, fd, st));
+    }
+    c->launches += nk + 1;
+    if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.Dx * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (fh) CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (xh || fh) CUDA_OR(c, cudaStreamSynchronize(st));
+    c->asked = true;
+    return ES_SUCCESS;
+  }
   if (fn == ES_FIT_MLP) {
     // N14′: the ask writes fp16(x) (and x unless NULL); the MLP streams that image with TMA
     if (s.dshard) return fail(c, ES_ERR_UNSUPPORTED, "the MLP fitness is not separable over dims");
@@ -645,6 +713,19 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
     CUDA_OR(c, launch_rank(s, fsrc, st));
   }
   c->launches += rank_launches(s);
+  if (s.algo == CMA_ES) {
+    // refresh the Cholesky factor after this tell for the runs whose k divides t + 1
+    bool refresh = false;
+    for (int r = 0; r < s.R; ++r) {
+      c->host_t[r] += 1;
+      if (c->host_t[r] % (uint32_t)c->host_rs[r].k_refresh == 0) refresh = true;
+    }
+    int nk = 0;
+    ProfScope ps(c, "cma_tell", st);
+    CUDA_OR(c, launch_cma_tell(s, refresh, st, &nk));
+    c->launches += nk;
+    return ES_SUCCESS;
+  }
   ProfScope ps(c, fused ? "tell" : "tell_reduce", st);
   CUDA_OR(c, launch_tell_reduce(s, fused, c->nchunk, st));
   c->launches += 1;
@@ -660,6 +741,7 @@ static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st, bool 
     CUDA_OR(c, launch_tell_update(s, st));
     c->launches += 1;
   }
+  if (s.algo == CMA_ES) return ES_SUCCESS;          // launch_cma_tell did every phase
   if (s.algo == SEP_CMA_ES) {
     if (s.dshard && !n2_summed) {
       CUDA_OR(c, launch_sepcma_n2(s, st));
@@ -752,6 +834,7 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !fitness || !out) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_weight_decay needs an asked generation");
+  if (c->s.algo == CMA_ES) return fail(c, ES_ERR_UNSUPPORTED, "CMA-ES: weight decay is not implemented");
   const size_t nloc = (size_t)c->s.R * c->s.Nloc;
   es_status_t err;
   const float* fd = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
@@ -832,6 +915,8 @@ static bool field_ok(const es_ctx* c, int f, void** base, size_t* elem, size_t* 
     case ES_FIELD_FITNESS: *base = s.fit; *count = RN; return true;
     case ES_FIELD_DIRSUM: *base = s.G; *count = 2 * (size_t)s.R * s.D; *elem = 8; return true;
     case ES_FIELD_NORM2: *base = s.n2; *count = (size_t)s.R; *elem = 8; return s.algo == SEP_CMA_ES;
+    case ES_FIELD_COV: *base = s.cov; *count = (size_t)s.R * s.D * s.D; return s.cov != nullptr;
+    case ES_FIELD_CHOL: *base = s.chol; *count = (size_t)s.R * s.D * s.D; return s.chol != nullptr;
   }
   return false;
 }
@@ -856,7 +941,8 @@ es_status_t es_get(es_ctx_t* c, es_field_t field, void* dst, es_stream_t stream_
 es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !src) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (field >= ES_FIELD_SHAPED && field != ES_FIELD_DIRSUM && field != ES_FIELD_NORM2)
+  if (field >= ES_FIELD_SHAPED && field != ES_FIELD_DIRSUM && field != ES_FIELD_NORM2 &&
+      field != ES_FIELD_COV && field != ES_FIELD_CHOL)
     return fail(c, ES_ERR_INVALID_ARG, "field %d is read-only", field);
   void* base = nullptr;
   size_t elem, count = 0, off = 0;
@@ -874,6 +960,7 @@ es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t s
     std::vector<uint32_t> t(c->s.R);
     CUDA_OR(c, cudaStreamSynchronize(st));
     CUDA_OR(c, cudaMemcpy(t.data(), src, c->s.R * sizeof(uint32_t), cudaMemcpyDefault));
+    c->host_t = t;                                 // CMA-ES refresh schedule follows t
     std::vector<double> p(2 * (size_t)c->s.R);
     for (int r = 0; r < c->s.R; ++r) {
       double b1 = 1.0, b2 = 1.0;

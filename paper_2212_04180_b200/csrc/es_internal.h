@@ -17,7 +17,8 @@
 
 namespace esb {
 
-enum Algo : int { OPENAI_ES = 0, PGPE = 1, SNES = 2, SEP_CMA_ES = 3, ARS = 4 };
+enum Algo : int { OPENAI_ES = 0, PGPE = 1, SNES = 2, SEP_CMA_ES = 3, ARS = 4, CMA_ES = 5 };
+static constexpr int64_t kCmaMaxDims = 4096;   // full CMA-ES: C is D×D per run (f4)
 enum Optim : int { OPT_ADAM = 0, OPT_SGD = 1, OPT_CLIPUP = 2 };
 __host__ __device__ constexpr bool is_anti(int a) { return a == OPENAI_ES || a == PGPE || a == ARS; }
 enum Field : int {
@@ -39,6 +40,7 @@ struct alignas(16) RunScal {
   float momentum, max_speed;
   float weight_decay, clip_lo, clip_hi;
   int32_t clip;                   // clip_lo or clip_hi finite
+  int32_t k_refresh;              // CMA-ES: Cholesky factor refreshed after every k-th tell
 };
 
 struct alignas(16) GenScal {
@@ -83,6 +85,13 @@ struct DevState {
   uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
   int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
   double* n2;          // [R] D-shard Sep-CMA ‖p_σ'‖² share, summed over ranks before the finish
+  // full-covariance CMA-ES (f4)
+  float* cov;          // [R][D][D] C, symmetric (both triangles stored)
+  float* chol;         // [R][D][D] A = chol(C) as of the last refresh, lower (upper = 0)
+  float* cw;           // [R][D][D] factorisation workspace
+  float* zbuf;         // [R][N][D] this generation's z
+  float* ybuf;         // [R][N][D] y = A z
+  int32_t* chol_fail;  // [R] the last refresh failed (A kept)
 };
 
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
@@ -109,6 +118,7 @@ cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaSt
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
 cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st);
+cudaError_t launch_sepcma_norm(const DevState& s, cudaStream_t st);   // σ', h_σ only
 // D-shard: per-member binary64 partial fitness of the owned dims (fused ask + evaluate), and the
 // conversion of the rank-summed partials to fp32 fitness
 cudaError_t launch_ask_eval_partial(const DevState& s, int fn, float* x, double* part,
@@ -119,6 +129,10 @@ cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,
                                 cudaStream_t st);
 int tell_blocks_per_run(const DevState& s);
+// CMA-ES (k_cma.cu)
+cudaError_t launch_cma_init(const DevState& s, cudaStream_t st);
+cudaError_t launch_cma_ask(const DevState& s, float* x, cudaStream_t st, int* nk);
+cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;
 int sm_count();

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) init_kernel(DevState s) {
     if (s.vec[F_PSIGMA]) {
       s.vec[F_PSIGMA][idx] = 0.0f;
       s.vec[F_PC][idx] = 0.0f;
-      s.vec[F_C][idx] = 1.0f;
+      if (s.vec[F_C]) s.vec[F_C][idx] = 1.0f;
     }
   }
 }

@@ -1,0 +1,495 @@
+// k_cma.cu — SURVEY §8(f) row f4: full-covariance CMA-ES ("weighted recombination-based mean
+// updates and iterative covariance matrix estimation ... evolution paths"; Table 1) with the
+// sampling reparametrisation the paper names, "the Cholesky decomposition of a covariance matrix"
+// (P:106). Readings in DESIGN.md §2 (R-CMA).
+//
+// One generation, R runs batched in the grid:
+//   ask   K-z      z_j = N2 normals (counter (⌊d/4⌋, j, t, ASK)), stored [R][N][D]
+//         K-samp   Y = Z·Aᵀ (A lower-triangular: an output tile's K range stops at its last dim),
+//                  x = clip(m + σ·y); Y stored for the tell
+//   tell  (rank kernel as Sep-CMA-ES: weights by sorted position)
+//         K-vec    ȳ = Σ w_j y_j, z̄ = Σ w_j z_j (binary64) → m, p_σ, ‖p_σ‖² partials, best_x
+//         (sepcma_norm_kernel: σ', h_σ)    K-pc  p_c
+//         K-cov    C ← a·C + c₁ p_c p_cᵀ + c_μ Σ w_j y_j y_jᵀ on lower tiles, mirrored (exactly symmetric)
+//         K-chol   every k-th tell: blocked right-looking Cholesky of C (64-wide panels: diagonal
+//                  block in binary64 in shared memory, row-parallel triangular solve, tiled trailing
+//                  update); a run whose C is not positive definite keeps its previous factor.
+// The contractions here are FP32 FFMA tiles on the CUDA cores.
+#include <algorithm>
+
+#include "es_internal.h"
+#include "noise.cuh"
+
+namespace esb {
+
+static constexpr int kTB = 64;    // output tile (rows × cols)
+static constexpr int kTK = 16;    // K step
+static constexpr int kNB = 64;    // Cholesky panel width
+
+__global__ void cma_init_kernel(DevState s) {
+  const int64_t DD = s.D * s.D, n = (int64_t)s.R * DD;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rem = g % DD;
+    const float v = (rem / s.D == rem % s.D) ? 1.0f : 0.0f;
+    s.cov[g] = v;
+    s.chol[g] = v;
+  }
+  if (blockIdx.x == 0)
+    for (int r = threadIdx.x; r < s.R; r += blockDim.x) s.chol_fail[r] = 0;
+}
+
+cudaError_t launch_cma_init(const DevState& s, cudaStream_t st) {
+  const int64_t n = (int64_t)s.R * s.D * s.D;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  cma_init_kernel<<<std::max(blocks, 1), 256, 0, st>>>(s);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------- ask
+__global__ void __launch_bounds__(128) cma_z_kernel(DevState s, int bpr, int jpb) {
+  const int r = blockIdx.x / bpr;
+  const int64_t q = (int64_t)(blockIdx.x % bpr) * 128 + threadIdx.x;
+  if (q >= s.Q) return;
+  const int j0 = blockIdx.y * jpb, j1 = min(s.N, j0 + jpb);
+  const RunScal& rs = s.rs[r];
+  const Philox ph(rs.seed);
+  const uint32_t t = rs.t;
+  const bool v4 = (s.D & 3) == 0;
+  for (int j = j0; j < j1; ++j) {
+    const float4 z = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)j, t);
+    float* p = s.zbuf + ((int64_t)r * s.N + j) * s.D + 4 * q;
+    if (v4) {
+      *reinterpret_cast<float4*>(p) = z;
+    } else {
+      const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (4 * q + k < s.D) p[k] = zz[k];
+    }
+  }
+}
+
+// Y = Z·Aᵀ for one 64-member × 64-dim tile of run blockIdx.z; 256 threads × (4 members × 4 dims),
+// FP32 FFMA in k order. Epilogue x = clip(fma(σ, y, m)) — the same expression best_x uses.
+__global__ void __launch_bounds__(256) cma_sample_kernel(DevState s, float* __restrict__ x) {
+  __shared__ __align__(16) float Zs[kTK][kTB + 4];
+  __shared__ __align__(16) float As[kTK][kTB + 4];
+  const int r = blockIdx.z;
+  const int64_t D = s.D;
+  const int d0 = blockIdx.x * kTB, j0 = blockIdx.y * kTB;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float* Z = s.zbuf + (int64_t)r * s.N * D;
+  const float* A = s.chol + (int64_t)r * D * D;
+  const int lr = threadIdx.x >> 2, lk = (threadIdx.x & 3) * 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = 0.0f;
+  const int kend = (int)std::min<int64_t>(D, d0 + kTB);      // A[d][k] = 0 for k > d
+  for (int k0 = 0; k0 < kend; k0 += kTK) {
+    const int jr = j0 + lr, dr = d0 + lr;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + lk + u;
+      Zs[lk + u][lr] = (jr < s.N && k < D) ? Z[(int64_t)jr * D + k] : 0.0f;
+      As[lk + u][lr] = (dr < D && k < D) ? A[(int64_t)dr * D + k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&Zs[kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&As[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = __fmaf_rn(av[i], bv[jj], acc[i][jj]);
+    }
+    __syncthreads();
+  }
+  const RunScal& rs = s.rs[r];
+  const float sig = rs.sigma;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int j = j0 + ty * 4 + i;
+    if (j >= s.N) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int d = d0 + tx * 4 + jj;
+      if (d >= D) continue;
+      const int64_t o = ((int64_t)r * s.N + j) * D + d;
+      s.ybuf[o] = acc[i][jj];
+      if (x) {
+        float xv = __fmaf_rn(sig, acc[i][jj], s.vec[F_MEAN][(int64_t)r * D + d]);
+        if (rs.clip) xv = fminf(fmaxf(xv, rs.clip_lo), rs.clip_hi);
+        x[o] = xv;
+      }
+    }
+  }
+}
+
+cudaError_t launch_cma_ask(const DevState& s, float* x, cudaStream_t st, int* nk) {
+  const int bpr = (int)((s.Q + 127) / 128);
+  const int64_t quads = (int64_t)s.R * bpr * 128;
+  const int64_t want = (int64_t)sm_count() * 2048 * 4;
+  int nchunk = (int)std::min<int64_t>(std::max<int64_t>(1, want / std::max<int64_t>(quads, 1)),
+                                      std::max(1, s.N / 4));
+  nchunk = std::min(nchunk, 65535);
+  const int jpb = (s.N + nchunk - 1) / nchunk;
+  nchunk = (s.N + jpb - 1) / jpb;
+  cma_z_kernel<<<dim3((unsigned)(s.R * bpr), (unsigned)nchunk), 128, 0, st>>>(s, bpr, jpb);
+  const dim3 g((unsigned)((s.D + kTB - 1) / kTB), (unsigned)((s.N + kTB - 1) / kTB), (unsigned)s.R);
+  cma_sample_kernel<<<g, 256, 0, st>>>(s, x);
+  if (nk) *nk = 2;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------ tell
+__device__ __forceinline__ double block_sum128(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t = __dadd_rn(t, red[k]);
+  return t;
+}
+
+// ȳ, z̄ over the weighted sorted positions; m, p_σ, best_x; ȳ to s.G[0] for p_c and C.
+__global__ void __launch_bounds__(128) cma_tellvec_kernel(DevState s, int bpr) {
+  __shared__ uint32_t sdir[256];
+  __shared__ double sw[256];
+  __shared__ double red[4];
+  const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
+  const int64_t q = (int64_t)qb * 128 + threadIdx.x;
+  const bool active = q < s.Q;
+  const GenScal& gs = s.gs[r];
+  const RunScal& rs = s.rs[r];
+  const int64_t D = s.D;
+  const int ne = gs.nentries;
+  const uint32_t* dir = s.dir + (int64_t)r * s.N;
+  const double* cA = s.coefA + (int64_t)r * s.N;
+  const float* Y = s.ybuf + (int64_t)r * s.N * D;
+  const float* Z = s.zbuf + (int64_t)r * s.N * D;
+  double yb[4] = {0.0, 0.0, 0.0, 0.0}, zb[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b0 = 0; b0 < ne; b0 += 256) {
+    const int nb = min(256, ne - b0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb; e += 128) {
+      sdir[e] = dir[b0 + e];
+      sw[e] = cA[b0 + e];
+    }
+    __syncthreads();
+    if (active) {
+      for (int e = 0; e < nb; ++e) {
+        const int64_t row = (int64_t)sdir[e] * D;
+        const double w = sw[e];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t d = 4 * q + k;
+          if (d < D) {
+            yb[k] = __fma_rn(w, (double)Y[row + d], yb[k]);
+            zb[k] = __fma_rn(w, (double)Z[row + d], zb[k]);
+          }
+        }
+      }
+    }
+  }
+  double norm2 = 0.0;
+  if (active) {
+    const float omcs = (float)__dsub_rn(1.0, rs.c_sigma);
+    const float ks = (float)sqrt(__dmul_rn(__dmul_rn(rs.c_sigma, __dsub_rn(2.0, rs.c_sigma)), rs.mueff));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t d = 4 * q + k;
+      if (d >= D) break;
+      const int64_t idx = (int64_t)r * D + d;
+      float mean = s.vec[F_MEAN][idx];
+      if (gs.improved) {                       // the member as asked (pre-update m, σ)
+        float xb = __fmaf_rn(gs.sigma, Y[(int64_t)gs.jbest * D + d], mean);
+        if (rs.clip) xb = fminf(fmaxf(xb, rs.clip_lo), rs.clip_hi);
+        s.vec[F_BEST_X][idx] = xb;
+      }
+      s.vec[F_MEAN][idx] = __fadd_rn(mean, __fmul_rn(gs.sigma, (float)yb[k]));
+      const float ps = __fadd_rn(__fmul_rn(omcs, s.vec[F_PSIGMA][idx]), __fmul_rn(ks, (float)zb[k]));
+      s.vec[F_PSIGMA][idx] = ps;
+      norm2 = __dadd_rn(norm2, __dmul_rn((double)ps, (double)ps));
+      s.G[idx] = yb[k];
+    }
+  }
+  const double tot = block_sum128(norm2, red);
+  if (threadIdx.x == 0) s.normpart[(int64_t)r * bpr + qb] = tot;
+}
+
+__global__ void __launch_bounds__(256) cma_pc_kernel(DevState s) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)s.R * s.D) return;
+  const int r = (int)(gid / s.D);
+  const RunScal& rs = s.rs[r];
+  const GenScal& gs = s.gs[r];
+  const float omcc = (float)(1.0 - rs.c_c);
+  const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
+  s.vec[F_PC][gid] = __fadd_rn(__fmul_rn(omcc, s.vec[F_PC][gid]), __fmul_rn(kc, (float)s.G[gid]));
+}
+
+// lower tile index t → (I, J), I ≥ J
+__device__ __forceinline__ void lower_tile(int t, int& I, int& J) {
+  I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  J = t - I * (I + 1) / 2;
+}
+
+// C ← a·C + c₁ p_c p_cᵀ + c_μ Σ_e w_e y_e y_eᵀ (lower tiles; mirrored).
+__global__ void __launch_bounds__(256) cma_cov_kernel(DevState s) {
+  __shared__ __align__(16) float Ui[kTK][kTB + 4];
+  __shared__ __align__(16) float Uj[kTK][kTB + 4];
+  const int r = blockIdx.y;
+  int I, J;
+  lower_tile(blockIdx.x, I, J);
+  const int64_t D = s.D;
+  const int i0 = I * kTB, j0 = J * kTB;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const GenScal& gs = s.gs[r];
+  const RunScal& rs = s.rs[r];
+  const int ne = gs.nentries;
+  const uint32_t* dir = s.dir + (int64_t)r * s.N;
+  const double* cA = s.coefA + (int64_t)r * s.N;
+  const float* Y = s.ybuf + (int64_t)r * s.N * D;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+  const int le = threadIdx.x >> 4, lc = (threadIdx.x & 15) * 4;   // 16 entries × 64 cols
+  for (int e0 = 0; e0 < ne; e0 += kTK) {
+    const int e = e0 + le;
+    const bool ok = e < ne;
+    const int64_t row = ok ? (int64_t)dir[e] * D : 0;
+    const float w = ok ? (float)cA[e] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int ci = i0 + lc + u, cj = j0 + lc + u;
+      Ui[le][lc + u] = (ok && ci < D) ? __fmul_rn(w, Y[row + ci]) : 0.0f;
+      Uj[le][lc + u] = (ok && cj < D) ? Y[row + cj] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&Ui[kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Uj[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = __fmaf_rn(av[p], bv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+  const double hs = gs.hsig ? 1.0 : 0.0;
+  const float af = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
+  const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
+  float* C = s.cov + (int64_t)r * D * D;
+  const float* pc = s.vec[F_PC] + (int64_t)r * D;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = i0 + ty * 4 + p;
+    if (i >= D) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + tx * 4 + q;
+      if (j > i) continue;                         // lower triangle; mirrored below
+      const float c = __fadd_rn(__fadd_rn(__fmul_rn(af, C[(int64_t)i * D + j]),
+                                          __fmul_rn(__fmul_rn(c1f, pc[i]), pc[j])),
+                                __fmul_rn(cmuf, acc[p][q]));
+      C[(int64_t)i * D + j] = c;
+      C[(int64_t)j * D + i] = c;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- Cholesky
+__device__ __forceinline__ bool chol_due(const DevState& s, int r) {
+  const RunScal& rs = s.rs[r];
+  return rs.k_refresh > 0 && (rs.t % (uint32_t)rs.k_refresh) == 0u;   // rs.t already = t + 1
+}
+
+__global__ void chol_copy_kernel(DevState s) {
+  const int r = blockIdx.y;
+  if (!chol_due(s, r)) return;
+  const int64_t DD = s.D * s.D;
+  const float* C = s.cov + (int64_t)r * DD;
+  float* Wk = s.cw + (int64_t)r * DD;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < DD;
+       g += (int64_t)gridDim.x * blockDim.x)
+    Wk[g] = C[g];
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.chol_fail[r] = 0;
+}
+
+// Diagonal block [kb, kb+b)² factorised in binary64 in shared memory (right-looking).
+__global__ void __launch_bounds__(256) chol_diag_kernel(DevState s, int kb) {
+  __shared__ double L[kNB][kNB + 1];
+  __shared__ int bad;
+  const int r = blockIdx.x;
+  if (!chol_due(s, r) || s.chol_fail[r]) return;
+  const int64_t D = s.D;
+  const int b = (int)std::min<int64_t>(kNB, D - kb);
+  float* Wk = s.cw + (int64_t)r * D * D;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e % b;
+    L[i][j] = j <= i ? (double)Wk[(int64_t)(kb + i) * D + kb + j] : 0.0;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = L[j][j];
+      if (!(d > 0.0)) bad = 1;
+      L[j][j] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x) L[i][j] = __ddiv_rn(L[i][j], L[j][j]);
+    __syncthreads();
+    const int m = b - j - 1;                       // trailing (i, k), j < k ≤ i < b
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e / m, k = j + 1 + e % m;
+      if (k <= i) L[i][k] = __fma_rn(-L[i][j], L[k][j], L[i][k]);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e % b;
+    if (j <= i) Wk[(int64_t)(kb + i) * D + kb + j] = (float)L[i][j];
+  }
+  if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
+}
+
+// Panel rows i ≥ kb+b: solve x·L11ᵀ = W[i][kb:kb+b] by forward substitution (one row per thread).
+__global__ void __launch_bounds__(128) chol_panel_kernel(DevState s, int kb) {
+  __shared__ float L11[kNB][kNB + 1];
+  const int r = blockIdx.y;
+  if (!chol_due(s, r) || s.chol_fail[r]) return;
+  const int64_t D = s.D;
+  const int b = (int)std::min<int64_t>(kNB, D - kb);
+  float* Wk = s.cw + (int64_t)r * D * D;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e % b;
+    L11[i][j] = j <= i ? Wk[(int64_t)(kb + i) * D + kb + j] : 0.0f;
+  }
+  __syncthreads();
+  const int64_t i = kb + b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= D) return;
+  float* row = Wk + i * D + kb;                 // overwritten in place by x as it is solved
+  for (int j = 0; j < b; ++j) {
+    double acc = (double)row[j];
+    for (int k = 0; k < j; ++k) acc = __fma_rn(-(double)row[k], (double)L11[j][k], acc);
+    row[j] = (float)__ddiv_rn(acc, (double)L11[j][j]);
+  }
+}
+
+// Trailing update W[i][j] −= Σ_k L21[i][k] L21[j][k] on the lower tiles of [kb+b, D)².
+__global__ void __launch_bounds__(256) chol_update_kernel(DevState s, int kb) {
+  __shared__ __align__(16) float Pi[kTK][kTB + 4];
+  __shared__ __align__(16) float Pj[kTK][kTB + 4];
+  const int r = blockIdx.y;
+  if (!chol_due(s, r) || s.chol_fail[r]) return;
+  const int64_t D = s.D;
+  const int b = (int)std::min<int64_t>(kNB, D - kb);
+  const int64_t t0 = kb + b;
+  int I, J;
+  lower_tile(blockIdx.x, I, J);
+  const int64_t i0 = t0 + (int64_t)I * kTB, j0 = t0 + (int64_t)J * kTB;
+  if (i0 >= D) return;
+  float* Wk = s.cw + (int64_t)r * D * D;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lr = threadIdx.x >> 2, lk = (threadIdx.x & 3) * 4;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0f;
+  for (int k0 = 0; k0 < b; k0 += kTK) {
+    const int64_t ri = i0 + lr, rj = j0 + lr;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + lk + u;
+      Pi[lk + u][lr] = (ri < D && k < b) ? Wk[ri * D + kb + k] : 0.0f;
+      Pj[lk + u][lr] = (rj < D && k < b) ? Wk[rj * D + kb + k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&Pi[kk][ty * 4]);
+      const float4 c = *reinterpret_cast<const float4*>(&Pj[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = __fmaf_rn(av[p], cv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int64_t i = i0 + ty * 4 + p;
+    if (i >= D) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + tx * 4 + q;
+      if (j > i) continue;
+      Wk[i * D + j] = __fsub_rn(Wk[i * D + j], acc[p][q]);
+    }
+  }
+}
+
+// A ← lower(W) for runs whose refresh succeeded.
+__global__ void chol_commit_kernel(DevState s) {
+  const int r = blockIdx.y;
+  if (!chol_due(s, r) || s.chol_fail[r]) return;
+  const int64_t DD = s.D * s.D;
+  const float* Wk = s.cw + (int64_t)r * DD;
+  float* A = s.chol + (int64_t)r * DD;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < DD;
+       g += (int64_t)gridDim.x * blockDim.x)
+    A[g] = (g % s.D) <= (g / s.D) ? Wk[g] : 0.0f;
+}
+
+cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk) {
+  int n = 0;
+  const int bpr = tell_blocks_per_run(s);
+  cma_tellvec_kernel<<<(unsigned)(s.R * bpr), 128, 0, st>>>(s, bpr);
+  launch_sepcma_norm(s, st);                      // σ', h_σ (shared with Sep-CMA-ES)
+  const int64_t RD = (int64_t)s.R * s.D;
+  cma_pc_kernel<<<(unsigned)((RD + 255) / 256), 256, 0, st>>>(s);
+  const int T = (int)((s.D + kTB - 1) / kTB);
+  cma_cov_kernel<<<dim3((unsigned)(T * (T + 1) / 2), (unsigned)s.R), 256, 0, st>>>(s);
+  n += 4;
+  if (refresh) {
+    const int64_t DD = s.D * s.D;
+    const unsigned cb = (unsigned)std::min<int64_t>((DD + 255) / 256, 1024);
+    chol_copy_kernel<<<dim3(cb, (unsigned)s.R), 256, 0, st>>>(s);
+    n += 1;
+    for (int64_t kb = 0; kb < s.D; kb += kNB) {
+      chol_diag_kernel<<<s.R, 256, 0, st>>>(s, (int)kb);
+      const int64_t rest = s.D - kb - std::min<int64_t>(kNB, s.D - kb);
+      n += 1;
+      if (rest > 0) {
+        chol_panel_kernel<<<dim3((unsigned)((rest + 127) / 128), (unsigned)s.R), 128, 0, st>>>(
+            s, (int)kb);
+        const int Tt = (int)((rest + kTB - 1) / kTB);
+        chol_update_kernel<<<dim3((unsigned)(Tt * (Tt + 1) / 2), (unsigned)s.R), 256, 0, st>>>(
+            s, (int)kb);
+        n += 2;
+      }
+    }
+    chol_commit_kernel<<<dim3(cb, (unsigned)s.R), 256, 0, st>>>(s);
+    n += 1;
+  }
+  if (nk) *nk = n + 1;
+  return cudaGetLastError();
+}
+
+}  // namespace esb

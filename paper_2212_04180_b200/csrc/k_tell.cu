@@ -486,6 +486,11 @@ cudaError_t launch_tell_update(const DevState& s, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_sepcma_norm(const DevState& s, cudaStream_t st) {
+  sepcma_norm_kernel<<<s.R, 256, 0, st>>>(s, tell_blocks_per_run(s));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st) {
   sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, tell_blocks_per_run(s));
   return cudaGetLastError();

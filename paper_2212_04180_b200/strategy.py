@@ -172,6 +172,8 @@ class Strategy:
             return (R, N)
         if name == "dirsum":
             return (2, R, D)
+        if name in ("cov", "chol"):
+            return (R, D, D)
         return (R, D)
 
     def get(self, name, stream=None):
