@@ -64,7 +64,7 @@ def handles_for(cfg_key, rank):
                       for r in range(cfg["R"])]
             out.append((key, cfg, params))
         return out
-    if cfg_key in ("c1", "c3"):
+    if cfg_key in ("c1", "c3", "c6"):
         cfg = W.CONFIGS[cfg_key]
         return [(cfg_key, cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
     if cfg_key == "c5":
@@ -157,6 +157,15 @@ def _oracle_gen(args):
         for j in range(gens):
             mlp.evaluate(run.member(j % N))
         return D * gens, time.perf_counter() - t0
+    if algo == W.CMA_ES:                     # f4: numpy binary64 oracle, one BLAS thread
+        from oracle import cma_oracle
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1):
+            run = cma_oracle.CMARun(N, D, **params)
+            t0 = time.perf_counter()
+            for _ in range(gens):
+                run.tell(O.evaluate(fn, run.ask()))
+            return N * D * gens, time.perf_counter() - t0
     run = O.Run(algo, N, D, **params)
     t0 = time.perf_counter()
     for _ in range(gens):
@@ -267,6 +276,12 @@ def config_block(cfg_key, world):
                             f"D~1e6 N=4096 point)", "R": 1, "N": cfg["N"], "D": cfg["D"],
                 "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
                 "l2": "x never materialised; state 12 MB resident in L2"}
+    if cfg_key == "c6":
+        return {"workload": "c6 (SURVEY 8(f) f4, not a BASELINE config): full-covariance CMA-ES on "
+                            "Rosenbrock, D=1024, popsize 256, 8 runs; Cholesky factor refreshed "
+                            "every generation (k = 1 at this D, N)", "R": cfg["R"], "N": cfg["N"],
+                "D": cfg["D"], "parallelism": "1 GPU",
+                "l2": "C, A, workspace 4 MB/run each; x, y, z 1 MB/run each (L2-resident)"}
     return {"workload": f"{cfg_key}: {cfg.get('name', '')}", "R": cfg.get("R"), "N": cfg.get("N"),
             "D": cfg.get("D"), "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
             "l2": "state resident; x > L2 only for D*N*4 > 126 MB"}
@@ -445,6 +460,13 @@ def main():
                 E = elite[label] / (1 if dsplit else W_) if algo == W.SEP_CMA_ES else P
                 ops += n * R * E * D * (NORMAL_OPS + TELL_USE[algo])
                 byt += n * R * D * STATE_BYTES[algo]
+            elif k == "cma_ask":                # z (N2) + y = A z (triangular FFMA) + x epilogue
+                ops += n * R * N * D * (NORMAL_OPS / 1.0 + D / 2.0 + 1.0)
+                byt += n * (12.0 * R * N * D + 2.0 * R * D * D)
+            elif k == "cma_tell":               # ȳ, z̄ + rank-μ (lower) + Cholesky (D³/6 FFMA)
+                mu = elite[label]
+                ops += n * R * (2.0 * mu * D + mu * D * D / 2.0 + D ** 3 / 6.0)
+                byt += n * R * (8.0 * mu * D + 12.0 * D * D)
             elif k == "rank":
                 byt += n * R * cfg["N"] * 40.0
             elif k == "eval_mlp":

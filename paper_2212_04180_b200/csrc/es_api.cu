@@ -376,7 +376,8 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   const int bpr = tell_blocks_per_run(s);
   if (c->nchunk > 1) TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->nchunk * 2 * RD * sizeof(double)));
   TRY(dalloc(c, (void**)&s.arrive, (size_t)R * bpr * sizeof(uint32_t)));
-  TRY(dalloc(c, (void**)&s.normpart, (size_t)R * bpr * sizeof(double)));
+  const size_t nparts = cma ? std::max<size_t>(bpr, (size_t)((s.D + 31) / 32)) : (size_t)bpr;
+  TRY(dalloc(c, (void**)&s.normpart, (size_t)R * nparts * sizeof(double)));
   {
     int npad = 1;
     while (npad < N) npad <<= 1;

@@ -159,69 +159,86 @@ __device__ __forceinline__ double block_sum128(double v, double* red) {
 }
 
 // ȳ, z̄ over the weighted sorted positions; m, p_σ, best_x; ȳ to s.G[0] for p_c and C.
-__global__ void __launch_bounds__(128) cma_tellvec_kernel(DevState s, int bpr) {
-  __shared__ uint32_t sdir[256];
-  __shared__ double sw[256];
-  __shared__ double red[4];
-  const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
-  const int64_t q = (int64_t)qb * 128 + threadIdx.x;
-  const bool active = q < s.Q;
+// Block = 32 dims × 8 entry groups (each group sums every 8th entry, the groups are then added in
+// group order: a fixed summation order); grid = R × ⌈D/32⌉.
+static constexpr int kVecDims = 32, kVecGroups = 8;
+__global__ void __launch_bounds__(256) cma_tellvec_kernel(DevState s, int bpr) {
+  __shared__ double sy[kVecGroups][kVecDims], sz[kVecGroups][kVecDims];
+  const int r = blockIdx.y;
+  const int lane = threadIdx.x & (kVecDims - 1), grp = threadIdx.x / kVecDims;
+  const int64_t D = s.D;
+  const int64_t d = (int64_t)blockIdx.x * kVecDims + lane;
   const GenScal& gs = s.gs[r];
   const RunScal& rs = s.rs[r];
-  const int64_t D = s.D;
   const int ne = gs.nentries;
   const uint32_t* dir = s.dir + (int64_t)r * s.N;
   const double* cA = s.coefA + (int64_t)r * s.N;
   const float* Y = s.ybuf + (int64_t)r * s.N * D;
   const float* Z = s.zbuf + (int64_t)r * s.N * D;
-  double yb[4] = {0.0, 0.0, 0.0, 0.0}, zb[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int b0 = 0; b0 < ne; b0 += 256) {
-    const int nb = min(256, ne - b0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb; e += 128) {
-      sdir[e] = dir[b0 + e];
-      sw[e] = cA[b0 + e];
+  double yb = 0.0, zb = 0.0;
+  if (d < D) {
+    for (int e = grp; e < ne; e += kVecGroups) {
+      const int64_t row = (int64_t)dir[e] * D;
+      const double w = cA[e];
+      yb = __fma_rn(w, (double)Y[row + d], yb);
+      zb = __fma_rn(w, (double)Z[row + d], zb);
     }
-    __syncthreads();
-    if (active) {
-      for (int e = 0; e < nb; ++e) {
-        const int64_t row = (int64_t)sdir[e] * D;
-        const double w = sw[e];
+  }
+  sy[grp][lane] = yb;
+  sz[grp][lane] = zb;
+  __syncthreads();
+  if (grp != 0) return;
+  yb = zb = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int64_t d = 4 * q + k;
-          if (d < D) {
-            yb[k] = __fma_rn(w, (double)Y[row + d], yb[k]);
-            zb[k] = __fma_rn(w, (double)Z[row + d], zb[k]);
-          }
-        }
-      }
-    }
+  for (int k = 0; k < kVecGroups; ++k) {
+    yb = __dadd_rn(yb, sy[k][lane]);
+    zb = __dadd_rn(zb, sz[k][lane]);
   }
   double norm2 = 0.0;
-  if (active) {
+  if (d < D) {
     const float omcs = (float)__dsub_rn(1.0, rs.c_sigma);
     const float ks = (float)sqrt(__dmul_rn(__dmul_rn(rs.c_sigma, __dsub_rn(2.0, rs.c_sigma)), rs.mueff));
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t d = 4 * q + k;
-      if (d >= D) break;
-      const int64_t idx = (int64_t)r * D + d;
-      float mean = s.vec[F_MEAN][idx];
-      if (gs.improved) {                       // the member as asked (pre-update m, σ)
-        float xb = __fmaf_rn(gs.sigma, Y[(int64_t)gs.jbest * D + d], mean);
-        if (rs.clip) xb = fminf(fmaxf(xb, rs.clip_lo), rs.clip_hi);
-        s.vec[F_BEST_X][idx] = xb;
-      }
-      s.vec[F_MEAN][idx] = __fadd_rn(mean, __fmul_rn(gs.sigma, (float)yb[k]));
-      const float ps = __fadd_rn(__fmul_rn(omcs, s.vec[F_PSIGMA][idx]), __fmul_rn(ks, (float)zb[k]));
-      s.vec[F_PSIGMA][idx] = ps;
-      norm2 = __dadd_rn(norm2, __dmul_rn((double)ps, (double)ps));
-      s.G[idx] = yb[k];
+    const int64_t idx = (int64_t)r * D + d;
+    const float mean = s.vec[F_MEAN][idx];
+    if (gs.improved) {                             // the member as asked (pre-update m, σ)
+      float xb = __fmaf_rn(gs.sigma, Y[(int64_t)gs.jbest * D + d], mean);
+      if (rs.clip) xb = fminf(fmaxf(xb, rs.clip_lo), rs.clip_hi);
+      s.vec[F_BEST_X][idx] = xb;
     }
+    s.vec[F_MEAN][idx] = __fadd_rn(mean, __fmul_rn(gs.sigma, (float)yb));
+    const float ps = __fadd_rn(__fmul_rn(omcs, s.vec[F_PSIGMA][idx]), __fmul_rn(ks, (float)zb));
+    s.vec[F_PSIGMA][idx] = ps;
+    norm2 = __dmul_rn((double)ps, (double)ps);
+    s.G[idx] = yb;
   }
-  const double tot = block_sum128(norm2, red);
-  if (threadIdx.x == 0) s.normpart[(int64_t)r * bpr + qb] = tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) norm2 = __dadd_rn(norm2, __shfl_xor_sync(0xffffffffu, norm2, o));
+  if (lane == 0) s.normpart[(int64_t)r * bpr + blockIdx.x] = norm2;
+}
+
+// σ', h_σ from the per-block ‖p_σ'‖² partials (bpr = ⌈D/32⌉ of them per run)
+__global__ void cma_norm_kernel(DevState s, int bpr) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < bpr; b += blockDim.x) v = __dadd_rn(v, s.normpart[(int64_t)r * bpr + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double n2 = 0.0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) n2 = __dadd_rn(n2, red[k]);
+  RunScal& rs = s.rs[r];
+  GenScal& gs = s.gs[r];
+  const double norm = sqrt(n2);
+  const float sig_new = __fmul_rn(
+      gs.sigma, (float)exp(__dmul_rn(__ddiv_rn(rs.c_sigma, rs.d_sigma),
+                                     __dsub_rn(__ddiv_rn(norm, rs.chi_d), 1.0))));
+  const double lhs = norm / sqrt(1.0 - pow(1.0 - rs.c_sigma, 2.0 * (double)(gs.t + 1)));
+  gs.hsig = lhs < (1.4 + 2.0 / ((double)s.Dg + 1.0)) * rs.chi_d;
+  gs.sigma_new = sig_new;
+  rs.sigma = sig_new;
 }
 
 __global__ void __launch_bounds__(256) cma_pc_kernel(DevState s) {
@@ -329,64 +346,151 @@ __global__ void chol_copy_kernel(DevState s) {
   if (blockIdx.x == 0 && threadIdx.x == 0) s.chol_fail[r] = 0;
 }
 
-// Diagonal block [kb, kb+b)² factorised in binary64 in shared memory (right-looking).
-__global__ void __launch_bounds__(256) chol_diag_kernel(DevState s, int kb) {
-  __shared__ double L[kNB][kNB + 1];
+// 32×32 Cholesky by one warp: lane i holds row i (a[k], k ≤ i) in registers; column j's pivot and
+// entries are broadcast with shuffles, so a column costs no barrier. Fully unrolled (register
+// indices must be static). Returns false if a pivot is not positive.
+__device__ __forceinline__ bool warp_chol32(float (&a)[32], int lane) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float d = __shfl_sync(0xffffffffu, a[j], j);
+    ok = ok && d > 0.0f;
+    const float piv = d > 0.0f ? __fsqrt_rn(d) : 1.0f;
+    const float inv = __frcp_rn(piv);
+    if (lane == j) a[j] = piv;
+    if (lane > j) a[j] = __fmul_rn(a[j], inv);
+    const float lij = a[j];
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const float lkj = __shfl_sync(0xffffffffu, lij, k);
+      if (lane >= k) a[k] = __fmaf_rn(-lij, lkj, a[k]);
+    }
+  }
+  return ok;
+}
+
+// Diagonal block [kb, kb+64)² (the last may be narrower) as a 2×2 blocked Cholesky of 32×32
+// tiles: warp 0 factors L00; warp 1 solves L10 = A10·L00⁻ᵀ (lane per row, L00 from shared
+// memory); A11 −= L10·L10ᵀ; warp 0 factors L11. fp32, as the rest of the factorisation.
+// This step is latency-bound (one serial 64-column chain per run); see DESIGN §5.
+__global__ void __launch_bounds__(64) chol_diag_kernel(DevState s, int kb) {
+  __shared__ float L00[32][33];
+  __shared__ float L10[32][33];
   __shared__ int bad;
   const int r = blockIdx.x;
   if (!chol_due(s, r) || s.chol_fail[r]) return;
   const int64_t D = s.D;
   const int b = (int)std::min<int64_t>(kNB, D - kb);
   float* Wk = s.cw + (int64_t)r * D * D;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int i = e / b, j = e % b;
-    L[i][j] = j <= i ? (double)Wk[(int64_t)(kb + i) * D + kb + j] : 0.0;
-  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto at = [&](int i, int j) -> float& { return Wk[(int64_t)(kb + i) * D + kb + j]; };
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  for (int j = 0; j < b; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = L[j][j];
-      if (!(d > 0.0)) bad = 1;
-      L[j][j] = d > 0.0 ? sqrt(d) : 1.0;
+  float a[32];
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) a[k] = (lane < b && k <= lane && k < b) ? at(lane, k) : (k == lane ? 1.0f : 0.0f);
+    const bool ok = warp_chol32(a, lane);
+    if (!ok && lane == 0) bad = 1;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      L00[lane][k] = k <= lane ? a[k] : 0.0f;
+      if (lane < b && k <= lane && k < b) at(lane, k) = a[k];
     }
-    __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x) L[i][j] = __ddiv_rn(L[i][j], L[j][j]);
-    __syncthreads();
-    const int m = b - j - 1;                       // trailing (i, k), j < k ≤ i < b
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int i = j + 1 + e / m, k = j + 1 + e % m;
-      if (k <= i) L[i][k] = __fma_rn(-L[i][j], L[k][j], L[i][k]);
+  }
+  __syncthreads();
+  if (b <= 32) {
+    if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
+    return;
+  }
+  const int b1 = b - 32;
+  if (warp == 1) {
+    float x[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = lane < b1 ? at(32 + lane, k) : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float acc = x[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) acc = __fmaf_rn(-x[k], L00[j][k], acc);
+      x[j] = __fdiv_rn(acc, L00[j][j]);
     }
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      L10[lane][k] = x[k];
+      if (lane < b1) at(32 + lane, k) = x[k];
+    }
   }
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int i = e / b, j = e % b;
-    if (j <= i) Wk[(int64_t)(kb + i) * D + kb + j] = (float)L[i][j];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      float v = (lane < b1 && k <= lane && k < b1) ? at(32 + lane, 32 + k) : (k == lane ? 1.0f : 0.0f);
+      if (lane < b1 && k <= lane && k < b1) {
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v = __fmaf_rn(-L10[lane][m], L10[k][m], v);
+      }
+      a[k] = v;
+    }
+    const bool ok = warp_chol32(a, lane);
+    if (!ok && lane == 0) bad = 1;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (lane < b1 && k <= lane && k < b1) at(32 + lane, 32 + k) = a[k];
   }
+  __syncthreads();
   if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
 }
 
-// Panel rows i ≥ kb+b: solve x·L11ᵀ = W[i][kb:kb+b] by forward substitution (one row per thread).
-__global__ void __launch_bounds__(128) chol_panel_kernel(DevState s, int kb) {
+// Panel rows i ≥ kb+64: solve x·L11ᵀ = W[i][kb:kb+64] by forward substitution, one row per thread,
+// the row held in registers (fully unrolled; many warps share the code, so it stays cached).
+static constexpr int kPanelRows = 128;
+__global__ void __launch_bounds__(kPanelRows) chol_panel_kernel(DevState s, int kb) {
   __shared__ float L11[kNB][kNB + 1];
+  __shared__ float dinv[kNB];
   const int r = blockIdx.y;
   if (!chol_due(s, r) || s.chol_fail[r]) return;
   const int64_t D = s.D;
-  const int b = (int)std::min<int64_t>(kNB, D - kb);
   float* Wk = s.cw + (int64_t)r * D * D;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int i = e / b, j = e % b;
+  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+    const int i = e >> 6, j = e & (kNB - 1);
     L11[i][j] = j <= i ? Wk[(int64_t)(kb + i) * D + kb + j] : 0.0f;
   }
   __syncthreads();
-  const int64_t i = kb + b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x < kNB) dinv[threadIdx.x] = 1.0f / L11[threadIdx.x][threadIdx.x];
+  __syncthreads();
+  const int64_t i = kb + kNB + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= D) return;
-  float* row = Wk + i * D + kb;                 // overwritten in place by x as it is solved
-  for (int j = 0; j < b; ++j) {
-    double acc = (double)row[j];
-    for (int k = 0; k < j; ++k) acc = __fma_rn(-(double)row[k], (double)L11[j][k], acc);
-    row[j] = (float)__ddiv_rn(acc, (double)L11[j][j]);
+  float* row = Wk + i * D + kb;
+  float x[kNB];
+  const bool v4 = (D & 3) == 0;                   // rows 16-B aligned (kb is a multiple of 64)
+#pragma unroll
+  for (int j = 0; j < kNB; j += 4) {
+    if (v4) {
+      const float4 v = *reinterpret_cast<const float4*>(row + j);
+      x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+    } else {
+      x[j] = row[j]; x[j + 1] = row[j + 1]; x[j + 2] = row[j + 2]; x[j + 3] = row[j + 3];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kNB; ++j) {
+    float a0 = x[j], a1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k + 1 < j; k += 2) {
+      a0 = __fmaf_rn(-x[k], L11[j][k], a0);
+      a1 = __fmaf_rn(-x[k + 1], L11[j][k + 1], a1);
+    }
+    if (j & 1) a0 = __fmaf_rn(-x[j - 1], L11[j][j - 1], a0);
+    x[j] = __fmul_rn(__fadd_rn(a0, a1), dinv[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kNB; j += 4) {
+    if (v4) {
+      *reinterpret_cast<float4*>(row + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+    } else {
+      row[j] = x[j]; row[j + 1] = x[j + 1]; row[j + 2] = x[j + 2]; row[j + 3] = x[j + 3];
+    }
   }
 }
 
@@ -459,9 +563,9 @@ __global__ void chol_commit_kernel(DevState s) {
 
 cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk) {
   int n = 0;
-  const int bpr = tell_blocks_per_run(s);
-  cma_tellvec_kernel<<<(unsigned)(s.R * bpr), 128, 0, st>>>(s, bpr);
-  launch_sepcma_norm(s, st);                      // σ', h_σ (shared with Sep-CMA-ES)
+  const int bpr = (int)((s.D + kVecDims - 1) / kVecDims);    // ≤ normpart's R·⌈Q/128⌉·… capacity
+  cma_tellvec_kernel<<<dim3((unsigned)bpr, (unsigned)s.R), 256, 0, st>>>(s, bpr);
+  cma_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr);
   const int64_t RD = (int64_t)s.R * s.D;
   cma_pc_kernel<<<(unsigned)((RD + 255) / 256), 256, 0, st>>>(s);
   const int T = (int)((s.D + kTB - 1) / kTB);
@@ -473,12 +577,12 @@ cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, in
     chol_copy_kernel<<<dim3(cb, (unsigned)s.R), 256, 0, st>>>(s);
     n += 1;
     for (int64_t kb = 0; kb < s.D; kb += kNB) {
-      chol_diag_kernel<<<s.R, 256, 0, st>>>(s, (int)kb);
+      chol_diag_kernel<<<s.R, 64, 0, st>>>(s, (int)kb);
       const int64_t rest = s.D - kb - std::min<int64_t>(kNB, s.D - kb);
       n += 1;
       if (rest > 0) {
-        chol_panel_kernel<<<dim3((unsigned)((rest + 127) / 128), (unsigned)s.R), 128, 0, st>>>(
-            s, (int)kb);
+        chol_panel_kernel<<<dim3((unsigned)((rest + kPanelRows - 1) / kPanelRows), (unsigned)s.R),
+                            kPanelRows, 0, st>>>(s, (int)kb);
         const int Tt = (int)((rest + kTB - 1) / kTB);
         chol_update_kernel<<<dim3((unsigned)(Tt * (Tt + 1) / 2), (unsigned)s.R), 256, 0, st>>>(
             s, (int)kb);

@@ -8,9 +8,9 @@ from __future__ import annotations
 
 import numpy as np
 
-OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS = 0, 1, 2, 3, 4
+OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS, CMA_ES = 0, 1, 2, 3, 4, 5
 ALGO_NAMES = {OPENAI_ES: "openai_es", PGPE: "pgpe", SNES: "snes", SEP_CMA_ES: "sep_cma_es",
-              ARS: "ars"}
+              ARS: "ars", CMA_ES: "cma_es"}
 ADAM, SGD, CLIPUP = 0, 1, 2
 SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
 FN_NAMES = {SPHERE: "sphere", ROSENBROCK: "rosenbrock", RASTRIGIN: "rastrigin", MLP: "mlp"}
@@ -27,6 +27,9 @@ ANT = {
     # ARS has no App. B column (Table 1 row only): OpenAI-ES-like schedules, top-50 % pairs
     ARS: dict(sigma_init=0.05, sigma_decay=0.999, sigma_limit=0.01, lrate_init=0.01,
               lrate_decay=0.999, lrate_limit=0.001, elite_ratio=0.5),
+    # full CMA-ES (f4) has no App. B column: Hansen's defaults (μ = N/2), σ0 a quarter of the
+    # [-2, 2] init box
+    CMA_ES: dict(sigma_init=0.5, elite_ratio=0.5),
 }
 # The four App. B columns (Ant, Fetch, HalfCheetah, Humanoid) for the hyperparameter-vmap variant.
 SEP_CMA_COLUMNS = [(0.05, 0.4), (0.125, 0.2), (0.05, 0.5), (0.1, 0.2)]
@@ -60,6 +63,10 @@ CONFIGS = {
                R=1, gens=1000, init=(-2.0, 2.0)),
     "c4": dict(name="openai_es-mlp-D985216-N4096-R1", algo=OPENAI_ES, fn=MLP, D=985_216, N=4096,
                R=1, gens=100, init=(-0.04, 0.04)),
+    # SURVEY 8(f) f4 (no BASELINE config): full-covariance CMA-ES at "moderate D", the paper's
+    # population 256, 8 runs batched
+    "c6": dict(name="cma_es-rosenbrock-D1024-N256-R8", algo=CMA_ES, fn=ROSENBROCK, D=1024, N=256,
+               R=8, gens=100, init=(-2.0, 2.0)),
 }
 
 
