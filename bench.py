@@ -299,8 +299,10 @@ def main():
     ap.add_argument("--fused", type=int, default=None,
                     help="1: es_ask_eval (BBOB: one fused kernel; MLP: ask writes the fp16 image "
                          "the TMA-fed tcgen05 kernel reads). Default: on for c4, off otherwise")
-    ap.add_argument("--write-x", type=int, default=1,
-                    help="with --fused 1: also materialise the fp32 population x (default 1)")
+    ap.add_argument("--write-x", type=int, default=None,
+                    help="with --fused 1: also materialise the fp32 population x (default: 0 for "
+                         "c4, whose fitness reads the fp16 parameter image the ask writes; 1 "
+                         "otherwise)")
     ap.add_argument("--graph", type=int, default=None,
                     help="1: time replays of one generation captured as a CUDA graph "
                          "(default on for the launch-bound c1/c3)")
@@ -354,7 +356,7 @@ def main():
 
     fused = bool(args.fused) if args.fused is not None else args.config == "c4"
     fused = fused or dsplit                       # a D-shard evaluates inside es_ask_eval
-    write_x = bool(args.write_x)
+    write_x = bool(args.write_x) if args.write_x is not None else args.config != "c4"
 
     def step():
         for _, cfg, es, x, f in hs:
@@ -505,7 +507,7 @@ def main():
     kernels_ms = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in kinds.items()}
 
     # --- end to end through the C ABI with HOST buffers (fitness read back and fed to tell)
-    e2e = e2e_run(hs, args, 1 if sharded else world, fused)
+    e2e = e2e_run(hs, args, 1 if sharded else world, fused, write_x)
 
     cb = config_block(args.config, world)
     if dsplit:
@@ -549,7 +551,7 @@ def ncu_traffic(cfg_key, kernel):
     return d.get(cfg_key, {}).get(kernel)
 
 
-def e2e_run(hs, args, world, fused=False):
+def e2e_run(hs, args, world, fused=False, write_x=True):
     """Same metric through the public API with host buffers: per step and handle, ask on the
     device, evaluate into PINNED HOST fitness (D2H), tell from that host buffer (H2D), and read
     best_fitness back (D2H)."""
@@ -567,7 +569,8 @@ def e2e_run(hs, args, world, fused=False):
             if cfg["fn"] is None:
                 check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
             elif fused:
-                check(lib().es_ask_eval(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()),
+                check(lib().es_ask_eval(es.ctx, cfg["fn"],
+                                        C.c_void_p(x.data_ptr()) if write_x else None,
                                         C.c_void_p(f.data_ptr()), s), es.ctx)
             else:
                 es.ask(out=x)

@@ -36,7 +36,7 @@ static constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
 static constexpr int kThreadsTma = (1 + kEpiWarps + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
-static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 512;
+static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 2048;   // + barriers, bias
 
 struct MlpParams {
   int nl;                       // layers L
@@ -96,6 +96,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -151,6 +157,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 × 32-bit per lane to / from TMEM (the warp's lane quarter); st is waited on before returning.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4* h) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      "r"(h[0].x), "r"(h[0].y), "r"(h[0].z), "r"(h[0].w), "r"(h[1].x), "r"(h[1].y), "r"(h[1].z),
+      "r"(h[1].w), "r"(h[2].x), "r"(h[2].y), "r"(h[2].z), "r"(h[2].w), "r"(h[3].x), "r"(h[3].y),
+      "r"(h[3].z), "r"(h[3].w)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint4* h) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(h[0].x), "=r"(h[0].y), "=r"(h[0].z), "=r"(h[0].w), "=r"(h[1].x), "=r"(h[1].y),
+        "=r"(h[1].z), "=r"(h[1].w), "=r"(h[2].x), "=r"(h[2].y), "=r"(h[2].z), "=r"(h[2].w),
+        "=r"(h[3].x), "=r"(h[3].y), "=r"(h[3].z), "=r"(h[3].w)
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Byte offset of the 16-byte chunk c (k = 8c..8c+7) of row r in a [rows × 64] fp16 K-major
 // SWIZZLE_128B tile: 8-row groups of 1024 B, chunk index XOR (row mod 8).
 __host__ __device__ __forceinline__ uint32_t swz(int r, int c) {
@@ -179,10 +207,12 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages * kTileBytes);
   uint64_t* full = bars;                             // [kStages]
   uint64_t* empty = bars + kStages;                  // [kStages]
-  uint64_t* dready = bars + 2 * kStages;
-  uint64_t* aready = bars + 2 * kStages + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
-  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 3);   // [kEpiWarps] (64 B)
+  uint64_t* dready = bars + 2 * kStages;             // [4] per 128-column n-tile of a layer
+  uint64_t* aready = bars + 2 * kStages + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
+  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 6);   // [kEpiWarps] (64 B)
+  // TMA mode: the layer's fp16 bias, staged once per layer (≤ 512 values)
+  __half* bias_s = reinterpret_cast<__half*>(smem + kABytes + kStages * kTileBytes + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (smem_u32(smem) & 1023) __trap();               // SWIZZLE_128B needs 1024-B alignment
@@ -192,7 +222,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
       mbar_init(&full[s], TMA ? 1 : kProdWarps);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(dready, 1);
+    for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
     mbar_init(aready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -214,11 +244,27 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap[l])));
       int stage = 0;
       uint32_t phase = 0;
+      // L2 look-ahead: keep kAhead tiles (256 KB) of the stream requested from HBM, so that the
+      // weight stream continues while the ring is full during the epilogues
+      constexpr int kAhead = 16;
+      int64_t pm = blockIdx.x;
+      int pl = 1, pt = 0;
+      auto ahead = [&]() {
+        if (pm >= P.n) return;
+        const int kcn = P.kpad[pl - 1] >> 6;
+        tma_prefetch_3d(&P.tmap[pl], (pt % kcn) * 64, (pt / kcn) * 128, (int)pm);
+        if (++pt == (P.npad[pl] >> 7) * kcn) {
+          pt = 0;
+          if (++pl > L) { pl = 1; pm += gridDim.x; }
+        }
+      };
+      for (int k = 0; k < kAhead; ++k) ahead();
       for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
         for (int l = 1; l <= L; ++l) {
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
           for (int tile = 0; tile < nt_n * kc_n; ++tile) {
             const int nt = tile / kc_n, kc = tile % kc_n;
+            ahead();
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], kTileBytes);
             tma_load_3d(Bst + stage * kTileBytes, &P.tmap[l], kc * 64, nt * 128, (int)m,
@@ -307,7 +353,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
     const int q = warp & 3, part = e >> 2;
     const int row = q * 32 + lane;                   // batch row = TMEM lane
     const int et = threadIdx.x - kProd * 32;         // 0..511
-    uint32_t dphase = 0;
+    uint32_t dphase = 0;                             // bit k: parity of dready[k]
     for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
       const float* xm = P.x + m * P.D;
       // A <- layer-1 inputs (fp16 image, L2-resident)
@@ -325,21 +371,29 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         const int in = P.w[l - 1], out = P.w[l];
         const float* bias = TMA ? nullptr : xm + P.off[l] + (int64_t)out * in;
         const __half* bias16 = TMA ? P.x16 + m * P.D + P.off[l] + (int64_t)out * in : nullptr;
-        const int quarter = P.npad[l] >> 2;          // columns per part (multiple of 32)
-        mbar_wait(dready, dphase);
-        dphase ^= 1;
-        tc_fence_after();
-        // hidden layers also zero-fill the padded K columns [out, kpad) of the next A
-        const int cend = min((part + 1) * quarter, l < L ? P.kpad[l] : out);
-        for (int c0 = part * quarter; c0 < cend; c0 += 32) {
-          if (c0 >= out) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = make_uint4(0, 0, 0, 0);
-            }
-            continue;
-          }
+        const int ntl = P.npad[l] >> 7;              // n-tiles (dready barriers) of this layer
+        if (TMA) {
+          // stage the bias while the layer's MMAs run (its HBM latency was exposed per chunk)
+          for (int o = et; o < (out >> 3); o += kEpiWarps * 32)
+            reinterpret_cast<uint4*>(bias_s)[o] = __ldg(reinterpret_cast<const uint4*>(bias16) + o);
+          for (int n = (out & ~7) + et; n < P.npad[l]; n += kEpiWarps * 32)
+            bias_s[n] = n < out ? bias16[n] : __float2half_rn(0.0f);   // padded columns finite
+          named_bar(1, kEpiWarps * 32);
+        }
+
+        // hidden layers also zero-fill the padded K columns [out, kpad) of the next A. The next
+        // A overwrites this layer's A, which the remaining n-tiles' MMAs are still reading, so the
+        // packed fp16 results wait in TMEM — in the first 16 of the chunk's own (already read)
+        // accumulator columns — until the layer's last n-tile has completed. Each n-tile's 128
+        // columns are split over the four parts (32 each), so all 16 warps work on every tile as
+        // soon as it completes and the last tile's epilogue is short.
+        const int cend = l < L ? P.kpad[l] : out;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        for (int t = 0; t < ntl; ++t) {
+          mbar_wait(&dready[t], (dphase >> t) & 1u);
+          tc_fence_after();
+          const int c0 = t * 128 + part * 32;
+          if (c0 >= cend || c0 >= out) continue;     // padded K columns: zeros, written below
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
           // bias (N14: fp16(b), uniform across the warp → broadcast loads)
@@ -348,7 +402,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
             for (int i = 0; i < 32; i += 8) {
               const int n = c0 + i;
               if (n < out) {
-                const uint4 hb = __ldg(reinterpret_cast<const uint4*>(bias16 + n));
+                const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + n);
                 const __half* hh = reinterpret_cast<const __half*>(&hb);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) v[i + u] = tanhf(__fadd_rn(v[i + u], __half2float(hh[u])));
@@ -375,11 +429,10 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
             }
           }
           if (l < L) {
+            uint4 h[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {            // 4 chunks of 8 k in k-block c0/64
-              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = pack8(v + 8 * c);
-            }
+            for (int c = 0; c < 4; ++c) h[c] = pack8(v + 8 * c);
+            tmem_st16(trow + (uint32_t)c0, h);
           } else if (P.mode == 0) {
             const float* yr = P.Y + (int64_t)row * out;
 #pragma unroll
@@ -396,6 +449,21 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
               if (c0 + i < out) P.Y[(int64_t)row * out + c0 + i] = v[i];
           }
         }
+        if (l < L) {
+          for (int t = 0; t < ntl; ++t) {
+            const int c0 = t * 128 + part * 32;
+            if (c0 >= cend) continue;
+            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                          make_uint4(0, 0, 0, 0)};
+            if (c0 < out) tmem_ld16(trow + (uint32_t)c0, h);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {            // 4 chunks of 8 k in k-block c0/64
+              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = h[c];
+            }
+          }
+        }
+        dphase ^= (1u << ntl) - 1u;                  // every n-tile barrier completed once
         tc_fence_before();
         if (l < L) {
           fence_async_smem();
@@ -439,9 +507,11 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
               mma_f16(tmem + (uint32_t)(nt * 128), ad, bd, idesc, (kc | ks) != 0);
             }
             mma_commit(&empty[stage]);               // frees the stage when these MMAs finish
+            // n-tile nt's accumulator is complete: its epilogue quarter starts while the
+            // remaining n-tiles of the layer are still being multiplied
+            if (kc == kc_n - 1) mma_commit(&dready[nt]);
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          mma_commit(dready);                        // the layer's accumulator is complete
         }
       }
     }
