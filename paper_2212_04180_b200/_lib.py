@@ -24,7 +24,9 @@ EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "
            "es_destroy", "es_last_error", "es_status_string", "es_nccl_unique_id_size",
            "es_nccl_get_unique_id", "es_debug_primitive", "es_profile_enable", "es_profile_read",
            "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay",
-           "es_init_dshard", "es_dshard_plan", "es_dshard_info", "es_ask_eval_partial"]
+           "es_init_dshard", "es_dshard_plan", "es_dshard_info", "es_ask_eval_partial",
+           "es_p2p_export", "es_p2p_set_peers", "es_tell_p2p_apply", "es_p2p_ipc_export",
+           "es_p2p_ipc_open"]
 
 
 class RunParams(C.Structure):
@@ -37,6 +39,11 @@ class RunParams(C.Structure):
                 ("temperature", C.c_float), ("elite_ratio", C.c_float), ("shaping", C.c_int32),
                 ("optimizer", C.c_int32), ("momentum", C.c_float), ("max_speed", C.c_float),
                 ("weight_decay", C.c_float), ("clip_min", C.c_float), ("clip_max", C.c_float)]
+
+
+class PeerT(C.Structure):
+    """es_peer_t: a rank's direction-sum buffer and state-field device pointers (f2)."""
+    _fields_ = [("dirsum", C.c_void_p), ("field", C.c_void_p * 8)]
 
 
 class ESError(RuntimeError):
@@ -86,6 +93,11 @@ def lib():
         "es_dshard_plan": (i32, [i64, i32, i32, C.POINTER(i64)]),
         "es_dshard_info": (i32, [vp, C.POINTER(i64)]),
         "es_ask_eval_partial": (i32, [vp, i32, vp, vp, vp]),
+        "es_p2p_export": (i32, [vp, C.POINTER(PeerT)]),
+        "es_p2p_set_peers": (i32, [vp, C.POINTER(PeerT), i32]),
+        "es_tell_p2p_apply": (i32, [vp, vp]),
+        "es_p2p_ipc_export": (i32, [vp, vp]),
+        "es_p2p_ipc_open": (i32, [vp, vp]),
         "es_shard_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
         "es_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(i64), i32]),
     }

@@ -47,6 +47,9 @@ using namespace esb;
 struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
+  PeerTable peers{};            // f2 peer-memory tell (peers.W = 0: not set)
+  std::vector<void*> ipc_open;  // peer mappings opened by es_p2p_ipc_open
+  int* bar = nullptr;           // 4-byte NCCL barrier word
   int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
   std::vector<uint32_t> host_t; // completed tells per run (CMA-ES Cholesky refresh schedule)
   int64_t d0 = 0;               // first owned global dim
@@ -230,6 +233,7 @@ es_status_t es_destroy(es_ctx_t* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->mlp) mlp_problem_destroy(c->mlp);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
@@ -804,6 +808,16 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
     fsrc = c->fgather;
   }
+  if (s.W > 1 && c->peers.W == s.W) {
+    // f2: barrier → fused peer-memory reduce-scatter / update / all-gather → barrier
+    if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) return err;
+    if (!c->bar) CUDA_OR(c, dalloc(c, (void**)&c->bar, sizeof(int)));
+    NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    c->told_local = true;
+    if ((err = es_tell_p2p_apply(c, stream_)) != ES_SUCCESS) return err;
+    NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    return ES_SUCCESS;
+  }
   if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
   if (s.W > 1) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
     const size_t cnt = (size_t)(s.algo == OPENAI_ES || s.algo == ARS ? 1 : 2) * s.R * s.D;
@@ -847,6 +861,91 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
     CUDA_OR(c, cudaStreamSynchronize(st));
   }
   return ES_SUCCESS;
+}
+
+static bool p2p_algo_ok(const es_ctx* c) {
+  const int a = c->s.algo;
+  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS) && !c->any_clipup && !c->s.dshard;
+}
+
+es_status_t es_p2p_export(const es_ctx_t* c, es_peer_t* out) {
+  if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  out->dirsum = c->s.G;
+  for (int f = 0; f < 8; ++f) out->field[f] = c->s.vec[f];
+  return ES_SUCCESS;
+}
+
+es_status_t es_p2p_set_peers(es_ctx_t* c, const es_peer_t* peers, int32_t W) {
+  if (!c || !peers) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (W != c->s.W) return fail(c, ES_ERR_INVALID_ARG, "peers for %d ranks, context has %d", W, c->s.W);
+  if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
+  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
+  PeerTable pt{};
+  pt.W = W;
+  for (int v = 0; v < W; ++v) {
+    if (!peers[v].dirsum) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL dirsum", v);
+    pt.G[v] = peers[v].dirsum;
+    for (int f = 0; f < NVEC; ++f) {
+      pt.vec[v][f] = peers[v].field[f];
+      if (c->s.vec[f] && (f == F_MEAN || f == F_BEST_X || f == F_SIGMA_D) && !pt.vec[v][f])
+        return fail(c, ES_ERR_INVALID_ARG, "peer %d: field %d missing", v, f);
+    }
+  }
+  c->peers = pt;
+  return ES_SUCCESS;
+}
+
+es_status_t es_tell_p2p_apply(es_ctx_t* c, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_p2p_apply without es_tell_local");
+  if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
+  {
+    ProfScope ps(c, "p2p_apply", st);
+    CUDA_OR(c, launch_p2p_apply(c->s, c->peers, st));
+  }
+  c->launches += 1;
+  c->told_local = false;
+  c->asked = false;
+  return ES_SUCCESS;
+}
+
+es_status_t es_p2p_ipc_export(const es_ctx_t* c, void* handles) {
+  if (!c || !handles) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
+  std::memset(handles, 0, 9 * sizeof(cudaIpcMemHandle_t));
+  cudaError_t e = cudaIpcGetMemHandle(&h[0], c->s.G);
+  for (int f = 0; f < 8 && e == cudaSuccess; ++f)
+    if (c->s.vec[f]) e = cudaIpcGetMemHandle(&h[1 + f], c->s.vec[f]);
+  if (e != cudaSuccess) return fail(nullptr, ES_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  return ES_SUCCESS;
+}
+
+es_status_t es_p2p_ipc_open(es_ctx_t* c, const void* all) {
+  if (!c || !all) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  const int W = c->s.W;
+  if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
+  const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
+  static const cudaIpcMemHandle_t zero{};
+  std::vector<es_peer_t> peers(W);
+  for (int v = 0; v < W; ++v) {
+    if (v == c->s.rank) {
+      es_p2p_export(c, &peers[v]);
+      continue;
+    }
+    void* p = nullptr;
+    CUDA_OR(c, cudaIpcOpenMemHandle(&p, h[9 * v], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p);
+    peers[v].dirsum = static_cast<const double*>(p);
+    for (int f = 0; f < 8; ++f) {
+      peers[v].field[f] = nullptr;
+      if (std::memcmp(&h[9 * v + 1 + f], &zero, sizeof zero) == 0) continue;
+      CUDA_OR(c, cudaIpcOpenMemHandle(&p, h[9 * v + 1 + f], cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_open.push_back(p);
+      peers[v].field[f] = static_cast<float*>(p);
+    }
+  }
+  return es_p2p_set_peers(c, peers.data(), W);
 }
 
 es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t stream_) {

@@ -94,6 +94,15 @@ struct DevState {
   int32_t* chol_fail;  // [R] the last refresh failed (A kept)
 };
 
+// f2 peer-memory tell: every rank's direction-sum buffer and state fields, as device pointers
+// valid in this process (peer mappings over NVLink, or plain pointers for ranks emulated on one GPU).
+static constexpr int kMaxPeers = 8;
+struct PeerTable {
+  int W;
+  const double* G[kMaxPeers];
+  float* vec[kMaxPeers][NVEC];
+};
+
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
 // tell kernel and es_shard_plan so that host plan and device split cannot disagree.
 __host__ __device__ __forceinline__ void shard_range(int ne, int W, int rank, int& e0, int& e1) {
@@ -125,6 +134,9 @@ cudaError_t launch_ask_eval_partial(const DevState& s, int fn, float* x, double*
                                     double* fpart, cudaStream_t st);
 cudaError_t launch_partial_to_fitness(const double* fsum, int64_t n, float* f, cudaStream_t st);
 cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
+// f2: reduce-scatter (peer loads, rank order) → update of this rank's quad slice → all-gather
+// (peer stores) in one kernel
+cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st);
 // f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)
 cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,
                                 cudaStream_t st);

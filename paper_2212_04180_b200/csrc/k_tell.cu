@@ -340,6 +340,67 @@ __global__ void sepcma_norm_kernel(DevState s, int bpr) {
   }
 }
 
+// f2: the all-reduce of the direction sums and the update, fused over peer memory.
+// Rank w owns quads [Q·w/W, Q·(w+1)/W) of every run: it reads the W partial sums of its slice from
+// the peers' buffers (NVLink loads; summed in rank order, so every rank and the emulation agree
+// bit for bit), applies the update to the slice (its optimizer state is the only copy — the
+// "memory split across devices" of P:226), and writes the updated mean / σ_d / best_x of the
+// slice into every peer's state (NVLink stores). Compute and communication are one kernel; the
+// stream-ordered barriers around it are the caller's (es_tell uses two 4-byte NCCL all-reduces).
+template <int ALGO>
+__global__ void __launch_bounds__(TT) p2p_apply_kernel(DevState s, PeerTable pt, int64_t qa,
+                                                       int64_t qe, int bps) {
+  __shared__ double red[TT / 32];
+  const int r = blockIdx.x / bps;
+  const int64_t q = qa + (int64_t)(blockIdx.x % bps) * TT + threadIdx.x;
+  const bool active = q < qe;
+  constexpr bool kTwo = !(ALGO == OPENAI_ES || ALGO == ARS);
+  double G0[4] = {0.0, 0.0, 0.0, 0.0}, G1[4] = {0.0, 0.0, 0.0, 0.0};
+  if (active) {
+    for (int v = 0; v < pt.W; ++v) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t d = 4 * q + k;
+        if (d < s.D) {
+          G0[k] = __dadd_rn(G0[k], __ldcg(pt.G[v] + gidx(s, 0, r, d)));
+          if (kTwo) G1[k] = __dadd_rn(G1[k], __ldcg(pt.G[v] + gidx(s, 1, r, d)));
+        }
+      }
+    }
+  }
+  apply_update<ALGO>(s, r, q, active, G0, G1, 0, 1, red);
+  if (!active) return;
+  constexpr int kF[3] = {F_MEAN, F_BEST_X, F_SIGMA_D};
+  constexpr int nf = (ALGO == PGPE || ALGO == SNES) ? 3 : 2;
+  for (int v = 0; v < pt.W; ++v) {
+    if (v == s.rank) continue;
+#pragma unroll
+    for (int fi = 0; fi < nf; ++fi) {
+      const float* src = s.vec[kF[fi]];
+      float* dst = pt.vec[v][kF[fi]];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t d = 4 * q + k;
+        if (d < s.D) __stcg(dst + (int64_t)r * s.D + d, src[(int64_t)r * s.D + d]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st) {
+  const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
+  const int bps = (int)std::max<int64_t>(1, (qe - qa + TT - 1) / TT);
+  const unsigned g = (unsigned)(s.R * bps);
+  switch (s.algo) {
+    case OPENAI_ES: p2p_apply_kernel<OPENAI_ES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
+    case PGPE: p2p_apply_kernel<PGPE><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
+    case SNES: p2p_apply_kernel<SNES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
+    case ARS: p2p_apply_kernel<ARS><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // Sep-CMA-ES phase 3: p_c and C from Z, Q (s.G) and h_σ.
 __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

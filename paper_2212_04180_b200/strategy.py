@@ -130,6 +130,29 @@ class Strategy:
         """Split phase 1: rank the gathered fitness [W, R, N/W] and reduce this rank's entries."""
         check(lib().es_tell_local(self.ctx, _ptr(fitness_all), _stream(stream)), self.ctx)
 
+    # -- f2: fused peer-memory tell -------------------------------------------------------------
+    def p2p_export(self):
+        out = _lib.PeerT()
+        check(lib().es_p2p_export(self.ctx, C.byref(out)), self.ctx)
+        return out
+
+    def p2p_set_peers(self, peers):
+        arr = (_lib.PeerT * len(peers))(*peers)
+        check(lib().es_p2p_set_peers(self.ctx, arr, len(peers)), self.ctx)
+
+    def tell_p2p_apply(self, stream=None):
+        """After tell_local on every rank: reduce-scatter → update → all-gather in one kernel."""
+        check(lib().es_tell_p2p_apply(self.ctx, _stream(stream)), self.ctx)
+
+    def p2p_connect(self, group):
+        """Real multi-GPU: exchange CUDA IPC handles over `group` and map the peers' buffers."""
+        h = torch.zeros(9 * 64, dtype=torch.uint8)
+        check(lib().es_p2p_ipc_export(self.ctx, C.c_void_p(h.data_ptr())), self.ctx)
+        allh = [None] * torch.distributed.get_world_size(group)
+        torch.distributed.all_gather_object(allh, bytes(h.numpy()), group=group)
+        buf = torch.frombuffer(bytearray(b"".join(allh)), dtype=torch.uint8)
+        check(lib().es_p2p_ipc_open(self.ctx, C.c_void_p(buf.data_ptr())), self.ctx)
+
     def weight_decay(self, fitness, out=None, stream=None):
         """f + weight_decay·‖x_j‖² for this rank's members of the asked generation (es_tell does
         this itself; split-phase callers apply it to their slice before gathering)."""

@@ -361,3 +361,69 @@ def test_weight_decay_emulated_shards(algo):
                 assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, fld
     for es in shards + [ref]:
         es.close()
+
+
+# ------------------------------------------------------------------------ f2 peer-memory tell
+@pytest.mark.parametrize("algo,per", [(W.OPENAI_ES, [dict(), dict(optimizer=W.SGD)]),
+                                      (W.PGPE, [dict(), dict(elite_ratio=0.5)]),
+                                      (W.SNES, [dict()]), (W.ARS, ARS_ELITES)])
+@pytest.mark.parametrize("Wn,D", [(2, 301), (4, 1003), (8, 4099), (3, 37)])
+def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
+    """W ranks emulated on one GPU, each running the SAME fused kernel it would
+    run on its own GPU (peer pointers here are plain device pointers): after tell_local on every
+    rank, tell_p2p_apply on each reads the W partial sums of its slice, updates it and writes the
+    slice into every peer. Populations bit-identical to the unsharded run; mean / best_x / σ_d
+    (all-gathered) on every rank and the owned optimizer-state slices within 1e-6."""
+    from paper_2212_04180_b200 import strategy as S
+    N, R = 48, 3                              # N/W even for W = 2, 3, 4, 8
+    params = _params(algo, R, per)
+    ref = S.Strategy(algo, N, D, params)
+    shards = [S.Strategy(algo, N, D, params, shard=(w, Wn)) for w in range(Wn)]
+    peers = [sh.p2p_export() for sh in shards]
+    for sh in shards:
+        sh.p2p_set_peers(peers)
+    nl = N // Wn
+    Q = (D + 3) // 4
+    for gen in range(4):
+        x = ref.ask()
+        f = ref.eval(W.RASTRIGIN, x)
+        ref.tell(f)
+        locs = []
+        for w, sh in enumerate(shards):
+            xs = sh.ask()
+            assert torch.equal(xs, x[:, w * nl:(w + 1) * nl]), (gen, w)
+            locs.append(sh.eval(W.RASTRIGIN, xs))
+        gathered = torch.stack(locs).contiguous()
+        for sh in shards:
+            sh.tell_local(gathered)
+        for sh in shards:                      # after every rank's partial sums exist
+            sh.tell_p2p_apply()
+        for w, sh in enumerate(shards):
+            assert torch.equal(sh.get("perm"), ref.get("perm"))
+            fields = ["mean", "best_x"] + (["sigma_d"] if algo in (W.PGPE, W.SNES) else [])
+            for fld in fields:
+                assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, (fld, w)
+            if algo in (W.OPENAI_ES, W.PGPE):   # the rank's own optimizer-state slice
+                d0, d1 = 4 * (Q * w // Wn), min(D, 4 * (Q * (w + 1) // Wn))
+                a = sh.get("adam_m")[:, d0:d1].cpu().numpy()
+                b = ref.get("adam_m")[:, d0:d1].cpu().numpy()
+                assert q24(a, b) <= 1e-6, w
+    for es in shards + [ref]:
+        es.close()
+
+
+def test_p2p_rejections():
+    from paper_2212_04180_b200 import strategy as S
+    from paper_2212_04180_b200._lib import ESError
+    a = [S.Strategy(W.SEP_CMA_ES, 16, 8, _params(W.SEP_CMA_ES, 1), shard=(w, 2)) for w in range(2)]
+    with pytest.raises(ESError):
+        a[0].p2p_set_peers([s.p2p_export() for s in a])
+    b = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1), shard=(w, 2)) for w in range(2)]
+    with pytest.raises(ESError):
+        b[0].p2p_set_peers([b[0].p2p_export()])           # wrong world size
+    b[0].ask()
+    b[0].tell_local(torch.zeros(2, 1, 8, device="cuda"))
+    with pytest.raises(ESError):
+        b[0].tell_p2p_apply()                             # peers not set
+    for s in a + b:
+        s.close()
