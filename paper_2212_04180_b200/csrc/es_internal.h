@@ -145,6 +145,9 @@ int tell_blocks_per_run(const DevState& s);
 cudaError_t launch_cma_init(const DevState& s, cudaStream_t st);
 cudaError_t launch_cma_ask(const DevState& s, float* x, cudaStream_t st, int* nk);
 cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk);
+// the sampling contraction on tcgen05 (kind::tf32, 3-pass split); needs D % 4 == 0
+bool cma_tc_supported(const DevState& s);
+cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;
 int sm_count();

@@ -16,6 +16,7 @@
 //                  update); a run whose C is not positive definite keeps its previous factor.
 // The contractions here are FP32 FFMA tiles on the CUDA cores.
 #include <algorithm>
+#include <cstdlib>
 
 #include "es_internal.h"
 #include "noise.cuh"
@@ -140,6 +141,12 @@ cudaError_t launch_cma_ask(const DevState& s, float* x, cudaStream_t st, int* nk
   const int jpb = (s.N + nchunk - 1) / nchunk;
   nchunk = (s.N + jpb - 1) / jpb;
   cma_z_kernel<<<dim3((unsigned)(s.R * bpr), (unsigned)nchunk), 128, 0, st>>>(s, bpr, jpb);
+  static const bool simt = std::getenv("ES_CMA_SIMT") != nullptr;   // A/B switch for profiling
+  if (!simt && cma_tc_supported(s)) {
+    const cudaError_t e = launch_cma_sample_tc(s, x, st);
+    if (nk) *nk = 2;
+    return e;
+  }
   const dim3 g((unsigned)((s.D + kTB - 1) / kTB), (unsigned)((s.N + kTB - 1) / kTB), (unsigned)s.R);
   cma_sample_kernel<<<g, 256, 0, st>>>(s, x);
   if (nk) *nk = 2;
