@@ -188,27 +188,11 @@ __global__ void __launch_bounds__(256, 1) cma_sample_tc_kernel(const __grid_cons
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-            cudaSuccess && q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(f);
-  }
-  return fn;
-}
 
 // (k, row, run) fp32 view of a [runs][rows][D] array: box 32 k × 128 rows × 1 run lands in smem in
 // the UMMA K-major SWIZZLE_128B layout; out-of-range rows / k are zero-filled.
 static bool encode_rows(CUtensorMap* m, const float* base, int64_t D, int64_t rows, int runs) {
-  EncodeTiledFn enc = encode_tiled();
+  EncodeTiledFn enc = encode_tiled_fn();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)rows, (cuuint64_t)runs};
   const cuuint64_t strides[2] = {(cuuint64_t)D * 4, (cuuint64_t)(D * rows * 4)};
@@ -219,7 +203,7 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t D, int64_t ro
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool cma_tc_supported(const DevState& s) { return (s.D % 4) == 0 && encode_tiled() != nullptr; }
+bool cma_tc_supported(const DevState& s) { return (s.D % 4) == 0 && encode_tiled_fn() != nullptr; }
 
 cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st) {
   static bool attr = false;

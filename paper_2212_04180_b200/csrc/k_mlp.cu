@@ -484,28 +484,12 @@ static cudaError_t launch_mlp(const MlpParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-            cudaSuccess && q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(f);
-  }
-  return fn;
-}
 
 // Per layer: the fp16 image viewed as a 3-D tensor (k = in, n = out, member) with strides
 // (2 B, in·2 B, D·2 B); a box of 64 k × 128 n × 1 member lands in smem in exactly the UMMA
 // K-major SWIZZLE_128B layout of a B stage (rows past `out` / columns past `in` are zero-filled).
 static cudaError_t encode_maps(MlpParams& q, const __half* x16, int64_t n) {
-  EncodeTiledFn enc = encode_fn();
+  EncodeTiledFn enc = encode_tiled_fn();
   if (!enc) return cudaErrorNotSupported;
   for (int l = 1; l <= q.nl; ++l) {
     const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};

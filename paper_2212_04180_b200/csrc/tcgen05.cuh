@@ -3,6 +3,8 @@
 // instruction descriptors, tcgen05.mma / commit / ld / st. sm_100a only.
 #pragma once
 #include <cuda.h>
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace esb {
@@ -122,6 +124,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint4* h) {
         "=r"(h[3].x), "=r"(h[3].y), "=r"(h[3].z), "=r"(h[3].w)
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Host: cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
 }
 
 }  // namespace esb
