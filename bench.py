@@ -309,6 +309,10 @@ def main():
     ap.add_argument("--split", default="population", choices=["population", "dims"],
                     help="multi-GPU c1/c3: shard the population (P:226) or the dimensions "
                          "(f1 D-sharding: only R*N partial fitness doubles are all-reduced)")
+    ap.add_argument("--p2p", type=int, default=0,
+                    help="population-sharded configs: 1 = fused peer-memory tell (f2: CUDA IPC "
+                         "peer mappings, one reduce-scatter/update/all-gather kernel) instead of "
+                         "the NCCL all-reduce of the direction sums")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--N", type=int, default=SWEEP["N"], help="c5 popsize")
     ap.add_argument("--D", type=int, default=SWEEP["D"], help="c5 dimensions")
@@ -345,6 +349,8 @@ def main():
         es = S.Strategy(cfg["algo"], cfg["N"], cfg["D"], params,
                         group=dist.group.WORLD if sharded else None,
                         split="dims" if dsplit else "population")
+        if sharded and not dsplit and args.p2p:
+            es.p2p_connect(dist.group.WORLD)
         nl = es.local_popsize
         x = (torch.empty((cfg["R"], nl, es.x_dims), dtype=torch.float32, device="cuda")
              if cfg["fn"] is not None else None)
@@ -512,6 +518,8 @@ def main():
     cb = config_block(args.config, world)
     if dsplit:
         cb["parallelism"] = f"dimensions sharded x{world} (R*N partial-fitness all-reduce only)"
+    elif sharded and args.p2p:
+        cb["parallelism"] = f"population sharded x{world}, fused peer-memory tell (f2)"
     if hs[0][1]["fn"] is None:
         cb["path"] = "synthetic fitness, tell"
     elif fused and hs[0][1]["fn"] == W.MLP:
