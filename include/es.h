@@ -245,6 +245,21 @@ es_status_t es_tell_p2p_apply(es_ctx_t *ctx, es_stream_t stream);
 es_status_t es_p2p_ipc_export(const es_ctx_t *ctx, void *handles /* 9 × 64 bytes */);
 es_status_t es_p2p_ipc_open(es_ctx_t *ctx, const void *handles_all /* W × 9 × 64 bytes */);
 
+/* f2, NVLS variant: the same fused tell with the reduction done INSIDE the NVSwitch. Every rank
+ * binds one symmetric buffer (direction sums, mean, best_x, σ_d) to a multicast object; the kernel
+ * reads Σ_ranks of its slice with multimem.ld_reduce.add.f64 and broadcasts the updated slice with
+ * multimem.st. Setup (collective): one rank calls es_nvls_open(creator = 1), which writes the
+ * 64-byte fabric handle of the multicast object to *handle; the others call it with creator = 0
+ * and that handle; after a barrier every rank calls es_nvls_bind (which moves those fields into
+ * the bound buffer); after another barrier es_tell uses this path (W > 1 with a communicator),
+ * or callers run es_tell_local → barrier → es_tell_nvls_apply → barrier. The in-switch sum
+ * order is the hardware's (results may differ from the rank-ordered paths in the last binary64
+ * bits). Errors: ES_ERR_UNSUPPORTED without multicast / fabric-handle support or for other
+ * algorithms; ES_ERR_BAD_STATE out of order. */
+es_status_t es_nvls_open(es_ctx_t *ctx, void *handle /* 64 bytes */, int32_t creator);
+es_status_t es_nvls_bind(es_ctx_t *ctx);
+es_status_t es_tell_nvls_apply(es_ctx_t *ctx, es_stream_t stream);
+
 /* Weight-decay regularisation of this rank's fitness slice:
  * out[r][j] = (float)((double)fitness[r][j] + (double)weight_decay_r · Σ_d (double)x_jd²) for the
  * members x_j of the current (asked, not yet told) generation, regenerated from the noise counter

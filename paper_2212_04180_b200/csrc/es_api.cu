@@ -48,6 +48,7 @@ struct es_ctx {
   DevState s{};
   std::vector<RunScal> host_rs;
   PeerTable peers{};            // f2 peer-memory tell (peers.W = 0: not set)
+  NvlsHost nvls;                // f2 NVLS multicast tell (stage 2: bound)
   std::vector<void*> ipc_open;  // peer mappings opened by es_p2p_ipc_open
   int* bar = nullptr;           // 4-byte NCCL barrier word
   int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
@@ -233,6 +234,10 @@ es_status_t es_destroy(es_ctx_t* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->nvls.stage) {
+    cudaDeviceSynchronize();
+    nvls_close(c->nvls);
+  }
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->mlp) mlp_problem_destroy(c->mlp);
   for (void* p : c->allocs) cudaFree(p);
@@ -808,6 +813,16 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
     fsrc = c->fgather;
   }
+  if (s.W > 1 && c->nvls.stage == 2) {
+    // f2 NVLS: barrier → in-switch reduce-scatter / update / multicast all-gather → barrier
+    if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) return err;
+    if (!c->bar) CUDA_OR(c, dalloc(c, (void**)&c->bar, sizeof(int)));
+    NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    c->told_local = true;
+    if ((err = es_tell_nvls_apply(c, stream_)) != ES_SUCCESS) return err;
+    NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    return ES_SUCCESS;
+  }
   if (s.W > 1 && c->peers.W == s.W) {
     // f2: barrier → fused peer-memory reduce-scatter / update / all-gather → barrier
     if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) return err;
@@ -903,6 +918,63 @@ es_status_t es_tell_p2p_apply(es_ctx_t* c, es_stream_t stream_) {
   {
     ProfScope ps(c, "p2p_apply", st);
     CUDA_OR(c, launch_p2p_apply(c->s, c->peers, st));
+  }
+  c->launches += 1;
+  c->told_local = false;
+  c->asked = false;
+  return ES_SUCCESS;
+}
+
+es_status_t es_nvls_open(es_ctx_t* c, void* handle, int32_t creator) {
+  if (!c || !handle) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "NVLS tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
+  if (c->nvls.stage) return fail(c, ES_ERR_BAD_STATE, "es_nvls_open called twice");
+  if (const char* e = nvls_open(c->s, c->nvls, handle, creator != 0)) {
+    nvls_close(c->nvls);
+    return fail(c, ES_ERR_UNSUPPORTED, "NVLS: %s", e);
+  }
+  return ES_SUCCESS;
+}
+
+es_status_t es_nvls_bind(es_ctx_t* c) {
+  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (const char* e = nvls_bind(c->nvls)) return fail(c, ES_ERR_BAD_STATE, "NVLS: %s", e);
+  // move the symmetric fields into the bound buffer (unicast alias) and repoint the state
+  DevState& s = c->s;
+  const size_t RD = (size_t)s.R * s.D;
+  char* base = reinterpret_cast<char*>(c->nvls.uva);
+  double* G = reinterpret_cast<double*>(base + c->nvls.off_g);
+  CUDA_OR(c, cudaMemcpy(G, s.G, 2 * RD * sizeof(double), cudaMemcpyDeviceToDevice));
+  s.G = G;
+  const int f[3] = {F_MEAN, F_BEST_X, F_SIGMA_D};
+  const size_t off[3] = {c->nvls.off_mean, c->nvls.off_best, c->nvls.off_sig};
+  for (int i = 0; i < 3; ++i) {
+    if (!s.vec[f[i]]) continue;
+    float* dst = reinterpret_cast<float*>(base + off[i]);
+    CUDA_OR(c, cudaMemcpy(dst, s.vec[f[i]], RD * sizeof(float), cudaMemcpyDeviceToDevice));
+    s.vec[f[i]] = dst;
+  }
+  return ES_SUCCESS;
+}
+
+static NvlsView nvls_view(const es_ctx* c) {
+  char* mc = reinterpret_cast<char*>(c->nvls.mcva);
+  NvlsView v;
+  v.G = reinterpret_cast<const double*>(mc + c->nvls.off_g);
+  v.mean = reinterpret_cast<float*>(mc + c->nvls.off_mean);
+  v.best = reinterpret_cast<float*>(mc + c->nvls.off_best);
+  v.sig = c->nvls.off_sig == (size_t)-1 ? nullptr : reinterpret_cast<float*>(mc + c->nvls.off_sig);
+  return v;
+}
+
+es_status_t es_tell_nvls_apply(es_ctx_t* c, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_nvls_apply without es_tell_local");
+  if (c->nvls.stage != 2) return fail(c, ES_ERR_BAD_STATE, "NVLS buffer not bound");
+  {
+    ProfScope ps(c, "nvls_apply", st);
+    CUDA_OR(c, launch_nvls_apply(c->s, nvls_view(c), st));
   }
   c->launches += 1;
   c->told_local = false;

@@ -13,6 +13,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+
 #include <cstdint>
 
 namespace esb {
@@ -103,6 +105,26 @@ struct PeerTable {
   float* vec[kMaxPeers][NVEC];
 };
 
+// f2 NVLS variant: one symmetric buffer per rank bound to a multicast object.
+struct NvlsHost {
+  CUdevice dev = 0;
+  size_t gran = 0, bytes = 0, used = 0;
+  size_t off_g = 0, off_mean = 0, off_best = 0, off_sig = (size_t)-1;
+  CUmemGenericAllocationHandle phys = 0, mc = 0;
+  CUdeviceptr uva = 0, mcva = 0;
+  bool have_mc = false, have_phys = false;
+  int stage = 0;                      // 1 opened (device added, memory mapped), 2 bound
+};
+struct NvlsView {                     // multicast addresses of the symmetric fields
+  const double* G;
+  float* mean;
+  float* best;
+  float* sig;                         // nullptr if σ_d is not kept
+};
+const char* nvls_open(const DevState& s, NvlsHost& h, void* handle, bool creator);
+const char* nvls_bind(NvlsHost& h);
+void nvls_close(NvlsHost& h);
+
 // Population sharding: rank's contiguous share [e0, e1) of ne tell entries. Shared by the
 // tell kernel and es_shard_plan so that host plan and device split cannot disagree.
 __host__ __device__ __forceinline__ void shard_range(int ne, int W, int rank, int& e0, int& e1) {
@@ -137,6 +159,8 @@ cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 // f2: reduce-scatter (peer loads, rank order) → update of this rank's quad slice → all-gather
 // (peer stores) in one kernel
 cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st);
+// f2 NVLS: the same with multimem.ld_reduce (sum in the switch) and multimem.st (broadcast)
+cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t st);
 // f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)
 cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f, float* out,
                                 cudaStream_t st);

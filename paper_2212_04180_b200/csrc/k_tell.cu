@@ -401,6 +401,68 @@ cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_
   return cudaGetLastError();
 }
 
+// f2 NVLS variant of p2p_apply_kernel: the W partial sums of the slice are added inside the switch
+// (multimem.ld_reduce on the multicast alias of every rank's G), and the updated slice is
+// broadcast with one multimem.st per value. Summation order is the switch's, so results can differ
+// from the rank-ordered P2P / NCCL paths in the last binary64 bits.
+__device__ __forceinline__ double mm_ld_add_f64(const double* mc) {
+  double v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];" : "=d"(v) : "l"(mc) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st_f32(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(TT) nvls_apply_kernel(DevState s, NvlsView v, int64_t qa,
+                                                        int64_t qe, int bps) {
+  __shared__ double red[TT / 32];
+  asm volatile("fence.proxy.alias;" ::: "memory");
+  const int r = blockIdx.x / bps;
+  const int64_t q = qa + (int64_t)(blockIdx.x % bps) * TT + threadIdx.x;
+  const bool active = q < qe;
+  constexpr bool kTwo = !(ALGO == OPENAI_ES || ALGO == ARS);
+  double G0[4] = {0.0, 0.0, 0.0, 0.0}, G1[4] = {0.0, 0.0, 0.0, 0.0};
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t d = 4 * q + k;
+      if (d < s.D) {
+        G0[k] = mm_ld_add_f64(v.G + gidx(s, 0, r, d));
+        if (kTwo) G1[k] = mm_ld_add_f64(v.G + gidx(s, 1, r, d));
+      }
+    }
+  }
+  apply_update<ALGO>(s, r, q, active, G0, G1, 0, 1, red);
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t d = 4 * q + k;
+      if (d >= s.D) break;
+      const int64_t idx = (int64_t)r * s.D + d;
+      mm_st_f32(v.mean + idx, s.vec[F_MEAN][idx]);
+      mm_st_f32(v.best + idx, s.vec[F_BEST_X][idx]);
+      if (v.sig) mm_st_f32(v.sig + idx, s.vec[F_SIGMA_D][idx]);
+    }
+  }
+  asm volatile("fence.proxy.alias;" ::: "memory");
+}
+
+cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t st) {
+  const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
+  const int bps = (int)std::max<int64_t>(1, (qe - qa + TT - 1) / TT);
+  const unsigned g = (unsigned)(s.R * bps);
+  switch (s.algo) {
+    case OPENAI_ES: nvls_apply_kernel<OPENAI_ES><<<g, TT, 0, st>>>(s, v, qa, qe, bps); break;
+    case PGPE: nvls_apply_kernel<PGPE><<<g, TT, 0, st>>>(s, v, qa, qe, bps); break;
+    case SNES: nvls_apply_kernel<SNES><<<g, TT, 0, st>>>(s, v, qa, qe, bps); break;
+    case ARS: nvls_apply_kernel<ARS><<<g, TT, 0, st>>>(s, v, qa, qe, bps); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // Sep-CMA-ES phase 3: p_c and C from Z, Q (s.G) and h_σ.
 __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -144,6 +144,34 @@ class Strategy:
         """After tell_local on every rank: reduce-scatter → update → all-gather in one kernel."""
         check(lib().es_tell_p2p_apply(self.ctx, _stream(stream)), self.ctx)
 
+    def nvls_open(self, creator, handle=None):
+        """f2 NVLS: create (creator) or join the multicast object; returns the 64-byte handle."""
+        h = torch.zeros(64, dtype=torch.uint8)
+        if handle is not None:
+            h[:] = torch.frombuffer(bytearray(handle), dtype=torch.uint8)
+        check(lib().es_nvls_open(self.ctx, C.c_void_p(h.data_ptr()), 1 if creator else 0),
+              self.ctx)
+        return bytes(h.numpy())
+
+    def nvls_bind(self):
+        check(lib().es_nvls_bind(self.ctx), self.ctx)
+
+    def tell_nvls_apply(self, stream=None):
+        check(lib().es_tell_nvls_apply(self.ctx, _stream(stream)), self.ctx)
+
+    def nvls_connect(self, group):
+        """Real multi-GPU: rank 0 creates the multicast object, the others join, all bind."""
+        rank = torch.distributed.get_rank(group)
+        h = self.nvls_open(True) if rank == 0 else None
+        obj = [h]
+        torch.distributed.broadcast_object_list(obj, src=torch.distributed.get_global_rank(group, 0),
+                                                group=group)
+        if rank != 0:
+            self.nvls_open(False, obj[0])
+        torch.distributed.barrier(group)
+        self.nvls_bind()
+        torch.distributed.barrier(group)
+
     def p2p_connect(self, group):
         """Real multi-GPU: exchange CUDA IPC handles over `group` and map the peers' buffers."""
         h = torch.zeros(9 * 64, dtype=torch.uint8)

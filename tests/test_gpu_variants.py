@@ -427,3 +427,34 @@ def test_p2p_rejections():
         b[0].tell_p2p_apply()                             # peers not set
     for s in a + b:
         s.close()
+
+
+# ------------------------------------------------------------------------ f2 NVLS (multicast)
+@pytest.mark.parametrize("algo", [W.OPENAI_ES, W.PGPE, W.SNES, W.ARS])
+def test_nvls_tell_single_rank(algo):
+    """The NVLS path on the one GPU available: a one-device multicast team. The fused kernel's
+    multimem.ld_reduce then returns this rank's sums and multimem.st writes back through the
+    switch alias — exercising the object lifecycle (VMM, bind, multicast mapping), the PTX and the
+    buffer relocation; the result must equal the ordinary tell bit for bit."""
+    from paper_2212_04180_b200 import strategy as S
+    from paper_2212_04180_b200._lib import ESError
+    N, D, R = 32, 1003, 3
+    params = _params(algo, R)
+    ref = S.Strategy(algo, N, D, params)
+    es = S.Strategy(algo, N, D, params)
+    try:
+        es.nvls_open(True)
+    except ESError as e:
+        pytest.skip(f"no multicast on this box: {e}")
+    es.nvls_bind()
+    for gen in range(3):
+        x = ref.ask()
+        f = ref.eval(W.RASTRIGIN, x)
+        ref.tell(f)
+        assert torch.equal(es.ask(), x)
+        es.tell_local(f)
+        es.tell_nvls_apply()
+        for fld in KEPT[algo]:
+            assert torch.equal(es.get(fld), ref.get(fld)), (gen, fld)
+    es.close()
+    ref.close()
