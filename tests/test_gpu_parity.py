@@ -493,3 +493,33 @@ def test_mlp_fused_fp16_image_path(widths, N):
     assert q24(f1[0].cpu().numpy(), ref) <= 1e-4
     es.tell(f1)
     es.close()
+
+
+def test_config4_full_size_sampled_members():
+    """C4 in the launch configuration bench.py times (es_ask_eval, the fp16 image and the TMA-fed
+    tcgen05 MLP, N = 4096, D = 985,216): the oracle's MLP fitness of sampled members (first, last,
+    both members of a middle pair) within the derived bar; the fp16 image of those members equals
+    fp16 of the oracle's x; one tell then moves sampled dims of the mean exactly as the oracle's
+    dimension-subset run fed the GPU's fitness."""
+    from paper_2212_04180_b200 import strategy as S
+    widths = [256, 512, 512, 512, 512, 128]
+    cfg = W.CONFIGS["c4"]
+    m = O.MLP(widths, 128, 0)
+    assert m.D == cfg["D"]
+    params = [W.config_params(cfg, 0)]
+    es = S.Strategy(W.OPENAI_ES, cfg["N"], cfg["D"], params)
+    es.set_mlp_problem(widths, 128, 0)
+    _, f = es.ask_eval(W.MLP, write_x=False)
+    fh = f.cpu().numpy()[0]
+    run = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], **params[0])
+    for j in (0, 2048, 2049, cfg["N"] - 1):
+        xo = run.member(j)
+        fo = m.evaluate(xo)[0]
+        assert abs(float(fh[j]) - float(fo)) <= 1e-5 * max(abs(float(fo)), 0.1), (j, fh[j], fo)
+    dims = np.sort(np.random.default_rng(3).choice(cfg["D"], 64, replace=False))
+    sub = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], dims=dims, **params[0])
+    es.tell(f)
+    sub.tell(fh)
+    got = es.get("mean")[0].cpu().numpy()[dims]
+    assert q24(got, sub.mean) <= 1e-5
+    es.close()
