@@ -523,3 +523,63 @@ def test_config4_full_size_sampled_members():
     got = es.get("mean")[0].cpu().numpy()[dims]
     assert q24(got, sub.mean) <= 1e-5
     es.close()
+
+
+def _ranks_equal(gpu, r, f_orc):
+    s, e, perm = O.rank(f_orc)
+    return (np.array_equal(gpu.get("perm")[r].cpu().numpy(), perm) and
+            np.array_equal(gpu.get("rank_s")[r].cpu().numpy(), s))
+
+
+@pytest.mark.parametrize("key", ["c2_sepcma", "c2_snes"])
+def test_config2_hundred_generations_sampled_runs(key):
+    """SURVEY §8(d) parity protocol at full C2 size (R = 512 runs in the GPU batch): runs 0 and 511
+    followed by free-running oracles (each side evaluates its own population) for 100 generations —
+    populations bit-exact and ranks identical at every generation, state within 1e-5 after
+    generation 1 and 1e-3 after 100."""
+    cfg = W.CONFIGS[key]
+    R, N, D = cfg["R"], cfg["N"], cfg["D"]
+    params = [W.config_params(cfg, r, hyper_vmap=True) for r in range(R)]
+    from paper_2212_04180_b200 import strategy as S
+    es = S.Strategy(cfg["algo"], N, D, params)
+    sample = (0, R - 1)
+    orcs = {r: O.Run(cfg["algo"], N, D, **params[r]) for r in sample}
+    names = ["mean", "sigma_d", "adam_m", "adam_v", "p_sigma", "p_c", "C", "best_x"]
+    for g in range(100):
+        x = es.ask()
+        f = es.eval(cfg["fn"], x)
+        es.tell(f)
+        xh = x.cpu().numpy()
+        for r, o in orcs.items():
+            xo = o.ask()
+            assert np.array_equal(bits(xh[r]), bits(xo)), (g, r)
+            fo = O.evaluate(cfg["fn"], xo)
+            o.tell(fo)
+            assert _ranks_equal(es, r, fo), (g, r)
+            if g in (0, 99):
+                tol = 1e-5 if g == 0 else 1e-3
+                for fld in KEPT[cfg["algo"]]:
+                    assert q24(es.get(fld)[r].cpu().numpy(), o.vec[names.index(fld)]) <= tol, (g, fld)
+    es.close()
+
+
+def test_config3_hundred_generations():
+    """C3 at full size (D = 1e5, N = 256) for 100 free-running generations: populations bit-exact
+    and ranks identical every generation, state within 1e-3 at the end."""
+    cfg = W.CONFIGS["c3"]
+    params = [W.config_params(cfg, 0)]
+    pair = Pair(cfg["algo"], cfg["N"], cfg["D"], params)
+    o = pair.orc[0]
+    for g in range(100):
+        x = pair.gpu.ask()
+        f = pair.gpu.eval(cfg["fn"], x)
+        pair.gpu.tell(f)
+        xo = o.ask()
+        assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo)), g
+        fo = O.evaluate(cfg["fn"], xo)
+        o.tell(fo)
+        assert _ranks_equal(pair.gpu, 0, fo), g
+        if g == 0:
+            pair.compare(0, 1e-5)
+    pair.compare(0, 1e-3)
+    pair.close()
