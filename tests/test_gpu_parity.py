@@ -424,25 +424,28 @@ def test_mlp_fitness_parity(widths, n):
 
 
 def test_mlp_openai_es_generations_teacher_forced():
-    """Config-4 path at reduced size ([32, 64x4, 16], D = 15,632, N = 256): ask bit-exact, MLP
-    fitness within the derived 1e-4 (Q24), tell fed the GPU's fitness within 1e-5, 5 generations."""
+    """Config-4 path (the bench's fused es_ask_eval with the fp16 image) at SURVEY §8(d)'s reduced
+    size ([32, 64x4, 16], D = 15,632, N = 256) for 100 generations: ask bit-exact every
+    generation, MLP fitness within the derived 1e-4 (Q24) on sampled generations, tell fed the
+    GPU's fitness within 1e-5 after one generation and 1e-3 after 100."""
     from paper_2212_04180_b200 import strategy as S
     widths = [32, 64, 64, 64, 64, 16]
     m = O.MLP(widths, 128, 3)
     params = [W.run_params(W.OPENAI_ES, 9, init_min=-0.04, init_max=0.04)]
     pair = Pair(W.OPENAI_ES, 256, m.D, params)
     pair.gpu.set_mlp_problem(widths, 128, 3)
-    for g in range(5):
-        x = pair.gpu.ask()
-        f = pair.gpu.eval(W.MLP, x)
+    for g in range(100):
+        x, f = pair.gpu.ask_eval(W.MLP)
         xo = pair.orc[0].ask()
-        assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo))
-        if g in (0, 4):
+        assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo)), g
+        if g in (0, 50, 99):
             fo = m.evaluate(xo[:32])
-            assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-4
+            assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-4, g
         pair.gpu.tell(f)
         pair.orc[0].tell(f[0].cpu().numpy())
-        pair.compare(0, 1e-5)
+        if g == 0:
+            pair.compare(0, 1e-5)
+    pair.compare(0, 1e-3)
     pair.close()
 
 
