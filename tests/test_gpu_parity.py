@@ -586,3 +586,23 @@ def test_config3_hundred_generations():
             pair.compare(0, 1e-5)
     pair.compare(0, 1e-3)
     pair.close()
+
+
+@pytest.mark.parametrize("N,D", [(256, 1000), (1024, 1000), (256, 10_000), (1024, 10_000)])
+def test_config5_corner_full(N, D):
+    """SURVEY §8(d) C5 corner (N ≤ 1024, D ≤ 1e4), the sweep's exact path: synthetic fitness
+    (N15, bit-exact vs the oracle's generator) → rank → tell, compared over the full D for 5
+    generations (ranks identical, state ≤ 1e-5 each generation)."""
+    cfg = dict(algo=W.OPENAI_ES, init=(-0.04, 0.04))
+    params = [W.config_params(cfg, 0)]
+    pair = Pair(W.OPENAI_ES, N, D, params)
+    o = pair.orc[0]
+    for g in range(5):
+        f = pair.gpu.synth_fitness()
+        fo = O.synth_fitness(params[0]["seed"], o.t, N)
+        assert np.array_equal(bits(f[0].cpu().numpy()), bits(fo)), g
+        pair.gpu.tell(f)
+        o.tell(fo)
+        assert _ranks_equal(pair.gpu, 0, fo), g
+        pair.compare(0, 1e-5)
+    pair.close()
