@@ -248,8 +248,69 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* keys, int n, int64_t gbas
   }
 }
 
-// N ≤ 16384: one CTA per run, the whole sort in shared memory.
-__global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad) {
+// Whole-block bitonic sort of npad = E·T keys held in registers, blocked layout (thread t owns
+// elements t·E .. t·E+E−1). Stride j < E: in-register compare-exchange; E ≤ j < 32E: partner in the
+// same warp, exchanged with shuffles; j ≥ 32E: through shared memory (two barriers). Same network
+// (and so the same result) as bitonic_smem, with a barrier only on the shared-memory strides.
+template <int E, int J>
+__device__ __forceinline__ void reg_stage(uint64_t (&a)[E], int t, int k) {
+  if constexpr (J < E) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & J) continue;                           // static: e, J are compile-time here
+      const int e2 = e | J;
+      const bool asc = (((t * E + e) & k) == 0);
+      const uint64_t x = a[e], y = a[e2];
+      if ((x > y) == asc) { a[e] = y; a[e2] = x; }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void bitonic_regs(uint64_t* keys, int npad) {
+  const int t = threadIdx.x;
+  uint64_t a[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) a[e] = keys[t * E + e];
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+        if (j == 1) reg_stage<E, 1>(a, t, k);
+        else if (j == 2) reg_stage<E, 2>(a, t, k);
+        else if (j == 4) reg_stage<E, 4>(a, t, k);
+        else reg_stage<E, 8>(a, t, k);
+      } else if (j < 32 * E) {
+        // j, k ≥ E: direction and half depend on the thread only (g = t·E + e, e < E ≤ j)
+        const int lm = j / E;                          // partner lane mask
+        const bool keep_min = (((t * E) & j) == 0) == (((t * E) & k) == 0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, a[e], lm);
+          a[e] = keep_min ? (a[e] < o ? a[e] : o) : (a[e] > o ? a[e] : o);
+        }
+      } else {
+        const bool keep_min = (((t * E) & j) == 0) == (((t * E) & k) == 0);
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) keys[t * E + e] = a[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t o = keys[(t * E + e) ^ j];
+          a[e] = keep_min ? (a[e] < o ? a[e] : o) : (a[e] > o ? a[e] : o);
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) keys[t * E + e] = a[e];
+  __syncthreads();
+}
+
+// 8192 < N ≤ 16384: one CTA per run, the classic shared-memory network (16 keys per thread would
+// not fit the register file at 1024 threads).
+__global__ void rank_kernel_smem(DevState s, const float* __restrict__ fsrc, int npad) {
   extern __shared__ uint64_t keys[];
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
@@ -257,6 +318,19 @@ __global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad
   for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p);
   __syncthreads();
   bitonic_smem(keys, npad, 0, 2, npad, npad);
+  rank_finish(s, r, keys, red, &sh_nw);
+}
+
+// N ≤ 8192: one CTA per run, the sort in registers (+ shared memory for the long strides).
+template <int E>
+__global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad) {
+  extern __shared__ uint64_t keys[];
+  __shared__ double red[32];
+  __shared__ int32_t sh_nw;
+  const int r = blockIdx.x;
+  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p);
+  __syncthreads();
+  bitonic_regs<E>(keys, npad);
   rank_finish(s, r, keys, red, &sh_nw);
 }
 
@@ -318,14 +392,24 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
   while (npad < s.N) npad <<= 1;
   static bool attr_set = false;
   if (!attr_set) {
-    for (const void* f : {(const void*)rank_kernel, (const void*)rank_chunk_sort_kernel,
-                          (const void*)rank_chunk_merge_kernel})
+    for (const void* f : {(const void*)rank_kernel<2>, (const void*)rank_kernel<4>,
+                          (const void*)rank_kernel<8>, (const void*)rank_kernel_smem,
+                          (const void*)rank_chunk_sort_kernel, (const void*)rank_chunk_merge_kernel})
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   if (npad <= kChunk) {
-    const int T = std::min(1024, std::max(32, npad / 2));
-    rank_kernel<<<s.R, T, (size_t)npad * sizeof(uint64_t), st>>>(s, fsrc, npad);
+    // E keys per thread: 2 while the block grows to 1024 threads, then 4, 8, 16 (npad ≥ 64)
+    const int pad = std::max(npad, 64);
+    const int T = std::min(1024, pad / 2);
+    const int E = pad / T;
+    const size_t sm = (size_t)pad * sizeof(uint64_t);
+    switch (E) {
+      case 2: rank_kernel<2><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
+      case 4: rank_kernel<4><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
+      case 8: rank_kernel<8><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
+      default: rank_kernel_smem<<<s.R, T, sm, st>>>(s, fsrc, pad); break;
+    }
     return cudaGetLastError();
   }
   const int nch = npad / kChunk;
