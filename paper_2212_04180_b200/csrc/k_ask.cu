@@ -88,10 +88,13 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   }
   const int dir0 = s.rank * Ploc;
   const float lo = CLIP ? rs.clip_lo : 0.0f, hi = CLIP ? rs.clip_hi : 0.0f;
-  float* xr = x ? x + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
-  __half* hr = W16 ? x16 + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
+  // row pointers advance by one direction's rows per iteration (no per-iteration 64-bit multiply)
+  const int64_t step = (kAnti ? 2 : 1) * s.Dx;
+  const int64_t first = (int64_t)r * s.Nloc * s.Dx + 4 * q + (int64_t)i0 * step;
+  float* p0 = x ? x + first : nullptr;
+  __half* h0 = W16 ? x16 + first : nullptr;
 #pragma unroll 2
-  for (int il = i0; il < i1; ++il) {
+  for (int il = i0; il < i1; ++il, p0 += (x ? step : 0), h0 += (W16 ? step : 0)) {
     const float4 z = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)(dir0 + il), t);
     const float zz[4] = {z.x, z.y, z.z, z.w};
     float xp[4], xm[4];
@@ -104,9 +107,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
         if (kAnti) xm[k] = fminf(fmaxf(xm[k], lo), hi);
       }
     }
-    const int64_t row = kAnti ? 2 * (int64_t)il : il;
     if (W16) {            // D % 4 == 0 is required for this path (8-byte stores)
-      __half* h0 = hr + row * s.Dx;
       __half2 a0 = __floats2half2_rn(xp[0], xp[1]), a1 = __floats2half2_rn(xp[2], xp[3]);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&a0);
@@ -118,9 +119,8 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
         u.y = *reinterpret_cast<uint32_t*>(&b1);
         __stcs(reinterpret_cast<uint2*>(h0 + s.Dx), u);
       }
-      if (!xr) continue;
+      if (!p0) continue;
     }
-    float* p0 = xr + row * s.Dx;
     if (V4) {
       __stcs(reinterpret_cast<float4*>(p0), make_float4(xp[0], xp[1], xp[2], xp[3]));
       if (kAnti)
