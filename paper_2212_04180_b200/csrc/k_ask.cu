@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   const int64_t first = (int64_t)r * s.Nloc * s.Dx + 4 * q + (int64_t)i0 * step;
   float* p0 = x ? x + first : nullptr;
   __half* h0 = W16 ? x16 + first : nullptr;
-#pragma unroll 2
+#pragma unroll 4
   for (int il = i0; il < i1; ++il, p0 += (x ? step : 0), h0 += (W16 ? step : 0)) {
     const float4 z = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)(dir0 + il), t);
     const float zz[4] = {z.x, z.y, z.z, z.w};
