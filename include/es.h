@@ -222,15 +222,18 @@ es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double
  * optimizer state — Adam m/v, SGD velocity — is the only copy: state memory is split across the
  * ranks), and writes the slice's mean, best_x and (PGPE, SNES) σ_d into every peer's state
  * (NVLink stores). No NCCL all-reduce of D doubles is involved. Supported: OpenAI-ES, PGPE, SNES,
- * ARS with Adam or SGD (Sep-CMA-ES's and ClipUp's global norms need a second exchange).
+ * ARS with Adam or SGD, and Sep-CMA-ES, whose global ‖p_σ'‖ needs a second exchange:
+ * es_tell_p2p_finish (after another barrier) sums the ranks' norm2 shares, updates σ, h_σ, and
+ * the slice's p_c and C, and stores the C slice into every peer (a no-op for the others).
+ * ClipUp's two global norms are not supported here.
  *   es_p2p_export     fill *out with this context's pointers (fields it does not keep are NULL).
  *   es_p2p_set_peers  peers[v] = rank v's export as mapped in THIS process (v = 0..W−1, W the
  *                     context's world size, ≤ 8; peers[rank] is this context's own export).
  *   es_tell_p2p_apply after es_tell_local on every rank (and a barrier: the peers' sums must be
  *                     complete), the fused reduce-scatter → update → all-gather; the caller
  *                     orders a second barrier before any rank's next es_ask.
- *   es_p2p_ipc_export / es_p2p_ipc_open  for real multi-GPU runs: 9 cudaIpcMemHandle_t (64 B
- *                     each: dirsum, then the 8 fields) per rank; es_p2p_ipc_open takes all W
+ *   es_p2p_ipc_export / es_p2p_ipc_open  for real multi-GPU runs: 10 cudaIpcMemHandle_t (64 B
+ *                     each: dirsum, the 8 fields, norm2) per rank; es_p2p_ipc_open takes all W
  *                     ranks' blocks (rank-major), maps the peers' and calls es_p2p_set_peers.
  * With a communicator and peers set, es_tell uses this path (all-gather of fitness, local
  * reduction, 4-byte NCCL barrier, the fused kernel, barrier). Errors: ES_ERR_UNSUPPORTED for other
@@ -238,12 +241,14 @@ es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double
 typedef struct {
   const double *dirsum;   /* [2][R][D] binary64 direction sums (this rank's share after tell_local) */
   float *field[8];        /* es_field_t 0..7 base pointers, float [R][D]; NULL if not kept        */
+  const double *norm2;    /* [R] Sep-CMA-ES: this rank's slice share of ‖p_σ'‖²                   */
 } es_peer_t;
 es_status_t es_p2p_export(const es_ctx_t *ctx, es_peer_t *out);
 es_status_t es_p2p_set_peers(es_ctx_t *ctx, const es_peer_t *peers, int32_t world_size);
 es_status_t es_tell_p2p_apply(es_ctx_t *ctx, es_stream_t stream);
-es_status_t es_p2p_ipc_export(const es_ctx_t *ctx, void *handles /* 9 × 64 bytes */);
-es_status_t es_p2p_ipc_open(es_ctx_t *ctx, const void *handles_all /* W × 9 × 64 bytes */);
+es_status_t es_tell_p2p_finish(es_ctx_t *ctx, es_stream_t stream);
+es_status_t es_p2p_ipc_export(const es_ctx_t *ctx, void *handles /* 10 × 64 bytes */);
+es_status_t es_p2p_ipc_open(es_ctx_t *ctx, const void *handles_all /* W × 10 × 64 bytes */);
 
 /* f2, NVLS variant: the same fused tell with the reduction done INSIDE the NVSwitch. Every rank
  * binds one symmetric buffer (direction sums, mean, best_x, σ_d) to a multicast object; the kernel

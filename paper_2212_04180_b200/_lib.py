@@ -26,7 +26,7 @@ EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "
            "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay",
            "es_init_dshard", "es_dshard_plan", "es_dshard_info", "es_ask_eval_partial",
            "es_p2p_export", "es_p2p_set_peers", "es_tell_p2p_apply", "es_p2p_ipc_export",
-           "es_p2p_ipc_open", "es_nvls_open", "es_nvls_bind", "es_tell_nvls_apply"]
+           "es_p2p_ipc_open", "es_tell_p2p_finish", "es_nvls_open", "es_nvls_bind", "es_tell_nvls_apply"]
 
 
 class RunParams(C.Structure):
@@ -43,7 +43,7 @@ class RunParams(C.Structure):
 
 class PeerT(C.Structure):
     """es_peer_t: a rank's direction-sum buffer and state-field device pointers (f2)."""
-    _fields_ = [("dirsum", C.c_void_p), ("field", C.c_void_p * 8)]
+    _fields_ = [("dirsum", C.c_void_p), ("field", C.c_void_p * 8), ("norm2", C.c_void_p)]
 
 
 class ESError(RuntimeError):
@@ -96,6 +96,7 @@ def lib():
         "es_p2p_export": (i32, [vp, C.POINTER(PeerT)]),
         "es_p2p_set_peers": (i32, [vp, C.POINTER(PeerT), i32]),
         "es_tell_p2p_apply": (i32, [vp, vp]),
+        "es_tell_p2p_finish": (i32, [vp, vp]),
         "es_p2p_ipc_export": (i32, [vp, vp]),
         "es_p2p_ipc_open": (i32, [vp, vp]),
         "es_nvls_open": (i32, [vp, vp, i32]),

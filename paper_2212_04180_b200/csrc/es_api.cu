@@ -831,6 +831,10 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     c->told_local = true;
     if ((err = es_tell_p2p_apply(c, stream_)) != ES_SUCCESS) return err;
     NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    if (s.algo == SEP_CMA_ES) {   // the global ‖p_σ'‖ and the C slices: one more exchange
+      if ((err = es_tell_p2p_finish(c, stream_)) != ES_SUCCESS) return err;
+      NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
+    }
     return ES_SUCCESS;
   }
   if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
@@ -878,15 +882,19 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
   return ES_SUCCESS;
 }
 
+static constexpr int kIpcHandles = 10;   // dirsum, the 8 fields, norm2
+
 static bool p2p_algo_ok(const es_ctx* c) {
   const int a = c->s.algo;
-  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS) && !c->any_clipup && !c->s.dshard;
+  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS || a == SEP_CMA_ES) &&
+         !c->any_clipup && !c->s.dshard;
 }
 
 es_status_t es_p2p_export(const es_ctx_t* c, es_peer_t* out) {
   if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
   out->dirsum = c->s.G;
   for (int f = 0; f < 8; ++f) out->field[f] = c->s.vec[f];
+  out->norm2 = c->s.n2;
   return ES_SUCCESS;
 }
 
@@ -894,15 +902,17 @@ es_status_t es_p2p_set_peers(es_ctx_t* c, const es_peer_t* peers, int32_t W) {
   if (!c || !peers) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (W != c->s.W) return fail(c, ES_ERR_INVALID_ARG, "peers for %d ranks, context has %d", W, c->s.W);
   if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
-  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
+  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: not with ClipUp / D-sharding");
   PeerTable pt{};
   pt.W = W;
   for (int v = 0; v < W; ++v) {
     if (!peers[v].dirsum) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL dirsum", v);
     pt.G[v] = peers[v].dirsum;
+    pt.n2[v] = peers[v].norm2;
+    if (c->s.algo == SEP_CMA_ES && !pt.n2[v]) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL norm2", v);
     for (int f = 0; f < NVEC; ++f) {
       pt.vec[v][f] = peers[v].field[f];
-      if (c->s.vec[f] && (f == F_MEAN || f == F_BEST_X || f == F_SIGMA_D) && !pt.vec[v][f])
+      if (c->s.vec[f] && (f == F_MEAN || f == F_BEST_X || f == F_SIGMA_D || f == F_C) && !pt.vec[v][f])
         return fail(c, ES_ERR_INVALID_ARG, "peer %d: field %d missing", v, f);
     }
   }
@@ -927,7 +937,8 @@ es_status_t es_tell_p2p_apply(es_ctx_t* c, es_stream_t stream_) {
 
 es_status_t es_nvls_open(es_ctx_t* c, void* handle, int32_t creator) {
   if (!c || !handle) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "NVLS tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
+  if (!p2p_algo_ok(c) || c->s.algo == SEP_CMA_ES)
+    return fail(c, ES_ERR_UNSUPPORTED, "NVLS tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
   if (c->nvls.stage) return fail(c, ES_ERR_BAD_STATE, "es_nvls_open called twice");
   if (const char* e = nvls_open(c->s, c->nvls, handle, creator != 0)) {
     nvls_close(c->nvls);
@@ -982,13 +993,27 @@ es_status_t es_tell_nvls_apply(es_ctx_t* c, es_stream_t stream_) {
   return ES_SUCCESS;
 }
 
+es_status_t es_tell_p2p_finish(es_ctx_t* c, es_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
+  int nk = 0;
+  {
+    ProfScope ps(c, "p2p_finish", st);
+    CUDA_OR(c, launch_p2p_finish(c->s, c->peers, st, &nk));
+  }
+  c->launches += nk;
+  return ES_SUCCESS;
+}
+
 es_status_t es_p2p_ipc_export(const es_ctx_t* c, void* handles) {
   if (!c || !handles) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
   auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
-  std::memset(handles, 0, 9 * sizeof(cudaIpcMemHandle_t));
+  std::memset(handles, 0, kIpcHandles * sizeof(cudaIpcMemHandle_t));
   cudaError_t e = cudaIpcGetMemHandle(&h[0], c->s.G);
   for (int f = 0; f < 8 && e == cudaSuccess; ++f)
     if (c->s.vec[f]) e = cudaIpcGetMemHandle(&h[1 + f], c->s.vec[f]);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[9], c->s.n2);
   if (e != cudaSuccess) return fail(nullptr, ES_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
   return ES_SUCCESS;
 }
@@ -1005,17 +1030,21 @@ es_status_t es_p2p_ipc_open(es_ctx_t* c, const void* all) {
       es_p2p_export(c, &peers[v]);
       continue;
     }
+    const cudaIpcMemHandle_t* hv = h + kIpcHandles * v;
     void* p = nullptr;
-    CUDA_OR(c, cudaIpcOpenMemHandle(&p, h[9 * v], cudaIpcMemLazyEnablePeerAccess));
+    CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[0], cudaIpcMemLazyEnablePeerAccess));
     c->ipc_open.push_back(p);
     peers[v].dirsum = static_cast<const double*>(p);
     for (int f = 0; f < 8; ++f) {
       peers[v].field[f] = nullptr;
-      if (std::memcmp(&h[9 * v + 1 + f], &zero, sizeof zero) == 0) continue;
-      CUDA_OR(c, cudaIpcOpenMemHandle(&p, h[9 * v + 1 + f], cudaIpcMemLazyEnablePeerAccess));
+      if (std::memcmp(&hv[1 + f], &zero, sizeof zero) == 0) continue;
+      CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[1 + f], cudaIpcMemLazyEnablePeerAccess));
       c->ipc_open.push_back(p);
       peers[v].field[f] = static_cast<float*>(p);
     }
+    CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[9], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p);
+    peers[v].norm2 = static_cast<const double*>(p);
   }
   return es_p2p_set_peers(c, peers.data(), W);
 }

@@ -103,6 +103,7 @@ struct PeerTable {
   int W;
   const double* G[kMaxPeers];
   float* vec[kMaxPeers][NVEC];
+  const double* n2[kMaxPeers];      // Sep-CMA-ES ‖p_σ'‖² share of each rank's slice
 };
 
 // f2 NVLS variant: one symmetric buffer per rank bound to a multicast object.
@@ -159,6 +160,8 @@ cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 // f2: reduce-scatter (peer loads, rank order) → update of this rank's quad slice → all-gather
 // (peer stores) in one kernel
 cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st);
+// Sep-CMA-ES second phase after a barrier (no-op for the other algorithms)
+cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, cudaStream_t st, int* nk);
 // f2 NVLS: the same with multimem.ld_reduce (sum in the switch) and multimem.st (broadcast)
 cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t st);
 // f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)

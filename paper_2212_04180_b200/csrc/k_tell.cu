@@ -321,23 +321,46 @@ __global__ void sepcma_n2_kernel(DevState s, int bpr) {
   if (threadIdx.x == 0) s.n2[blockIdx.x] = n2;
 }
 
+// σ' and h_σ of run r from the global ‖p_σ'‖² (one thread).
+__device__ __forceinline__ void sepcma_sigma(const DevState& s, int r, double n2) {
+  RunScal& rs = s.rs[r];
+  GenScal& gs = s.gs[r];
+  const double norm = sqrt(n2);
+  const double Dd = (double)s.Dg;
+  const float sig_new = __fmul_rn(
+      gs.sigma, (float)exp(__dmul_rn(__ddiv_rn(rs.c_sigma, rs.d_sigma),
+                                     __dsub_rn(__ddiv_rn(norm, rs.chi_d), 1.0))));
+  const double lhs = norm / sqrt(1.0 - pow(1.0 - rs.c_sigma, 2.0 * (double)(gs.t + 1)));
+  gs.hsig = lhs < (1.4 + 2.0 / (Dd + 1.0)) * rs.chi_d;
+  gs.sigma_new = sig_new;
+  rs.sigma = sig_new;
+}
+
 __global__ void sepcma_norm_kernel(DevState s, int bpr) {
   __shared__ double red[32];
   const int r = blockIdx.x;
   const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
-  if (threadIdx.x == 0) {
-    RunScal& rs = s.rs[r];
-    GenScal& gs = s.gs[r];
-    const double norm = sqrt(n2);
-    const double Dd = (double)s.Dg;
-    const float sig_new = __fmul_rn(
-        gs.sigma, (float)exp(__dmul_rn(__ddiv_rn(rs.c_sigma, rs.d_sigma),
-                                       __dsub_rn(__ddiv_rn(norm, rs.chi_d), 1.0))));
-    const double lhs = norm / sqrt(1.0 - pow(1.0 - rs.c_sigma, 2.0 * (double)(gs.t + 1)));
-    gs.hsig = lhs < (1.4 + 2.0 / (Dd + 1.0)) * rs.chi_d;
-    gs.sigma_new = sig_new;
-    rs.sigma = sig_new;
-  }
+  if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
+}
+
+// p_c and C of element idx (run r, dim d) from Z, Q (s.G) and h_σ.
+__device__ __forceinline__ void sepcma_pc_elem(const DevState& s, int r, int64_t d) {
+  const RunScal& rs = s.rs[r];
+  const GenScal& gs = s.gs[r];
+  const double hs = gs.hsig ? 1.0 : 0.0;
+  const float omcc = (float)(1.0 - rs.c_c);
+  const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
+  const float aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
+  const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
+  const float Z = (float)s.G[gidx(s, 0, r, d)];
+  const float Qv = (float)s.G[gidx(s, 1, r, d)];
+  const int64_t idx = (int64_t)r * s.D + d;
+  const float C0 = s.vec[F_C][idx];
+  const float y = __fmul_rn(__fsqrt_rn(C0), Z);
+  const float pcn = __fadd_rn(__fmul_rn(omcc, s.vec[F_PC][idx]), __fmul_rn(kc, y));
+  s.vec[F_PC][idx] = pcn;
+  s.vec[F_C][idx] = __fadd_rn(__fadd_rn(__fmul_rn(aC, C0), __fmul_rn(c1f, __fmul_rn(pcn, pcn))),
+                              __fmul_rn(cmuf, __fmul_rn(C0, Qv)));
 }
 
 // f2: the all-reduce of the direction sums and the update, fused over peer memory.
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(TT) p2p_apply_kernel(DevState s, PeerTable pt,
       }
     }
   }
-  apply_update<ALGO>(s, r, q, active, G0, G1, 0, 1, red);
+  apply_update<ALGO>(s, r, q, active, G0, G1, blockIdx.x % bps, bps, red);
   if (!active) return;
   constexpr int kF[3] = {F_MEAN, F_BEST_X, F_SIGMA_D};
   constexpr int nf = (ALGO == PGPE || ALGO == SNES) ? 3 : 2;
@@ -396,8 +419,47 @@ cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_
     case PGPE: p2p_apply_kernel<PGPE><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
     case SNES: p2p_apply_kernel<SNES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
     case ARS: p2p_apply_kernel<ARS><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
+    case SEP_CMA_ES:
+      p2p_apply_kernel<SEP_CMA_ES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps);
+      sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bps);     // this slice's ‖p_σ'‖² share → s.n2
+      break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// Sep-CMA-ES under the peer-memory tell, after a barrier: the global ‖p_σ'‖² (peer n2 shares in
+// rank order → identical σ', h_σ on every rank), then p_c and C of this rank's slice, and C's slice
+// stored into every peer (the ask needs the full C).
+__global__ void p2p_sepcma_sigma_kernel(DevState s, PeerTable pt) {
+  if (threadIdx.x != 0) return;
+  const int r = blockIdx.x;
+  double n2 = 0.0;
+  for (int v = 0; v < pt.W; ++v) n2 = __dadd_rn(n2, __ldcg(pt.n2[v] + r));
+  sepcma_sigma(s, r, n2);
+}
+
+__global__ void __launch_bounds__(256) p2p_sepcma_pc_kernel(DevState s, PeerTable pt, int64_t d0,
+                                                            int64_t d1) {
+  const int r = blockIdx.y;
+  const int64_t d = d0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= d1) return;
+  sepcma_pc_elem(s, r, d);
+  const int64_t idx = (int64_t)r * s.D + d;
+  const float c = s.vec[F_C][idx];
+  for (int v = 0; v < pt.W; ++v)
+    if (v != s.rank) __stcg(pt.vec[v][F_C] + idx, c);
+}
+
+cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, cudaStream_t st, int* nk) {
+  if (nk) *nk = 0;
+  if (s.algo != SEP_CMA_ES) return cudaSuccess;
+  const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
+  const int64_t d0 = 4 * qa, d1 = std::min<int64_t>(4 * qe, s.D);
+  p2p_sepcma_sigma_kernel<<<s.R, 32, 0, st>>>(s, pt);
+  const int64_t n = std::max<int64_t>(1, d1 - d0);
+  p2p_sepcma_pc_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)s.R), 256, 0, st>>>(s, pt, d0, d1);
+  if (nk) *nk = 2;
   return cudaGetLastError();
 }
 
@@ -467,24 +529,7 @@ cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t
 __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)s.R * s.D) return;
-  const int r = (int)(gid / s.D);
-  const int64_t d = gid % s.D;
-  const RunScal& rs = s.rs[r];
-  const GenScal& gs = s.gs[r];
-  const double hs = gs.hsig ? 1.0 : 0.0;
-  const float omcc = (float)(1.0 - rs.c_c);
-  const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
-  const float aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
-  const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
-  const float Z = (float)s.G[gidx(s, 0, r, d)];
-  const float Qv = (float)s.G[gidx(s, 1, r, d)];
-  const int64_t idx = (int64_t)r * s.D + d;
-  const float C0 = s.vec[F_C][idx];
-  const float y = __fmul_rn(__fsqrt_rn(C0), Z);
-  const float pcn = __fadd_rn(__fmul_rn(omcc, s.vec[F_PC][idx]), __fmul_rn(kc, y));
-  s.vec[F_PC][idx] = pcn;
-  s.vec[F_C][idx] = __fadd_rn(__fadd_rn(__fmul_rn(aC, C0), __fmul_rn(c1f, __fmul_rn(pcn, pcn))),
-                              __fmul_rn(cmuf, __fmul_rn(C0, Qv)));
+  sepcma_pc_elem(s, (int)(gid / s.D), gid % s.D);
 }
 
 // ClipUp (Toklu et al. 2020), phases after the gradient g is parked in s.G:

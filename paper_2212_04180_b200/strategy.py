@@ -144,6 +144,10 @@ class Strategy:
         """After tell_local on every rank: reduce-scatter → update → all-gather in one kernel."""
         check(lib().es_tell_p2p_apply(self.ctx, _stream(stream)), self.ctx)
 
+    def tell_p2p_finish(self, stream=None):
+        """Sep-CMA-ES: after every rank's tell_p2p_apply, the global-norm phase (no-op otherwise)."""
+        check(lib().es_tell_p2p_finish(self.ctx, _stream(stream)), self.ctx)
+
     def nvls_open(self, creator, handle=None):
         """f2 NVLS: create (creator) or join the multicast object; returns the 64-byte handle."""
         h = torch.zeros(64, dtype=torch.uint8)
@@ -174,7 +178,7 @@ class Strategy:
 
     def p2p_connect(self, group):
         """Real multi-GPU: exchange CUDA IPC handles over `group` and map the peers' buffers."""
-        h = torch.zeros(9 * 64, dtype=torch.uint8)
+        h = torch.zeros(10 * 64, dtype=torch.uint8)
         check(lib().es_p2p_ipc_export(self.ctx, C.c_void_p(h.data_ptr())), self.ctx)
         allh = [None] * torch.distributed.get_world_size(group)
         torch.distributed.all_gather_object(allh, bytes(h.numpy()), group=group)

@@ -366,7 +366,8 @@ def test_weight_decay_emulated_shards(algo):
 # ------------------------------------------------------------------------ f2 peer-memory tell
 @pytest.mark.parametrize("algo,per", [(W.OPENAI_ES, [dict(), dict(optimizer=W.SGD)]),
                                       (W.PGPE, [dict(), dict(elite_ratio=0.5)]),
-                                      (W.SNES, [dict()]), (W.ARS, ARS_ELITES)])
+                                      (W.SNES, [dict()]), (W.ARS, ARS_ELITES),
+                                      (W.SEP_CMA_ES, [dict(), dict(elite_ratio=0.25)])])
 @pytest.mark.parametrize("Wn,D", [(2, 301), (4, 1003), (8, 4099), (3, 37)])
 def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
     """W ranks emulated on one GPU, each running the SAME fused kernel it would
@@ -398,9 +399,15 @@ def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
             sh.tell_local(gathered)
         for sh in shards:                      # after every rank's partial sums exist
             sh.tell_p2p_apply()
+        for sh in shards:                      # Sep-CMA-ES: global ‖p_σ'‖, p_c and C slices
+            sh.tell_p2p_finish()
         for w, sh in enumerate(shards):
             assert torch.equal(sh.get("perm"), ref.get("perm"))
-            fields = ["mean", "best_x"] + (["sigma_d"] if algo in (W.PGPE, W.SNES) else [])
+            fields = ["mean", "best_x"] + (["sigma_d"] if algo in (W.PGPE, W.SNES) else []) + \
+                (["C"] if algo == W.SEP_CMA_ES else [])
+            if algo == W.SEP_CMA_ES:
+                assert abs(float(sh.get("sigma")[0]) - float(ref.get("sigma")[0])) <= \
+                    1e-6 * float(ref.get("sigma")[0])
             for fld in fields:
                 assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, (fld, w)
             if algo in (W.OPENAI_ES, W.PGPE):   # the rank's own optimizer-state slice
@@ -415,8 +422,9 @@ def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
 def test_p2p_rejections():
     from paper_2212_04180_b200 import strategy as S
     from paper_2212_04180_b200._lib import ESError
-    a = [S.Strategy(W.SEP_CMA_ES, 16, 8, _params(W.SEP_CMA_ES, 1), shard=(w, 2)) for w in range(2)]
-    with pytest.raises(ESError):
+    a = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1, optimizer=W.CLIPUP), shard=(w, 2))
+         for w in range(2)]
+    with pytest.raises(ESError):                          # ClipUp: two global norms
         a[0].p2p_set_peers([s.p2p_export() for s in a])
     b = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1), shard=(w, 2)) for w in range(2)]
     with pytest.raises(ESError):
