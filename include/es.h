@@ -222,10 +222,14 @@ es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double
  * optimizer state — Adam m/v, SGD velocity — is the only copy: state memory is split across the
  * ranks), and writes the slice's mean, best_x and (PGPE, SNES) σ_d into every peer's state
  * (NVLink stores). No NCCL all-reduce of D doubles is involved. Supported: OpenAI-ES, PGPE, SNES,
- * ARS with Adam or SGD, and Sep-CMA-ES, whose global ‖p_σ'‖ needs a second exchange:
- * es_tell_p2p_finish (after another barrier) sums the ranks' norm2 shares, updates σ, h_σ, and
- * the slice's p_c and C, and stores the C slice into every peer (a no-op for the others).
- * ClipUp's two global norms are not supported here.
+ * ARS with Adam or SGD; Sep-CMA-ES and ClipUp need global norms, so they run
+ * es_p2p_finish_phases(ctx) more phases, each an es_tell_p2p_finish after a barrier:
+ *   Sep-CMA-ES (1 phase): sum the ranks' norm2 shares of ‖p_σ'‖² (rank order), update σ, h_σ and
+ *     the slice's p_c and C, and store the C slice into every peer;
+ *   ClipUp (2 phases, Toklu et al. 2020): the apply kernel parks g and leaves the slice's
+ *     ‖g‖² share; phase 0 sums the shares → v' = μ v + lr g/‖g‖ on the slice and its ‖v'‖² share;
+ *     phase 1 sums those → the max_speed clip, m −= v on the slice, mean slice stored into every
+ *     peer (the velocity stays with its owner).
  *   es_p2p_export     fill *out with this context's pointers (fields it does not keep are NULL).
  *   es_p2p_set_peers  peers[v] = rank v's export as mapped in THIS process (v = 0..W−1, W the
  *                     context's world size, ≤ 8; peers[rank] is this context's own export).
@@ -236,17 +240,21 @@ es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double
  *                     each: dirsum, the 8 fields, norm2) per rank; es_p2p_ipc_open takes all W
  *                     ranks' blocks (rank-major), maps the peers' and calls es_p2p_set_peers.
  * With a communicator and peers set, es_tell uses this path (all-gather of fitness, local
- * reduction, 4-byte NCCL barrier, the fused kernel, barrier). Errors: ES_ERR_UNSUPPORTED for other
- * algorithms / ClipUp / W > 8; ES_ERR_BAD_STATE out of order or without peers. */
+ * reduction, 4-byte NCCL barrier, the fused kernel, barrier, then each finish phase and a
+ * barrier). es_tell_p2p_finish is a no-op when es_p2p_finish_phases is 0. Errors:
+ * ES_ERR_UNSUPPORTED for CMA-ES / D-shard contexts / W > 8; ES_ERR_BAD_STATE out of order or
+ * without peers (also a finish phase with no es_tell_p2p_apply pending). */
 typedef struct {
   const double *dirsum;   /* [2][R][D] binary64 direction sums (this rank's share after tell_local) */
   float *field[8];        /* es_field_t 0..7 base pointers, float [R][D]; NULL if not kept        */
-  const double *norm2;    /* [R] Sep-CMA-ES: this rank's slice share of ‖p_σ'‖²                   */
+  const double *norm2;    /* [2R] this rank's slice shares: Sep-CMA ‖p_σ'‖² at [0,R); ClipUp ‖g‖²
+                             at [0,R) and ‖v'‖² at [R,2R)                                        */
 } es_peer_t;
 es_status_t es_p2p_export(const es_ctx_t *ctx, es_peer_t *out);
 es_status_t es_p2p_set_peers(es_ctx_t *ctx, const es_peer_t *peers, int32_t world_size);
 es_status_t es_tell_p2p_apply(es_ctx_t *ctx, es_stream_t stream);
 es_status_t es_tell_p2p_finish(es_ctx_t *ctx, es_stream_t stream);
+int32_t es_p2p_finish_phases(const es_ctx_t *ctx);   /* 0, 1 or 2; −1 for a NULL context */
 es_status_t es_p2p_ipc_export(const es_ctx_t *ctx, void *handles /* 10 × 64 bytes */);
 es_status_t es_p2p_ipc_open(es_ctx_t *ctx, const void *handles_all /* W × 10 × 64 bytes */);
 

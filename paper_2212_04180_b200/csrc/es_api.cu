@@ -61,6 +61,7 @@ struct es_ctx {
   ncclComm_t comm = nullptr;
   bool asked = false;
   bool told_local = false;
+  int p2p_phase = -1;           // next es_tell_p2p_finish phase (-1: no apply pending)
   bool broken = false;
   int nchunk = 1;
   float* fgather = nullptr;     // [W][R][Nloc]
@@ -189,6 +190,17 @@ static void sepcma_setup(int N, int64_t D, float elite, RunScal& rs, std::vector
   rs.c_1 = c1 * (Dd + 2.0) / 3.0;      // Ros & Hansen (2008): separable learning-rate boost
   rs.c_mu = cmu * (Dd + 2.0) / 3.0;
   rs.chi_d = std::sqrt(Dd) * (1.0 - 1.0 / (4.0 * Dd) + 1.0 / (21.0 * Dd * Dd));
+}
+
+// f2 peer-memory tell: supported contexts, and the es_tell_p2p_finish calls (each after a
+// barrier) one generation needs.
+static bool p2p_algo_ok(const es_ctx* c) {
+  const int a = c->s.algo;
+  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS || a == SEP_CMA_ES) && !c->s.dshard;
+}
+
+static int p2p_phases(const es_ctx* c) {
+  return c->s.algo == SEP_CMA_ES ? 1 : (c->any_clipup ? 2 : 0);
 }
 
 extern "C" {
@@ -364,7 +376,7 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   TRY(dalloc(c, (void**)&s.rs_e, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.perm, RN * sizeof(int32_t)));
   TRY(dalloc(c, (void**)&s.pos, RN * sizeof(int32_t)));
-  TRY(dalloc(c, (void**)&s.n2, R * sizeof(double)));
+  TRY(dalloc(c, (void**)&s.n2, 2 * (size_t)R * sizeof(double)));   // [0,R) shares, [R,2R) ClipUp ‖v'‖²
   s.cov = s.chol = s.cw = s.zbuf = s.ybuf = nullptr;
   s.chol_fail = nullptr;
   if (cma) {
@@ -831,7 +843,7 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     c->told_local = true;
     if ((err = es_tell_p2p_apply(c, stream_)) != ES_SUCCESS) return err;
     NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
-    if (s.algo == SEP_CMA_ES) {   // the global ‖p_σ'‖ and the C slices: one more exchange
+    for (int ph = p2p_phases(c); ph > 0; --ph) {   // Sep-CMA σ / C, ClipUp's two norms
       if ((err = es_tell_p2p_finish(c, stream_)) != ES_SUCCESS) return err;
       NCCL_OR(c, ncclAllReduce(c->bar, c->bar, 1, ncclInt32, ncclSum, c->comm, st));
     }
@@ -884,12 +896,6 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
 
 static constexpr int kIpcHandles = 10;   // dirsum, the 8 fields, norm2
 
-static bool p2p_algo_ok(const es_ctx* c) {
-  const int a = c->s.algo;
-  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS || a == SEP_CMA_ES) &&
-         !c->any_clipup && !c->s.dshard;
-}
-
 es_status_t es_p2p_export(const es_ctx_t* c, es_peer_t* out) {
   if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
   out->dirsum = c->s.G;
@@ -902,14 +908,14 @@ es_status_t es_p2p_set_peers(es_ctx_t* c, const es_peer_t* peers, int32_t W) {
   if (!c || !peers) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (W != c->s.W) return fail(c, ES_ERR_INVALID_ARG, "peers for %d ranks, context has %d", W, c->s.W);
   if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
-  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: not with ClipUp / D-sharding");
+  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: not with CMA-ES / D-sharding");
   PeerTable pt{};
   pt.W = W;
   for (int v = 0; v < W; ++v) {
     if (!peers[v].dirsum) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL dirsum", v);
     pt.G[v] = peers[v].dirsum;
     pt.n2[v] = peers[v].norm2;
-    if (c->s.algo == SEP_CMA_ES && !pt.n2[v]) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL norm2", v);
+    if (p2p_phases(c) && !pt.n2[v]) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL norm2", v);
     for (int f = 0; f < NVEC; ++f) {
       pt.vec[v][f] = peers[v].field[f];
       if (c->s.vec[f] && (f == F_MEAN || f == F_BEST_X || f == F_SIGMA_D || f == F_C) && !pt.vec[v][f])
@@ -925,19 +931,21 @@ es_status_t es_tell_p2p_apply(es_ctx_t* c, es_stream_t stream_) {
   if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_p2p_apply without es_tell_local");
   if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
+  int nk = 0;
   {
     ProfScope ps(c, "p2p_apply", st);
-    CUDA_OR(c, launch_p2p_apply(c->s, c->peers, st));
+    CUDA_OR(c, launch_p2p_apply(c->s, c->peers, c->any_clipup, st, &nk));
   }
-  c->launches += 1;
+  c->launches += nk;
   c->told_local = false;
   c->asked = false;
+  c->p2p_phase = p2p_phases(c) ? 0 : -1;
   return ES_SUCCESS;
 }
 
 es_status_t es_nvls_open(es_ctx_t* c, void* handle, int32_t creator) {
   if (!c || !handle) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (!p2p_algo_ok(c) || c->s.algo == SEP_CMA_ES)
+  if (!p2p_algo_ok(c) || c->s.algo == SEP_CMA_ES || c->any_clipup)
     return fail(c, ES_ERR_UNSUPPORTED, "NVLS tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
   if (c->nvls.stage) return fail(c, ES_ERR_BAD_STATE, "es_nvls_open called twice");
   if (const char* e = nvls_open(c->s, c->nvls, handle, creator != 0)) {
@@ -997,13 +1005,19 @@ es_status_t es_tell_p2p_finish(es_ctx_t* c, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
+  if (!p2p_phases(c)) return ES_SUCCESS;             // nothing after the apply kernel
+  if (c->p2p_phase < 0) return fail(c, ES_ERR_BAD_STATE, "es_tell_p2p_finish without es_tell_p2p_apply");
   int nk = 0;
   {
     ProfScope ps(c, "p2p_finish", st);
-    CUDA_OR(c, launch_p2p_finish(c->s, c->peers, st, &nk));
+    CUDA_OR(c, launch_p2p_finish(c->s, c->peers, c->p2p_phase, st, &nk));
   }
   c->launches += nk;
+  c->p2p_phase = c->p2p_phase + 1 < p2p_phases(c) ? c->p2p_phase + 1 : -1;
   return ES_SUCCESS;
+}
+
+int32_t es_p2p_finish_phases(const es_ctx_t* c) { return c ? p2p_phases(c) : -1;
 }
 
 es_status_t es_p2p_ipc_export(const es_ctx_t* c, void* handles) {

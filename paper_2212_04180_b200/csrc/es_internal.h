@@ -159,9 +159,11 @@ cudaError_t launch_partial_to_fitness(const double* fsum, int64_t n, float* f, c
 cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
 // f2: reduce-scatter (peer loads, rank order) → update of this rank's quad slice → all-gather
 // (peer stores) in one kernel
-cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st);
-// Sep-CMA-ES second phase after a barrier (no-op for the other algorithms)
-cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, cudaStream_t st, int* nk);
+cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, bool clipup, cudaStream_t st,
+                             int* nk);
+// the phases after a barrier each: Sep-CMA-ES one (σ, p_c, C), ClipUp two (‖g‖, ‖v'‖)
+cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, int phase, cudaStream_t st,
+                              int* nk);
 // f2 NVLS: the same with multimem.ld_reduce (sum in the switch) and multimem.st (broadcast)
 cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t st);
 // f_out = f + weight_decay_r ‖x_j‖² for this rank's members (2 kernels; part as ask_eval's)

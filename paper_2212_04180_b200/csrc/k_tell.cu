@@ -315,10 +315,11 @@ __device__ __forceinline__ double normpart_total(const DevState& s, int r, int b
 // Sep-CMA-ES phase 2: global ‖p_σ'‖ (fixed-order sum of the block partials), σ', h_σ.
 // D-sharded contexts split it: sepcma_n2_kernel writes this rank's ‖p_σ'‖² share to s.n2, the
 // shares are summed over ranks (NCCL or the caller), then sepcma_norm_kernel reads s.n2.
-__global__ void sepcma_n2_kernel(DevState s, int bpr) {
+// (Also ClipUp's shares under the peer-memory tell: ‖g‖² at off 0, ‖v'‖² at off R.)
+__global__ void sepcma_n2_kernel(DevState s, int bpr, int off) {
   __shared__ double red[32];
   const double n2 = normpart_total(s, blockIdx.x, bpr, red);
-  if (threadIdx.x == 0) s.n2[blockIdx.x] = n2;
+  if (threadIdx.x == 0) s.n2[off + blockIdx.x] = n2;
 }
 
 // σ' and h_σ of run r from the global ‖p_σ'‖² (one thread).
@@ -410,10 +411,12 @@ __global__ void __launch_bounds__(TT) p2p_apply_kernel(DevState s, PeerTable pt,
   }
 }
 
-cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_t st) {
+cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, bool clipup, cudaStream_t st,
+                             int* nk) {
   const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
   const int bps = (int)std::max<int64_t>(1, (qe - qa + TT - 1) / TT);
   const unsigned g = (unsigned)(s.R * bps);
+  if (nk) *nk = (s.algo == SEP_CMA_ES || clipup) ? 2 : 1;
   switch (s.algo) {
     case OPENAI_ES: p2p_apply_kernel<OPENAI_ES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
     case PGPE: p2p_apply_kernel<PGPE><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
@@ -421,10 +424,12 @@ cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, cudaStream_
     case ARS: p2p_apply_kernel<ARS><<<g, TT, 0, st>>>(s, pt, qa, qe, bps); break;
     case SEP_CMA_ES:
       p2p_apply_kernel<SEP_CMA_ES><<<g, TT, 0, st>>>(s, pt, qa, qe, bps);
-      sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bps);     // this slice's ‖p_σ'‖² share → s.n2
+      sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bps, 0);  // this slice's ‖p_σ'‖² share → s.n2
       break;
     default: return cudaErrorInvalidValue;
   }
+  // ClipUp parked g in the slice and left ‖g‖² block partials: this slice's share → s.n2[0, R)
+  if (clipup) sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bps, 0);
   return cudaGetLastError();
 }
 
@@ -451,17 +456,6 @@ __global__ void __launch_bounds__(256) p2p_sepcma_pc_kernel(DevState s, PeerTabl
     if (v != s.rank) __stcg(pt.vec[v][F_C] + idx, c);
 }
 
-cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, cudaStream_t st, int* nk) {
-  if (nk) *nk = 0;
-  if (s.algo != SEP_CMA_ES) return cudaSuccess;
-  const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
-  const int64_t d0 = 4 * qa, d1 = std::min<int64_t>(4 * qe, s.D);
-  p2p_sepcma_sigma_kernel<<<s.R, 32, 0, st>>>(s, pt);
-  const int64_t n = std::max<int64_t>(1, d1 - d0);
-  p2p_sepcma_pc_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)s.R), 256, 0, st>>>(s, pt, d0, d1);
-  if (nk) *nk = 2;
-  return cudaGetLastError();
-}
 
 // f2 NVLS variant of p2p_apply_kernel: the W partial sums of the slice are added inside the switch
 // (multimem.ld_reduce on the multicast alias of every rank's G), and the updated slice is
@@ -536,32 +530,36 @@ __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
 //   norm(0): inv = 1/‖g‖ (0 if ‖g‖ = 0)      vel: v' = μ v + lr (g · inv), ‖v'‖² partials
 //   norm(1): clip = max_speed/‖v'‖ if ‖v'‖ > max_speed else 1      apply: v = v' clip, m −= v.
 // Runs using another optimizer skip every phase.
+__device__ __forceinline__ void clipup_scalar(const DevState& s, int r, double n2, int phase) {
+  const double n = sqrt(n2);
+  GenScal& gs = s.gs[r];
+  if (phase == 0) {
+    gs.clip_inv = n > 0.0 ? (float)(1.0 / n) : 0.0f;
+  } else {
+    const double ms = (double)s.rs[r].max_speed;
+    gs.clip_inv = n > ms ? (float)(ms / n) : 1.0f;
+  }
+}
+
 __global__ void clipup_norm_kernel(DevState s, int bpr, int phase) {
   __shared__ double red[32];
   const int r = blockIdx.x;
   if (s.rs[r].optimizer != OPT_CLIPUP) return;
   const double n2 = normpart_total(s, r, bpr, red);
-  if (threadIdx.x == 0) {
-    const double n = sqrt(n2);
-    GenScal& gs = s.gs[r];
-    if (phase == 0) {
-      gs.clip_inv = n > 0.0 ? (float)(1.0 / n) : 0.0f;
-    } else {
-      const double ms = (double)s.rs[r].max_speed;
-      gs.clip_inv = n > ms ? (float)(ms / n) : 1.0f;
-    }
-  }
+  if (threadIdx.x == 0) clipup_scalar(s, r, n2, phase);
 }
 
-__global__ void __launch_bounds__(TT) clipup_vel_kernel(DevState s, int bpr) {
+// Quads [qa, qe) of every run (the whole run, or a peer-memory rank's slice), bpr blocks each.
+__global__ void __launch_bounds__(TT) clipup_vel_kernel(DevState s, int bpr, int64_t qa,
+                                                        int64_t qe) {
   __shared__ double red[TT / 32];
   const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
   const RunScal& rs = s.rs[r];
   if (rs.optimizer != OPT_CLIPUP) return;              // block-uniform
   const GenScal& gs = s.gs[r];
-  const int64_t q = (int64_t)qb * TT + threadIdx.x;
+  const int64_t q = qa + (int64_t)qb * TT + threadIdx.x;
   double v2 = 0.0;
-  if (q < s.Q) {
+  if (q < qe) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t d = 4 * q + k;
@@ -660,7 +658,7 @@ cudaError_t launch_sepcma_norm(const DevState& s, cudaStream_t st) {
 }
 
 cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st) {
-  sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, tell_blocks_per_run(s));
+  sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, tell_blocks_per_run(s), 0);
   return cudaGetLastError();
 }
 
@@ -677,10 +675,62 @@ cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk) {
   const int bpr = tell_blocks_per_run(s);
   const int64_t n = (int64_t)s.R * s.D;
   clipup_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr, 0);
-  clipup_vel_kernel<<<(unsigned)(s.R * bpr), TT, 0, st>>>(s, bpr);
+  clipup_vel_kernel<<<(unsigned)(s.R * bpr), TT, 0, st>>>(s, bpr, 0, s.Q);
   clipup_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr, 1);
   clipup_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
   if (nk) *nk = 4;
+  return cudaGetLastError();
+}
+
+// ClipUp under the peer-memory tell, two phases after the apply kernel, each after a barrier:
+//   phase 0: 1/‖g‖ from the ranks' ‖g‖² shares (rank order), v' = μ v + lr g/‖g‖ on the slice,
+//            the slice's ‖v'‖² share → s.n2[R, 2R) (a second slot: peers may still read [0, R));
+//   phase 1: the clip factor from the ‖v'‖² shares, v = v'·clip, m −= v on the slice, and the
+//            slice's mean stored into every peer (the velocity stays with its owner).
+__global__ void p2p_clipup_norm_kernel(DevState s, PeerTable pt, int phase) {
+  const int r = blockIdx.x;
+  if (threadIdx.x != 0 || s.rs[r].optimizer != OPT_CLIPUP) return;
+  double n2 = 0.0;
+  for (int v = 0; v < pt.W; ++v) n2 = __dadd_rn(n2, __ldcg(pt.n2[v] + phase * s.R + r));
+  clipup_scalar(s, r, n2, phase);
+}
+
+__global__ void __launch_bounds__(256) p2p_clipup_apply_kernel(DevState s, PeerTable pt,
+                                                               int64_t d0, int64_t d1) {
+  const int r = blockIdx.y;
+  const int64_t d = d0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= d1 || s.rs[r].optimizer != OPT_CLIPUP) return;
+  const int64_t idx = (int64_t)r * s.D + d;
+  const float v = __fmul_rn(s.vec[F_ADAM_M][idx], s.gs[r].clip_inv);
+  s.vec[F_ADAM_M][idx] = v;
+  const float m = __fsub_rn(s.vec[F_MEAN][idx], v);
+  s.vec[F_MEAN][idx] = m;
+  for (int w = 0; w < pt.W; ++w)
+    if (w != s.rank) __stcg(pt.vec[w][F_MEAN] + idx, m);
+}
+
+cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, int phase, cudaStream_t st,
+                              int* nk) {
+  if (nk) *nk = 0;
+  const int64_t qa = s.Q * s.rank / s.W, qe = s.Q * (s.rank + 1) / s.W;
+  const int64_t d0 = 4 * qa, d1 = std::min<int64_t>(4 * qe, s.D);
+  const int64_t n = std::max<int64_t>(1, d1 - d0);
+  const dim3 eg((unsigned)((n + 255) / 256), (unsigned)s.R);
+  if (s.algo == SEP_CMA_ES) {
+    p2p_sepcma_sigma_kernel<<<s.R, 32, 0, st>>>(s, pt);
+    p2p_sepcma_pc_kernel<<<eg, 256, 0, st>>>(s, pt, d0, d1);
+    if (nk) *nk = 2;
+  } else if (phase == 0) {
+    const int bps = (int)std::max<int64_t>(1, (qe - qa + TT - 1) / TT);
+    p2p_clipup_norm_kernel<<<s.R, 32, 0, st>>>(s, pt, 0);
+    clipup_vel_kernel<<<(unsigned)(s.R * bps), TT, 0, st>>>(s, bps, qa, qe);
+    sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bps, s.R);
+    if (nk) *nk = 3;
+  } else {
+    p2p_clipup_norm_kernel<<<s.R, 32, 0, st>>>(s, pt, 1);
+    p2p_clipup_apply_kernel<<<eg, 256, 0, st>>>(s, pt, d0, d1);
+    if (nk) *nk = 2;
+  }
   return cudaGetLastError();
 }
 

@@ -145,8 +145,11 @@ class Strategy:
         check(lib().es_tell_p2p_apply(self.ctx, _stream(stream)), self.ctx)
 
     def tell_p2p_finish(self, stream=None):
-        """Sep-CMA-ES: after every rank's tell_p2p_apply, the global-norm phase (no-op otherwise)."""
+        """One global-norm phase after a barrier (Sep-CMA-ES: 1, ClipUp: 2; no-op otherwise)."""
         check(lib().es_tell_p2p_finish(self.ctx, _stream(stream)), self.ctx)
+
+    def p2p_finish_phases(self):
+        return int(lib().es_p2p_finish_phases(self.ctx))
 
     def nvls_open(self, creator, handle=None):
         """f2 NVLS: create (creator) or join the multicast object; returns the 64-byte handle."""

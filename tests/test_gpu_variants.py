@@ -365,7 +365,11 @@ def test_weight_decay_emulated_shards(algo):
 
 # ------------------------------------------------------------------------ f2 peer-memory tell
 @pytest.mark.parametrize("algo,per", [(W.OPENAI_ES, [dict(), dict(optimizer=W.SGD)]),
+                                      (W.OPENAI_ES, [dict(optimizer=W.CLIPUP, max_speed=0.05),
+                                                     dict(), dict(optimizer=W.CLIPUP, max_speed=50.0)]),
                                       (W.PGPE, [dict(), dict(elite_ratio=0.5)]),
+                                      (W.PGPE, [dict(optimizer=W.CLIPUP, max_speed=0.1,
+                                                     momentum=0.5)]),
                                       (W.SNES, [dict()]), (W.ARS, ARS_ELITES),
                                       (W.SEP_CMA_ES, [dict(), dict(elite_ratio=0.25)])])
 @pytest.mark.parametrize("Wn,D", [(2, 301), (4, 1003), (8, 4099), (3, 37)])
@@ -399,8 +403,9 @@ def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
             sh.tell_local(gathered)
         for sh in shards:                      # after every rank's partial sums exist
             sh.tell_p2p_apply()
-        for sh in shards:                      # Sep-CMA-ES: global ‖p_σ'‖, p_c and C slices
-            sh.tell_p2p_finish()
+        for _ in range(shards[0].p2p_finish_phases()):   # Sep-CMA ‖p_σ'‖; ClipUp ‖g‖, ‖v'‖
+            for sh in shards:                  # (a barrier between phases)
+                sh.tell_p2p_finish()
         for w, sh in enumerate(shards):
             assert torch.equal(sh.get("perm"), ref.get("perm"))
             fields = ["mean", "best_x"] + (["sigma_d"] if algo in (W.PGPE, W.SNES) else []) + \
@@ -422,10 +427,12 @@ def test_p2p_fused_tell_matches_unsharded(algo, per, Wn, D):
 def test_p2p_rejections():
     from paper_2212_04180_b200 import strategy as S
     from paper_2212_04180_b200._lib import ESError
-    a = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1, optimizer=W.CLIPUP), shard=(w, 2))
-         for w in range(2)]
-    with pytest.raises(ESError):                          # ClipUp: two global norms
-        a[0].p2p_set_peers([s.p2p_export() for s in a])
+    a = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1, optimizer=W.CLIPUP, max_speed=1.0),
+                    shard=(w, 2)) for w in range(2)]
+    a[0].p2p_set_peers([s.p2p_export() for s in a])
+    assert a[0].p2p_finish_phases() == 2
+    with pytest.raises(ESError):                          # no apply pending
+        a[0].tell_p2p_finish()
     b = [S.Strategy(W.OPENAI_ES, 16, 8, _params(W.OPENAI_ES, 1), shard=(w, 2)) for w in range(2)]
     with pytest.raises(ESError):
         b[0].p2p_set_peers([b[0].p2p_export()])           # wrong world size
