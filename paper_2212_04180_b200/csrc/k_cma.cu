@@ -353,36 +353,49 @@ __global__ void chol_copy_kernel(DevState s) {
   if (blockIdx.x == 0 && threadIdx.x == 0) s.chol_fail[r] = 0;
 }
 
+// Register rotation a[k] ← a[k+1], a[31] ← v: lets a ROLLED loop visit column j as a[0].
+__device__ __forceinline__ void rot32(float (&a)[32], float v) {
+#pragma unroll
+  for (int k = 0; k < 31; ++k) a[k] = a[k + 1];
+  a[31] = v;
+}
+
 // 32×32 Cholesky by one warp: lane i holds row i (a[k], k ≤ i) in registers; column j's pivot and
-// entries are broadcast with shuffles, so a column costs no barrier. Fully unrolled (register
-// indices must be static). Returns false if a pivot is not positive.
+// entries are broadcast with shuffles, so a column costs no barrier. The column loop is rolled
+// (the row rotates one register per column, so column j is always a[0] and the finished entry
+// goes to a[31]; after 32 columns the row is back in order): the body stays in the instruction
+// cache — the fully unrolled loop (~2.5 K instructions per call) was instruction-fetch-bound.
+// Same operations in the same order as the unrolled form. Returns false if a pivot is not positive.
 __device__ __forceinline__ bool warp_chol32(float (&a)[32], int lane) {
   bool ok = true;
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < 32; ++j) {
-    const float d = __shfl_sync(0xffffffffu, a[j], j);
+    const float d = __shfl_sync(0xffffffffu, a[0], j);
     ok = ok && d > 0.0f;
     const float piv = d > 0.0f ? __fsqrt_rn(d) : 1.0f;
     const float inv = __frcp_rn(piv);
-    if (lane == j) a[j] = piv;
-    if (lane > j) a[j] = __fmul_rn(a[j], inv);
-    const float lij = a[j];
+    float lij = a[0];
+    if (lane == j) lij = piv;
+    if (lane > j) lij = __fmul_rn(lij, inv);
 #pragma unroll
-    for (int k = j + 1; k < 32; ++k) {
-      const float lkj = __shfl_sync(0xffffffffu, lij, k);
-      if (lane >= k) a[k] = __fmaf_rn(-lij, lkj, a[k]);
+    for (int k = 1; k < 32; ++k) {
+      const float lkj = __shfl_sync(0xffffffffu, lij, j + k);   // lane j+k (≥ 32: predicated off)
+      if (lane >= j + k) a[k] = __fmaf_rn(-lij, lkj, a[k]);
     }
+    rot32(a, lij);
   }
   return ok;
 }
 
 // Diagonal block [kb, kb+64)² (the last may be narrower) as a 2×2 blocked Cholesky of 32×32
-// tiles: warp 0 factors L00; warp 1 solves L10 = A10·L00⁻ᵀ (lane per row, L00 from shared
-// memory); A11 −= L10·L10ᵀ; warp 0 factors L11. fp32, as the rest of the factorisation.
-// This step is latency-bound (one serial 64-column chain per run); see DESIGN §5.
+// tiles: warp 0 factors L00; warp 1 solves L10 = A10·L00⁻ᵀ (lane per row, right-looking with the
+// row rotating as in warp_chol32 — the same fma sequence as forward substitution); warp 1 forms
+// A11 − L10·L10ᵀ row by row into shared memory; warp 0 factors L11. fp32, as the rest of the
+// factorisation. Every loop over columns is rolled (instruction-cache resident). This step is
+// latency-bound (one serial 64-column chain per run); see DESIGN §5.
 __global__ void __launch_bounds__(64) chol_diag_kernel(DevState s, int kb) {
-  __shared__ float L00[32][33];
-  __shared__ float L10[32][33];
+  __shared__ float L00[64][33];   // rows 32..63 zero: the rolled solve reads L00[j+k][j] unguarded
+  __shared__ float S[32][33];     // L10, then A11 − L10·L10ᵀ
   __shared__ int bad;
   const int r = blockIdx.x;
   if (!chol_due(s, r) || s.chol_fail[r]) return;
@@ -392,16 +405,24 @@ __global__ void __launch_bounds__(64) chol_diag_kernel(DevState s, int kb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto at = [&](int i, int j) -> float& { return Wk[(int64_t)(kb + i) * D + kb + j]; };
   if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  float a[32];
+  const int b1 = b - 32;
+  float a[32], x[32], row[32];
+  if (warp == 1 && b1 > 0) {      // warp 1 fetches its A10 and A11 rows while warp 0 factors L00
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      x[k] = lane < b1 ? at(32 + lane, k) : 0.0f;
+      row[k] = (lane < b1 && k <= lane && k < b1) ? at(32 + lane, 32 + k) : (k == lane ? 1.0f : 0.0f);
+    }
+  }
   if (warp == 0) {
 #pragma unroll
     for (int k = 0; k < 32; ++k) a[k] = (lane < b && k <= lane && k < b) ? at(lane, k) : (k == lane ? 1.0f : 0.0f);
     const bool ok = warp_chol32(a, lane);
-    if (!ok && lane == 0) bad = 1;
+    if (!ok) bad = 1;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       L00[lane][k] = k <= lane ? a[k] : 0.0f;
+      L00[32 + lane][k] = 0.0f;
       if (lane < b && k <= lane && k < b) at(lane, k) = a[k];
     }
   }
@@ -410,37 +431,42 @@ __global__ void __launch_bounds__(64) chol_diag_kernel(DevState s, int kb) {
     if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
     return;
   }
-  const int b1 = b - 32;
   if (warp == 1) {
-    float x[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = lane < b1 ? at(32 + lane, k) : 0.0f;
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < 32; ++j) {
-      float acc = x[j];
+      const float xj = __fdiv_rn(x[0], L00[j][j]);
 #pragma unroll
-      for (int k = 0; k < j; ++k) acc = __fmaf_rn(-x[k], L00[j][k], acc);
-      x[j] = __fdiv_rn(acc, L00[j][j]);
+      for (int k = 1; k < 32; ++k) x[k] = __fmaf_rn(-xj, L00[j + k][j], x[k]);
+      rot32(x, xj);
     }
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      L10[lane][k] = x[k];
+      S[lane][k] = x[k];
       if (lane < b1) at(32 + lane, k) = x[k];
     }
+    __syncwarp();
+    // row `lane` of A11 − L10·L10ᵀ (k ≤ lane), the m-sum in order as before; the row rotates
+    // through row[0] like warp_chol32's
+#pragma unroll 1
+    for (int k = 0; k < 32; ++k) {
+      const bool in = lane < b1 && k <= lane && k < b1;
+      float v = row[0];
+      if (in) {
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v = __fmaf_rn(-x[m], S[k][m], v);
+      }
+      rot32(row, v);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) S[lane][k] = row[k];
   }
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      float v = (lane < b1 && k <= lane && k < b1) ? at(32 + lane, 32 + k) : (k == lane ? 1.0f : 0.0f);
-      if (lane < b1 && k <= lane && k < b1) {
-#pragma unroll
-        for (int m = 0; m < 32; ++m) v = __fmaf_rn(-L10[lane][m], L10[k][m], v);
-      }
-      a[k] = v;
-    }
+    for (int k = 0; k < 32; ++k) a[k] = S[lane][k];
     const bool ok = warp_chol32(a, lane);
-    if (!ok && lane == 0) bad = 1;
+    if (!ok) bad = 1;
 #pragma unroll
     for (int k = 0; k < 32; ++k)
       if (lane < b1 && k <= lane && k < b1) at(32 + lane, 32 + k) = a[k];
