@@ -4,13 +4,15 @@
 // Per run r: Y[r] (N × D) = Z[r] (N × D) · A[r]ᵀ (D × D, lower-triangular). One CTA computes a
 // 128-member × 128-dim tile with tcgen05.mma.kind::tf32 (M = 128, N = 128, K = 8), fp32 accumulator
 // in 128 TMEM columns. fp32 accuracy from the 3-pass split: every operand x = big + small with
-// big = tf32_rna(x) and small = tf32_rna(x − big), both exact tf32 values, and
-//   a·b ≈ big_a·big_b + big_a·small_b + small_a·big_b      (the dropped small·small is ~2⁻²² |ab|).
+// big = x with its low 13 mantissa bits cleared — exactly what the tensor core reads from the raw
+// fp32 tile, so the raw tile IS big — and small = x − big (exact in fp32; the MMA keeps its top 11
+// bits, 2⁻²¹|x|), and
+//   a·b ≈ big_a·big_b + big_a·small_b + small_a·big_b      (the dropped small·small is ~2⁻²⁰ |ab|).
 // An output tile's K range stops at its last dim (A[d][k] = 0 for k > d).
 //
 // Warp roles (256 threads): warp 0 lane 0 — TMA producer (Z and A tiles, [128 rows × 32 k] fp32,
 // K-major SWIZZLE_128B, 3-stage ring); warp 1 — TMEM allocation + the single MMA-issuing thread;
-// warps 4–7 — split each landed stage in place (big over the raw tile, small into its twin), then
+// warps 4–7 — write each landed stage's small parts into the tile's twin (one FADD per element), then
 // the epilogue: tcgen05.ld (TMEM lane = member row), x = fma(σ, y, m) (+ box clip), Y and x out.
 #include <cuda.h>
 
@@ -49,10 +51,9 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// The tf32 value the tensor core reads from an fp32 operand: the low 13 mantissa bits ignored.
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
 __global__ void __launch_bounds__(256, 1) cma_sample_tc_kernel(const __grid_constant__ CmaTcParams P) {
@@ -136,48 +137,53 @@ __global__ void __launch_bounds__(256, 1) cma_sample_tc_kernel(const __grid_cons
       uint8_t* st = smem + s * kTcStageBytes;
 #pragma unroll
       for (int op = 0; op < 2; ++op) {                 // Z tile, then A tile
-        float4* big = reinterpret_cast<float4*>(st + op * 2 * kTcTile);
+        const float4* raw = reinterpret_cast<const float4*>(st + op * 2 * kTcTile);
         float4* small = reinterpret_cast<float4*>(st + op * 2 * kTcTile + kTcTile);
 #pragma unroll
         for (int i = 0; i < kTcTile / 16 / 128; ++i) {
           const int o = t + 128 * i;
-          float4 v = big[o], b, sm;
-          b.x = tf32_rna(v.x); b.y = tf32_rna(v.y); b.z = tf32_rna(v.z); b.w = tf32_rna(v.w);
-          sm.x = tf32_rna(__fsub_rn(v.x, b.x)); sm.y = tf32_rna(__fsub_rn(v.y, b.y));
-          sm.z = tf32_rna(__fsub_rn(v.z, b.z)); sm.w = tf32_rna(__fsub_rn(v.w, b.w));
-          big[o] = b;
-          small[o] = sm;
+          const float4 v = raw[o];
+          small[o] = make_float4(__fsub_rn(v.x, tf32_trunc(v.x)), __fsub_rn(v.y, tf32_trunc(v.y)),
+                                 __fsub_rn(v.z, tf32_trunc(v.z)), __fsub_rn(v.w, tf32_trunc(v.w)));
         }
       }
       fence_async_smem();
       named_bar(1, 128);
       if (t == 0) mbar_arrive(&split[s]);
     }
-    // epilogue: lane quarter q = warp & 3 → member rows j0 + 32q + lane
+    // epilogue: lane quarter q = warp & 3 → member rows j0 + 32q + lane. Each 32 × 32 sub-tile is
+    // transposed through shared memory (the ring is idle once the accumulator is complete) so that
+    // every store is one member's 32 consecutive dims — a full 128-B line, not 32 scattered words.
     mbar_wait(accum, 0);
     tc_fence_after();
     const int q = warp & 3;
-    const int j = j0 + q * 32 + lane;
     const RunScal& rs = P.rs[r];
     const float sig = rs.sigma;
     const float* m = P.mean + (int64_t)r * D;
+    float (*T)[33] = reinterpret_cast<float (*)[33]>(smem + q * (32 * 33 * 4));
     for (int c0 = 0; c0 < 128; c0 += 32) {
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      if (j >= P.N) continue;
-      const int64_t row = ((int64_t)r * P.N + j) * D;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int64_t d = d0 + c0 + i;
-        if (d < D) {
-          P.y[row + d] = v[i];
-          if (P.x) {
-            float xv = __fmaf_rn(sig, v[i], m[d]);
-            if (rs.clip) xv = fminf(fmaxf(xv, rs.clip_lo), rs.clip_hi);
-            P.x[row + d] = xv;
-          }
+      for (int i = 0; i < 32; ++i) T[lane][i] = v[i];
+      __syncwarp();
+      const int64_t d = d0 + c0 + lane;
+      const bool dok = d < D;
+      const float md = dok ? m[d] : 0.0f;
+#pragma unroll 4
+      for (int rr = 0; rr < 32; ++rr) {
+        const int j = j0 + q * 32 + rr;
+        if (j >= P.N || !dok) continue;
+        const float yv = T[rr][lane];
+        const int64_t o = ((int64_t)r * P.N + j) * D + d;
+        P.y[o] = yv;
+        if (P.x) {
+          float xv = __fmaf_rn(sig, yv, md);
+          if (rs.clip) xv = fminf(fmaxf(xv, rs.clip_lo), rs.clip_hi);
+          P.x[o] = xv;
         }
       }
+      __syncwarp();
     }
   }
   tc_fence_before();

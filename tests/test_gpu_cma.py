@@ -116,6 +116,28 @@ def test_one_generation(R, N, D, fn):
     pair.close()
 
 
+@pytest.mark.parametrize("R,N,D", [(2, 64, 128), (1, 256, 1024), (1, 40, 300)])
+def test_sampling_through_the_factor_is_fp32_accurate(R, N, D):
+    """The second population is x = m + σ·A·z with the FIRST refreshed factor A (≠ I). Checked
+    against binary64 A·z built from the GPU's own A, m, σ and the oracle's bit-identical z, so the
+    only error left is the contraction's: fp32-level (3-pass tf32 split on the tensor cores), far
+    below what a one-tf32-ulp operand error (2⁻¹¹ relative) would give."""
+    pair = CmaPair(N, D, _params(R))
+    pair.step(W.ROSENBROCK)
+    A = pair.gpu.get("chol").cpu().numpy().astype(np.float64)
+    m = pair.gpu.get("mean").cpu().numpy().astype(np.float64)
+    sg = pair.gpu.get("sigma").cpu().numpy().astype(np.float64)
+    x = pair.gpu.ask().cpu().numpy().astype(np.float64)
+    for r in range(R):
+        assert not np.allclose(A[r], np.eye(D)), "the factor was not refreshed"
+        pair.orc[r].ask()                              # advances the oracle; its Z is this gen's
+        y_ref = pair.orc[r].Z @ A[r].T
+        y_gpu = (x[r] - m[r][None, :]) / sg[r]
+        e = np.abs(y_gpu - y_ref).max() / np.abs(y_ref).max()
+        assert e <= 2e-6, (r, e)
+    pair.close()
+
+
 # fn None: synthetic fitness (N15) — no convergence, so the state keeps its scale and the check
 # isolates arithmetic drift; a converging run (sphere) shrinks ‖x‖ geometrically while the
 # teacher-forced oracle's own-x error does not shrink with it.
