@@ -18,6 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
          "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("ES_NVCC_EXTRA", "").split()   # e.g. instrumentation macros (profiling only)
 
 
 def sources():

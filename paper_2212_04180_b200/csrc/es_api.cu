@@ -379,6 +379,8 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   TRY(dalloc(c, (void**)&s.n2, 2 * (size_t)R * sizeof(double)));   // [0,R) shares, [R,2R) ClipUp ‖v'‖²
   s.cov = s.chol = s.cw = s.zbuf = s.ybuf = nullptr;
   s.chol_fail = nullptr;
+  s.ut = s.vt = nullptr;
+  s.kp = 0;
   if (cma) {
     const size_t RDD = (size_t)R * s.D * s.D, RND = (size_t)R * N * s.D;
     TRY(dalloc(c, (void**)&s.cov, RDD * sizeof(float)));
@@ -387,6 +389,9 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     TRY(dalloc(c, (void**)&s.zbuf, RND * sizeof(float)));
     TRY(dalloc(c, (void**)&s.ybuf, RND * sizeof(float)));
     TRY(dalloc(c, (void**)&s.chol_fail, R * sizeof(int32_t)));
+    s.kp = (N + 31) / 32 * 32;
+    TRY(dalloc(c, (void**)&s.ut, (size_t)R * s.D * s.kp * sizeof(float)));
+    TRY(dalloc(c, (void**)&s.vt, (size_t)R * s.D * s.kp * sizeof(float)));
   }
   if (dsh) TRY(dalloc(c, (void**)&c->fpart, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.dir, RN * sizeof(uint32_t)));

@@ -94,7 +94,23 @@ struct DevState {
   float* zbuf;         // [R][N][D] this generation's z
   float* ybuf;         // [R][N][D] y = A z
   int32_t* chol_fail;  // [R] the last refresh failed (A kept)
+  float* ut;           // [R][D][kp] w_e·y_e transposed (tensor-core covariance update operand)
+  float* vt;           // [R][D][kp] y_e transposed
+  int kp;              // entry capacity of ut / vt (N rounded up to 32)
 };
+
+// full CMA-ES helpers shared by k_cma.cu and k_cma_syrk.cu
+// the Cholesky factor is refreshed after this tell (rs.t already counts it)
+__device__ __forceinline__ bool chol_due_rs(const RunScal& rs) {
+  return rs.k_refresh > 0 && (rs.t % (uint32_t)rs.k_refresh) == 0u;
+}
+// lower tile index t → (I, J), I ≥ J
+__device__ __forceinline__ void lower_tile(int t, int& I, int& J) {
+  I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  J = t - I * (I + 1) / 2;
+}
 
 // f2 peer-memory tell: every rank's direction-sum buffer and state fields, as device pointers
 // valid in this process (peer mappings over NVLink, or plain pointers for ranks emulated on one GPU).
@@ -176,6 +192,9 @@ cudaError_t launch_cma_ask(const DevState& s, float* x, cudaStream_t st, int* nk
 cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk);
 // the sampling contraction on tcgen05 (kind::tf32, 3-pass split); needs D % 4 == 0
 bool cma_tc_supported(const DevState& s);
+bool syrk_tc_supported(const DevState& s);
+cudaError_t launch_chol_update_tc(const DevState& s, int kb, cudaStream_t st);
+cudaError_t launch_cma_cov_tc(const DevState& s, cudaStream_t st);
 cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;

@@ -16,6 +16,7 @@
 //                  update); a run whose C is not positive definite keeps its previous factor.
 // The contractions here are FP32 FFMA tiles on the CUDA cores.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "es_internal.h"
@@ -259,14 +260,6 @@ __global__ void __launch_bounds__(256) cma_pc_kernel(DevState s) {
   s.vec[F_PC][gid] = __fadd_rn(__fmul_rn(omcc, s.vec[F_PC][gid]), __fmul_rn(kc, (float)s.G[gid]));
 }
 
-// lower tile index t → (I, J), I ≥ J
-__device__ __forceinline__ void lower_tile(int t, int& I, int& J) {
-  I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-  while ((I + 1) * (I + 2) / 2 <= t) ++I;
-  while (I * (I + 1) / 2 > t) --I;
-  J = t - I * (I + 1) / 2;
-}
-
 // C ← a·C + c₁ p_c p_cᵀ + c_μ Σ_e w_e y_e y_eᵀ (lower tiles; mirrored).
 __global__ void __launch_bounds__(256) cma_cov_kernel(DevState s) {
   __shared__ __align__(16) float Ui[kTK][kTB + 4];
@@ -336,10 +329,7 @@ __global__ void __launch_bounds__(256) cma_cov_kernel(DevState s) {
 }
 
 // ---------------------------------------------------------------------------------- Cholesky
-__device__ __forceinline__ bool chol_due(const DevState& s, int r) {
-  const RunScal& rs = s.rs[r];
-  return rs.k_refresh > 0 && (rs.t % (uint32_t)rs.k_refresh) == 0u;   // rs.t already = t + 1
-}
+__device__ __forceinline__ bool chol_due(const DevState& s, int r) { return chol_due_rs(s.rs[r]); }
 
 __global__ void chol_copy_kernel(DevState s) {
   const int r = blockIdx.y;
@@ -353,123 +343,129 @@ __global__ void chol_copy_kernel(DevState s) {
   if (blockIdx.x == 0 && threadIdx.x == 0) s.chol_fail[r] = 0;
 }
 
-// Register rotation a[k] ← a[k+1], a[31] ← v: lets a ROLLED loop visit column j as a[0].
-__device__ __forceinline__ void rot32(float (&a)[32], float v) {
+// ---- 64 × 64 diagonal block: left-looking, one warp per 32 × 32 step, rows in shared memory.
+// Row stride 36 floats: 16-B aligned rows for LDS.128, and a lane's own-row LDS.128 spreads over
+// the banks in the minimum 4 wavefronts.
+static constexpr int kLs = 36;
+
+// Dot product of two 32-float shared-memory rows (x: this lane's, r: broadcast), 4 partial sums.
+__device__ __forceinline__ float dot32_smem(const float* x, const float* r) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-  for (int k = 0; k < 31; ++k) a[k] = a[k + 1];
-  a[31] = v;
+  for (int q = 0; q < 8; ++q) {
+    const float4 a = reinterpret_cast<const float4*>(x)[q];
+    const float4 b = reinterpret_cast<const float4*>(r)[q];
+    s0 = __fmaf_rn(a.x, b.x, s0);
+    s1 = __fmaf_rn(a.y, b.y, s1);
+    s2 = __fmaf_rn(a.z, b.z, s2);
+    s3 = __fmaf_rn(a.w, b.w, s3);
+  }
+  return __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
 }
 
-// 32×32 Cholesky by one warp: lane i holds row i (a[k], k ≤ i) in registers; column j's pivot and
-// entries are broadcast with shuffles, so a column costs no barrier. The column loop is rolled
-// (the row rotates one register per column, so column j is always a[0] and the finished entry
-// goes to a[31]; after 32 columns the row is back in order): the body stays in the instruction
-// cache — the fully unrolled loop (~2.5 K instructions per call) was instruction-fetch-bound.
-// Same operations in the same order as the unrolled form. Returns false if a pivot is not positive.
-__device__ __forceinline__ bool warp_chol32(float (&a)[32], int lane) {
+// 1/√d and √d to ~1 ulp: the MUFU estimate plus one Newton step (no IEEE slow-path branches on
+// the serial chain).
+__device__ __forceinline__ void rsqrt_sqrt(float d, float& inv, float& piv) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
+  const float h = __fmul_rn(0.5f, d);
+  y = __fmul_rn(y, __fmaf_rn(-h, __fmul_rn(y, y), 1.5f));
+  inv = y;
+  piv = __fmul_rn(d, y);
+}
+
+// 32 × 32 Cholesky by one warp, left-looking (column j from the finished columns k < j):
+//   c_i = A[i][j] − Σ_{k<j} L[i][k]·L[j][k],  L[j][j] = √c_j,  L[i][j] = c_i / L[j][j] (i > j).
+// Lane i owns row i. A: [32][33] input; L: [32][kLs] output rows, ZERO on entry (so the dot
+// product may run over all 32 k: the not-yet-computed entries are 0). dinv[j] = 1/L[j][j].
+// One shuffle (the pivot) and one __syncwarp per column. Returns false if a pivot is not positive.
+__device__ bool warp_chol32(const float (*A)[33], float (*L)[kLs], float* dinv, int lane) {
   bool ok = true;
 #pragma unroll 1
   for (int j = 0; j < 32; ++j) {
-    const float d = __shfl_sync(0xffffffffu, a[0], j);
+    const float c = __fsub_rn(A[lane][j], dot32_smem(L[lane], L[j]));
+    const float d = __shfl_sync(0xffffffffu, c, j);
     ok = ok && d > 0.0f;
-    const float piv = d > 0.0f ? __fsqrt_rn(d) : 1.0f;
-    const float inv = __frcp_rn(piv);
-    float lij = a[0];
-    if (lane == j) lij = piv;
-    if (lane > j) lij = __fmul_rn(lij, inv);
-#pragma unroll
-    for (int k = 1; k < 32; ++k) {
-      const float lkj = __shfl_sync(0xffffffffu, lij, j + k);   // lane j+k (≥ 32: predicated off)
-      if (lane >= j + k) a[k] = __fmaf_rn(-lij, lkj, a[k]);
-    }
-    rot32(a, lij);
+    float inv = 1.0f, piv = 1.0f;
+    if (d > 0.0f) rsqrt_sqrt(d, inv, piv);
+    const float v = lane == j ? piv : (lane > j ? __fmul_rn(c, inv) : 0.0f);
+    L[lane][j] = v;
+    if (lane == j) dinv[j] = inv;
+    __syncwarp();
   }
   return ok;
 }
 
-// Diagonal block [kb, kb+64)² (the last may be narrower) as a 2×2 blocked Cholesky of 32×32
-// tiles: warp 0 factors L00; warp 1 solves L10 = A10·L00⁻ᵀ (lane per row, right-looking with the
-// row rotating as in warp_chol32 — the same fma sequence as forward substitution); warp 1 forms
-// A11 − L10·L10ᵀ row by row into shared memory; warp 0 factors L11. fp32, as the rest of the
-// factorisation. Every loop over columns is rolled (instruction-cache resident). This step is
-// latency-bound (one serial 64-column chain per run); see DESIGN §5.
+// Diagonal block [kb, kb+64)² (the last may be narrower) as a 2 × 2 blocked Cholesky of 32 × 32
+// tiles: warp 0 factors L00; warp 1 solves L10 = A10·L00⁻ᵀ (left-looking forward substitution,
+// x_j = (a_j − Σ_{k<j} x_k L00[j][k]) / L00[j][j]) and forms A11 − L10·L10ᵀ; warp 0 factors L11.
+// Every step is a rolled loop over shared-memory rows (instruction-cache resident; the earlier
+// fully unrolled register form was instruction-fetch-bound). fp32 throughout. Latency-bound:
+// one serial 64-column chain per run.
 __global__ void __launch_bounds__(64) chol_diag_kernel(DevState s, int kb) {
-  __shared__ float L00[64][33];   // rows 32..63 zero: the rolled solve reads L00[j+k][j] unguarded
-  __shared__ float S[32][33];     // L10, then A11 − L10·L10ᵀ
+  __shared__ __align__(16) float L0[32][kLs];   // L00 rows
+  __shared__ __align__(16) float L1[32][kLs];   // L11 rows
+  __shared__ __align__(16) float X[32][kLs];    // L10 rows
+  __shared__ float A0[32][33];                  // A00 (identity-padded)
+  __shared__ float A1[32][33];                  // A11, then A11 − L10·L10ᵀ
+  __shared__ float B[32][33];                   // A10
+  __shared__ float dinv0[32], dinv1[32];
   __shared__ int bad;
   const int r = blockIdx.x;
   if (!chol_due(s, r) || s.chol_fail[r]) return;
   const int64_t D = s.D;
   const int b = (int)std::min<int64_t>(kNB, D - kb);
+  const int b1 = b - 32;
   float* Wk = s.cw + (int64_t)r * D * D;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto at = [&](int i, int j) -> float& { return Wk[(int64_t)(kb + i) * D + kb + j]; };
   if (threadIdx.x == 0) bad = 0;
-  const int b1 = b - 32;
-  float a[32], x[32], row[32];
-  if (warp == 1 && b1 > 0) {      // warp 1 fetches its A10 and A11 rows while warp 0 factors L00
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      x[k] = lane < b1 ? at(32 + lane, k) : 0.0f;
-      row[k] = (lane < b1 && k <= lane && k < b1) ? at(32 + lane, 32 + k) : (k == lane ? 1.0f : 0.0f);
-    }
-  }
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) a[k] = (lane < b && k <= lane && k < b) ? at(lane, k) : (k == lane ? 1.0f : 0.0f);
-    const bool ok = warp_chol32(a, lane);
-    if (!ok) bad = 1;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      L00[lane][k] = k <= lane ? a[k] : 0.0f;
-      L00[32 + lane][k] = 0.0f;
-      if (lane < b && k <= lane && k < b) at(lane, k) = a[k];
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {               // zero the L rows; stage the inputs (row = lane)
+    if (warp == 0) {
+      L0[lane][k] = 0.0f;
+      L1[lane][k] = 0.0f;
+      A0[lane][k] = (lane < b && k <= lane && k < b) ? at(lane, k) : (k == lane ? 1.0f : 0.0f);
+    } else {
+      X[lane][k] = 0.0f;
+      B[lane][k] = b1 > 0 && lane < b1 ? at(32 + lane, k) : 0.0f;
+      A1[lane][k] = (lane < b1 && k <= lane && k < b1) ? at(32 + lane, 32 + k) : (k == lane ? 1.0f : 0.0f);
     }
   }
   __syncthreads();
-  if (b <= 32) {
+  if (warp == 0) {
+    if (!warp_chol32(A0, L0, dinv0, lane)) bad = 1;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k)
+      if (lane < b && k <= lane && k < b) at(lane, k) = L0[lane][k];
+  }
+  __syncthreads();
+  if (b1 <= 0) {
     if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
     return;
   }
   if (warp == 1) {
 #pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-      const float xj = __fdiv_rn(x[0], L00[j][j]);
-#pragma unroll
-      for (int k = 1; k < 32; ++k) x[k] = __fmaf_rn(-xj, L00[j + k][j], x[k]);
-      rot32(x, xj);
+    for (int j = 0; j < 32; ++j) {               // L10: left-looking forward substitution
+      const float c = __fsub_rn(B[lane][j], dot32_smem(X[lane], L0[j]));
+      X[lane][j] = __fmul_rn(c, dinv0[j]);
+      __syncwarp();
     }
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      S[lane][k] = x[k];
-      if (lane < b1) at(32 + lane, k) = x[k];
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k)
+      if (lane < b1) at(32 + lane, k) = X[lane][k];
+#pragma unroll 2
+    for (int k = 0; k < 32; ++k) {               // A11 − L10·L10ᵀ, row `lane`, k ≤ lane
+      if (lane < b1 && k <= lane && k < b1)
+        A1[lane][k] = __fsub_rn(A1[lane][k], dot32_smem(X[lane], X[k]));
     }
-    __syncwarp();
-    // row `lane` of A11 − L10·L10ᵀ (k ≤ lane), the m-sum in order as before; the row rotates
-    // through row[0] like warp_chol32's
-#pragma unroll 1
-    for (int k = 0; k < 32; ++k) {
-      const bool in = lane < b1 && k <= lane && k < b1;
-      float v = row[0];
-      if (in) {
-#pragma unroll
-        for (int m = 0; m < 32; ++m) v = __fmaf_rn(-x[m], S[k][m], v);
-      }
-      rot32(row, v);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 32; ++k) S[lane][k] = row[k];
   }
   __syncthreads();
   if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) a[k] = S[lane][k];
-    const bool ok = warp_chol32(a, lane);
-    if (!ok) bad = 1;
-#pragma unroll
+    if (!warp_chol32(A1, L1, dinv1, lane)) bad = 1;
+#pragma unroll 4
     for (int k = 0; k < 32; ++k)
-      if (lane < b1 && k <= lane && k < b1) at(32 + lane, 32 + k) = a[k];
+      if (lane < b1 && k <= lane && k < b1) at(32 + lane, 32 + k) = L1[lane][k];
   }
   __syncthreads();
   if (threadIdx.x == 0 && bad) s.chol_fail[r] = 1;
@@ -601,9 +597,16 @@ cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, in
   cma_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr);
   const int64_t RD = (int64_t)s.R * s.D;
   cma_pc_kernel<<<(unsigned)((RD + 255) / 256), 256, 0, st>>>(s);
-  const int T = (int)((s.D + kTB - 1) / kTB);
-  cma_cov_kernel<<<dim3((unsigned)(T * (T + 1) / 2), (unsigned)s.R), 256, 0, st>>>(s);
-  n += 4;
+  static const bool simt = std::getenv("ES_CMA_SIMT") != nullptr;   // A/B switch for profiling
+  const bool tc = !simt && syrk_tc_supported(s);
+  if (tc) {
+    if (cudaError_t e = launch_cma_cov_tc(s, st)) return e;
+    n += 5;
+  } else {
+    const int T = (int)((s.D + kTB - 1) / kTB);
+    cma_cov_kernel<<<dim3((unsigned)(T * (T + 1) / 2), (unsigned)s.R), 256, 0, st>>>(s);
+    n += 4;
+  }
   if (refresh) {
     const int64_t DD = s.D * s.D;
     const unsigned cb = (unsigned)std::min<int64_t>((DD + 255) / 256, 1024);
@@ -616,9 +619,13 @@ cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, in
       if (rest > 0) {
         chol_panel_kernel<<<dim3((unsigned)((rest + kPanelRows - 1) / kPanelRows), (unsigned)s.R),
                             kPanelRows, 0, st>>>(s, (int)kb);
-        const int Tt = (int)((rest + kTB - 1) / kTB);
-        chol_update_kernel<<<dim3((unsigned)(Tt * (Tt + 1) / 2), (unsigned)s.R), 256, 0, st>>>(
-            s, (int)kb);
+        if (tc) {
+          if (cudaError_t e = launch_chol_update_tc(s, (int)kb, st)) return e;
+        } else {
+          const int Tt = (int)((rest + kTB - 1) / kTB);
+          chol_update_kernel<<<dim3((unsigned)(Tt * (Tt + 1) / 2), (unsigned)s.R), 256, 0, st>>>(
+              s, (int)kb);
+        }
         n += 2;
       }
     }
