@@ -114,7 +114,7 @@ typedef enum {
                             uses only the first R*D entries                                    */
   ES_FIELD_NORM2 = 18,   /* double [R] Sep-CMA-ES: a D-shard's share of ‖p_σ'‖² after
                             es_tell_local; the caller sets the rank sum before es_tell_apply     */
-  ES_FIELD_COV = 19,     /* float [R][D][D] CMA-ES covariance C (symmetric, both triangles)   */
+  ES_FIELD_COV = 19,     /* float [R][D][D] CMA-ES covariance C (symmetric, both triangles kept) */
   ES_FIELD_CHOL = 20,    /* float [R][D][D] CMA-ES sampling factor A (lower; upper = 0)       */
   ES_NUM_FIELDS = 21
 } es_field_t;

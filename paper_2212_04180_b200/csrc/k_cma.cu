@@ -331,15 +331,25 @@ __global__ void __launch_bounds__(256) cma_cov_kernel(DevState s) {
 // ---------------------------------------------------------------------------------- Cholesky
 __device__ __forceinline__ bool chol_due(const DevState& s, int r) { return chol_due_rs(s.rs[r]); }
 
-__global__ void chol_copy_kernel(DevState s) {
+// W ← lower(C): the factorisation reads and writes nothing above the diagonal. One row per
+// block iteration, float4 when rows are 16-B aligned (the ≤ 3 entries past the diagonal that a
+// last float4 carries are never read).
+__global__ void __launch_bounds__(256) chol_copy_kernel(DevState s) {
   const int r = blockIdx.y;
   if (!chol_due(s, r)) return;
-  const int64_t DD = s.D * s.D;
+  const int64_t D = s.D, DD = D * D;
   const float* C = s.cov + (int64_t)r * DD;
   float* Wk = s.cw + (int64_t)r * DD;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < DD;
-       g += (int64_t)gridDim.x * blockDim.x)
-    Wk[g] = C[g];
+  const bool v4 = (D & 3) == 0;
+  for (int64_t i = blockIdx.x; i < D; i += gridDim.x) {
+    if (v4) {
+      const float4* src = reinterpret_cast<const float4*>(C + i * D);
+      float4* dst = reinterpret_cast<float4*>(Wk + i * D);
+      for (int64_t c = threadIdx.x; c < (i + 4) / 4; c += blockDim.x) dst[c] = src[c];
+    } else {
+      for (int64_t c = threadIdx.x; c <= i; c += blockDim.x) Wk[i * D + c] = C[i * D + c];
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) s.chol_fail[r] = 0;
 }
 
@@ -579,15 +589,29 @@ __global__ void __launch_bounds__(256) chol_update_kernel(DevState s, int kb) {
 }
 
 // A ← lower(W) for runs whose refresh succeeded.
-__global__ void chol_commit_kernel(DevState s) {
+__global__ void __launch_bounds__(256) chol_commit_kernel(DevState s) {
   const int r = blockIdx.y;
   if (!chol_due(s, r) || s.chol_fail[r]) return;
-  const int64_t DD = s.D * s.D;
+  const int64_t D = s.D, DD = D * D;
   const float* Wk = s.cw + (int64_t)r * DD;
-  float* A = s.chol + (int64_t)r * DD;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < DD;
-       g += (int64_t)gridDim.x * blockDim.x)
-    A[g] = (g % s.D) <= (g / s.D) ? Wk[g] : 0.0f;
+  float* A = s.chol + (int64_t)r * DD;                 // its upper triangle is 0 from cma_init on
+  const bool v4 = (D & 3) == 0;
+  for (int64_t i = blockIdx.x; i < D; i += gridDim.x) {
+    if (v4) {
+      const float4* src = reinterpret_cast<const float4*>(Wk + i * D);
+      float4* dst = reinterpret_cast<float4*>(A + i * D);
+      for (int64_t c = threadIdx.x; c < (i + 4) / 4; c += blockDim.x) {
+        float4 v = src[c];
+        const int64_t j = 4 * c;
+        if (j + 1 > i) v.y = 0.0f;
+        if (j + 2 > i) v.z = 0.0f;
+        if (j + 3 > i) v.w = 0.0f;
+        dst[c] = v;
+      }
+    } else {
+      for (int64_t c = threadIdx.x; c <= i; c += blockDim.x) A[i * D + c] = Wk[i * D + c];
+    }
+  }
 }
 
 cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, int* nk) {
@@ -609,7 +633,7 @@ cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, in
   }
   if (refresh) {
     const int64_t DD = s.D * s.D;
-    const unsigned cb = (unsigned)std::min<int64_t>((DD + 255) / 256, 1024);
+    const unsigned cb = (unsigned)std::min<int64_t>(s.D, 1024);   // one row per block iteration
     chol_copy_kernel<<<dim3(cb, (unsigned)s.R), 256, 0, st>>>(s);
     n += 1;
     for (int64_t kb = 0; kb < s.D; kb += kNB) {
