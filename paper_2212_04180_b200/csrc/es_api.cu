@@ -1,6 +1,7 @@
 // es_api.cu — the C ABI (include/es.h): context lifetime, argument validation, host-side constant
 // tables (binary64, NUMERICS N11/N12), host↔device staging, NCCL plumbing and the launch sequence
 // of one generation. No exception crosses the ABI; every CUDA/NCCL failure becomes a status code.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -117,7 +118,9 @@ static cudaError_t dalloc(es_ctx* c, void** p, size_t bytes) {
   return e;
 }
 
-// Profiling brackets (bench only): an event pair around each launch on the launching stream.
+// Profiling brackets: an NVTX range around each launch group (host side, for nsys / ncu --nvtx;
+// header-only NVTX 3 — a no-op branch when no tool is attached) and, when profiling is enabled
+// (bench), an event pair on the launching stream.
 static cudaEvent_t prof_event(es_ctx* c) {
   if (!c->pool.empty()) {
     cudaEvent_t e = c->pool.back();
@@ -133,6 +136,7 @@ struct ProfScope {
   cudaStream_t st;
   size_t idx = (size_t)-1;
   ProfScope(es_ctx* c_, const char* name, cudaStream_t st_) : c(c_), st(st_) {
+    nvtxRangePushA(name);
     if (c && c->profiling) {
       es_ctx::Rec r{name, prof_event(c), prof_event(c)};
       cudaEventRecord(r.a, st);
@@ -142,6 +146,7 @@ struct ProfScope {
   }
   ~ProfScope() {
     if (idx != (size_t)-1) cudaEventRecord(c->recs[idx].b, st);
+    nvtxRangePop();
   }
 };
 
