@@ -334,6 +334,16 @@ int32_t es_profile_read(es_ctx_t *ctx, char *names /* [max_kinds][32] */, double
 es_status_t es_debug_primitive(int32_t which, const void *in, void *out, int64_t n,
                                es_stream_t stream);
 
+/* Out-of-bounds-write detection for every device buffer the library allocates (compute-sanitizer
+ * is unavailable on the target pool). When the environment variable ES_GUARD_ALLOCS=1 is set at
+ * es_init / es_init_dshard, each state / workspace allocation of the context (all but the MLP
+ * problem's read-only data set) gets 256-byte guard zones before and after it, filled
+ * with 0xA5; es_debug_check_guards synchronises the device and writes to *bad_bytes the number of
+ * guard bytes that no longer hold 0xA5 (0 = no write outside any buffer so far). Guard mode
+ * rejects es_p2p_ipc_export (an IPC handle maps the allocation base). Errors: ES_ERR_BAD_STATE
+ * when the context was not created in guard mode. */
+es_status_t es_debug_check_guards(es_ctx_t *ctx, int64_t *bad_bytes);
+
 es_status_t es_destroy(es_ctx_t *ctx);
 
 /* Last error message of the context (or of the calling thread when ctx is NULL). */

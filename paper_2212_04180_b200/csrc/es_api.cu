@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -77,7 +78,10 @@ struct es_ctx {
   struct Rec { const char* name; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
-  std::vector<void*> allocs;
+  std::vector<void*> allocs;     // cudaMalloc bases
+  bool guard = false;            // ES_GUARD_ALLOCS=1: 256-B 0xA5 zones around every allocation
+  struct Zone { const unsigned char* p; size_t bytes; };
+  std::vector<Zone> zones;
   std::string err;
 };
 
@@ -111,11 +115,26 @@ static es_status_t fail(es_ctx* c, es_status_t st, const char* fmt, ...) {
     }                                                                                  \
   } while (0)
 
+static constexpr size_t kGuard = 256;   // keeps the 256-B alignment of the returned pointer
+
 static cudaError_t dalloc(es_ctx* c, void** p, size_t bytes) {
   bytes = std::max<size_t>(bytes, 256);
-  cudaError_t e = cudaMalloc(p, bytes);
-  if (e == cudaSuccess) c->allocs.push_back(*p);
-  return e;
+  if (!c->guard) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) c->allocs.push_back(*p);
+    return e;
+  }
+  bytes = (bytes + kGuard - 1) / kGuard * kGuard;
+  unsigned char* base = nullptr;
+  cudaError_t e = cudaMalloc((void**)&base, bytes + 2 * kGuard);
+  if (e != cudaSuccess) return e;
+  c->allocs.push_back(base);
+  if ((e = cudaMemset(base, 0xA5, kGuard)) != cudaSuccess) return e;
+  if ((e = cudaMemset(base + kGuard + bytes, 0xA5, kGuard)) != cudaSuccess) return e;
+  c->zones.push_back({base, kGuard});
+  c->zones.push_back({base + kGuard + bytes, kGuard});
+  *p = base + kGuard;
+  return cudaSuccess;
 }
 
 // Profiling brackets: an NVTX range around each launch group (host side, for nsys / ncu --nvtx;
@@ -336,6 +355,10 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
                   "not implemented for D-sharded contexts", r);
   }
   es_ctx* c = new (std::nothrow) es_ctx();
+  if (c) {
+    const char* g = std::getenv("ES_GUARD_ALLOCS");
+    c->guard = g && g[0] == '1';
+  }
   if (!c) return fail(nullptr, ES_ERR_OOM, "host allocation failed");
   DevState& s = c->s;
   s.algo = algo; s.R = R; s.N = N; s.W = pW; s.rank = prank; s.Nloc = N / pW;
@@ -1032,6 +1055,7 @@ int32_t es_p2p_finish_phases(const es_ctx_t* c) { return c ? p2p_phases(c) : -1;
 
 es_status_t es_p2p_ipc_export(const es_ctx_t* c, void* handles) {
   if (!c || !handles) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
+  if (c->guard) return fail(nullptr, ES_ERR_UNSUPPORTED, "IPC export in guard mode (ES_GUARD_ALLOCS)");
   auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
   std::memset(handles, 0, kIpcHandles * sizeof(cudaIpcMemHandle_t));
   cudaError_t e = cudaIpcGetMemHandle(&h[0], c->s.G);
@@ -1200,6 +1224,20 @@ es_status_t es_set(es_ctx_t* c, es_field_t field, const void* src, es_stream_t s
                                  p.data(), 16, 16, c->s.R, cudaMemcpyHostToDevice, st));
   }
   CUDA_OR(c, cudaStreamSynchronize(st));
+  return ES_SUCCESS;
+}
+
+es_status_t es_debug_check_guards(es_ctx_t* c, int64_t* bad_bytes) {
+  if (!c || !bad_bytes) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->guard) return fail(c, ES_ERR_BAD_STATE, "context not created with ES_GUARD_ALLOCS=1");
+  CUDA_OR(c, cudaDeviceSynchronize());
+  std::vector<unsigned char> h(kGuard);
+  int64_t bad = 0;
+  for (const auto& z : c->zones) {
+    CUDA_OR(c, cudaMemcpy(h.data(), z.p, z.bytes, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < z.bytes; ++k) bad += h[k] != 0xA5;
+  }
+  *bad_bytes = bad;
   return ES_SUCCESS;
 }
 

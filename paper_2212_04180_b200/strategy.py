@@ -151,6 +151,12 @@ class Strategy:
     def p2p_finish_phases(self):
         return int(lib().es_p2p_finish_phases(self.ctx))
 
+    def check_guards(self):
+        """ES_GUARD_ALLOCS=1 contexts: guard bytes overwritten so far (0 = no out-of-bounds write)."""
+        n = C.c_int64(-1)
+        check(lib().es_debug_check_guards(self.ctx, C.byref(n)), self.ctx)
+        return int(n.value)
+
     def nvls_open(self, creator, handle=None):
         """f2 NVLS: create (creator) or join the multicast object; returns the 64-byte handle."""
         h = torch.zeros(64, dtype=torch.uint8)

@@ -3,7 +3,9 @@ weight decay, fused ask+eval, SGD / ClipUp, shared-memory and global sorts, peer
 Sep-CMA and ClipUp phases, D-sharding, tcgen05 MLP, full CMA-ES on the tensor-core and SIMT
 paths), with ragged sizes so the tails and masks run. Meant for compute-sanitizer
 (`compute-sanitizer --tool memcheck python tools/sanitize_driver.py`); the GPU pool has it closed
-(r18: "runs under it have left GPUs needing a reset"), so it serves as an all-kernel smoke."""
+(r18: "runs under it have left GPUs needing a reset"), so it serves as an all-kernel smoke, and
+with ES_GUARD_ALLOCS=1 as an out-of-bounds-write check: every context's 256-B guard zones around
+its allocations are verified before it is closed (tests/test_gpu_guards.py)."""
 import os
 import sys
 
@@ -12,6 +14,17 @@ import torch  # noqa: E402
 
 import workloads as W  # noqa: E402
 from paper_2212_04180_b200 import strategy as S  # noqa: E402
+
+
+GUARD = os.environ.get("ES_GUARD_ALLOCS") == "1"
+
+
+def done(*ess):
+    for es in ess:
+        if GUARD:
+            bad = es.check_guards()
+            assert bad == 0, f"{bad} guard bytes overwritten (algo {es.algo}, D {es.num_dims})"
+        es.close()
 
 
 def params(algo, R, **over):
@@ -32,21 +45,21 @@ def diagonal_family():
                     es.tell(es.eval(fn, es.ask()))
                 x, f = es.ask_eval(W.RASTRIGIN)
                 es.tell(f)
-                es.close()
+                done(es)
     for opt in (W.SGD, W.CLIPUP):
         es = S.Strategy(W.OPENAI_ES, 16, 37, params(W.OPENAI_ES, 2, optimizer=opt, max_speed=0.1))
         for _ in range(2):
             es.tell(es.eval(W.SPHERE, es.ask()))
-        es.close()
+        done(es)
 
 
 def big_rank():
     es = S.Strategy(W.OPENAI_ES, 16384, 4, params(W.OPENAI_ES, 1))      # shared-memory sort
     es.tell(es.eval(W.SPHERE, es.ask()))
-    es.close()
+    done(es)
     es = S.Strategy(W.SNES, 20000, 4, params(W.SNES, 1))                 # global hybrid sort
     es.tell(es.eval(W.SPHERE, es.ask()))
-    es.close()
+    done(es)
 
 
 def shards():
@@ -66,8 +79,7 @@ def shards():
             for _ in range(sh[0].p2p_finish_phases()):
                 for s in sh:
                     s.tell_p2p_finish()
-        for s in sh:
-            s.close()
+        done(*sh)
     for algo in (W.SNES, W.SEP_CMA_ES):
         sh = [S.Strategy(algo, N, D, params(algo, R), shard=(w, Wn), split="dims")
               for w in range(Wn)]
@@ -81,8 +93,7 @@ def shards():
                 for s in sh:
                     s.set("norm2", n2)
                     s.tell_apply()
-        for s in sh:
-            s.close()
+        done(*sh)
 
 
 def mlp():
@@ -95,7 +106,7 @@ def mlp():
     es.tell(es.eval(W.MLP, es.ask()))
     x, f = es.ask_eval(W.MLP)
     es.tell(f)
-    es.close()
+    done(es)
 
 
 def cma():
@@ -103,7 +114,7 @@ def cma():
         es = S.Strategy(5, 16, D, params(W.SEP_CMA_ES, 2, sigma_init=0.3))
         for _ in range(3):
             es.tell(es.eval(W.ROSENBROCK, es.ask()))
-        es.close()
+        done(es)
 
 
 if __name__ == "__main__":
