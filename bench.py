@@ -399,7 +399,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    use_graph = args.graph if args.graph is not None else (args.config in ("c1", "c3")
+    use_graph = args.graph if args.graph is not None else (args.config in ("c1", "c3", "c6")
                                                            and world == 1)
     graph = None
     if use_graph:

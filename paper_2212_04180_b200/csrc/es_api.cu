@@ -55,6 +55,7 @@ struct es_ctx {
   int* bar = nullptr;           // 4-byte NCCL barrier word
   int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
   std::vector<uint32_t> host_t; // completed tells per run (CMA-ES Cholesky refresh schedule)
+  bool graph_seen = false;      // a tell was stream-captured: always launch the refresh kernels
   int64_t d0 = 0;               // first owned global dim
   double* fpart = nullptr;      // [R][N] D-shard binary64 partial fitness
   bool any_clipup = false;
@@ -769,8 +770,14 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
   }
   c->launches += rank_launches(s);
   if (s.algo == CMA_ES) {
-    // refresh the Cholesky factor after this tell for the runs whose k divides t + 1
-    bool refresh = false;
+    // refresh the Cholesky factor after this tell for the runs whose k divides t + 1. Every
+    // refresh kernel re-checks that per run on the device (t is device state), so the host
+    // counter only skips launches that would all be no-ops; once a generation has been captured
+    // into a CUDA graph (replays do not run this host code) the launches are always issued.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      c->graph_seen = true;
+    bool refresh = c->graph_seen;
     for (int r = 0; r < s.R; ++r) {
       c->host_t[r] += 1;
       if (c->host_t[r] % (uint32_t)c->host_rs[r].k_refresh == 0) refresh = true;

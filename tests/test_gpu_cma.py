@@ -138,6 +138,41 @@ def test_sampling_through_the_factor_is_fp32_accurate(R, N, D):
     pair.close()
 
 
+def test_graph_replay_equals_eager_with_lazy_refresh():
+    """D = 300, N = 8: the factor is refreshed every k = 6 generations (Hansen's lazy schedule).
+    Eager calls skip the refresh launches on the other generations; a generation captured as a
+    CUDA graph always launches them and the kernels decide per run on the device (t is device
+    state). Ten replays after two eager generations must equal twelve eager generations bit for
+    bit."""
+    from paper_2212_04180_b200 import strategy as S
+    N, D = 8, 300
+    a = S.Strategy(CMA, N, D, _params(2))
+    b = S.Strategy(CMA, N, D, _params(2))
+    eye = torch.eye(D, device="cuda").expand(2, D, D)
+    for g in range(12):
+        a.tell(a.eval(W.ROSENBROCK, a.ask()))
+        if g == 4:                                     # t = 5: no refresh yet (k = 6)
+            assert torch.equal(a.get("chol"), eye)
+    assert not torch.equal(a.get("chol"), eye)         # refreshed at t = 6 and t = 12
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            b.tell(b.eval(W.ROSENBROCK, b.ask()))
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+        b.tell(b.eval(W.ROSENBROCK, b.ask()))
+    for _ in range(10):
+        g.replay()
+    torch.cuda.synchronize()
+    for k in ("mean", "cov", "chol", "p_sigma", "p_c", "sigma", "gen", "best_f"):
+        assert torch.equal(a.get(k), b.get(k)), k
+    assert int(a.get("gen")[0]) == 12
+    a.close()
+    b.close()
+
+
 # fn None: synthetic fitness (N15) — no convergence, so the state keeps its scale and the check
 # isolates arithmetic drift; a converging run (sphere) shrinks ‖x‖ geometrically while the
 # teacher-forced oracle's own-x error does not shrink with it.
