@@ -201,9 +201,18 @@ es_status_t es_tell_apply(es_ctx_t *ctx, es_stream_t stream);
  *                      (x, if given, is this rank's column slice [R][N][d_end − d_begin]).
  *   es_ask_eval_partial  this rank's binary64 partial fitness [R][N] (host or device) for callers
  *                      that sum over ranks themselves; fitness = (float)(Σ_ranks partial).
- *   es_tell            fitness [R][N] (the full population's); no gradient collective.
- *   es_tell_local / es_tell_apply  (no communicator) as es_tell, with Sep-CMA-ES's ES_FIELD_NORM2
- *                      share summed by the caller in between.
+ *   es_tell            fitness [R][N] (the full population's); no gradient collective. Global
+ *                      norms are sums of the ranks' shares, all-reduced with the communicator:
+ *                      ‖p_σ'‖² (Sep-CMA-ES, R doubles), weight decay's ‖x_j‖² (R·N doubles,
+ *                      P:213) and ClipUp's ‖g‖², ‖v'‖² (R doubles each).
+ *   es_tell_local / es_tell_apply  (no communicator) as es_tell; the caller sums the ES_FIELD_NORM2
+ *                      shares over the ranks and es_set's the sum before each es_tell_apply
+ *                      call; es_tell_apply_phases(ctx) calls are needed (2 with ClipUp: after
+ *                      the first, NORM2 holds the ‖v'‖² share; 1 otherwise).
+ *   es_sqnorm_partial  this rank's binary64 Σ_{owned d} x_jd² [R][N] of the asked generation
+ *                      (device memory); es_weight_decay_apply(f, Σ_ranks sqnorm, out) then gives
+ *                      out = f + weight_decay·‖x_j‖² — the split-phase weight decay, whose result
+ *                      goes to es_tell_local (which applies no weight decay itself).
  * State fields (es_get / es_set) have the context's state dims (d_end − d_begin + halo). */
 es_status_t es_init_dshard(es_ctx_t **out, es_algo_t algo, int32_t num_runs, int32_t popsize,
                            int64_t num_dims, const es_run_params_t *params, int32_t world_rank,
@@ -212,6 +221,10 @@ es_status_t es_dshard_plan(int64_t num_dims, int32_t world_size, int32_t rank, i
 es_status_t es_dshard_info(const es_ctx_t *ctx, int64_t out[4]);
 es_status_t es_ask_eval_partial(es_ctx_t *ctx, es_fitness_t fn, float *x, double *partial,
                                 es_stream_t stream);
+int32_t es_tell_apply_phases(const es_ctx_t *ctx);   /* 1 or 2; −1 for a NULL context */
+es_status_t es_sqnorm_partial(es_ctx_t *ctx, double *sqnorm, es_stream_t stream);
+es_status_t es_weight_decay_apply(es_ctx_t *ctx, const float *fitness, const double *sqnorm,
+                                  float *out, es_stream_t stream);
 
 /* the population-sharded tell with its collective fused into one kernel over
  * peer memory ("batch evolutionary gradients ... aggregated via map-reduce", memory split

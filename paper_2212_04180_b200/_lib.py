@@ -26,7 +26,7 @@ EXPORTS = ["es_init", "es_ask", "es_eval_bbob", "es_tell", "es_synth_fitness", "
            "es_tell_local", "es_tell_apply", "es_shard_plan", "es_ask_eval", "es_weight_decay",
            "es_init_dshard", "es_dshard_plan", "es_dshard_info", "es_ask_eval_partial",
            "es_p2p_export", "es_p2p_set_peers", "es_tell_p2p_apply", "es_p2p_ipc_export",
-           "es_p2p_ipc_open", "es_tell_p2p_finish", "es_p2p_finish_phases", "es_debug_check_guards", "es_nvls_open", "es_nvls_bind", "es_tell_nvls_apply"]
+           "es_p2p_ipc_open", "es_tell_p2p_finish", "es_p2p_finish_phases", "es_debug_check_guards", "es_tell_apply_phases", "es_sqnorm_partial", "es_weight_decay_apply", "es_nvls_open", "es_nvls_bind", "es_tell_nvls_apply"]
 
 
 class RunParams(C.Structure):
@@ -99,6 +99,9 @@ def lib():
         "es_tell_p2p_finish": (i32, [vp, vp]),
         "es_p2p_finish_phases": (i32, [vp]),
         "es_debug_check_guards": (i32, [vp, vp]),
+        "es_tell_apply_phases": (i32, [vp]),
+        "es_sqnorm_partial": (i32, [vp, vp, vp]),
+        "es_weight_decay_apply": (i32, [vp, vp, vp, vp, vp]),
         "es_p2p_ipc_export": (i32, [vp, vp]),
         "es_p2p_ipc_open": (i32, [vp, vp]),
         "es_nvls_open": (i32, [vp, vp, i32]),

@@ -64,6 +64,8 @@ struct es_ctx {
   ncclComm_t comm = nullptr;
   bool asked = false;
   bool told_local = false;
+  int apply_phase = 0;          // D-shard ClipUp: next es_tell_apply phase (0 or 1)
+  double* wdn2 = nullptr;       // [R][N] D-shard squared norms (weight decay)
   int p2p_phase = -1;           // next es_tell_p2p_finish phase (-1: no apply pending)
   bool broken = false;
   int nchunk = 1;
@@ -351,9 +353,6 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: weight_decay must be finite and >= 0", r);
     if (!(p.clip_min <= p.clip_max))
       return fail(nullptr, ES_ERR_INVALID_ARG, "run %d: need clip_min <= clip_max", r);
-    if (dsh && W > 1 && (p.weight_decay != 0.0f || p.optimizer == ES_OPT_CLIPUP))
-      return fail(nullptr, ES_ERR_UNSUPPORTED, "run %d: weight decay / ClipUp need global norms, "
-                  "not implemented for D-sharded contexts", r);
   }
   es_ctx* c = new (std::nothrow) es_ctx();
   if (c) {
@@ -821,7 +820,22 @@ static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st, bool 
   if (c->any_clipup) {
     int nk = 0;
     ProfScope ps(c, "clipup_finish", st);
-    CUDA_OR(c, launch_clipup_finish(s, st, &nk));
+    if (s.dshard && c->dW > 1) {
+      // the two global norms of a D-shard: shares summed by NCCL here; in the split-phase API
+      // (n2_summed) es_tell_apply drives the phases and the caller sums
+      if (!n2_summed) {
+        CUDA_OR(c, launch_sepcma_n2(s, st));                      // ‖g‖² share
+        for (int ph = 0; ph < 2; ++ph) {
+          NCCL_OR(c, ncclAllReduce(s.n2, s.n2, (size_t)s.R, ncclFloat64, ncclSum, c->comm, st));
+          int k = 0;
+          CUDA_OR(c, launch_clipup_dshard_phase(s, ph, st, &k));
+          nk += k;
+        }
+        nk += 1;
+      }
+    } else {
+      CUDA_OR(c, launch_clipup_finish(s, st, &nk));
+    }
     c->launches += nk;
   }
   return ES_SUCCESS;
@@ -848,8 +862,9 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_tell without a preceding es_ask");
   const DevState& s = c->s;
-  if ((s.W > 1 || (c->dW > 1 && s.algo == SEP_CMA_ES)) && !c->comm)
-    return fail(c, ES_ERR_BAD_STATE, "no communicator: use es_tell_local / es_tell_apply");
+  if ((s.W > 1 || (c->dW > 1 && (s.algo == SEP_CMA_ES || c->any_clipup || c->any_wd))) && !c->comm)
+    return fail(c, ES_ERR_BAD_STATE, "no communicator: use es_tell_local / es_tell_apply "
+                "(and es_sqnorm_partial / es_weight_decay_apply for weight decay)");
   const size_t nloc = (size_t)s.R * s.Nloc;
   es_status_t err;
   const float* fl = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
@@ -911,6 +926,16 @@ static es_status_t weight_decay_impl(es_ctx* c, const float* fd, float* out, cud
     out = c->wdbuf;
   }
   ProfScope ps(c, "weight_decay", st);
+  if (s.dshard && c->dW > 1) {
+    // ‖x_j‖² is a sum over every rank's dims: this rank's binary64 share, summed by NCCL (R·N
+    // doubles, the same collective as the partial fitness), then f + wd·‖x‖²
+    if (!c->wdn2) CUDA_OR(c, dalloc(c, (void**)&c->wdn2, nloc * sizeof(double)));
+    CUDA_OR(c, launch_ask_eval_partial(s, (int)ES_FIT_SPHERE, nullptr, c->aepart, c->wdn2, st));
+    NCCL_OR(c, ncclAllReduce(c->wdn2, c->wdn2, nloc, ncclFloat64, ncclSum, c->comm, st));
+    CUDA_OR(c, launch_wd_apply(s, c->wdn2, fd, out, st));
+    c->launches += 3;
+    return ES_SUCCESS;
+  }
   CUDA_OR(c, launch_weight_decay(s, c->aepart, fd, out, st));
   c->launches += 2;
   return ES_SUCCESS;
@@ -921,6 +946,9 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
   if (!c || !fitness || !out) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_weight_decay needs an asked generation");
   if (c->s.algo == CMA_ES) return fail(c, ES_ERR_UNSUPPORTED, "CMA-ES: weight decay is not implemented");
+  if (c->s.dshard && c->dW > 1 && !c->comm)
+    return fail(c, ES_ERR_BAD_STATE, "D-shard without communicator: sum es_sqnorm_partial over "
+                "the ranks and use es_weight_decay_apply");
   const size_t nloc = (size_t)c->s.R * c->s.Nloc;
   es_status_t err;
   const float* fd = stage_fitness(c, fitness, nloc, st, &c->fstage, &err);
@@ -1115,10 +1143,11 @@ es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t str
     // D-shard: every rank ranks the full fitness and updates its own dims in place; only
     // Sep-CMA-ES leaves a share (ES_FIELD_NORM2) for the caller to sum before es_tell_apply
     if ((err = tell_local_impl(c, fsrc, true, st)) != ES_SUCCESS) return err;
-    if (c->s.algo == SEP_CMA_ES) {
+    if (c->s.algo == SEP_CMA_ES || c->any_clipup) {   // ‖p_σ'‖² / ‖g‖² share → ES_FIELD_NORM2
       CUDA_OR(c, launch_sepcma_n2(c->s, st));
       c->launches += 1;
     }
+    c->apply_phase = 0;
   } else if ((err = tell_local_impl(c, fsrc, false, st)) != ES_SUCCESS) {
     return err;
   }
@@ -1126,13 +1155,62 @@ es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t str
   return ES_SUCCESS;
 }
 
+static int tell_apply_phases(const es_ctx* c) {
+  return c->s.dshard && c->dW > 1 && c->any_clipup ? 2 : 1;
+}
+
+int32_t es_tell_apply_phases(const es_ctx_t* c) { return c ? tell_apply_phases(c) : -1; }
+
 es_status_t es_tell_apply(es_ctx_t* c, es_stream_t stream_) {
   if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_apply without es_tell_local");
-  es_status_t err = tell_apply_impl(c, c->s.dshard != 0, (cudaStream_t)stream_, true);
-  if (err != ES_SUCCESS) return err;
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (tell_apply_phases(c) == 2) {
+    // D-shard ClipUp: phase 0 reads the summed ‖g‖² and leaves the ‖v'‖² share in NORM2;
+    // phase 1 reads its sum and finishes the step
+    int nk = 0;
+    {
+      ProfScope ps(c, "clipup_finish", st);
+      CUDA_OR(c, launch_clipup_dshard_phase(c->s, c->apply_phase, st, &nk));
+    }
+    c->launches += nk;
+    if (c->apply_phase == 0) {
+      c->apply_phase = 1;
+      return ES_SUCCESS;
+    }
+    c->apply_phase = 0;
+  } else {
+    es_status_t err = tell_apply_impl(c, c->s.dshard != 0, st, true);
+    if (err != ES_SUCCESS) return err;
+  }
   c->told_local = false;
   c->asked = false;
+  return ES_SUCCESS;
+}
+
+es_status_t es_sqnorm_partial(es_ctx_t* c, double* out, es_stream_t stream_) {
+  if (!c || !out) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!c->asked) return fail(c, ES_ERR_BAD_STATE, "es_sqnorm_partial needs an asked generation");
+  if (c->s.algo == CMA_ES) return fail(c, ES_ERR_UNSUPPORTED, "not for CMA-ES");
+  if (!is_device_ptr(out)) return fail(c, ES_ERR_INVALID_ARG, "out must be device memory");
+  const DevState& s = c->s;
+  if (!c->aepart)
+    CUDA_OR(c, dalloc(c, (void**)&c->aepart,
+                      (size_t)s.R * s.Nloc * ask_eval_blocks_per_run(s) * sizeof(double)));
+  ProfScope ps(c, "sqnorm_partial", (cudaStream_t)stream_);
+  CUDA_OR(c, launch_ask_eval_partial(s, (int)ES_FIT_SPHERE, nullptr, c->aepart, out, (cudaStream_t)stream_));
+  c->launches += 2;
+  return ES_SUCCESS;
+}
+
+es_status_t es_weight_decay_apply(es_ctx_t* c, const float* f, const double* sqnorm, float* out,
+                                  es_stream_t stream_) {
+  if (!c || !f || !sqnorm || !out) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
+  if (!is_device_ptr(f) || !is_device_ptr(sqnorm) || !is_device_ptr(out))
+    return fail(c, ES_ERR_INVALID_ARG, "f, sqnorm and out must be device memory");
+  ProfScope ps(c, "weight_decay", (cudaStream_t)stream_);
+  CUDA_OR(c, launch_wd_apply(c->s, sqnorm, f, out, (cudaStream_t)stream_));
+  c->launches += 1;
   return ES_SUCCESS;
 }
 
@@ -1170,7 +1248,7 @@ static bool field_ok(const es_ctx* c, int f, void** base, size_t* elem, size_t* 
     case ES_FIELD_PERM: *base = s.perm; *count = RN; return true;
     case ES_FIELD_FITNESS: *base = s.fit; *count = RN; return true;
     case ES_FIELD_DIRSUM: *base = s.G; *count = 2 * (size_t)s.R * s.D; *elem = 8; return true;
-    case ES_FIELD_NORM2: *base = s.n2; *count = (size_t)s.R; *elem = 8; return s.algo == SEP_CMA_ES;
+    case ES_FIELD_NORM2: *base = s.n2; *count = (size_t)s.R; *elem = 8; return s.algo == SEP_CMA_ES || c->any_clipup;
     case ES_FIELD_COV: *base = s.cov; *count = (size_t)s.R * s.D * s.D; return s.cov != nullptr;
     case ES_FIELD_CHOL: *base = s.chol; *count = (size_t)s.R * s.D * s.D; return s.chol != nullptr;
   }

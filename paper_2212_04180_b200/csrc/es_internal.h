@@ -173,6 +173,11 @@ cudaError_t launch_ask_eval_partial(const DevState& s, int fn, float* x, double*
                                     double* fpart, cudaStream_t st);
 cudaError_t launch_partial_to_fitness(const double* fsum, int64_t n, float* f, cudaStream_t st);
 cudaError_t launch_clipup_finish(const DevState& s, cudaStream_t st, int* nk);
+// ClipUp phase 0 / 1 of a D-sharded context from the summed norms in s.n2 (k_tell.cu)
+cudaError_t launch_clipup_dshard_phase(const DevState& s, int phase, cudaStream_t st, int* nk);
+// weight decay from per-member squared norms summed over the D-shard ranks (k_ask_eval.cu)
+cudaError_t launch_wd_apply(const DevState& s, const double* sqnorm, const float* f, float* out,
+                            cudaStream_t st);
 // f2: reduce-scatter (peer loads, rank order) → update of this rank's quad slice → all-gather
 // (peer stores) in one kernel
 cudaError_t launch_p2p_apply(const DevState& s, const PeerTable& pt, bool clipup, cudaStream_t st,

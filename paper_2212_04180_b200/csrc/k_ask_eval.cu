@@ -216,6 +216,15 @@ cudaError_t launch_weight_decay(const DevState& s, double* part, const float* f,
   return cudaGetLastError();
 }
 
+// out = f + weight_decay·‖x‖² from per-member squared norms already summed (over the D-shard
+// ranks): the finalize with one partial per member.
+cudaError_t launch_wd_apply(const DevState& s, const double* sqnorm, const float* f, float* out,
+                            cudaStream_t st) {
+  const int64_t rows = (int64_t)s.R * s.Nloc;
+  wd_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(s, sqnorm, 1, f, out);
+  return cudaGetLastError();
+}
+
 static cudaError_t ask_eval_impl(const DevState& s, int fn, float* x, double* part, float* f,
                                  double* fpart, cudaStream_t st);
 

@@ -734,4 +734,32 @@ cudaError_t launch_p2p_finish(const DevState& s, const PeerTable& pt, int phase,
   return cudaGetLastError();
 }
 
+// ClipUp on a D-sharded context (f1 × f3): the norms are sums of the ranks' shares, formed by
+// NCCL (es_tell) or by the caller (es_tell_local / es_tell_apply), and read from s.n2:
+//   after the fused tell  this rank's ‖g‖² share → s.n2 (launch_sepcma_n2)
+//   phase 0               1/‖g‖ from the summed s.n2; v' = μv + lr·g/‖g‖ on the local dims; this
+//                         rank's ‖v'‖² share → s.n2 (halo dims are not counted: d < Dx)
+//   phase 1               the max_speed clip from the summed s.n2; v = v'·clip, m −= v.
+__global__ void clipup_scalar_kernel(DevState s, int phase) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= s.R || s.rs[r].optimizer != OPT_CLIPUP) return;
+  clipup_scalar(s, r, s.n2[r], phase);
+}
+
+cudaError_t launch_clipup_dshard_phase(const DevState& s, int phase, cudaStream_t st, int* nk) {
+  const unsigned rb = (unsigned)((s.R + 127) / 128);
+  clipup_scalar_kernel<<<rb, 128, 0, st>>>(s, phase);
+  if (phase == 0) {
+    const int bpr = tell_blocks_per_run(s);
+    clipup_vel_kernel<<<(unsigned)(s.R * bpr), TT, 0, st>>>(s, bpr, 0, s.Q);
+    sepcma_n2_kernel<<<s.R, 256, 0, st>>>(s, bpr, 0);
+    if (nk) *nk = 3;
+  } else {
+    const int64_t n = (int64_t)s.R * s.D;
+    clipup_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);
+    if (nk) *nk = 2;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace esb

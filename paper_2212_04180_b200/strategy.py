@@ -202,8 +202,25 @@ class Strategy:
         return o
 
     def tell_apply(self, stream=None):
-        """Split phase 2: apply the update from the (summed) 'dirsum' field."""
+        """Split phase 2: apply the update from the (summed) 'dirsum' field (D-shard: from the
+        summed 'norm2' shares; tell_apply_phases() calls)."""
         check(lib().es_tell_apply(self.ctx, _stream(stream)), self.ctx)
+
+    def tell_apply_phases(self):
+        return int(lib().es_tell_apply_phases(self.ctx))
+
+    def sqnorm_partial(self, stream=None):
+        """D-shard: this rank's binary64 Σ_{owned d} x² per member [R, N] of the asked generation."""
+        out = torch.empty((self.R, self.local_popsize), dtype=torch.float64, device=self.device)
+        check(lib().es_sqnorm_partial(self.ctx, _ptr(out), _stream(stream)), self.ctx)
+        return out
+
+    def weight_decay_apply(self, fitness, sqnorm, out=None, stream=None):
+        """f + weight_decay·‖x‖² from squared norms summed over the D-shard ranks."""
+        o = out if out is not None else torch.empty_like(fitness)
+        check(lib().es_weight_decay_apply(self.ctx, _ptr(fitness), _ptr(sqnorm), _ptr(o),
+                                          _stream(stream)), self.ctx)
+        return o
 
     def synth_fitness(self, out=None, stream=None):
         f = out if out is not None else torch.empty(

@@ -103,6 +103,57 @@ def test_dshard_variants(algo, per):
     _run(algo, 32, 301, 2, 3, W.ROSENBROCK, 3, per)
 
 
+@pytest.mark.parametrize("algo,per", [
+    (W.OPENAI_ES, [dict(optimizer=W.CLIPUP, max_speed=0.05), dict(weight_decay=0.05)]),
+    (W.PGPE, [dict(optimizer=W.CLIPUP, max_speed=0.1, momentum=0.5, weight_decay=0.02)]),
+    (W.SNES, [dict(weight_decay=0.1), dict()]),
+    (W.SEP_CMA_ES, [dict(weight_decay=0.05, clip_max=1.0)]),
+    (W.ARS, [dict(weight_decay=0.03, elite_ratio=0.5)]),
+])
+@pytest.mark.parametrize("D,Wn", [(301, 2), (1003, 3)])
+def test_dshard_global_norms(algo, per, D, Wn):
+    """f1 × f3: weight decay (‖x_j‖²) and ClipUp (‖g‖, ‖v'‖) on D-sharded contexts,
+    whose norms are sums of the ranks' binary64 shares. Split-phase ABI, sums formed here in rank
+    order (what the all-reduce computes): es_sqnorm_partial → es_weight_decay_apply →
+    es_tell_local → per phase: sum ES_FIELD_NORM2, es_tell_apply. Equal to the unsharded run
+    (which applies both itself) up to the binary64 summation order: perm bit-exact, state ≤ 1e-6."""
+    from paper_2212_04180_b200 import strategy as S
+    N, R, fn = 32, 2, W.RASTRIGIN
+    params = _params(algo, R, per)
+    ref = S.Strategy(algo, N, D, params)
+    shards = [S.Strategy(algo, N, D, params, shard=(w, Wn), split="dims") for w in range(Wn)]
+    has_n2 = algo == W.SEP_CMA_ES or any(p.get("optimizer") == W.CLIPUP for p in per)
+    for g in range(4):
+        x, f_ref = ref.ask_eval(fn)
+        parts = [sh.ask_eval_partial(fn)[1] for sh in shards]
+        f = sum(parts[1:], parts[0].clone()).float()
+        ref.tell(f)                                      # applies weight decay / ClipUp itself
+        sq = [sh.sqnorm_partial() for sh in shards]
+        sq = sum(sq[1:], sq[0].clone())                  # rank order
+        fw = [sh.weight_decay_apply(f, sq) for sh in shards]
+        for a in fw[1:]:
+            assert torch.equal(a, fw[0])
+        for sh, fws in zip(shards, fw):
+            sh.tell_local(fws)
+        for _ in range(shards[0].tell_apply_phases()):
+            if has_n2:
+                n2 = [sh.get("norm2") for sh in shards]
+                n2 = sum(n2[1:], n2[0].clone())
+                for sh in shards:
+                    sh.set("norm2", n2)
+            for sh in shards:
+                sh.tell_apply()
+        for sh in shards:
+            d0, ds = sh.d_begin, sh.state_dims
+            assert torch.equal(sh.get("perm"), ref.get("perm")), g
+            for fld in KEPT[algo]:
+                a = sh.get(fld).cpu().numpy()
+                b = ref.get(fld)[:, d0:d0 + ds].cpu().numpy()
+                assert q24(a, b) <= 1e-6, (g, fld, d0)
+    for es in shards + [ref]:
+        es.close()
+
+
 def test_dshard_single_rank_equals_plain():
     """W = 1 D-shard: es_ask_eval's partial → fitness path reproduces the plain context bit for bit."""
     from paper_2212_04180_b200 import strategy as S
@@ -126,9 +177,14 @@ def test_dshard_rejections():
     p = _params(W.OPENAI_ES, 1)
     with pytest.raises(ESError):                      # ceil(D/4) < W
         S.Strategy(W.OPENAI_ES, 16, 5, p, shard=(0, 3), split="dims")
-    with pytest.raises(ESError):                      # weight decay needs a global norm
-        S.Strategy(W.OPENAI_ES, 16, 64, _params(W.OPENAI_ES, 1, [dict(weight_decay=0.1)]),
-                   shard=(0, 2), split="dims")
+    wd = S.Strategy(W.OPENAI_ES, 16, 64, _params(W.OPENAI_ES, 1, [dict(weight_decay=0.1)]),
+                    shard=(0, 2), split="dims")
+    wd.ask_eval_partial(W.SPHERE)
+    with pytest.raises(ESError):                      # weight decay needs the ranks' ‖x‖² sum
+        wd.tell(torch.zeros(1, 16, device="cuda"))
+    with pytest.raises(ESError):
+        wd.weight_decay(torch.zeros(1, 16, device="cuda"))
+    wd.close()
     sh = S.Strategy(W.OPENAI_ES, 16, 64, p, shard=(0, 2), split="dims")
     with pytest.raises(ESError):                      # no communicator: full fitness impossible
         sh.ask_eval(W.SPHERE)
