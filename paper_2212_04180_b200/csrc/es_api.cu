@@ -1,23 +1,14 @@
 // es_api.cu — the C ABI (include/es.h): context lifetime, argument validation, host-side constant
 // tables (binary64, NUMERICS N11/N12), host↔device staging, NCCL plumbing and the launch sequence
 // of one generation. No exception crosses the ABI; every CUDA/NCCL failure becomes a status code.
-#include <nvtx3/nvToolsExt.h>
-#include <cuda_fp16.h>
-#include <cuda_runtime.h>
-#include <nccl.h>
-
-#include <algorithm>
 #include <cmath>
-#include <cstdarg>
-#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
-#include <string>
-#include <vector>
 
-#include "../../include/es.h"
-#include "es_internal.h"
+#include "es_ctx.h"
+
+thread_local std::string g_err;
 
 namespace esb {
 int sm_count() {
@@ -30,156 +21,7 @@ int sm_count() {
   }
   return n;
 }
-cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
-void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
-                         cudaStream_t st, std::string* err);
-void mlp_problem_destroy(void* prob);
-int64_t mlp_problem_dims(const void* prob);
-cudaError_t launch_primitive(int which, const void* in, void* out, int64_t n, cudaStream_t st);
-cudaError_t launch_ask_eval(const DevState& s, int fn, float* x, double* part, float* f,
-                            cudaStream_t st);
-cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st);
-cudaError_t launch_mlp_eval16(void* prob, const __half* x16, int64_t n, float* f,
-                              cudaStream_t st);
-int ask_eval_blocks_per_run(const DevState& s);
 }  // namespace esb
-
-using namespace esb;
-
-struct es_ctx {
-  DevState s{};
-  std::vector<RunScal> host_rs;
-  PeerTable peers{};            // f2 peer-memory tell (peers.W = 0: not set)
-  NvlsHost nvls;                // f2 NVLS multicast tell (stage 2: bound)
-  std::vector<void*> ipc_open;  // peer mappings opened by es_p2p_ipc_open
-  int* bar = nullptr;           // 4-byte NCCL barrier word
-  int dW = 1, drank = 0;        // D-shard world (f1); population world is s.W
-  std::vector<uint32_t> host_t; // completed tells per run (CMA-ES Cholesky refresh schedule)
-  bool graph_seen = false;      // a tell was stream-captured: always launch the refresh kernels
-  int64_t d0 = 0;               // first owned global dim
-  double* fpart = nullptr;      // [R][N] D-shard binary64 partial fitness
-  bool any_clipup = false;
-  bool any_wd = false;
-  float* wdbuf = nullptr;       // [R][Nloc] weight-decayed fitness
-  ncclComm_t comm = nullptr;
-  bool asked = false;
-  bool told_local = false;
-  int apply_phase = 0;          // D-shard ClipUp: next es_tell_apply phase (0 or 1)
-  double* wdn2 = nullptr;       // [R][N] D-shard squared norms (weight decay)
-  int p2p_phase = -1;           // next es_tell_p2p_finish phase (-1: no apply pending)
-  bool broken = false;
-  int nchunk = 1;
-  float* fgather = nullptr;     // [W][R][Nloc]
-  float* fstage = nullptr;      // [R][Nloc] staging of host fitness
-  float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
-  float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
-  double* aepart = nullptr;     // [R][Nloc][blocks] fused ask+eval partial sums
-  __half* x16 = nullptr;        // [R][Nloc][D] fp16 parameter image (MLP fused path, N14′)
-  void* mlp = nullptr;
-  int64_t launches = 0;
-  bool profiling = false;
-  struct Rec { const char* name; cudaEvent_t a, b; };
-  std::vector<Rec> recs;
-  std::vector<cudaEvent_t> pool;
-  std::vector<void*> allocs;     // cudaMalloc bases
-  bool guard = false;            // ES_GUARD_ALLOCS=1: 256-B 0xA5 zones around every allocation
-  struct Zone { const unsigned char* p; size_t bytes; };
-  std::vector<Zone> zones;
-  std::string err;
-};
-
-static thread_local std::string g_err;
-
-static es_status_t fail(es_ctx* c, es_status_t st, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  if (c) c->err = buf;
-  g_err = buf;
-  return st;
-}
-
-#define CUDA_OR(c, expr)                                                                     \
-  do {                                                                                      \
-    cudaError_t _e = (expr);                                                                \
-    if (_e != cudaSuccess)                                                                  \
-      return fail((c), _e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA, "%s: %s", \
-                  #expr, cudaGetErrorString(_e));                                           \
-  } while (0)
-
-#define NCCL_OR(c, expr)                                                                \
-  do {                                                                                 \
-    ncclResult_t _r = (expr);                                                          \
-    if (_r != ncclSuccess) {                                                           \
-      if (c) (c)->broken = true;                                                       \
-      return fail((c), ES_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(_r));           \
-    }                                                                                  \
-  } while (0)
-
-static constexpr size_t kGuard = 256;   // keeps the 256-B alignment of the returned pointer
-
-static cudaError_t dalloc(es_ctx* c, void** p, size_t bytes) {
-  bytes = std::max<size_t>(bytes, 256);
-  if (!c->guard) {
-    cudaError_t e = cudaMalloc(p, bytes);
-    if (e == cudaSuccess) c->allocs.push_back(*p);
-    return e;
-  }
-  bytes = (bytes + kGuard - 1) / kGuard * kGuard;
-  unsigned char* base = nullptr;
-  cudaError_t e = cudaMalloc((void**)&base, bytes + 2 * kGuard);
-  if (e != cudaSuccess) return e;
-  c->allocs.push_back(base);
-  if ((e = cudaMemset(base, 0xA5, kGuard)) != cudaSuccess) return e;
-  if ((e = cudaMemset(base + kGuard + bytes, 0xA5, kGuard)) != cudaSuccess) return e;
-  c->zones.push_back({base, kGuard});
-  c->zones.push_back({base + kGuard + bytes, kGuard});
-  *p = base + kGuard;
-  return cudaSuccess;
-}
-
-// Profiling brackets: an NVTX range around each launch group (host side, for nsys / ncu --nvtx;
-// header-only NVTX 3 — a no-op branch when no tool is attached) and, when profiling is enabled
-// (bench), an event pair on the launching stream.
-static cudaEvent_t prof_event(es_ctx* c) {
-  if (!c->pool.empty()) {
-    cudaEvent_t e = c->pool.back();
-    c->pool.pop_back();
-    return e;
-  }
-  cudaEvent_t e = nullptr;
-  cudaEventCreate(&e);
-  return e;
-}
-struct ProfScope {
-  es_ctx* c;
-  cudaStream_t st;
-  size_t idx = (size_t)-1;
-  ProfScope(es_ctx* c_, const char* name, cudaStream_t st_) : c(c_), st(st_) {
-    nvtxRangePushA(name);
-    if (c && c->profiling) {
-      es_ctx::Rec r{name, prof_event(c), prof_event(c)};
-      cudaEventRecord(r.a, st);
-      c->recs.push_back(r);
-      idx = c->recs.size() - 1;
-    }
-  }
-  ~ProfScope() {
-    if (idx != (size_t)-1) cudaEventRecord(c->recs[idx].b, st);
-    nvtxRangePop();
-  }
-};
-
-static bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
 
 static bool antithetic(int algo) { return is_anti(algo); }
 
@@ -217,17 +59,6 @@ static void sepcma_setup(int N, int64_t D, float elite, RunScal& rs, std::vector
   rs.c_1 = c1 * (Dd + 2.0) / 3.0;      // Ros & Hansen (2008): separable learning-rate boost
   rs.c_mu = cmu * (Dd + 2.0) / 3.0;
   rs.chi_d = std::sqrt(Dd) * (1.0 - 1.0 / (4.0 * Dd) + 1.0 / (21.0 * Dd * Dd));
-}
-
-// f2 peer-memory tell: supported contexts, and the es_tell_p2p_finish calls (each after a
-// barrier) one generation needs.
-static bool p2p_algo_ok(const es_ctx* c) {
-  const int a = c->s.algo;
-  return (a == OPENAI_ES || a == PGPE || a == SNES || a == ARS || a == SEP_CMA_ES) && !c->s.dshard;
-}
-
-static int p2p_phases(const es_ctx* c) {
-  return c->s.algo == SEP_CMA_ES ? 1 : (c->any_clipup ? 2 : 0);
 }
 
 extern "C" {
@@ -960,176 +791,6 @@ es_status_t es_weight_decay(es_ctx_t* c, const float* fitness, float* out, es_st
     CUDA_OR(c, cudaStreamSynchronize(st));
   }
   return ES_SUCCESS;
-}
-
-static constexpr int kIpcHandles = 10;   // dirsum, the 8 fields, norm2
-
-es_status_t es_p2p_export(const es_ctx_t* c, es_peer_t* out) {
-  if (!c || !out) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
-  out->dirsum = c->s.G;
-  for (int f = 0; f < 8; ++f) out->field[f] = c->s.vec[f];
-  out->norm2 = c->s.n2;
-  return ES_SUCCESS;
-}
-
-es_status_t es_p2p_set_peers(es_ctx_t* c, const es_peer_t* peers, int32_t W) {
-  if (!c || !peers) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (W != c->s.W) return fail(c, ES_ERR_INVALID_ARG, "peers for %d ranks, context has %d", W, c->s.W);
-  if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
-  if (!p2p_algo_ok(c)) return fail(c, ES_ERR_UNSUPPORTED, "peer-memory tell: not with CMA-ES / D-sharding");
-  PeerTable pt{};
-  pt.W = W;
-  for (int v = 0; v < W; ++v) {
-    if (!peers[v].dirsum) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL dirsum", v);
-    pt.G[v] = peers[v].dirsum;
-    pt.n2[v] = peers[v].norm2;
-    if (p2p_phases(c) && !pt.n2[v]) return fail(c, ES_ERR_INVALID_ARG, "peer %d: NULL norm2", v);
-    for (int f = 0; f < NVEC; ++f) {
-      pt.vec[v][f] = peers[v].field[f];
-      if (c->s.vec[f] && (f == F_MEAN || f == F_BEST_X || f == F_SIGMA_D || f == F_C) && !pt.vec[v][f])
-        return fail(c, ES_ERR_INVALID_ARG, "peer %d: field %d missing", v, f);
-    }
-  }
-  c->peers = pt;
-  return ES_SUCCESS;
-}
-
-es_status_t es_tell_p2p_apply(es_ctx_t* c, es_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_p2p_apply without es_tell_local");
-  if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
-  int nk = 0;
-  {
-    ProfScope ps(c, "p2p_apply", st);
-    CUDA_OR(c, launch_p2p_apply(c->s, c->peers, c->any_clipup, st, &nk));
-  }
-  c->launches += nk;
-  c->told_local = false;
-  c->asked = false;
-  c->p2p_phase = p2p_phases(c) ? 0 : -1;
-  return ES_SUCCESS;
-}
-
-es_status_t es_nvls_open(es_ctx_t* c, void* handle, int32_t creator) {
-  if (!c || !handle) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (!p2p_algo_ok(c) || c->s.algo == SEP_CMA_ES || c->any_clipup)
-    return fail(c, ES_ERR_UNSUPPORTED, "NVLS tell: OpenAI-ES/PGPE/SNES/ARS, Adam/SGD");
-  if (c->nvls.stage) return fail(c, ES_ERR_BAD_STATE, "es_nvls_open called twice");
-  if (const char* e = nvls_open(c->s, c->nvls, handle, creator != 0)) {
-    nvls_close(c->nvls);
-    return fail(c, ES_ERR_UNSUPPORTED, "NVLS: %s", e);
-  }
-  return ES_SUCCESS;
-}
-
-es_status_t es_nvls_bind(es_ctx_t* c) {
-  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (const char* e = nvls_bind(c->nvls)) return fail(c, ES_ERR_BAD_STATE, "NVLS: %s", e);
-  // move the symmetric fields into the bound buffer (unicast alias) and repoint the state
-  DevState& s = c->s;
-  const size_t RD = (size_t)s.R * s.D;
-  char* base = reinterpret_cast<char*>(c->nvls.uva);
-  double* G = reinterpret_cast<double*>(base + c->nvls.off_g);
-  CUDA_OR(c, cudaMemcpy(G, s.G, 2 * RD * sizeof(double), cudaMemcpyDeviceToDevice));
-  s.G = G;
-  const int f[3] = {F_MEAN, F_BEST_X, F_SIGMA_D};
-  const size_t off[3] = {c->nvls.off_mean, c->nvls.off_best, c->nvls.off_sig};
-  for (int i = 0; i < 3; ++i) {
-    if (!s.vec[f[i]]) continue;
-    float* dst = reinterpret_cast<float*>(base + off[i]);
-    CUDA_OR(c, cudaMemcpy(dst, s.vec[f[i]], RD * sizeof(float), cudaMemcpyDeviceToDevice));
-    s.vec[f[i]] = dst;
-  }
-  return ES_SUCCESS;
-}
-
-static NvlsView nvls_view(const es_ctx* c) {
-  char* mc = reinterpret_cast<char*>(c->nvls.mcva);
-  NvlsView v;
-  v.G = reinterpret_cast<const double*>(mc + c->nvls.off_g);
-  v.mean = reinterpret_cast<float*>(mc + c->nvls.off_mean);
-  v.best = reinterpret_cast<float*>(mc + c->nvls.off_best);
-  v.sig = c->nvls.off_sig == (size_t)-1 ? nullptr : reinterpret_cast<float*>(mc + c->nvls.off_sig);
-  return v;
-}
-
-es_status_t es_tell_nvls_apply(es_ctx_t* c, es_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (!c->told_local) return fail(c, ES_ERR_BAD_STATE, "es_tell_nvls_apply without es_tell_local");
-  if (c->nvls.stage != 2) return fail(c, ES_ERR_BAD_STATE, "NVLS buffer not bound");
-  {
-    ProfScope ps(c, "nvls_apply", st);
-    CUDA_OR(c, launch_nvls_apply(c->s, nvls_view(c), st));
-  }
-  c->launches += 1;
-  c->told_local = false;
-  c->asked = false;
-  return ES_SUCCESS;
-}
-
-es_status_t es_tell_p2p_finish(es_ctx_t* c, es_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!c) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if (c->peers.W != c->s.W) return fail(c, ES_ERR_BAD_STATE, "es_p2p_set_peers was not called");
-  if (!p2p_phases(c)) return ES_SUCCESS;             // nothing after the apply kernel
-  if (c->p2p_phase < 0) return fail(c, ES_ERR_BAD_STATE, "es_tell_p2p_finish without es_tell_p2p_apply");
-  int nk = 0;
-  {
-    ProfScope ps(c, "p2p_finish", st);
-    CUDA_OR(c, launch_p2p_finish(c->s, c->peers, c->p2p_phase, st, &nk));
-  }
-  c->launches += nk;
-  c->p2p_phase = c->p2p_phase + 1 < p2p_phases(c) ? c->p2p_phase + 1 : -1;
-  return ES_SUCCESS;
-}
-
-int32_t es_p2p_finish_phases(const es_ctx_t* c) { return c ? p2p_phases(c) : -1;
-}
-
-es_status_t es_p2p_ipc_export(const es_ctx_t* c, void* handles) {
-  if (!c || !handles) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
-  if (c->guard) return fail(nullptr, ES_ERR_UNSUPPORTED, "IPC export in guard mode (ES_GUARD_ALLOCS)");
-  auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
-  std::memset(handles, 0, kIpcHandles * sizeof(cudaIpcMemHandle_t));
-  cudaError_t e = cudaIpcGetMemHandle(&h[0], c->s.G);
-  for (int f = 0; f < 8 && e == cudaSuccess; ++f)
-    if (c->s.vec[f]) e = cudaIpcGetMemHandle(&h[1 + f], c->s.vec[f]);
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[9], c->s.n2);
-  if (e != cudaSuccess) return fail(nullptr, ES_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
-  return ES_SUCCESS;
-}
-
-es_status_t es_p2p_ipc_open(es_ctx_t* c, const void* all) {
-  if (!c || !all) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  const int W = c->s.W;
-  if (W > kMaxPeers) return fail(c, ES_ERR_UNSUPPORTED, "more than %d peers", kMaxPeers);
-  const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
-  static const cudaIpcMemHandle_t zero{};
-  std::vector<es_peer_t> peers(W);
-  for (int v = 0; v < W; ++v) {
-    if (v == c->s.rank) {
-      es_p2p_export(c, &peers[v]);
-      continue;
-    }
-    const cudaIpcMemHandle_t* hv = h + kIpcHandles * v;
-    void* p = nullptr;
-    CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[0], cudaIpcMemLazyEnablePeerAccess));
-    c->ipc_open.push_back(p);
-    peers[v].dirsum = static_cast<const double*>(p);
-    for (int f = 0; f < 8; ++f) {
-      peers[v].field[f] = nullptr;
-      if (std::memcmp(&hv[1 + f], &zero, sizeof zero) == 0) continue;
-      CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[1 + f], cudaIpcMemLazyEnablePeerAccess));
-      c->ipc_open.push_back(p);
-      peers[v].field[f] = static_cast<float*>(p);
-    }
-    CUDA_OR(c, cudaIpcOpenMemHandle(&p, hv[9], cudaIpcMemLazyEnablePeerAccess));
-    c->ipc_open.push_back(p);
-    peers[v].norm2 = static_cast<const double*>(p);
-  }
-  return es_p2p_set_peers(c, peers.data(), W);
 }
 
 es_status_t es_tell_local(es_ctx_t* c, const float* fitness_all, es_stream_t stream_) {

@@ -632,7 +632,6 @@ cudaError_t launch_cma_tell(const DevState& s, bool refresh, cudaStream_t st, in
     n += 4;
   }
   if (refresh) {
-    const int64_t DD = s.D * s.D;
     const unsigned cb = (unsigned)std::min<int64_t>(s.D, 1024);   // one row per block iteration
     chol_copy_kernel<<<dim3(cb, (unsigned)s.R), 256, 0, st>>>(s);
     n += 1;
