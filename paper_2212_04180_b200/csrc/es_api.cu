@@ -397,8 +397,11 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
   const size_t nloc = (size_t)s.R * s.Nloc;
   if (s.dshard && c->dW > 1 && !c->comm)
     return fail(c, ES_ERR_BAD_STATE, "D-shard without communicator: use es_ask_eval_partial");
-  if (s.algo == CMA_ES) {     // sample (tiled contraction) then evaluate
-    if (fn == ES_FIT_MLP) return fail(c, ES_ERR_UNSUPPORTED, "CMA-ES with the MLP fitness");
+  if (s.algo == CMA_ES) {     // sample (tiled contraction) then evaluate (BBOB or the MLP)
+    if (fn == ES_FIT_MLP) {
+      if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
+      if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
+    }
     const bool xh = x && !is_device_ptr(x), fh = !is_device_ptr(f);
     float* xd = x;
     if (!x || xh) {
@@ -416,8 +419,9 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
       CUDA_OR(c, launch_cma_ask(s, xd, st, &nk));
     }
     {
-      ProfScope ps(c, "eval_bbob", st);
-      CUDA_OR(c, launch_eval_bbob((int)fn, xd, (int64_t)nloc, s.D, fd, st));
+      ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : "eval_bbob", st);
+      CUDA_OR(c, fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, (int64_t)nloc, fd, st)
+                                  : launch_eval_bbob((int)fn, xd, (int64_t)nloc, s.D, fd, st));
     }
     c->launches += nk + 1;
     if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.Dx * sizeof(float), cudaMemcpyDeviceToHost, st));

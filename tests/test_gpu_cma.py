@@ -173,6 +173,39 @@ def test_graph_replay_equals_eager_with_lazy_refresh():
     b.close()
 
 
+def test_cma_es_with_the_mlp_fitness():
+    """f4 × the MLP fitness (N14): full CMA-ES sampling feeds the tensor-core MLP evaluation.
+    The fused es_ask_eval equals es_ask + es_eval bit for bit; the fitness matches the oracle's
+    binary64 forward within the MLP parity bar (Q24 ≤ 1e-4, test_gpu_parity.py); and 40
+    generations reduce the best fitness on the teacher problem."""
+    from paper_2212_04180_b200 import strategy as S
+    widths = [16, 32, 16]                              # D = 1072 (multiples of 16, N14)
+    m = O.MLP(widths, 128, 5)
+    N, D = 16, m.D
+    params = _params(2, sigma_init=0.05, init_min=-0.3, init_max=0.3)
+    a = S.Strategy(CMA, N, D, params)
+    b = S.Strategy(CMA, N, D, params)
+    for es in (a, b):
+        es.set_mlp_problem(widths, 128, 5)
+    first = None
+    for g in range(40):
+        xa, fa = a.ask_eval(W.MLP)
+        xb = b.ask()
+        fb = b.eval(W.MLP, xb)
+        assert torch.equal(xa, xb) and torch.equal(fa, fb), g
+        if g in (0, 39):
+            ref = m.evaluate(xa.reshape(-1, D).cpu().numpy()).astype(np.float64)
+            assert q24(fa.reshape(-1).cpu().numpy().astype(np.float64), ref) <= 1e-4, g
+        a.tell(fa)
+        b.tell(fb)
+        if g == 0:
+            first = a.get("best_f").clone()
+    assert torch.all(a.get("best_f") < first)
+    assert torch.equal(a.get("mean"), b.get("mean"))
+    a.close()
+    b.close()
+
+
 # fn None: synthetic fitness (N15) — no convergence, so the state keeps its scale and the check
 # isolates arithmetic drift; a converging run (sphere) shrinks ‖x‖ geometrically while the
 # teacher-forced oracle's own-x error does not shrink with it.
