@@ -146,7 +146,8 @@ es_status_t es_ask(es_ctx_t *ctx, float *x, es_stream_t stream);
  * [R][N/W][D] unless x is NULL — then it is never materialised in fp32) and writes its fitness (as
  * es_eval_bbob) to fitness [R][N/W]. BBOB: one kernel that evaluates while sampling. ES_FIT_MLP
  * (N14′): the ask kernel writes the fp16 parameter image the fitness uses, which the tcgen05 MLP
- * kernel streams with TMA (x, if given, must be device memory; D % 4 == 0). Counts as the
+ * kernel streams with TMA (x, if given, must be device memory; D % 4 == 0). ES_CMA_ES: the
+ * tensor-core sampling, then es_eval_bbob's kernels (BBOB or the MLP on fp32 x). Counts as the
  * generation's ask. Errors: ES_ERR_INVALID_ARG for NULL fitness; ES_ERR_BAD_STATE for ES_FIT_MLP
  * without es_set_mlp_problem. */
 es_status_t es_ask_eval(es_ctx_t *ctx, es_fitness_t fn, float *x, float *fitness,
@@ -193,7 +194,7 @@ es_status_t es_tell_apply(es_ctx_t *ctx, es_stream_t stream);
  * d_end whose state each rank updates redundantly (identical arithmetic, identical bits).
  *   es_init_dshard     as es_init, W = world size of the dimension split; nccl_unique_id as there
  *                      (NULL: a communicator-less shard, split phase only). Weight decay and
- *                      ClipUp (global norms) are ES_ERR_UNSUPPORTED when W > 1.
+ *                      ClipUp take their global norms from the ranks' shares (below).
  *   es_dshard_plan     out = (d_begin, d_end, state end = min(d_end + 1, D)); ES_ERR_INVALID_ARG
  *                      if ceil(D/4) < W (a rank would own no dims).
  *   es_dshard_info     out = (d_begin, d_end, state end, D) of a context.
