@@ -39,8 +39,10 @@ typedef enum {
   ES_SEP_CMA_ES = 3,/* P:179 */
   ES_ARS = 4,       /* antithetic, top-k directions, sigma_R normalised */
   ES_CMA_ES = 5     /* full covariance, x = m + σ·A·z with A = chol(C)
-                       (P:106), refreshed every k = max(1, ⌊1/(10·D·(c₁+c_μ))⌋) tells; D ≤ 4096,
-                       world_size 1; es_ask / es_ask_eval (BBOB) / es_tell as the others        */
+                       (P:106), refreshed every k = max(1, ⌊1/(10·D·(c₁+c_μ))⌋) tells; D ≤ 4096.
+                       Population sharding: every rank samples all N members and runs the
+                       identical tell on the all-gathered fitness (replicated state, no gradient
+                       collective); x / fitness cover this rank's N/W members. No D-sharding  */
 } es_algo_t;
 
 typedef enum { ES_OPT_ADAM = 0, ES_OPT_SGD = 1, ES_OPT_CLIPUP = 2 } es_optimizer_t;

@@ -147,8 +147,8 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   if (D >= (int64_t(1) << 34)) return fail(nullptr, ES_ERR_INVALID_ARG, "num_dims must be < 2^34");
   if (W < 1 || rank < 0 || rank >= W) return fail(nullptr, ES_ERR_INVALID_ARG, "bad rank/world_size");
   const int32_t pW = dsh ? 1 : W, prank = dsh ? 0 : rank;   // population sharding
-  if (algo == ES_CMA_ES && (W > 1 || dsh))
-    return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: sharding is not implemented");
+  if (algo == ES_CMA_ES && dsh)
+    return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: D-sharding is not implemented");
   for (int r = 0; r < R && algo == ES_CMA_ES; ++r)
     if (params && params[r].weight_decay != 0.0f)
       return fail(nullptr, ES_ERR_UNSUPPORTED, "CMA-ES: weight decay is not implemented");
@@ -632,12 +632,12 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
 // n2_summed: a D-shard's ‖p_σ'‖² share was already summed over ranks by the caller (split phase).
 static es_status_t tell_apply_impl(es_ctx* c, bool fused, cudaStream_t st, bool n2_summed = false) {
   const DevState& s = c->s;
+  if (s.algo == CMA_ES) return ES_SUCCESS;          // launch_cma_tell did every phase
   if (!fused) {
     ProfScope ps(c, "tell_update", st);
     CUDA_OR(c, launch_tell_update(s, st));
     c->launches += 1;
   }
-  if (s.algo == CMA_ES) return ES_SUCCESS;          // launch_cma_tell did every phase
   if (s.algo == SEP_CMA_ES) {
     if (s.dshard && !n2_summed) {
       CUDA_OR(c, launch_sepcma_n2(s, st));
@@ -740,7 +740,7 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     return ES_SUCCESS;
   }
   if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
-  if (s.W > 1) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
+  if (s.W > 1 && s.algo != CMA_ES) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
     const size_t cnt = (size_t)(s.algo == OPENAI_ES || s.algo == ARS ? 1 : 2) * s.R * s.D;
     ProfScope ps(c, "allreduce", st);
     NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));

@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(128) cma_z_kernel(DevState s, int bpr, int jpb
 }
 
 // Y = Z·Aᵀ for one 64-member × 64-dim tile of run blockIdx.z; 256 threads × (4 members × 4 dims),
-// FP32 FFMA in k order. Epilogue x = clip(fma(σ, y, m)) — the same expression best_x uses.
+// FP32 FFMA in k order. Epilogue x = clip(fma(σ, y, m)) — the same expression best_x uses. Every
+// rank samples all N members (Y feeds the replicated tell); x holds only this rank's members
+// [rank·Nloc, (rank+1)·Nloc), locally indexed (population sharding).
 __global__ void __launch_bounds__(256) cma_sample_kernel(DevState s, float* __restrict__ x) {
   __shared__ __align__(16) float Zs[kTK][kTB + 4];
   __shared__ __align__(16) float As[kTK][kTB + 4];
@@ -123,10 +125,11 @@ __global__ void __launch_bounds__(256) cma_sample_kernel(DevState s, float* __re
       if (d >= D) continue;
       const int64_t o = ((int64_t)r * s.N + j) * D + d;
       s.ybuf[o] = acc[i][jj];
-      if (x) {
+      const int jl = j - s.rank * s.Nloc;
+      if (x && jl >= 0 && jl < s.Nloc) {
         float xv = __fmaf_rn(sig, acc[i][jj], s.vec[F_MEAN][(int64_t)r * D + d]);
         if (rs.clip) xv = fminf(fmaxf(xv, rs.clip_lo), rs.clip_hi);
-        x[o] = xv;
+        x[((int64_t)r * s.Nloc + jl) * D + d] = xv;
       }
     }
   }

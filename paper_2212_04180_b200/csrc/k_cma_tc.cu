@@ -31,10 +31,11 @@ static constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 + 256;
 struct CmaTcParams {
   CUtensorMap tz, ta;          // Z [R][N][D], A [R][D][D] as 3-D (k, row, run) fp32 maps
   float* y;                    // [R][N][D]
-  float* x;                    // [R][N][D] or nullptr
+  float* x;                    // [R][Nloc][D] (this rank's members) or nullptr
   const float* mean;           // [R][D]
   const RunScal* rs;
   int N;
+  int jl0, Nloc;               // this rank's members [jl0, jl0 + Nloc) (population sharding)
   int64_t D;
 };
 
@@ -177,10 +178,11 @@ __global__ void __launch_bounds__(256, 1) cma_sample_tc_kernel(const __grid_cons
         const float yv = T[rr][lane];
         const int64_t o = ((int64_t)r * P.N + j) * D + d;
         P.y[o] = yv;
-        if (P.x) {
+        const int jl = j - P.jl0;
+        if (P.x && jl >= 0 && jl < P.Nloc) {
           float xv = __fmaf_rn(sig, yv, md);
           if (rs.clip) xv = fminf(fmaxf(xv, rs.clip_lo), rs.clip_hi);
-          P.x[o] = xv;
+          P.x[((int64_t)r * P.Nloc + jl) * D + d] = xv;
         }
       }
       __syncwarp();
@@ -227,6 +229,8 @@ cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st) {
   P.mean = s.vec[F_MEAN];
   P.rs = s.rs;
   P.N = s.N;
+  P.jl0 = s.rank * s.Nloc;
+  P.Nloc = s.Nloc;
   P.D = s.D;
   const dim3 g((unsigned)((s.D + 127) / 128), (unsigned)((s.N + 127) / 128), (unsigned)s.R);
   cma_sample_tc_kernel<<<g, 256, kTcSmem, st>>>(P);

@@ -206,6 +206,37 @@ def test_cma_es_with_the_mlp_fitness():
     b.close()
 
 
+@pytest.mark.parametrize("Wn,D", [(2, 64), (4, 130), (2, 37)])
+def test_population_sharded_cma_es(Wn, D):
+    """P:226 for f4: W ranks (emulated on one GPU through the communicator-less split-phase ABI)
+    each sample all N members (Y feeds the tell), evaluate only their N/W, and run the identical
+    tell on the all-gathered fitness. Populations are the unsharded one's slices and every rank's
+    state equals the unsharded state bit for bit (tensor-core path D % 4 == 0, SIMT D = 37)."""
+    from paper_2212_04180_b200 import strategy as S
+    N, R = 32, 2
+    params = _params(R)
+    ref = S.Strategy(CMA, N, D, params)
+    shards = [S.Strategy(CMA, N, D, params, shard=(w, Wn)) for w in range(Wn)]
+    nl = N // Wn
+    for g in range(6):
+        x = ref.ask()
+        ref.tell(ref.eval(W.ROSENBROCK, x))
+        locs = []
+        for w, sh in enumerate(shards):
+            xs = sh.ask()
+            assert torch.equal(xs, x[:, w * nl:(w + 1) * nl]), (g, w)
+            locs.append(sh.eval(W.ROSENBROCK, xs))
+        gathered = torch.stack(locs).contiguous()
+        for sh in shards:
+            sh.tell_local(gathered)
+            sh.tell_apply()
+        for sh in shards:
+            for k in ("mean", "cov", "chol", "p_sigma", "p_c", "sigma", "best_f", "best_x", "gen"):
+                assert torch.equal(sh.get(k), ref.get(k)), (g, k)
+    for es in shards + [ref]:
+        es.close()
+
+
 # fn None: synthetic fitness (N15) — no convergence, so the state keeps its scale and the check
 # isolates arithmetic drift; a converging run (sphere) shrinks ‖x‖ geometrically while the
 # teacher-forced oracle's own-x error does not shrink with it.
@@ -289,6 +320,6 @@ def test_cma_rejections():
     with pytest.raises(ESError):
         S.Strategy(CMA, 16, 5000, _params(1))                  # D > 4096
     with pytest.raises(ESError):
-        S.Strategy(CMA, 16, 8, _params(1), shard=(0, 2))       # sharding
+        S.Strategy(CMA, 16, 8, _params(1), shard=(0, 2), split="dims")   # D-sharding
     with pytest.raises(ESError):
         S.Strategy(CMA, 16, 8, _params(1, weight_decay=0.1))
