@@ -1,7 +1,8 @@
 // fitness.cuh — per-element BBOB fitness accumulation (NUMERICS N7), shared by the standalone
 // evaluation kernel (k_eval.cu) and the fused ask+evaluate kernel (k_ask_eval.cu).
 // Binary64 accumulation; Sphere uses exact-product DFMAs (= the oracle's mul-then-add), Rastrigin
-// accumulates Σx² and ΣS² separately and combines them once as Σx² + 20·ΣS² (N7).
+// accumulates Σx² and ΣS² separately and combines them once as Σx² + 20·ΣS² (N7). The eval is
+// XU-bound on the binary32 → binary64 converts: S (≥ 0) is converted on the FMA pipe instead.
 #pragma once
 #include "noise.cuh"
 
@@ -21,6 +22,15 @@ __device__ __forceinline__ double rosen_term(float a, float b) {
   return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
 }
 
+// (double)v for v ≥ 0 without the XU-pipe F2F convert: the binary64 bits of a positive normal
+// binary32 with bits u are u·2²⁹ + (896 << 52) — one IMAD.WIDE on the FMA pipe. Exact for normal
+// v; v = 0 or subnormal becomes a ~2⁻¹²⁷-scale value whose square (≤ 2⁻²⁵⁰) cannot move a
+// binary64 sum of the BBOB terms, nor its binary32 rounding (a sum that small rounds to 0).
+__device__ __forceinline__ double pos_f2d(float v) {
+  const uint64_t b = (uint64_t)__float_as_uint(v) * (1ull << 29) + 0x3800000000000000ull;
+  return __longlong_as_double((long long)b);
+}
+
 // Add element x (and, for Rosenbrock, the pair term with its successor xn when has_next).
 template <int FN>
 __device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has_next) {
@@ -32,8 +42,8 @@ __device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has
   } else {
     const float ab = fabsf(x);
     const float fr = __fsub_rn(ab, floorf(ab));
-    const double S = (double)sinpi_half(fminf(fr, __fsub_rn(1.0f, fr)));
-    const double d = (double)x;
+    const double S = pos_f2d(sinpi_half(fminf(fr, __fsub_rn(1.0f, fr))));   // S ∈ [0, 1]
+    const double d = (double)x;      // (on the XU pipe; moving it to the FMA pipe as well was slower)
     acc.a = __fma_rn(d, d, acc.a);
     acc.b = __fma_rn(S, S, acc.b);
   }
