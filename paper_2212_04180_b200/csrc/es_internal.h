@@ -11,6 +11,7 @@
 //   dir, coefA, coefB [R][N]  per-entry tell coefficients: direction index and its weights.
 //   Gpart       double [R][2][D] (+ chunk partials) reduction workspace.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cuda.h>
@@ -203,6 +204,18 @@ cudaError_t launch_cma_cov_tc(const DevState& s, cudaStream_t st);
 cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st);
 int tell_pick_nchunk(const DevState& s);
 constexpr int kTellThreads = 128;
-int sm_count();
+int sm_count();   // of the current device
+
+// Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is per device:
+// a process driving several GPUs sets it on each). `done` is the call site's device bitmask.
+inline cudaError_t smem_attr_once(const void* kernel, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_relaxed);
+  return e;
+}
 
 }  // namespace esb

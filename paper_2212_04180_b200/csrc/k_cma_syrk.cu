@@ -284,12 +284,8 @@ static bool encode_kmajor(CUtensorMap* m, const float* base, int64_t kdim, int64
 }
 
 static cudaError_t syrk_attr() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSySmem);
-  if (e == cudaSuccess) done = true;
-  return e;
+  static std::atomic<uint64_t> done{0};
+  return smem_attr_once((const void*)syrk_tc_kernel, kSySmem, done);
 }
 
 bool syrk_tc_supported(const DevState& s) { return (s.D % 4) == 0 && encode_tiled_fn() != nullptr; }

@@ -214,13 +214,8 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t D, int64_t ro
 bool cma_tc_supported(const DevState& s) { return (s.D % 4) == 0 && encode_tiled_fn() != nullptr; }
 
 cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(cma_sample_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once((const void*)cma_sample_tc_kernel, kTcSmem, attr)) return e;
   CmaTcParams P;
   if (!encode_rows(&P.tz, s.zbuf, s.D, s.N, s.R) || !encode_rows(&P.ta, s.chol, s.D, s.D, s.R))
     return cudaErrorInvalidValue;

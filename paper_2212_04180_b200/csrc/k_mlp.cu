@@ -468,16 +468,9 @@ static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
 }
 
 static cudaError_t launch_mlp(const MlpParams& p, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mlp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr0{0}, attr1{0};
+  if (cudaError_t e = smem_attr_once((const void*)mlp_kernel<false>, kSmemBytes, attr0)) return e;
+  if (cudaError_t e = smem_attr_once((const void*)mlp_kernel<true>, kSmemBytes, attr1)) return e;
   const int grid = (int)std::min<int64_t>(p.n, sm_count());
   if (p.x16) mlp_kernel<true><<<grid, kThreadsTma, kSmemBytes, st>>>(p);
   else mlp_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);

@@ -390,13 +390,13 @@ __global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkey
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
   int npad = 1;
   while (npad < s.N) npad <<= 1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    for (const void* f : {(const void*)rank_kernel<2>, (const void*)rank_kernel<4>,
-                          (const void*)rank_kernel<8>, (const void*)rank_kernel_smem,
-                          (const void*)rank_chunk_sort_kernel, (const void*)rank_chunk_merge_kernel})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  static std::atomic<uint64_t> attr[6];
+  {
+    const void* fs[6] = {(const void*)rank_kernel<2>, (const void*)rank_kernel<4>,
+                         (const void*)rank_kernel<8>, (const void*)rank_kernel_smem,
+                         (const void*)rank_chunk_sort_kernel, (const void*)rank_chunk_merge_kernel};
+    for (int i = 0; i < 6; ++i)
+      if (cudaError_t e = smem_attr_once(fs[i], 200 * 1024, attr[i])) return e;
   }
   if (npad <= kChunk) {
     // E keys per thread: 2 while the block grows to 1024 threads, then 4, 8, 16 (npad ≥ 64)
