@@ -5,7 +5,10 @@
  * diagonal-Gaussian ES family of Table 1 — OpenAI-ES, PGPE, SNES and
  * Sep-CMA-ES — batched over R independent runs (the paper's vmap over seeds or
  * hyperparameters) and optionally population-sharded over W GPUs with NCCL (the paper's
- * Future Work). The arithmetic is frozen in NUMERICS.md (N1–N15).
+ * Future Work), plus the SURVEY §8(f) rows: fused ask + evaluate and D-sharding (f1), the
+ * peer-memory fused tell (f2), the variants ARS / z-score / weight decay / SGD / ClipUp / PGPE
+ * elite pairs / box bounds (f3) and full-covariance CMA-ES (f4). The arithmetic is frozen in
+ * NUMERICS.md (N1–N17).
  *
  * Conventions (all entry points):
  *   - Minimisation. Fitness is "lower is better".
