@@ -135,6 +135,26 @@ def test_eval_parity(fn, n, D):
     assert ulp.max() <= 1 and (ulp > 0).sum() <= max(1, n // 1000), ulp
 
 
+def test_rastrigin_special_values():
+    """The Rastrigin kernel forms (double)S from S's bit pattern (NUMERICS N7 GPU detail): exact for
+    normal S; S = 0 (integer x) and subnormal S (subnormal x) take ~2⁻¹²⁷-scale values whose squares
+    cannot move the sum. Rows of integers, zeros, ±0, subnormals, halves and large values — alone
+    and mixed — must still agree with the oracle's binary64 evaluation to ≤ 1 ulp."""
+    from paper_2212_04180_b200 import strategy as S
+    sub = np.float32(1e-40)
+    rows = [np.zeros(64), -np.zeros(64), np.arange(-32, 32), np.full(64, sub),
+            np.full(64, 0.5), np.full(64, -2.5), np.linspace(-5.12, 5.12, 64),
+            np.concatenate([np.zeros(32), np.full(32, 1e-3)]),
+            np.concatenate([np.arange(16), np.full(16, sub), np.full(32, 3.75)]),
+            np.full(64, 1e10), np.full(64, 2.0 ** -20)]
+    x = np.stack(rows).astype(np.float32)
+    got = S.eval_bbob(W.RASTRIGIN, torch.from_numpy(x).cuda()).cpu().numpy()
+    ref = O.evaluate(W.RASTRIGIN, x)
+    ulp = np.abs(bits(got).astype(np.int64) - bits(ref).astype(np.int64))
+    assert ulp.max() <= 1, (got, ref)
+    assert got[0] == 0.0 and got[1] == 0.0 and got[2] == ref[2]
+
+
 def test_eval_empty_and_host_buffers():
     n, D = 5, 37
     x = W.random_population(np.random.default_rng(1), n, D)
