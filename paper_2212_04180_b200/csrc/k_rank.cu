@@ -33,10 +33,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // Sorted (key, index) pairs → tie groups, shaping, tell coefficients and the generation's
 // scalars (N9–N12 bookkeeping). `keys` is the run's sorted array (shared or global memory).
+// fit: the run's fitness in sorted-input order (shared memory when the caller staged it there —
+// load_key also writes the global copy es_get reads).
 __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, double* red,
-                            int32_t* sh_nw_p) {
+                            int32_t* sh_nw_p, const float* fit) {
   const int N = s.N, T = blockDim.x;
-  float* fit = s.fit + (int64_t)r * N;
   int32_t& sh_nw = *sh_nw_p;
   // tie groups and shaping
   const RunScal& rs = s.rs[r];
@@ -219,11 +220,12 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
 
 // fsrc layout [W][R][Nloc] (for W == 1 simply [R][N]).
 __device__ __forceinline__ uint64_t load_key(const DevState& s, const float* __restrict__ fsrc,
-                                             int r, int p) {
+                                             int r, int p, float* fs = nullptr) {
   if (p >= s.N) return ~0ull;
   const int w = p / s.Nloc, jl = p % s.Nloc;
   const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
   s.fit[(int64_t)r * s.N + p] = f;
+  if (fs) fs[p] = f;
   return ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
 }
 
@@ -311,14 +313,15 @@ __device__ __forceinline__ void bitonic_regs(uint64_t* keys, int npad) {
 // 8192 < N ≤ 16384: one CTA per run, the classic shared-memory network (16 keys per thread would
 // not fit the register file at 1024 threads).
 __global__ void rank_kernel_smem(DevState s, const float* __restrict__ fsrc, int npad) {
-  extern __shared__ uint64_t keys[];
+  extern __shared__ uint64_t keys[];              // [npad] keys, then [npad] fitness values
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
   const int r = blockIdx.x;
-  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p);
+  float* fs = reinterpret_cast<float*>(keys + npad);
+  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
   __syncthreads();
   bitonic_smem(keys, npad, 0, 2, npad, npad);
-  rank_finish(s, r, keys, red, &sh_nw);
+  rank_finish(s, r, keys, red, &sh_nw, fs);
 }
 
 // N ≤ 8192: one CTA per run, the sort in registers (+ shared memory for the long strides).
@@ -328,10 +331,11 @@ __global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
   const int r = blockIdx.x;
-  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p);
+  float* fs = reinterpret_cast<float*>(keys + npad);   // the fitness, kept on chip for the finish
+  for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
   __syncthreads();
   bitonic_regs<E>(keys, npad);
-  rank_finish(s, r, keys, red, &sh_nw);
+  rank_finish(s, r, keys, red, &sh_nw, fs);
 }
 
 // N > 16384: hybrid bitonic sort over global memory. Chunks of kChunk keys are sorted and merged
@@ -384,7 +388,8 @@ __global__ void rank_chunk_merge_kernel(uint64_t* __restrict__ gkeys, int npad, 
 __global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkeys, int npad) {
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
-  rank_finish(s, blockIdx.x, gkeys + (int64_t)blockIdx.x * npad, red, &sh_nw);
+  rank_finish(s, blockIdx.x, gkeys + (int64_t)blockIdx.x * npad, red, &sh_nw,
+              s.fit + (int64_t)blockIdx.x * s.N);
 }
 
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
@@ -403,7 +408,7 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
     const int pad = std::max(npad, 64);
     const int T = std::min(1024, pad / 2);
     const int E = pad / T;
-    const size_t sm = (size_t)pad * sizeof(uint64_t);
+    const size_t sm = (size_t)pad * (sizeof(uint64_t) + sizeof(float));   // keys + fitness
     switch (E) {
       case 2: rank_kernel<2><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
       case 4: rank_kernel<4><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
