@@ -175,7 +175,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
       cA[j] = (double)shaped[j];
     }
   } else {
-    if (threadIdx.x == 0) sh_nw = E[perm[rs.mu - 1]] + 1;   // end of the tie group at μ−1
+    if (threadIdx.x == 0) sh_nw = E[(uint32_t)keys[rs.mu - 1]] + 1;   // end of μ−1's tie group
     __syncthreads();
     for (int p = threadIdx.x; p < sh_nw; p += T) {
       const int j = perm[p];
@@ -188,7 +188,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     RunScal& w = s.rs[r];
     GenScal g;
     g.t = w.t;
-    g.jbest = perm[0];
+    g.jbest = (int)(uint32_t)keys[0];            // = perm[0], without the global round trip
     const float fb = fit[g.jbest];
     g.improved = fb < w.best_f;                 // strict; false for NaN
     if (g.improved) w.best_f = fb;
