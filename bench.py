@@ -102,7 +102,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -111,23 +111,29 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Samples inside the host window [t0, t1] of the timed region (±20 ms, one sampling
+        period); if that window is shorter than a period and caught none, the nearest sample."""
         if self.proc is None:
             return None
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = [(ts, r) for ts, r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        if t0 is not None and rows:
+            inside = [(ts, r) for ts, r in rows if t0 - 0.02 <= ts <= t1 + 0.02]
+            rows = inside or [min(rows, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))]
+        sm = [float(r[0]) for _, r in rows]
+        mx = [float(r[1]) for _, r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 7
-                          for k in range(4) if r[3 + k].lower().startswith("active")})
+        reasons = sorted({names[k] for _, r in rows for k in range(4)
+                          if r[3 + k].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
@@ -434,10 +440,12 @@ def main():
     # timed pass: exactly K steps (graph replays, or eager with the handles on their streams)
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(0.3)                     # the sampler is running before the timed region starts
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
     e0.record(stream)
     for _ in range(args.steps):
         if graph is not None:
@@ -446,10 +454,11 @@ def main():
             step()
     e1.record(stream)
     torch.cuda.synchronize()
+    tw1 = time.time()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(tw0, tw1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
