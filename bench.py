@@ -161,7 +161,7 @@ def _oracle_gen(args):
         run = O.Run(algo, N, D, **params)
         t0 = time.perf_counter()
         for j in range(gens):
-            mlp.evaluate(run.member(j % N))
+            mlp.evaluate_f16(run.member(j % N))
         return D * gens, time.perf_counter() - t0
     if algo == W.CMA_ES:                     # f4: numpy binary64 oracle, one BLAS thread
         from oracle import cma_oracle

@@ -565,6 +565,16 @@ static int tell_impl(orc_run_t *r, const float *f) {
 
   double *G = (double *)malloc(sizeof(double) * 2 * (size_t)D);
   orc_reduce(r, f, G);
+  int rc = orc_tell_apply(r, f, G);
+  free(G);
+  return rc;
+}
+
+/* The update of N12 from the direction sums G[2][D] (what orc_reduce, or the sum over ranks of
+ * orc_reduce_range, produced), then t <- t+1. f is needed only by ARS (selection, sigma_R). */
+int orc_tell_apply(orc_run_t *r, const float *f, const double *G) {
+  const int64_t D = r->num_dims;
+  const int32_t N = r->popsize;
   const double *G0 = G, *G1 = G + D;
   float *mean = vf(r, ORC_V_MEAN), *sd = vf(r, ORC_V_SIGMA);
 
@@ -668,7 +678,6 @@ static int tell_impl(orc_run_t *r, const float *f) {
     }
     r->sigma = sig_new;
   }
-  free(G);
   r->t = r->t + 1;
   return 0;
 }
@@ -727,7 +736,8 @@ struct orc_mlp {
   uint64_t seed;
   int64_t D;
   float *U;      /* [batch][w0] */
-  float *Y;      /* [batch][wL] teacher outputs */
+  double *Y;     /* [batch][wL] teacher outputs g_L(theta*) under the N14 definition */
+  float *Y16;    /* [batch][wL] teacher outputs under the N14' fp16-image model */
 };
 
 int64_t orc_mlp_dims(const orc_mlp_t *p) { return p->D; }
@@ -753,8 +763,40 @@ void orc_mlp_teacher(const orc_mlp_t *p, float *theta) {
   }
 }
 
-/* g_L of one parameter vector (N14); out [batch][wL] */
-static void mlp_forward(const orc_mlp_t *p, const float *x, float *out) {
+/* N14 (the definition; P:265-270 tanh MLP, fp32 parameters as the paper's JAX networks):
+ * every layer a_l = h_{l-1} W_l^T + b_l and h_l = tanh(a_l) in binary64 from the fp32 inputs U and
+ * the fp32 parameter vector x, nothing rounded in between; out [batch][wL]. */
+static void mlp_forward(const orc_mlp_t *p, const float *x, double *out) {
+  const int B = p->batch;
+  int maxw = 0;
+  for (int l = 0; l < p->nw; ++l) maxw = p->w[l] > maxw ? p->w[l] : maxw;
+  double *h = (double *)malloc(sizeof(double) * (size_t)B * maxw);
+  double *hn = (double *)malloc(sizeof(double) * (size_t)B * maxw);
+  for (int b = 0; b < B; ++b)
+    for (int k = 0; k < p->w[0]; ++k) h[(int64_t)b * p->w[0] + k] = (double)p->U[(int64_t)b * p->w[0] + k];
+  for (int l = 1; l < p->nw; ++l) {
+    const int in = p->w[l - 1], nout = p->w[l];
+    const float *W = x + layer_off(p, l);
+    const float *bias = W + (int64_t)nout * in;
+    for (int b = 0; b < B; ++b)
+      for (int n = 0; n < nout; ++n) {
+        double acc = 0.0;
+        for (int k = 0; k < in; ++k) acc += h[(int64_t)b * in + k] * (double)W[(int64_t)n * in + k];
+        double g = tanh(acc + (double)bias[n]);
+        if (l + 1 < p->nw) hn[(int64_t)b * nout + n] = g;
+        else out[(int64_t)b * nout + n] = g;
+      }
+    double *t = h; h = hn; hn = t;
+  }
+  free(h); free(hn);
+}
+
+/* N14' (a labelled APPROXIMATION, not the definition): the model of what the fp16-image fast path
+ * computes — every parameter (weights and biases) and the inputs rounded to binary16, products of
+ * binary16 values summed (here in binary64), + fp16(b), tanh rounded to fp32, hidden activations
+ * rounded to binary16. Its distance to N14 is measured member by member (orc_mlp_eval vs
+ * orc_mlp_eval_f16), which is the fast path's derived error bound. */
+static void mlp_forward_f16(const orc_mlp_t *p, const float *x, float *out) {
   const int B = p->batch;
   int maxw = 0;
   for (int l = 0; l < p->nw; ++l) maxw = p->w[l] > maxw ? p->w[l] : maxw;
@@ -797,25 +839,28 @@ orc_mlp_t *orc_mlp_create(const int32_t *widths, int32_t nw, int32_t batch, uint
     }
   float *theta = (float *)malloc(sizeof(float) * (size_t)p->D);
   orc_mlp_teacher(p, theta);
-  p->Y = (float *)malloc(sizeof(float) * (size_t)batch * outL);
+  p->Y = (double *)malloc(sizeof(double) * (size_t)batch * outL);
+  p->Y16 = (float *)malloc(sizeof(float) * (size_t)batch * outL);
   mlp_forward(p, theta, p->Y);
+  mlp_forward_f16(p, theta, p->Y16);
   free(theta);
   return p;
 }
 
 void orc_mlp_destroy(orc_mlp_t *p) {
   if (!p) return;
-  free(p->U); free(p->Y); free(p);
+  free(p->U); free(p->Y); free(p->Y16); free(p);
 }
 
+/* f(x) = mean over (b, n) of (g_L(x) - g_L(theta*))^2, in binary64, rounded once (N14). */
 void orc_mlp_eval(const orc_mlp_t *p, const float *x, int32_t n, float *f) {
   const int B = p->batch, outL = p->w[p->nw - 1];
-  float *g = (float *)malloc(sizeof(float) * (size_t)B * outL);
+  double *g = (double *)malloc(sizeof(double) * (size_t)B * outL);
   for (int32_t j = 0; j < n; ++j) {
     mlp_forward(p, x + (int64_t)j * p->D, g);
     double acc = 0.0;
     for (int64_t e = 0; e < (int64_t)B * outL; ++e) {
-      double d = (double)g[e] - (double)p->Y[e];
+      double d = g[e] - p->Y[e];
       acc += d * d;
     }
     f[j] = (float)(acc / ((double)B * outL));
@@ -823,5 +868,22 @@ void orc_mlp_eval(const orc_mlp_t *p, const float *x, int32_t n, float *f) {
   free(g);
 }
 
-const float *orc_mlp_targets(const orc_mlp_t *p) { return p->Y; }
+/* The N14' approximation model's fitness (fp16 parameter image; teacher under the same model). */
+void orc_mlp_eval_f16(const orc_mlp_t *p, const float *x, int32_t n, float *f) {
+  const int B = p->batch, outL = p->w[p->nw - 1];
+  float *g = (float *)malloc(sizeof(float) * (size_t)B * outL);
+  for (int32_t j = 0; j < n; ++j) {
+    mlp_forward_f16(p, x + (int64_t)j * p->D, g);
+    double acc = 0.0;
+    for (int64_t e = 0; e < (int64_t)B * outL; ++e) {
+      double d = (double)g[e] - (double)p->Y16[e];
+      acc += d * d;
+    }
+    f[j] = (float)(acc / ((double)B * outL));
+  }
+  free(g);
+}
+
+const double *orc_mlp_targets(const orc_mlp_t *p) { return p->Y; }
+const float *orc_mlp_targets_f16(const orc_mlp_t *p) { return p->Y16; }
 const float *orc_mlp_inputs(const orc_mlp_t *p) { return p->U; }

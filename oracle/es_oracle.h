@@ -104,6 +104,8 @@ void orc_reduce(const orc_run_t *r, const float *f, double *G /* [2][D] */);
 int orc_num_entries(const orc_run_t *r, const float *f);
 void orc_reduce_range(const orc_run_t *r, const float *f, int32_t e0, int32_t e1, double *G);
 int orc_tell(orc_run_t *r, const float *f);
+/* the update half of orc_tell (no best tracking, no weight decay): N12 from G[2][D], then t+1 */
+int orc_tell_apply(orc_run_t *r, const float *f, const double *G);
 
 /* batch helpers for exhaustive / statistical tests */
 void orc_ln_n(const float *u, float *out, int64_t n);
@@ -111,7 +113,9 @@ void orc_sincos2pi_n(const float *u, float *c, float *s, int64_t n);
 void orc_sinpi_half_n(const float *b, float *out, int64_t n);
 void orc_normals_n(uint64_t seed, uint32_t i, uint32_t t, uint32_t tag, int64_t n, float *out);
 
-/* N14 synthetic MLP fitness */
+/* N14 synthetic MLP fitness: orc_mlp_eval is the definition (binary64 forward of the fp32
+ * parameters); orc_mlp_eval_f16 is the N14' fp16-image approximation model (labelled, not the
+ * definition) whose distance to N14 is the fp16 fast path's derived bound. */
 typedef struct orc_mlp orc_mlp_t;
 float orc_fp16(float f);
 orc_mlp_t *orc_mlp_create(const int32_t *widths, int32_t nw, int32_t batch, uint64_t seed);
@@ -119,7 +123,9 @@ void orc_mlp_destroy(orc_mlp_t *p);
 int64_t orc_mlp_dims(const orc_mlp_t *p);
 void orc_mlp_teacher(const orc_mlp_t *p, float *theta);
 void orc_mlp_eval(const orc_mlp_t *p, const float *x, int32_t n, float *f);
-const float *orc_mlp_targets(const orc_mlp_t *p);
+void orc_mlp_eval_f16(const orc_mlp_t *p, const float *x, int32_t n, float *f);
+const double *orc_mlp_targets(const orc_mlp_t *p);
+const float *orc_mlp_targets_f16(const orc_mlp_t *p);
 const float *orc_mlp_inputs(const orc_mlp_t *p);
 
 /* N15 synthetic fitness */

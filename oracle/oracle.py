@@ -88,6 +88,7 @@ def lib():
             "orc_reduce_range": (None, [C.POINTER(RunT), fp, C.c_int32, C.c_int32, dp]),
             "orc_num_entries": (C.c_int, [C.POINTER(RunT), fp]),
             "orc_tell": (C.c_int, [C.POINTER(RunT), fp]),
+            "orc_tell_apply": (C.c_int, [C.POINTER(RunT), fp, dp]),
             "orc_weight_decay": (None, [fp, fp, C.c_int32, C.c_int64, C.c_float, fp]),
             "orc_run_weight_decay": (None, [C.POINTER(RunT), fp, fp]),
             "orc_synth_fitness": (None, [C.c_uint64, C.c_uint32, C.c_int32, fp]),
@@ -97,7 +98,9 @@ def lib():
             "orc_mlp_dims": (C.c_int64, [C.c_void_p]),
             "orc_mlp_teacher": (None, [C.c_void_p, fp]),
             "orc_mlp_eval": (None, [C.c_void_p, fp, C.c_int32, fp]),
-            "orc_mlp_targets": (fp, [C.c_void_p]),
+            "orc_mlp_eval_f16": (None, [C.c_void_p, fp, C.c_int32, fp]),
+            "orc_mlp_targets": (dp, [C.c_void_p]),
+            "orc_mlp_targets_f16": (fp, [C.c_void_p]),
             "orc_mlp_inputs": (fp, [C.c_void_p]),
         }
         for name, (res, args) in sig.items():
@@ -293,6 +296,12 @@ class Run:
         f = np.ascontiguousarray(f, dtype=np.float32)
         lib().orc_tell(C.byref(self.r), _p(f, C.c_float))
 
+    def tell_apply(self, f, G):
+        """The update half of tell from direction sums G [2][D] (no best tracking), then t+1."""
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        G = np.ascontiguousarray(G, dtype=np.float64).reshape(2, self.r.num_dims)
+        lib().orc_tell_apply(C.byref(self.r), _p(f, C.c_float), _p(G, C.c_double))
+
     def weight_decay(self, f):
         """f_j + weight_decay ||x_j||^2 for the current members (what tell ranks)."""
         f = np.ascontiguousarray(f, dtype=np.float32)
@@ -302,7 +311,8 @@ class Run:
 
 
 class MLP:
-    """N14 synthetic MLP regression problem (oracle side)."""
+    """N14 synthetic MLP regression problem (oracle side). evaluate() is the definition (binary64
+    forward of the fp32 parameters); evaluate_f16() is the N14' fp16-image approximation model."""
 
     def __init__(self, widths, batch=128, seed=0):
         w = (C.c_int32 * len(widths))(*widths)
@@ -322,16 +332,27 @@ class MLP:
         return np.ctypeslib.as_array(p, shape=(self.batch * self.widths[-1],)).reshape(
             self.batch, self.widths[-1]).copy()
 
+    def targets_f16(self):
+        p = lib().orc_mlp_targets_f16(self.h)
+        return np.ctypeslib.as_array(p, shape=(self.batch * self.widths[-1],)).reshape(
+            self.batch, self.widths[-1]).copy()
+
     def inputs(self):
         p = lib().orc_mlp_inputs(self.h)
         return np.ctypeslib.as_array(p, shape=(self.batch * self.widths[0],)).reshape(
             self.batch, self.widths[0]).copy()
 
-    def evaluate(self, x):
+    def _eval(self, fn, x):
         x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1, self.D)
         f = np.empty(x.shape[0], dtype=np.float32)
-        lib().orc_mlp_eval(self.h, _p(x, C.c_float), x.shape[0], _p(f, C.c_float))
+        fn(self.h, _p(x, C.c_float), x.shape[0], _p(f, C.c_float))
         return f
+
+    def evaluate(self, x):
+        return self._eval(lib().orc_mlp_eval, x)
+
+    def evaluate_f16(self, x):
+        return self._eval(lib().orc_mlp_eval_f16, x)
 
     def __del__(self):
         try:

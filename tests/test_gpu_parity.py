@@ -430,7 +430,7 @@ def test_mlp_fitness_parity(widths, n):
     xs = np.stack([theta + s * rng.standard_normal(m.D) for s in scales]).astype(np.float32)
     got = es.eval(W.MLP, torch.from_numpy(xs).cuda(), out=torch.empty(n, device="cuda"))
     got = got.cpu().numpy().astype(np.float64)
-    ref = m.evaluate(xs).astype(np.float64)
+    ref = m.evaluate_f16(xs).astype(np.float64)
     # DESIGN §3 / NUMERICS N14: the tensor cores accumulate in fp32, the oracle in binary64; the
     # accumulation order flips rare fp16 roundings of activations. An fp32-vs-binary64 emulation of
     # the same forward (numpy sgemm vs dgemm) differs by the same amounts (≤ 6e-5 relative at
@@ -459,7 +459,7 @@ def test_mlp_openai_es_generations_teacher_forced():
         xo = pair.orc[0].ask()
         assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo)), g
         if g in (0, 50, 99):
-            fo = m.evaluate(xo[:32])
+            fo = m.evaluate_f16(xo[:32])
             assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-4, g
         pair.gpu.tell(f)
         pair.orc[0].tell(f[0].cpu().numpy())
@@ -512,7 +512,7 @@ def test_mlp_fused_fp16_image_path(widths, N):
     assert torch.equal(x1, x0)
     assert np.array_equal(bits(f1.cpu().numpy()), bits(f0.cpu().numpy()))
     assert np.array_equal(bits(f2.cpu().numpy()), bits(f0.cpu().numpy()))
-    ref = m.evaluate(x0[0].cpu().numpy())
+    ref = m.evaluate_f16(x0[0].cpu().numpy())
     assert q24(f1[0].cpu().numpy(), ref) <= 1e-4
     es.tell(f1)
     es.close()
@@ -537,7 +537,7 @@ def test_config4_full_size_sampled_members():
     run = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], **params[0])
     for j in (0, 2048, 2049, cfg["N"] - 1):
         xo = run.member(j)
-        fo = m.evaluate(xo)[0]
+        fo = m.evaluate_f16(xo)[0]
         assert abs(float(fh[j]) - float(fo)) <= 1e-5 * max(abs(float(fo)), 0.1), (j, fh[j], fo)
     dims = np.sort(np.random.default_rng(3).choice(cfg["D"], 64, replace=False))
     sub = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], dims=dims, **params[0])

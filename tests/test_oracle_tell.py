@@ -258,3 +258,64 @@ def test_determinism(orc):
         a.tell(fa)
         b.tell(fb)
     assert np.array_equal(a.vec, b.vec)
+
+
+# ---------------------------------------------------------------- round-2 pins
+def test_pgpe_sigma_gradient_expectation(orc):
+    """PGPE sigma gradient (reading Q12: eps = sigma z, baseline = mean shaped fitness,
+    divided by P) on f = sum_d a_d x_d^2 in raw mode: E[g^sigma_d] = sigma_d^2 dE[f]/dsigma_d =
+    2 a_d sigma_d^3 (E f = sum a (m^2 + sigma^2)), brute force over 10^6 antithetic pairs, within 5
+    analytic standard errors (Var[h (z_d^2-1)] = 56 a_d^2 sigma_d^4 + 4 sum_{e!=d} a_e^2 sigma_e^4,
+    from the chi^2_1 central moments). Checked both on the raw direction sum and through the sigma
+    step of the tell (sigma' = sigma - 0.2 g^sigma, no clip hit, no decay): sigma shrinks where
+    a > 0 and grows where a < 0. A sign error, /N instead of /P, or a missing sigma factor fails."""
+    D, P, s0 = 3, 1_000_000, 0.5
+    a = np.array([1.0, 1.5, -0.5])
+    run = mk(orc, W.PGPE, 2 * P, D, seed=31, shaping=1, sigma_init=s0, sigma_decay=1.0,
+             sigma_limit=0.0, init_min=-0.1, init_max=0.1)
+    x = run.ask().astype(np.float64)
+    f = ((x * x) @ a).astype(np.float32)
+    expect = 2 * a * s0 ** 3
+    var = 56 * a ** 2 * s0 ** 4 + 4 * ((a ** 2 * s0 ** 4).sum() - a ** 2 * s0 ** 4)
+    se = s0 * np.sqrt(var / P)
+    gs = s0 * run.reduce(f)[1] / P
+    assert np.all(np.abs(gs - expect) < 5 * se), (gs, expect, se)
+    run.tell(f)
+    g_tell = (s0 - run.sigma_d.astype(np.float64)) / 0.2
+    assert np.all(np.abs(g_tell - expect) < 5 * se + 1e-6), (g_tell, expect)
+    assert run.sigma_d[0] < s0 and run.sigma_d[1] < s0 and run.sigma_d[2] > s0
+
+
+def test_sepcma_constants_vs_appendix_a(orc):
+    """mu, mu_eff, c_sigma, d_sigma, c_c, c_1 (D+2)/3, c_mu (D+2)/3, chi_D against SURVEY App. A's
+    table (tests/golden/sepcma_constants.json) at both elite ratios of the C2 variant and at D=10."""
+    g = json.load(open(os.path.join(GOLD, "sepcma_constants.json")))
+    for row in g["rows"]:
+        run = mk(orc, W.SEP_CMA_ES, row["N"], row["D"], elite_ratio=row["elite"])
+        assert run.mu == row["mu"]
+        for k in ("mueff", "c_sigma", "d_sigma", "c_c", "c_1", "c_mu", "chi_d"):
+            got = getattr(run, k)
+            assert abs(got - row[k]) <= 5e-4 * abs(row[k]), (row, k, got)
+    for row in g["snes_eta_sigma"]:
+        run = mk(orc, W.SNES, 4, row["D"]) if row["D"] <= 100000 else None
+        if run is not None:
+            assert abs(run.eta_sigma - row["eta"]) <= 5e-4 * row["eta"], (row, run.eta_sigma)
+
+
+def test_sepcma_zero_path_s438(orc):
+    """S:438 zero-path limit on the C oracle's Sep-CMA-ES: every selected parent at m (Z^w = 0,
+    Q = 0) from the initial zero paths -> m unchanged, p_sigma = p_c = 0, sigma shrinks by exactly
+    exp(-c_sigma/d_sigma) (||p_sigma|| = 0 < threshold so h_sigma = 1), and
+    C' = (1 - c_1 - c_mu) C (no rank-one or rank-mu contribution)."""
+    for D, N, er in ((10, 16, 0.5), (1000, 256, 0.4)):
+        run = mk(orc, W.SEP_CMA_ES, N, D, seed=3, elite_ratio=er, sigma_init=0.05)
+        m0 = run.mean.copy()
+        f = np.arange(N, dtype=np.float32)
+        run.tell_apply(f, np.zeros((2, D)))
+        assert np.array_equal(run.mean, m0)
+        assert np.all(run.vec[4] == 0) and np.all(run.vec[5] == 0)
+        expect = 0.05 * np.exp(-run.c_sigma / run.d_sigma)
+        assert abs(run.sigma - expect) <= 2 * np.spacing(np.float32(expect)), (run.sigma, expect)
+        cexp = 1.0 - run.c_1 - run.c_mu
+        assert np.allclose(run.vec[6], cexp, rtol=1e-7, atol=0), (run.vec[6][:3], cexp)
+        assert run.t == 1
