@@ -71,12 +71,16 @@ def handles_for(cfg_key, rank):
         cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
         return [("c5", cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
     if cfg_key == "c4":
-        cfg = dict(W.CONFIGS["c4"], widths=MLP_WIDTHS, batch=128, data_seed=0)
+        cfg = dict(W.CONFIGS["c4"], widths=MLP_WIDTHS, batch=128, data_seed=0,
+                   fn=W.MLP16 if MLP_MODE["mode"] == "fp16" else W.MLP)
         return [("c4", cfg, [W.config_params(cfg, r) for r in range(cfg["R"])])]
     raise SystemExit(f"unknown config {cfg_key}")
 
 
 SWEEP = {"N": 4096, "D": 985_216}     # the north-star tell point (config 4's shape)
+# c4's MLP fitness: "fp32" = N14, the definition (fp32-accurate tcgen05 kernel); "fp16" = N14',
+# the labelled fp16-parameter-image approximation
+MLP_MODE = {"mode": "fp32"}
 MLP_WIDTHS = [256, 512, 512, 512, 512, 128]   # config 4: D = 985,216
 
 
@@ -154,14 +158,15 @@ def _oracle_gen(args):
         for _ in range(gens):
             run.tell(O.synth_fitness(params["seed"], run.t, N))
         return N * len(dims) * gens, time.perf_counter() - t0
-    if fn == W.MLP:
+    if fn in (W.MLP, W.MLP16):
         # config 4: ask + MLP fitness of `gens` members (the tell, a third of the oracle's
         # per-generation work, is excluded from this sample)
         mlp = O.MLP(MLP_WIDTHS, 128, 0)
         run = O.Run(algo, N, D, **params)
+        ev = mlp.evaluate if fn == W.MLP else mlp.evaluate_f16
         t0 = time.perf_counter()
         for j in range(gens):
-            mlp.evaluate_f16(run.member(j % N))
+            ev(run.member(j % N))
         return D * gens, time.perf_counter() - t0
     if algo == W.CMA_ES:                     # f4: numpy binary64 oracle, one BLAS thread
         from oracle import cma_oracle
@@ -180,23 +185,50 @@ def _oracle_gen(args):
     return N * D * gens, time.perf_counter() - t0
 
 
+def host_description():
+    """nproc, lscpu model / sockets / SMT of the host the oracle is timed on."""
+    d = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        d.update(model=kv.get("Model name"), sockets=kv.get("Socket(s)"),
+                 cores_per_socket=kv.get("Core(s) per socket"),
+                 threads_per_core=kv.get("Thread(s) per core"))
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return d
+
+
 def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
     """The oracle as it stands, on the host cores, on a bounded sample of the same workload:
-    independent runs in parallel processes (one oracle run per process)."""
+    (i) one thread (one process, run 0 of each handle) and (ii) all cores — independent runs in
+    parallel processes (c2: one oracle run per process, as vmap over runs; single-run
+    configs: one replica of the run per process, the same per-core work). The all-cores figure is
+    `value`."""
     import multiprocessing as mp
     from oracle import oracle as O
     O.build()
     hs = handles_for(cfg_key, 0)
-    procs = procs or min(os.cpu_count() or 1, 8)
-    # calibrate one generation of run 0 of each handle
+    procs = procs or (os.cpu_count() or 1)
+    # (i) single thread: calibrate one generation of run 0 of each handle, then ~budget/3 seconds
     per_gen = []
     for _, cfg, params in hs:
         s, t = _oracle_gen((cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[0], 1))
         per_gen.append(t)
+    g1 = max(1, int(budget_s / 3 / (sum(per_gen) + 1e-9)))
+    t0 = time.perf_counter()
+    s1 = sum(_oracle_gen((cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[0], g1))[0]
+             for _, cfg, params in hs)
+    w1 = time.perf_counter() - t0
+    # (ii) all cores
     n_runs = min(procs, min(len(p) for _, _, p in hs))
-    if hs[0][1]["fn"] == W.MLP:
-        n_runs = procs                     # one run, members spread over processes
-    gens = max(1, int(budget_s / (sum(per_gen) * math.ceil(len(hs) * n_runs / procs) + 1e-9)))
+    if hs[0][1]["fn"] in (W.MLP, W.MLP16) or len(hs[0][2]) == 1:
+        n_runs = procs                     # one run: a replica per process
+    gens = max(1, int(2 * budget_s / 3 / (sum(per_gen) * math.ceil(len(hs) * n_runs / procs) + 1e-9)))
     jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r % len(params)], gens)
             for _, cfg, params in hs for r in range(n_runs)]
     t0 = time.perf_counter()
@@ -204,14 +236,17 @@ def cpu_baseline(cfg_key, budget_s=15.0, procs=None):
         res = pool.map(_oracle_gen, jobs)
     wall = time.perf_counter() - t0
     samples = sum(s for s, _ in res)
+    unit_desc = ("generations each (tell on synthetic fitness, first %d dims; samples = N x those "
+                 "dims)" % SWEEP_ORACLE_DIMS if hs[0][1]["fn"] is None else
+                 "members each (ask + MLP fitness; tell excluded)"
+                 if hs[0][1]["fn"] in (W.MLP, W.MLP16) else "generations each (ask+eval+tell)")
     return {"value": samples / wall, "unit": "samples/s", "cores": min(procs, len(jobs)),
             "kind": "oracle",
-            "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} "
-                      + ("generations each (tell on synthetic fitness, first %d dims; samples = "
-                         "N x those dims)" % SWEEP_ORACLE_DIMS if hs[0][1]["fn"] is None else
-                         "members each (ask + MLP fitness; tell excluded)"
-                         if hs[0][1]["fn"] == W.MLP else "generations each (ask+eval+tell)")
-                      + f", {procs} processes, {wall:.1f} s wall"}
+            "sample": f"{n_runs} runs of each of {[h[0] for h in hs]}, {gens} {unit_desc}, "
+                      f"{procs} processes, {wall:.1f} s wall",
+            "single_thread": {"value": s1 / w1, "unit": "samples/s", "cores": 1,
+                              "sample": f"run 0 of each handle, {g1} {unit_desc}, {w1:.1f} s"},
+            "host": host_description()}
 
 
 def run_reference(args):
@@ -223,9 +258,9 @@ def run_reference(args):
     O.build()
     import multiprocessing as mp
     hs = handles_for(args.config, 0)
-    procs = min(os.cpu_count() or 1, 8)
+    procs = os.cpu_count() or 1
     n_runs = min(procs, min(len(p) for _, _, p in hs))
-    if hs[0][1]["fn"] == W.MLP:
+    if hs[0][1]["fn"] in (W.MLP, W.MLP16):
         n_runs = procs
     jobs = [(cfg["algo"], cfg["fn"], cfg["N"], cfg["D"], params[r % len(params)], 1)
             for _, cfg, params in hs for r in range(n_runs)]
@@ -246,7 +281,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": config_block(args.config, 1),
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": procs, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_description()},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -293,6 +328,77 @@ def config_block(cfg_key, world):
             "l2": "state resident; x > L2 only for D*N*4 > 126 MB"}
 
 
+# ----------------------------------------------------------------------------- sub-records
+def sub_bench(cfg_key, world, sharded, steps, peaks, group=None):
+    """One generation of a config timed on its own (warm-up, a profiled pass for per-kernel CUDA
+    events, then `steps` timed steps, max over ranks): the north-star tell cell at W = 1 and the
+    population-sharded C5 / C4 records at W > 1 (the path north_star scales)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2212_04180_b200 import strategy as S
+    (label, cfg, params), = handles_for(cfg_key, 0)
+    es = S.Strategy(cfg["algo"], cfg["N"], cfg["D"], params, group=group if sharded else None)
+    nl = es.local_popsize
+    f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
+    if cfg["fn"] in (W.MLP, W.MLP16):
+        es.set_mlp_problem(cfg["widths"], cfg["batch"], cfg["data_seed"])
+
+    def step():
+        if cfg["fn"] is None:
+            es.synth_fitness(out=f)
+        else:
+            es.ask_eval(cfg["fn"], out_f=f, write_x=False)
+        es.tell(f)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    es.profile(True)
+    for _ in range(max(2, steps // 2)):
+        step()
+    torch.cuda.synchronize()
+    prof = es.profile_read()
+    es.profile(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    per_rank = [ms]
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [float(v.item()) for v in allt]
+        ms = max(per_rank)
+    kern = {k: round(t / max(n, 1), 4) for k, (t, n) in prof.items()}
+    W_ = world if sharded else 1
+    P = (cfg["N"] // W_) // (2 if cfg["algo"] in (W.OPENAI_ES, W.PGPE) else 1)
+    out = {"workload": config_block(cfg_key, W_)["workload"], "N": cfg["N"], "D": cfg["D"],
+           "ms_per_generation": ms, "generations_per_s": 1e3 / ms,
+           "samples_per_s": cfg["R"] * cfg["N"] * cfg["D"] / (ms / 1e3),
+           "kernel_ms_per_launch": kern}
+    if world > 1:
+        out["per_rank_ms"] = per_rank
+        out["allgather_us"] = round(1e3 * kern.get("allgather", 0.0), 2)
+        out["allreduce_us"] = round(1e3 * kern.get("allreduce", 0.0), 2)
+    tk = "tell" if "tell" in kern else "tell_reduce"
+    if tk in kern:
+        ops = cfg["R"] * P * cfg["D"] * (NORMAL_OPS + TELL_USE[cfg["algo"]])
+        ach = ops / (kern[tk] / 1e3) / 1e12
+        out["tell_roofline"] = {"bound": "alu", "kernel": tk, "achieved": ach,
+                                "peak": alu_peak(peaks) / 1e12, "unit": "Tlane-op/s",
+                                "frac": ach / (alu_peak(peaks) / 1e12),
+                                "traffic": ncu_traffic("c5", "tell") if cfg_key == "c5" else None}
+    es.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -321,11 +427,18 @@ def main():
                          "the NCCL all-reduce of the direction sums")
     ap.add_argument("--streams", type=int, default=1,
                     help="run independent handles (c2's two algorithms) on separate streams")
+    ap.add_argument("--mlp", default="fp32", choices=["fp32", "fp16"],
+                    help="c4 MLP fitness: fp32 = N14 (the definition, fp32-accurate kernel); "
+                         "fp16 = N14' (the fp16-parameter-image approximation)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--sub", type=int, default=1,
+                    help="c2: add the north_star_tell record (W=1) or the population-sharded "
+                         "c5/c4 records (W>1)")
     ap.add_argument("--N", type=int, default=SWEEP["N"], help="c5 popsize")
     ap.add_argument("--D", type=int, default=SWEEP["D"], help="c5 dimensions")
     args = ap.parse_args()
     SWEEP.update(N=args.N, D=args.D)
+    MLP_MODE["mode"] = args.mlp
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
@@ -338,6 +451,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        # communicator creation logged (INIT subsystem only, on stderr) so the NCCL INIT lines show
+        # every rank's nranks; algorithm and protocol pinned for run-to-run determinism of the
+        # binary64 direction-sum all-reduce
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import __graft_entry__
     if rank == 0:
@@ -364,7 +485,7 @@ def main():
              if cfg["fn"] is not None else None)
         f = torch.empty((cfg["R"], nl), dtype=torch.float32, device="cuda")
         es.params = params
-        if cfg["fn"] == W.MLP:
+        if cfg["fn"] in (W.MLP, W.MLP16):
             es.set_mlp_problem(cfg["widths"], cfg["batch"], cfg["data_seed"])
         hs.append((label, cfg, es, x, f))
 
@@ -508,8 +629,9 @@ def main():
                 byt += n * R * (8.0 * mu * D + 12.0 * D * D)
             elif k == "rank":
                 byt += n * R * cfg["N"] * 40.0
-            elif k == "eval_mlp":
-                byt += n * ((2.0 if fused else 4.0) * R * N * D + 4.0 * R * N)
+            elif k in ("eval_mlp", "eval_mlp16"):
+                # N14 reads the fp32 parameters; N14' the fp16 image when fused
+                byt += n * ((2.0 if fused and k == "eval_mlp16" else 4.0) * R * N * D + 4.0 * R * N)
                 wd = cfg["widths"]
                 flops += n * R * N * 2.0 * cfg["batch"] * sum(wd[i] * wd[i + 1]
                                                               for i in range(len(wd) - 1))
@@ -554,9 +676,13 @@ def main():
         cb["parallelism"] = f"population sharded x{world}, fused peer-memory tell (f2)"
     if hs[0][1]["fn"] is None:
         cb["path"] = "synthetic fitness, tell"
-    elif fused and hs[0][1]["fn"] == W.MLP:
+    elif fused and hs[0][1]["fn"] == W.MLP16:
         cb["path"] = ("es_ask_eval: ask writes " + ("x and " if write_x else "") +
-                      "the fp16 parameter image (N14'), TMA-fed tcgen05 MLP fitness, then tell")
+                      "the fp16 parameter image (N14', a labelled approximation of N14), "
+                      "TMA-fed tcgen05 MLP fitness, then tell")
+    elif fused and hs[0][1]["fn"] == W.MLP:
+        cb["path"] = ("es_ask_eval: ask writes x (fp32, internal buffer), fp32-accurate tcgen05 MLP "
+                      "fitness (N14: binary16 hi/lo split, three products in TMEM), then tell")
     elif fused:
         cb["path"] = "fused ask+evaluate kernel" + (" (x written)" if write_x else "") + ", tell"
     else:
@@ -571,12 +697,24 @@ def main():
             "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra,
             "timing": "CUDA-graph replays of one generation" if graph is not None else
                       "eager C-ABI calls, CUDA events on the stream"}
+    for h in hs:
+        h[2].close()
+    hs = []
+    if args.config == "c2" and args.sub:
+        if world == 1:
+            # the north star's own target (fused tell >= 70 % of the ALU roofline at D ~ 1e6,
+            # N = 4096) measured under the same clock as the headline
+            line["north_star_tell"] = sub_bench("c5", 1, False, 10, peaks)
+        else:
+            # the path north_star scales: one population sharded over the ranks
+            line["sharded"] = {"c5": sub_bench("c5", world, True, 10, peaks, dist.group.WORLD),
+                               "c4": sub_bench("c4", world, True, 3, peaks, dist.group.WORLD),
+                               "nccl": {k: os.environ.get(k) for k in
+                                        ("NCCL_ALGO", "NCCL_PROTO", "NCCL_DEBUG_SUBSYS")}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    for h in hs:
-        h[2].close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -16,7 +16,9 @@
  *     default stream); no call synchronises the device unless it is handed host memory.
  *   - Buffer arguments may be DEVICE pointers (no copy) or HOST pointers (pinned or pageable; the
  *     library stages them through device scratch with cudaMemcpyAsync and, for host outputs,
- *     synchronises the stream before returning). Layouts are row-major and dense.
+ *     synchronises the stream before returning). Host fitness INPUTS of es_tell / es_tell_local /
+ *     es_weight_decay are read before the call returns (copied into a pinned staging buffer), so
+ *     the caller may refill them at once. Layouts are row-major and dense.
  *   - Arguments are validated before any launch or state change; on error nothing is modified.
  *   - No C++ exception crosses the ABI. One context is used by one host thread at a time.
  *   - Member j of run r on rank w is global member w*(N/W) + j (antithetic pairs never straddle
@@ -54,7 +56,12 @@ typedef enum {
   ES_FIT_SPHERE = 0,     /* Σ x_d²                                  (P:212 BBOB)      */
   ES_FIT_ROSENBROCK = 1, /* Σ 100(x_{d+1} − x_d²)² + (1 − x_d)²                              */
   ES_FIT_RASTRIGIN = 2,  /* 10D + Σ (x_d² − 10 cos 2πx_d), cancellation-free form (N7)         */
-  ES_FIT_MLP = 3         /* synthetic tanh-MLP regression fitness (N14)     */
+  ES_FIT_MLP = 3,        /* synthetic tanh-MLP regression fitness (N14): the
+                            MLP of the fp32 parameters, fp32-accurate (binary16 hi/lo split of
+                            every operand, three-product tensor-core sums; parameters |x| < 255) */
+  ES_FIT_MLP16 = 4       /* the same MLP at binary16 parameter and activation precision (N14′):
+                            a labelled APPROXIMATION of ES_FIT_MLP (its distance to N14 is
+                            measured per member in the tests), half the bytes per parameter   */
 } es_fitness_t;
 
 typedef enum {
@@ -149,20 +156,23 @@ es_status_t es_ask(es_ctx_t *ctx, float *x, es_stream_t stream);
 /* Fused ask + evaluate ("sampling ... can become a burden", P:225
  * memory): forms this rank's population exactly as es_ask (bit-identical x, written to x
  * [R][N/W][D] unless x is NULL — then it is never materialised in fp32) and writes its fitness (as
- * es_eval_bbob) to fitness [R][N/W]. BBOB: one kernel that evaluates while sampling. ES_FIT_MLP
- * (N14′): the ask kernel writes the fp16 parameter image the fitness uses, which the tcgen05 MLP
- * kernel streams with TMA (x, if given, must be device memory; D % 4 == 0). ES_CMA_ES: the
- * tensor-core sampling, then es_eval_bbob's kernels (BBOB or the MLP on fp32 x). Counts as the
- * generation's ask. Errors: ES_ERR_INVALID_ARG for NULL fitness; ES_ERR_BAD_STATE for ES_FIT_MLP
- * without es_set_mlp_problem. */
+ * es_eval_bbob) to fitness [R][N/W]. BBOB: one kernel that evaluates while sampling. ES_FIT_MLP:
+ * the ask, then the fp32-accurate tensor-core MLP on the fp32 population (x NULL: an internal
+ * [R][N/W][D] buffer holds it). ES_FIT_MLP16 (N14′): the ask kernel writes the fp16 parameter
+ * image the fitness uses, which the tcgen05 MLP kernel streams with TMA. For both MLP fitnesses x,
+ * if given, must be 16-byte aligned device memory. ES_CMA_ES: the tensor-core sampling, then
+ * es_eval_bbob's kernels (BBOB or the MLP on fp32 x). Counts as the generation's ask. Errors:
+ * ES_ERR_INVALID_ARG for NULL fitness or a misaligned / host x with an MLP fitness;
+ * ES_ERR_BAD_STATE for an MLP fitness without es_set_mlp_problem. */
 es_status_t es_ask_eval(es_ctx_t *ctx, es_fitness_t fn, float *x, float *fitness,
                         es_stream_t stream);
 
-/* evaluate: fitness[n] = f(x[n]) for n rows of length D (N7; MLP: N14).
- * Context-free for the BBOB functions (ctx may be NULL); ES_FIT_MLP needs a context on which
- * es_set_mlp_problem was called and D equal to its parameter count. x float [n][D], fitness
- * float [n]. Errors: ES_ERR_INVALID_ARG (n < 0, D < 1, unknown fn), ES_ERR_BAD_STATE (MLP
- * problem not set). */
+/* evaluate: fitness[n] = f(x[n]) for n rows of length D (N7; MLP: N14, N14′).
+ * Context-free for the BBOB functions (ctx may be NULL); ES_FIT_MLP / ES_FIT_MLP16 need a context
+ * on which es_set_mlp_problem was called and D equal to its parameter count. x float [n][D],
+ * fitness float [n]; host pointers are staged through the context's buffers (temporaries only
+ * beyond their size), and the call then synchronises the stream. Errors: ES_ERR_INVALID_ARG
+ * (n < 0, D < 1, unknown fn), ES_ERR_BAD_STATE (MLP problem not set). */
 es_status_t es_eval_bbob(es_ctx_t *ctx, es_fitness_t fn, const float *x, int64_t n, int64_t num_dims,
                     float *fitness, es_stream_t stream);
 
@@ -317,7 +327,8 @@ es_status_t es_set(es_ctx_t *ctx, es_field_t field, const void *src, es_stream_t
 
 /* MLP fitness problem (N14): widths[0..n_widths) layer widths (input first; every layer tanh,
  * P:268–269), `batch` inputs drawn from the DATA stream of data_seed, teacher θ* from the TEACHER
- * stream, targets Y* = MLP_θ*(U) computed on the device by the same kernel. Flattening of a
+ * stream, targets Y* = MLP_θ*(U) computed on the device by the same kernels (one set per MLP
+ * fitness, so f(θ*) = 0 exactly for each). Flattening of a
  * parameter vector: per layer W as [out][in] row-major (nn.Linear layout) then b[out], layers in
  * order. Synchronises the stream. Errors: ES_ERR_INVALID_ARG for n_widths outside 2..16;
  * ES_ERR_UNSUPPORTED for widths not multiples of 16 in [16, 512] or batch != 128. */

@@ -14,7 +14,7 @@ STATUS = {0: "success", 1: "invalid argument", 2: "bad state", 3: "CUDA error", 
 
 OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS, CMA_ES = 0, 1, 2, 3, 4, 5
 ADAM, SGD, CLIPUP = 0, 1, 2
-SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
+SPHERE, ROSENBROCK, RASTRIGIN, MLP, MLP16 = 0, 1, 2, 3, 4
 FIELDS = dict(mean=0, sigma_d=1, adam_m=2, adam_v=3, p_sigma=4, p_c=5, C=6, best_x=7, best_f=8,
               sigma=9, lrate=10, gen=11, shaped=12, rank_s=13, rank_e=14, perm=15, fitness=16,
               dirsum=17, norm2=18, cov=19, chol=20)

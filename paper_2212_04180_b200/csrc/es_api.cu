@@ -113,6 +113,10 @@ es_status_t es_destroy(es_ctx_t* c) {
   }
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->mlp) mlp_problem_destroy(c->mlp);
+  for (int k = 0; k < 2; ++k) {
+    if (c->hstage[k]) cudaFreeHost(c->hstage[k]);
+    if (c->hstage_ev[k]) cudaEventDestroy(c->hstage_ev[k]);
+  }
   for (void* p : c->allocs) cudaFree(p);
   delete c;
   return ES_SUCCESS;
@@ -260,9 +264,7 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   TRY(dalloc(c, (void**)&s.coefA, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.coefB, RN * sizeof(double)));
   TRY(dalloc(c, (void**)&s.G, 2 * RD * sizeof(double)));
-  c->nchunk = tell_pick_nchunk(s);
   const int bpr = tell_blocks_per_run(s);
-  if (c->nchunk > 1) TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->nchunk * 2 * RD * sizeof(double)));
   TRY(dalloc(c, (void**)&s.arrive, (size_t)R * bpr * sizeof(uint32_t)));
   const size_t nparts = cma ? std::max<size_t>(bpr, (size_t)((s.D + 31) / 32)) : (size_t)bpr;
   TRY(dalloc(c, (void**)&s.normpart, (size_t)R * nparts * sizeof(double)));
@@ -312,6 +314,20 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
       rs.k_refresh = std::max(1, (int)std::floor(1.0 / (10.0 * Dd * (rs.c_1 + rs.c_mu))));
     }
     std::copy(wr.begin(), wr.end(), wpos.begin() + (size_t)r * N);
+  }
+  {
+    // tell entry split from each run's expected entry count on this rank (Sep-CMA-ES: μ_r)
+    std::vector<int> ent(R);
+    for (int r = 0; r < R; ++r) {
+      int ne = algo == ES_SEP_CMA_ES ? c->host_rs[r].mu : (antithetic(algo) ? N / 2 : N);
+      if (algo == ES_ARS || (algo == ES_PGPE && c->host_rs[r].ars_k < N / 2)) ne = c->host_rs[r].ars_k;
+      int e0, e1;
+      shard_range(ne, pW, prank, e0, e1);
+      ent[r] = std::max(1, e1 - e0);
+    }
+    c->split = tell_pick_split(s, ent);
+    if (c->split.nchunk > 1)
+      TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->split.nchunk * 2 * RD * sizeof(double)));
   }
   TRY(cudaMemcpyAsync(s.rs, c->host_rs.data(), R * sizeof(RunScal), cudaMemcpyHostToDevice, st));
   TRY(cudaMemcpyAsync(s.wpos, wpos.data(), RN * sizeof(float), cudaMemcpyHostToDevice, st));
@@ -394,17 +410,20 @@ static es_status_t ask_eval_bbob(es_ctx* c, es_fitness_t fn, float* x, float* f,
 es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!c || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
-  if ((int)fn < 0 || (int)fn > 3) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
+  if ((int)fn < 0 || (int)fn > 4) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
   if (c->broken) return fail(c, ES_ERR_BAD_STATE, "context unusable after an NCCL error");
   const DevState& s = c->s;
   const size_t nloc = (size_t)s.R * s.Nloc;
   if (s.dshard && c->dW > 1 && !c->comm)
     return fail(c, ES_ERR_BAD_STATE, "D-shard without communicator: use es_ask_eval_partial");
+  if (is_mlp(fn)) {
+    if (s.dshard) return fail(c, ES_ERR_UNSUPPORTED, "the MLP fitness is not separable over dims");
+    if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
+    if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
+    if (s.algo != CMA_ES && x && (!is_device_ptr(x) || (reinterpret_cast<uintptr_t>(x) & 15)))
+      return fail(c, ES_ERR_INVALID_ARG, "x must be 16-byte aligned device memory (MLP fitness)");
+  }
   if (s.algo == CMA_ES) {     // sample (tiled contraction) then evaluate (BBOB or the MLP)
-    if (fn == ES_FIT_MLP) {
-      if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
-      if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
-    }
     const bool xh = x && !is_device_ptr(x), fh = !is_device_ptr(f);
     float* xd = x;
     if (!x || xh) {
@@ -422,9 +441,10 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
       CUDA_OR(c, launch_cma_ask(s, xd, st, &nk));
     }
     {
-      ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : "eval_bbob", st);
+      ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : fn == ES_FIT_MLP16 ? "eval_mlp16" : "eval_bbob", st);
       CUDA_OR(c, fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, (int64_t)nloc, fd, st)
-                                  : launch_eval_bbob((int)fn, xd, (int64_t)nloc, s.D, fd, st));
+                 : fn == ES_FIT_MLP16 ? launch_mlp_eval_f16(c->mlp, xd, (int64_t)nloc, fd, st)
+                                      : launch_eval_bbob((int)fn, xd, (int64_t)nloc, s.D, fd, st));
     }
     c->launches += nk + 1;
     if (xh) CUDA_OR(c, cudaMemcpyAsync(x, xd, nloc * s.Dx * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -434,11 +454,36 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
     return ES_SUCCESS;
   }
   if (fn == ES_FIT_MLP) {
+    // N14: the ask writes x (into the internal buffer when x is NULL), the fp32-accurate MLP reads it
+    float* xd = x;
+    if (!xd) {
+      if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.Dx * sizeof(float)));
+      xd = c->xstage;
+    }
+    float* fd = f;
+    const bool fh = !is_device_ptr(f);
+    if (fh) {
+      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, nloc * sizeof(float)));
+      fd = c->fstage;
+    }
+    {
+      ProfScope ps(c, "ask", st);
+      CUDA_OR(c, launch_ask(s, xd, st));
+    }
+    {
+      ProfScope ps(c, "eval_mlp", st);
+      CUDA_OR(c, launch_mlp_eval(c->mlp, xd, (int64_t)nloc, fd, st));
+    }
+    c->launches += 2;
+    if (fh) {
+      CUDA_OR(c, cudaMemcpyAsync(f, fd, nloc * sizeof(float), cudaMemcpyDeviceToHost, st));
+      CUDA_OR(c, cudaStreamSynchronize(st));
+    }
+    c->asked = true;
+    return ES_SUCCESS;
+  }
+  if (fn == ES_FIT_MLP16) {
     // N14′: the ask writes fp16(x) (and x unless NULL); the MLP streams that image with TMA
-    if (s.dshard) return fail(c, ES_ERR_UNSUPPORTED, "the MLP fitness is not separable over dims");
-    if (!c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
-    if (mlp_problem_dims(c->mlp) != s.D) return fail(c, ES_ERR_INVALID_ARG, "D != MLP parameters");
-    if (x && !is_device_ptr(x)) return fail(c, ES_ERR_INVALID_ARG, "x must be device memory");
     if (!c->x16) CUDA_OR(c, dalloc(c, (void**)&c->x16, nloc * s.D * sizeof(__half)));
     float* fd = f;
     const bool fh = !is_device_ptr(f);
@@ -451,7 +496,7 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
       CUDA_OR(c, launch_ask16(s, x, c->x16, st));
     }
     {
-      ProfScope ps(c, "eval_mlp", st);
+      ProfScope ps(c, "eval_mlp16", st);
       CUDA_OR(c, launch_mlp_eval16(c->mlp, c->x16, (int64_t)nloc, fd, st));
     }
     c->launches += 2;
@@ -551,8 +596,8 @@ es_status_t es_eval_bbob(es_ctx_t* c, es_fitness_t fn, const float* x, int64_t n
   cudaStream_t st = (cudaStream_t)stream_;
   if (!x || !f) return fail(c, ES_ERR_INVALID_ARG, "NULL argument");
   if (n < 0 || D < 1) return fail(c, ES_ERR_INVALID_ARG, "bad sizes n=%lld D=%lld", (long long)n, (long long)D);
-  if ((int)fn < 0 || (int)fn > 3) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
-  if (fn == ES_FIT_MLP) {
+  if ((int)fn < 0 || (int)fn > 4) return fail(c, ES_ERR_INVALID_ARG, "unknown fitness %d", fn);
+  if (is_mlp(fn)) {
     if (!c || !c->mlp) return fail(c, ES_ERR_BAD_STATE, "es_set_mlp_problem was not called");
     if (mlp_problem_dims(c->mlp) != D)
       return fail(c, ES_ERR_INVALID_ARG, "D=%lld != MLP parameter count %lld", (long long)D,
@@ -562,39 +607,50 @@ es_status_t es_eval_bbob(es_ctx_t* c, es_fitness_t fn, const float* x, int64_t n
   const bool xh = !is_device_ptr(x), fh = !is_device_ptr(f);
   const float* xd = x;
   float* fd = f;
-  void* tmpx = nullptr;
-  void* tmpf = nullptr;
+  // host buffers are staged through the context's cached buffers when they fit (no cudaMalloc /
+  // cudaFree per call, which would synchronise the device); temporaries beyond that are freed on
+  // every exit path
+  struct Tmp {
+    void* p = nullptr;
+    ~Tmp() { if (p) cudaFree(p); }
+  } tmpx, tmpf;
+  const size_t cap = c ? (size_t)c->s.R * c->s.Nloc : 0;
   if (xh) {
-    CUDA_OR(c, cudaMalloc(&tmpx, (size_t)n * D * sizeof(float)));
-    CUDA_OR(c, cudaMemcpyAsync(tmpx, x, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st));
-    xd = (const float*)tmpx;
+    if (c && (size_t)n <= cap && D == c->s.Dx) {
+      if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, cap * c->s.Dx * sizeof(float)));
+      xd = c->xstage;
+    } else {
+      CUDA_OR(c, cudaStreamSynchronize(st));
+      CUDA_OR(c, cudaMalloc(&tmpx.p, (size_t)n * D * sizeof(float)));
+      xd = (const float*)tmpx.p;
+    }
+    CUDA_OR(c, cudaMemcpyAsync(const_cast<float*>(xd), x, (size_t)n * D * sizeof(float),
+                               cudaMemcpyHostToDevice, st));
   }
   if (fh) {
-    if (c && (size_t)n <= (size_t)c->s.R * c->s.Nloc) {
-      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, (size_t)c->s.R * c->s.Nloc * sizeof(float)));
+    if (c && (size_t)n <= cap) {
+      if (!c->fstage) CUDA_OR(c, dalloc(c, (void**)&c->fstage, cap * sizeof(float)));
       fd = c->fstage;
     } else {
-      CUDA_OR(c, cudaMalloc(&tmpf, (size_t)n * sizeof(float)));
-      fd = (float*)tmpf;
+      CUDA_OR(c, cudaMalloc(&tmpf.p, (size_t)n * sizeof(float)));
+      fd = (float*)tmpf.p;
     }
   }
   cudaError_t e;
   {
-    ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : "eval_bbob", st);
+    ProfScope ps(c, fn == ES_FIT_MLP ? "eval_mlp" : fn == ES_FIT_MLP16 ? "eval_mlp16" : "eval_bbob", st);
     e = fn == ES_FIT_MLP ? launch_mlp_eval(c->mlp, xd, n, fd, st)
-                         : launch_eval_bbob((int)fn, xd, n, D, fd, st);
+        : fn == ES_FIT_MLP16 ? launch_mlp_eval_f16(c->mlp, xd, n, fd, st)
+                             : launch_eval_bbob((int)fn, xd, n, D, fd, st);
   }
-  if (e != cudaSuccess) return fail(c, ES_ERR_CUDA, "eval launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(st);
+    return fail(c, ES_ERR_CUDA, "eval launch: %s", cudaGetErrorString(e));
+  }
   if (c) c->launches += 1;
-  if (fh) {
-    CUDA_OR(c, cudaMemcpyAsync(f, fd, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CUDA_OR(c, cudaStreamSynchronize(st));
-  }
-  if (tmpx || tmpf) {
-    CUDA_OR(c, cudaStreamSynchronize(st));
-    if (tmpx) cudaFree(tmpx);
-    if (tmpf) cudaFree(tmpf);
-  }
+  if (fh) CUDA_OR(c, cudaMemcpyAsync(f, fd, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  // host x / fitness: the copies complete (and temporaries may be freed) before returning
+  if (xh || fh || tmpx.p || tmpf.p) CUDA_OR(c, cudaStreamSynchronize(st));
   return ES_SUCCESS;
 }
 
@@ -626,7 +682,7 @@ static es_status_t tell_local_impl(es_ctx* c, const float* fsrc, bool fused, cud
     return ES_SUCCESS;
   }
   ProfScope ps(c, fused ? "tell" : "tell_reduce", st);
-  CUDA_OR(c, launch_tell_reduce(s, fused, c->nchunk, st));
+  CUDA_OR(c, launch_tell_reduce(s, fused, c->split, st));
   c->launches += 1;
   return ES_SUCCESS;
 }
@@ -687,7 +743,33 @@ static const float* stage_fitness(es_ctx* c, const float* f, size_t n, cudaStrea
     cudaError_t e = dalloc(c, (void**)buf, n * sizeof(float));
     if (e != cudaSuccess) { *err = fail(c, ES_ERR_OOM, "staging: %s", cudaGetErrorString(e)); return nullptr; }
   }
-  cudaError_t e = cudaMemcpyAsync(*buf, f, n * sizeof(float), cudaMemcpyHostToDevice, st);
+  // the caller's host buffer is read synchronously (into a pinned staging buffer) so it may be
+  // refilled as soon as this call returns; the asynchronous H2D copy reads the staging buffer
+  cudaError_t e = cudaSuccess;
+  if (c->hstage_n < n) {
+    for (int k = 0; k < 2; ++k) {
+      if (c->hstage_ev[k]) cudaEventSynchronize(c->hstage_ev[k]);
+      if (c->hstage[k]) cudaFreeHost(c->hstage[k]);
+      c->hstage[k] = nullptr;
+    }
+    c->hstage_n = 0;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaMallocHost((void**)&c->hstage[k], n * sizeof(float));
+      if (e == cudaSuccess && !c->hstage_ev[k])
+        e = cudaEventCreateWithFlags(&c->hstage_ev[k], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) { *err = fail(c, ES_ERR_OOM, "host staging: %s", cudaGetErrorString(e)); return nullptr; }
+    c->hstage_n = n;
+  }
+  const int k = c->hstage_k;
+  c->hstage_k ^= 1;
+  if ((e = cudaEventSynchronize(c->hstage_ev[k])) != cudaSuccess) {   // its previous copy is done
+    *err = fail(c, ES_ERR_CUDA, "staging event: %s", cudaGetErrorString(e));
+    return nullptr;
+  }
+  std::memcpy(c->hstage[k], f, n * sizeof(float));
+  e = cudaMemcpyAsync(*buf, c->hstage[k], n * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(c->hstage_ev[k], st);
   if (e != cudaSuccess) { *err = fail(c, ES_ERR_CUDA, "H2D fitness: %s", cudaGetErrorString(e)); return nullptr; }
   return *buf;
 }
@@ -1054,6 +1136,12 @@ es_status_t es_set_mlp_problem(es_ctx_t* c, const int32_t* widths, int32_t nw, i
   void* p = mlp_problem_create(widths, nw, batch, seed, (cudaStream_t)stream_, &err);
   if (!p) return fail(c, err.rfind("unsupported", 0) == 0 ? ES_ERR_UNSUPPORTED : ES_ERR_INVALID_ARG,
                       "%s", err.c_str());
+  // the fp32-accurate kernel's per-member scratch for a whole population, so that generations
+  // can be graph-captured (the scratch only grows outside capture, for larger es_eval_bbob calls)
+  if (cudaError_t e = mlp_problem_reserve(p, (int64_t)c->s.R * c->s.Nloc, (cudaStream_t)stream_)) {
+    mlp_problem_destroy(p);
+    return fail(c, ES_ERR_CUDA, "MLP scratch: %s", cudaGetErrorString(e));
+  }
   if (c->mlp) mlp_problem_destroy(c->mlp);
   c->mlp = p;
   return ES_SUCCESS;

@@ -18,6 +18,9 @@
 
 namespace esb {
 cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
+cudaError_t launch_mlp_eval_f16(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
+cudaError_t mlp_problem_reserve(void* prob, int64_t n, cudaStream_t st);
+inline bool is_mlp(int fn) { return fn == ES_FIT_MLP || fn == ES_FIT_MLP16; }
 void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
                          cudaStream_t st, std::string* err);
 void mlp_problem_destroy(void* prob);
@@ -55,10 +58,16 @@ struct es_ctx {
   double* wdn2 = nullptr;       // [R][N] D-shard squared norms (weight decay)
   int p2p_phase = -1;           // next es_tell_p2p_finish phase (-1: no apply pending)
   bool broken = false;
-  int nchunk = 1;
+  TellSplit split{1, 1};
   float* fgather = nullptr;     // [W][R][Nloc]
   float* fstage = nullptr;      // [R][Nloc] staging of host fitness
   float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
+  // host inputs are first copied (CPU memcpy) into one of two pinned host buffers, so the
+  // caller may reuse its buffer as soon as the call returns; an event per buffer guards its reuse
+  float* hstage[2] = {nullptr, nullptr};
+  size_t hstage_n = 0;
+  cudaEvent_t hstage_ev[2] = {nullptr, nullptr};
+  int hstage_k = 0;
   float* xstage = nullptr;      // [R][Nloc][D] staging of a host population
   double* aepart = nullptr;     // [R][Nloc][blocks] fused ask+eval partial sums
   __half* x16 = nullptr;        // [R][Nloc][D] fp16 parameter image (MLP fused path, N14′)

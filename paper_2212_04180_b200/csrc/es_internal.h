@@ -17,6 +17,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace esb {
 
@@ -163,7 +164,9 @@ cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
 // the same kernel; otherwise the sums land in s.G for the all-reduce and launch_tell_update
 // applies them. Sep-CMA-ES additionally needs launch_sepcma_finish (global ‖p_σ‖, σ, h_σ, p_c, C).
 // Each returns the number of kernels it launched through *nk.
-cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st);
+// grid.y = nchunk; run r's entries are cut into chunks of echunk (see tell_kernel)
+struct TellSplit { int nchunk, echunk; };
+cudaError_t launch_tell_reduce(const DevState& s, bool fused, TellSplit sp, cudaStream_t st);
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);
 cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st);
@@ -202,7 +205,8 @@ bool syrk_tc_supported(const DevState& s);
 cudaError_t launch_chol_update_tc(const DevState& s, int kb, cudaStream_t st);
 cudaError_t launch_cma_cov_tc(const DevState& s, cudaStream_t st);
 cudaError_t launch_cma_sample_tc(const DevState& s, float* x, cudaStream_t st);
-int tell_pick_nchunk(const DevState& s);
+// ent[r]: expected tell entries of run r on this rank
+TellSplit tell_pick_split(const DevState& s, const std::vector<int>& ent);
 constexpr int kTellThreads = 128;
 int sm_count();   // of the current device
 

@@ -54,6 +54,11 @@ struct MlpParams {
   int mode;
   const __half* x16;            // TMA mode: the fp16 parameter image [n][D] (N14′)
   CUtensorMap tmap[kMaxLayers + 1];   // TMA mode: per layer, 3-D (in, out, member) fp16 tiles
+  // fp32-accurate kernel (N14): per batch half, the layer-1 A image of the scaled hi/lo split of U
+  const __half* uimg32[2];
+  float* Y32;                   // [128][w_L] teacher outputs of the fp32-accurate kernel
+  double* part;                 // [n][2] per-half squared-error sums
+  uint32_t* cnt;                // [n] arrival counters (zero between launches)
 };
 
 struct MlpProblem {
@@ -61,6 +66,11 @@ struct MlpProblem {
   __half* uimg = nullptr;
   float* Y = nullptr;
   float* theta = nullptr;
+  __half* uimg32 = nullptr;     // [2 halves][kpad0/64 k-blocks][128 rows][64] fp16
+  float* Y32 = nullptr;
+  double* part = nullptr;
+  uint32_t* cnt = nullptr;
+  int64_t cap = 0;              // members part/cnt can hold
 };
 
 
@@ -410,6 +420,334 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- fp32-accurate kernel (N14)
+// The definition (N14) is the MLP of the fp32 parameters. Each operand a is split into two binary16
+// parts of the scaled value a·2^8: hi = fp16(a·2^8), lo = fp16(a·2^8 − hi) (≈ 22 significant bits
+// together; the 2^8 scale keeps lo out of the binary16 subnormal range for |a| ≥ 2^-10, below which
+// its absolute error is ≤ 2^-33). D = Σ_k A·W with A = [A_hi; A_lo] stacked as the 128 MMA rows
+// (64 batch rows per CTA) and W = W_hi + W_lo accumulated into the same TMEM columns:
+// row b of D + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b] to fp32 accuracy.
+// Two CTAs per member (batch rows 0–63 and 64–127); each streams the member's weights (the pair's
+// second read is an L2 hit) and the pair's squared-error halves are combined in a fixed order by
+// whichever CTA finishes second. Warp roles as mlp_kernel; the epilogue's lane quarters 2–3 (the lo
+// rows) hand their accumulator to quarters 0–1 through shared memory.
+static constexpr int kStages32 = 2;
+static constexpr int kStage32Bytes = 2 * kTileBytes;            // hi tile + lo tile
+static constexpr int kXbufBytes = 8 * 32 * 32 * 4;               // 8 warp pairs × 32 lanes × 32 cols
+static constexpr int kSmem32Bytes = kABytes + kStages32 * kStage32Bytes + kXbufBytes + 1024;
+static constexpr float kSplitScale = 256.0f, kUnscale = 1.0f / 65536.0f;
+
+// hi / lo binary16 parts of 8 scaled values
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+  float s[8], r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s[i] = __fmul_rn(v[i], kSplitScale);
+  hi = pack8(s);
+  const __half* h = reinterpret_cast<const __half*>(&hi);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = __fsub_rn(s[i], __half2float(h[i]));
+  lo = pack8(r);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constant__ MlpParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* A = smem;                                              // [8][128 rows][64] fp16
+  uint8_t* Bst = smem + kABytes;                                  // [2][hi, lo][128][64] fp16
+  float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
+                                               kXbufBytes);
+  uint64_t* full = bars;                                          // [kStages32]
+  uint64_t* empty = bars + kStages32;
+  uint64_t* dready = bars + 2 * kStages32;                        // [4]
+  uint64_t* aready = bars + 2 * kStages32 + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages32 + 5);
+  double* red = reinterpret_cast<double*>(bars + 2 * kStages32 + 6);   // [kEpiWarps]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = blockIdx.x & 1;
+  const int64_t pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
+  if (smem_u32(smem) & 1023) __trap();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages32; ++s) {
+      mbar_init(&full[s], kProdWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
+    mbar_init(aready, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProdWarps + kEpiWarps) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int L = P.nl;
+
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ producers: fp32 W → hi, lo
+    const int t = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    auto block_of = [&](int64_t m, int l, int nt, const float** ptr, uint32_t* bytes) {
+      const int in = P.w[l - 1], out = P.w[l];
+      const int rows = min(128, out - nt * 128);
+      *ptr = P.x + m * P.D + P.off[l] + (int64_t)nt * 128 * in;
+      *bytes = rows > 0 ? (uint32_t)rows * in * 4u : 0u;
+    };
+    auto prefetch_block = [&](int64_t m, int l, int nt) {
+      if (++nt >= (P.npad[l] >> 7)) { nt = 0; if (++l > L) { l = 1; m += npair; } }
+      if (m >= P.n) return;
+      const float* ptr;
+      uint32_t bytes;
+      block_of(m, l, nt, &ptr, &bytes);
+      for (uint32_t o = lane * 8192u; o < bytes; o += 32 * 8192u)
+        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(8192u, bytes - o));
+    };
+    if (warp == 0 && pair < P.n) {
+      const float* ptr;
+      uint32_t bytes;
+      block_of(pair, 1, 0, &ptr, &bytes);
+      for (uint32_t o = lane * 8192u; o < bytes; o += 32 * 8192u)
+        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(8192u, bytes - o));
+    }
+    for (int64_t m = pair; m < P.n; m += npair) {
+      const float* xm = P.x + m * P.D;
+      for (int l = 1; l <= L; ++l) {
+        const int in = P.w[l - 1], out = P.w[l];
+        const float* W = xm + P.off[l];
+        const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+        for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+          const int nt = tile / kc_n, kc = tile % kc_n;
+          if (kc == 0 && warp == 0 && half == 0) prefetch_block(m, l, nt);
+          mbar_wait(&empty[stage], phase ^ 1);
+          float4 v[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
+            const int n = nt * 128 + r, k = kc * 64 + c * 8;
+            if (n < out && k < in) {
+              const float4* src = reinterpret_cast<const float4*>(W + (int64_t)n * in + k);
+              v[2 * j] = __ldg(src);
+              v[2 * j + 1] = __ldg(src + 1);
+            } else {
+              v[2 * j] = v[2 * j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          uint8_t* dst = Bst + stage * kStage32Bytes;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
+            const float e[8] = {v[2 * j].x, v[2 * j].y, v[2 * j].z, v[2 * j].w,
+                                v[2 * j + 1].x, v[2 * j + 1].y, v[2 * j + 1].z, v[2 * j + 1].w};
+            uint4 hi, lo;
+            split8(e, hi, lo);
+            *reinterpret_cast<uint4*>(dst + swz(r, c)) = hi;
+            *reinterpret_cast<uint4*>(dst + kTileBytes + swz(r, c)) = lo;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+          if (++stage == kStages32) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp < kProdWarps + kEpiWarps) {
+    // ------------------------------------------------------------ epilogue
+    const int e = warp - kProdWarps;                 // 0..15
+    const int q = warp & 3, part = e >> 2;           // TMEM lane quarter, 32-column quarter
+    const bool hiw = q < 2;                          // lanes 0–63: the A_hi rows (and the result)
+    const int pr = part * 2 + (q & 1);               // warp pair (hi warp q, lo warp q + 2)
+    float* xb = xbuf + pr * 32 * 32;                 // [col][lane]
+    const int brow = half * 64 + (q & 1) * 32 + lane;   // batch row of this lane
+    const int et = threadIdx.x - kProdWarps * 32;    // 0..511
+    uint32_t dphase = 0;
+    for (int64_t m = pair; m < P.n; m += npair) {
+      const float* xm = P.x + m * P.D;
+      {
+        const int bytes = (P.kpad[0] >> 6) * kTileBytes;
+        const uint4* src = reinterpret_cast<const uint4*>(P.uimg32[half]);
+        for (int o = et; o < bytes / 16; o += kEpiWarps * 32)
+          reinterpret_cast<uint4*>(A)[o] = __ldg(src + o);
+        fence_async_smem();
+        named_bar(1, kEpiWarps * 32);
+        if (et == 0) mbar_arrive(aready);
+      }
+      double sq = 0.0;
+      for (int l = 1; l <= L; ++l) {
+        const int in = P.w[l - 1], out = P.w[l];
+        const float* bias = xm + P.off[l] + (int64_t)out * in;
+        const int ntl = P.npad[l] >> 7;
+        const int cend = l < L ? P.kpad[l] : out;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        for (int t = 0; t < ntl; ++t) {
+          mbar_wait(&dready[t], (dphase >> t) & 1u);
+          tc_fence_after();
+          const int c0 = t * 128 + part * 32;
+          if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
+          float v[32];
+          tmem_ld32(trow + (uint32_t)c0, v);
+          if (!hiw) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) xb[i * 32 + lane] = v[i];
+            named_bar(2 + pr, 64);
+            named_bar(2 + pr, 64);                   // the hi warp has consumed xb
+            continue;
+          }
+          named_bar(2 + pr, 64);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(v[i], xb[i * 32 + lane]);
+          named_bar(2 + pr, 64);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int n = c0 + i;
+            v[i] = n < out ? tanhf(__fadd_rn(__fmul_rn(v[i], kUnscale), __ldg(bias + n))) : 0.0f;
+          }
+          if (l < L) {
+            uint4 h[4], g[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) split8(v + 8 * c, h[c], g[c]);
+            tmem_st16(trow + (uint32_t)c0, h);        // parked in the tile's consumed columns
+            tmem_st16(trow + (uint32_t)c0 + 16, g);
+          } else if (P.mode == 0) {
+            const float* yr = P.Y32 + (int64_t)brow * out;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int n = c0 + i;
+              if (n < out) {
+                const double d = (double)v[i] - (double)__ldg(yr + n);
+                sq = __fma_rn(d, d, sq);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i < out) P.Y32[(int64_t)brow * out + c0 + i] = v[i];
+          }
+        }
+        if (l < L && hiw) {
+          const int rh = (q & 1) * 32 + lane;        // A rows: rh (hi), 64 + rh (lo)
+          for (int t = 0; t < ntl; ++t) {
+            const int c0 = t * 128 + part * 32;
+            if (c0 >= cend) continue;
+            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                          make_uint4(0, 0, 0, 0)};
+            uint4 g[4] = {h[0], h[1], h[2], h[3]};
+            if (c0 < out) {
+              tmem_ld16(trow + (uint32_t)c0, h);
+              tmem_ld16(trow + (uint32_t)c0 + 16, g);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck)) = h[c];
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck)) = g[c];
+            }
+          }
+        }
+        dphase ^= (1u << ntl) - 1u;
+        tc_fence_before();
+        if (l < L) {
+          fence_async_smem();
+          named_bar(1, kEpiWarps * 32);
+          if (et == 0) mbar_arrive(aready);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+      if (lane == 0) red[e] = sq;
+      named_bar(1, kEpiWarps * 32);
+      if (et == 0 && P.mode == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < kEpiWarps; ++k) tot = __dadd_rn(tot, red[k]);
+        // combine the two halves in a fixed order, whichever CTA arrives second
+        P.part[2 * m + half] = tot;
+        __threadfence();
+        const uint32_t prev = atomicAdd(&P.cnt[m], 1u);
+        if (prev == 1u) {
+          __threadfence();
+          const double s2 = __dadd_rn(__ldcg(&P.part[2 * m]), __ldcg(&P.part[2 * m + 1]));
+          P.f[m] = (float)(s2 / ((double)kBatch * P.w[L]));
+          P.cnt[m] = 0u;
+        }
+      }
+      named_bar(1, kEpiWarps * 32);
+    }
+  } else {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16(128, 128);
+      int stage = 0;
+      uint32_t phase = 0, aphase = 0;
+      const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      for (int64_t m = pair; m < P.n; m += npair) {
+        for (int l = 1; l <= L; ++l) {
+          mbar_wait(aready, aphase);
+          aphase ^= 1;
+          tc_fence_after();
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+            const int nt = tile / kc_n, kc = tile % kc_n;
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t bs = b_base + stage * kStage32Bytes;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
+              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc(bs + ks * 32), idesc,
+                      (kc | ks) != 0);
+              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc(bs + kTileBytes + ks * 32), idesc,
+                      1u);
+            }
+            mma_commit(&empty[stage]);
+            if (kc == kc_n - 1) mma_commit(&dready[nt]);
+            if (++stage == kStages32) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProdWarps + kEpiWarps) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// U (DATA stream) → the layer-1 A images of the fp32-accurate kernel: for batch half h, rows
+// 0–63 = hi(U[64h + r]·2^8), rows 64–127 = lo (same pre-swizzled layout as mlp_uimg_kernel).
+__global__ void mlp_uimg32_kernel(uint64_t seed, int w0, int kpad0, __half* img) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;   // one thread per (half, row, 8-k chunk)
+  const int chunks = kpad0 / 8;
+  if (idx >= 2 * 64 * chunks) return;
+  const int hf = idx / (64 * chunks), r = (idx / chunks) % 64, cc = idx % chunks;
+  const Philox ph(seed);
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    const int k = cc * 8 + i;
+    if (k < w0) {
+      const float4 z = normal4(ph, (uint32_t)(k / 4), (uint32_t)(64 * hf + r), 0u, TAG_DATA);
+      v[i] = z.x; v[i + 1] = z.y; v[i + 2] = z.z; v[i + 3] = z.w;
+    } else {
+      v[i] = v[i + 1] = v[i + 2] = v[i + 3] = 0.f;
+    }
+  }
+  uint4 hi, lo;
+  split8(v, hi, lo);
+  const int kb = cc / 8, c = cc % 8;
+  uint8_t* base = reinterpret_cast<uint8_t*>(img) + (size_t)hf * (kpad0 / 64) * kTileBytes +
+                  kb * kTileBytes;
+  *reinterpret_cast<uint4*>(base + swz(r, c)) = hi;
+  *reinterpret_cast<uint4*>(base + swz(64 + r, c)) = lo;
+}
+
 // ---------------------------------------------------------------- problem setup kernels
 // U (DATA stream) → fp16 → the pre-swizzled layer-1 A image.
 __global__ void mlp_uimg_kernel(uint64_t seed, int w0, int kpad0, __half* img) {
@@ -465,6 +803,14 @@ static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
   }
   p.off[0] = 0;
   p.D = off;
+}
+
+static cudaError_t launch_mlp32(const MlpParams& p, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once((const void*)mlp32_kernel, kSmem32Bytes, attr)) return e;
+  const int pairs = (int)std::min<int64_t>(p.n, std::max(1, sm_count() / 2));
+  mlp32_kernel<<<2 * pairs, kThreads, kSmem32Bytes, st>>>(p);
+  return cudaGetLastError();
 }
 
 static cudaError_t launch_mlp(const MlpParams& p, cudaStream_t st) {
@@ -528,20 +874,57 @@ void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint6
     mlp_teacher_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(
         seed, l, widths[l - 1], widths[l], sc, pr->theta + p.off[l]);
   }
+  if ((e = cudaMalloc(&pr->uimg32, 2 * img)) != cudaSuccess ||
+      (e = cudaMalloc(&pr->Y32, (size_t)kBatch * widths[nw - 1] * sizeof(float))) != cudaSuccess) {
+    *err = std::string("allocation: ") + cudaGetErrorString(e);
+    mlp_problem_destroy(pr);
+    return nullptr;
+  }
+  {
+    const int n32 = 2 * 64 * (p.kpad[0] / 8);
+    mlp_uimg32_kernel<<<(n32 + 255) / 256, 256, 0, st>>>(seed, widths[0], p.kpad[0], pr->uimg32);
+  }
   pr->p.uimg = pr->uimg;
   pr->p.Y = pr->Y;
   pr->p.x16 = nullptr;
+  pr->p.uimg32[0] = pr->uimg32;
+  pr->p.uimg32[1] = pr->uimg32 + img / sizeof(__half);
+  pr->p.Y32 = pr->Y32;
+  pr->p.part = nullptr;
+  pr->p.cnt = nullptr;
   MlpParams q = pr->p;
   q.x = pr->theta;
   q.n = 1;
   q.f = nullptr;
-  q.mode = 1;                                   // write Y* = g_L(θ*)
-  if ((e = launch_mlp(q, st)) != cudaSuccess || (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+  q.mode = 1;                                   // write Y* = g_L(θ*) (both kernels)
+  if ((e = launch_mlp(q, st)) != cudaSuccess || (e = launch_mlp32(q, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess) {
     *err = std::string("teacher forward: ") + cudaGetErrorString(e);
     mlp_problem_destroy(pr);
     return nullptr;
   }
   return pr;
+}
+
+// per-member scratch of the fp32-accurate kernel (two half sums + a counter), grown on demand
+static cudaError_t mlp_reserve(MlpProblem* pr, int64_t n, cudaStream_t st) {
+  if (n <= pr->cap) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  cudaFree(pr->part);
+  cudaFree(pr->cnt);
+  pr->part = nullptr;
+  pr->cnt = nullptr;
+  pr->cap = 0;
+  if ((e = cudaMalloc(&pr->part, (size_t)n * 2 * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&pr->cnt, (size_t)n * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = cudaMemset(pr->cnt, 0, (size_t)n * sizeof(uint32_t))) != cudaSuccess) return e;
+  pr->cap = n;
+  return cudaSuccess;
+}
+
+cudaError_t mlp_problem_reserve(void* prob, int64_t n, cudaStream_t st) {
+  return mlp_reserve(static_cast<MlpProblem*>(prob), n, st);
 }
 
 void mlp_problem_destroy(void* prob) {
@@ -550,6 +933,10 @@ void mlp_problem_destroy(void* prob) {
   cudaFree(pr->uimg);
   cudaFree(pr->Y);
   cudaFree(pr->theta);
+  cudaFree(pr->uimg32);
+  cudaFree(pr->Y32);
+  cudaFree(pr->part);
+  cudaFree(pr->cnt);
   delete pr;
 }
 
@@ -557,7 +944,25 @@ int64_t mlp_problem_dims(const void* prob) {
   return prob ? static_cast<const MlpProblem*>(prob)->p.D : -1;
 }
 
+// N14 (the definition): the fp32-accurate kernel on the fp32 parameters.
 cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
+  if (n == 0) return cudaSuccess;
+  if (cudaError_t e = mlp_reserve(pr, n, st)) return e;
+  MlpParams q = pr->p;
+  q.x = x;
+  q.x16 = nullptr;
+  q.n = n;
+  q.f = f;
+  q.mode = 0;
+  q.part = pr->part;
+  q.cnt = pr->cnt;
+  return launch_mlp32(q, st);
+}
+
+// N14′ (the fp16-image approximation) on fp32 parameters: the producers round to binary16.
+cudaError_t launch_mlp_eval_f16(void* prob, const float* x, int64_t n, float* f, cudaStream_t st) {
   MlpProblem* pr = static_cast<MlpProblem*>(prob);
   if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
   MlpParams q = pr->p;
@@ -587,6 +992,7 @@ cudaError_t launch_mlp_eval16(void* prob, const __half* x16, int64_t n, float* f
 
 // es_get helpers for tests: teacher parameters and targets (device pointers).
 const float* mlp_problem_theta(const void* prob) { return static_cast<const MlpProblem*>(prob)->theta; }
-const float* mlp_problem_targets(const void* prob) { return static_cast<const MlpProblem*>(prob)->Y; }
+const float* mlp_problem_targets(const void* prob) { return static_cast<const MlpProblem*>(prob)->Y32; }
+const float* mlp_problem_targets_f16(const void* prob) { return static_cast<const MlpProblem*>(prob)->Y; }
 
 }  // namespace esb

@@ -177,8 +177,12 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
   }
 }
 
+// grid.y = the largest per-run chunk count; run r's entries [e0, e1) are cut into chunks of
+// `echunk` entries, nch_r = max(1, ⌈(e1 − e0)/echunk⌉) of them — so runs with few weighted entries
+// (Sep-CMA-ES elite ratios vmapped over runs) occupy few CTAs and the block scheduler packs
+// the SMs instead of one wave waiting on the longest runs. CTAs past nch_r exit at once.
 template <int ALGO>
-__global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nchunk, int fused) {
+__global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int echunk, int fused) {
   __shared__ uint32_t sdir[kTile];
   __shared__ double sA[kTile];
   __shared__ double sB[kTile];
@@ -193,8 +197,9 @@ __global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int nc
   const int ne = gs.nentries;
   int e0, e1;
   shard_range(ne, s.W, s.rank, e0, e1);
-  const int cper = (e1 - e0 + nchunk - 1) / nchunk;
-  const int c0 = min(e1, e0 + chunk * cper), c1 = min(e1, c0 + cper);
+  const int nchunk = max(1, (e1 - e0 + echunk - 1) / echunk);
+  if (chunk >= nchunk) return;
+  const int c0 = min(e1, e0 + chunk * echunk), c1 = min(e1, c0 + echunk);
   const Philox ph(s.rs[r].seed);
   const uint32_t t = gs.t;
   const uint32_t* dir = s.dir + (int64_t)r * s.N;
@@ -588,53 +593,77 @@ __global__ void __launch_bounds__(256) clipup_apply_kernel(DevState s) {
 
 int tell_blocks_per_run(const DevState& s) { return (int)((s.Q + TT - 1) / TT); }
 
-// Entry-range split: choose n minimising waves(n) · (entries/n + c0), waves(n) = ⌈blocks·n / slots⌉,
-// slots = resident CTAs of the kernel on all SMs, c0 ≈ the per-CTA fixed cost in entry-equivalents
-// (coefficient staging, partial write-back, last-CTA reduction).
+// Entry-chunk size: choose echunk minimising the estimated makespan of the tell grid. Each CTA costs
+// (its entries + c0) entry-times, c0 ≈ the per-CTA fixed cost (coefficient staging, partial
+// write-back, last-CTA reduction); `ent[r]` is run r's expected entry count on this rank (P, N, or
+// Sep-CMA-ES's μ_r). For grids up to 2^16 CTAs the makespan is simulated the way the block
+// scheduler dispatches (blockIdx.x fastest, each CTA onto the earliest-free of `slots` resident
+// slots); beyond that, waves(n) · (max entries/n + c0).
 template <int ALGO>
-static int pick_nchunk_t(const DevState& s) {
+static TellSplit pick_split_t(const DevState& s, const std::vector<int>& ent) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tell_kernel<ALGO>, TT, 0);
   occ = std::max(occ, 1);
   const int64_t slots = (int64_t)sm_count() * occ;
-  const int64_t blocks = (int64_t)s.R * tell_blocks_per_run(s);
-  int ent = (is_anti(s.algo) ? s.N / 2 : s.N);
-  ent = std::max(1, (ent + s.W - 1) / s.W);
-  const double c0 = 8.0;
-  int best = 1;
+  const int bpr = tell_blocks_per_run(s);
+  const int64_t blocks = (int64_t)s.R * bpr;
+  int emax = 1;
+  for (int e : ent) emax = std::max(emax, e);
+  const double c0 = 8.0, cempty = 0.25;
+  TellSplit best{1, emax};
   double best_t = 1e300;
-  for (int n = 1; n <= std::min(64, ent); ++n) {
-    const double waves = (double)((blocks * n + slots - 1) / slots);
-    const double tn = waves * ((double)ent / n + c0);
-    if (tn < best_t * 0.999) { best_t = tn; best = n; }
+  std::vector<double> heap;
+  for (int n = 1; n <= std::min(64, emax); ++n) {
+    const int ec = (emax + n - 1) / n;
+    if (n > 1 && (emax + ec - 1) / ec != n) continue;         // same echunk as a smaller n
+    double tn;
+    if (blocks * n <= 65536) {
+      heap.assign((size_t)slots, 0.0);                         // min-heap of slot free times
+      std::make_heap(heap.begin(), heap.end(), std::greater<double>());
+      for (int y = 0; y < n; ++y) {
+        for (int r = 0; r < s.R; ++r) {
+          const int nch = std::max(1, (ent[r] + ec - 1) / ec);
+          const double len = y < nch ? std::min(ec, ent[r] - y * ec) + c0 : cempty;
+          for (int b = 0; b < bpr; ++b) {
+            std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
+            heap.back() += len;
+            std::push_heap(heap.begin(), heap.end(), std::greater<double>());
+          }
+        }
+      }
+      tn = *std::max_element(heap.begin(), heap.end());
+    } else {
+      tn = (double)((blocks * n + slots - 1) / slots) * ((double)ec + c0);
+    }
+    if (tn < best_t * 0.999) { best_t = tn; best = TellSplit{n, ec}; }
   }
   return best;
 }
 
-int tell_pick_nchunk(const DevState& s) {
+TellSplit tell_pick_split(const DevState& s, const std::vector<int>& ent) {
   switch (s.algo) {
-    case OPENAI_ES: return pick_nchunk_t<OPENAI_ES>(s);
-    case PGPE: return pick_nchunk_t<PGPE>(s);
-    case SNES: return pick_nchunk_t<SNES>(s);
-    case ARS: return pick_nchunk_t<ARS>(s);
-    default: return pick_nchunk_t<SEP_CMA_ES>(s);
+    case OPENAI_ES: return pick_split_t<OPENAI_ES>(s, ent);
+    case PGPE: return pick_split_t<PGPE>(s, ent);
+    case SNES: return pick_split_t<SNES>(s, ent);
+    case ARS: return pick_split_t<ARS>(s, ent);
+    default: return pick_split_t<SEP_CMA_ES>(s, ent);
   }
 }
 
 template <int ALGO>
-static void launch_tell_t(const DevState& s, bool fused, int nchunk, cudaStream_t st) {
+static void launch_tell_t(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {
   const int bpr = tell_blocks_per_run(s);
-  dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
-  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, bpr, nchunk, fused ? 1 : 0);
+  dim3 grid((unsigned)(s.R * bpr), (unsigned)sp.nchunk);
+  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, bpr, sp.echunk, fused ? 1 : 0);
 }
 
-cudaError_t launch_tell_reduce(const DevState& s, bool fused, int nchunk, cudaStream_t st) {
+cudaError_t launch_tell_reduce(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {
   switch (s.algo) {
-    case OPENAI_ES: launch_tell_t<OPENAI_ES>(s, fused, nchunk, st); break;
-    case PGPE: launch_tell_t<PGPE>(s, fused, nchunk, st); break;
-    case SNES: launch_tell_t<SNES>(s, fused, nchunk, st); break;
-    case ARS: launch_tell_t<ARS>(s, fused, nchunk, st); break;
-    default: launch_tell_t<SEP_CMA_ES>(s, fused, nchunk, st); break;
+    case OPENAI_ES: launch_tell_t<OPENAI_ES>(s, fused, sp, st); break;
+    case PGPE: launch_tell_t<PGPE>(s, fused, sp, st); break;
+    case SNES: launch_tell_t<SNES>(s, fused, sp, st); break;
+    case ARS: launch_tell_t<ARS>(s, fused, sp, st); break;
+    default: launch_tell_t<SEP_CMA_ES>(s, fused, sp, st); break;
   }
   return cudaGetLastError();
 }

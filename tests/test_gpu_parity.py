@@ -413,41 +413,67 @@ def test_emulated_shards_match_single_gpu(algo, Wn):
 
 
 # ------------------------------------------------------------------------ MLP fitness (N14, tcgen05)
+def _mlp_population(m, n, seed):
+    theta = m.teacher()
+    rng = np.random.default_rng(seed)
+    scales = np.geomspace(1e-3, 0.5, n)
+    return theta, np.stack([theta + s * rng.standard_normal(m.D) for s in scales]).astype(np.float32)
+
+
 @pytest.mark.parametrize("widths,n", [([32, 64, 64, 64, 64, 16], 24), ([16, 32], 8),
                                       ([256, 512, 512, 512, 512, 128], 6),
-                                      ([96, 160, 48], 10)])
+                                      ([96, 160, 48], 10), ([48, 16, 32], 5)])
 def test_mlp_fitness_parity(widths, n):
+    """N14, the definition (fp32 parameters) on the fp32-accurate tcgen05 kernel
+    (binary16 hi/lo split, three products summed in TMEM): within the north star's 1e-5 of the
+    oracle's binary64 forward (Q24 metric over the population's fitness vector, and per member for
+    f >= 1e-3); f(theta*) = 0 exactly (the GPU's own teacher targets)."""
     from paper_2212_04180_b200 import strategy as S
     m = O.MLP(widths, 128, 7)
     es = S.Strategy(W.OPENAI_ES, 16, m.D, [W.run_params(W.OPENAI_ES, 1, init_min=-0.04,
                                                        init_max=0.04)])
     es.set_mlp_problem(widths, 128, 7)
-    theta = m.teacher()
+    theta, xs = _mlp_population(m, n, len(widths))
     f0 = es.eval(W.MLP, torch.from_numpy(theta[None]).cuda(), out=torch.empty(1, device="cuda"))
-    assert float(f0[0]) == 0.0           # GPU teacher stream and targets identical to the spec
-    rng = np.random.default_rng(len(widths))
-    scales = np.geomspace(1e-3, 0.5, n)
-    xs = np.stack([theta + s * rng.standard_normal(m.D) for s in scales]).astype(np.float32)
+    assert float(f0[0]) == 0.0
     got = es.eval(W.MLP, torch.from_numpy(xs).cuda(), out=torch.empty(n, device="cuda"))
     got = got.cpu().numpy().astype(np.float64)
-    ref = m.evaluate_f16(xs).astype(np.float64)
-    # DESIGN §3 / NUMERICS N14: the tensor cores accumulate in fp32, the oracle in binary64; the
-    # accumulation order flips rare fp16 roundings of activations. An fp32-vs-binary64 emulation of
-    # the same forward (numpy sgemm vs dgemm) differs by the same amounts (≤ 6e-5 relative at
-    # f ≈ 3e-3, ≤ 3e-6 at f ≈ 1), so the derived bar is Q24 ≤ 1e-4 over the population's fitness
-    # vector and 1e-5 relative for members with f ≥ 0.1.
-    assert q24(got, ref) <= 1e-4, (got, ref)
-    big = ref >= 1e-1
-    rel = np.abs(got[big] - ref[big]) / ref[big]
-    assert np.all(rel <= 1e-5), (rel, got, ref)
+    ref = m.evaluate(xs).astype(np.float64)
+    assert q24(got, ref) <= 1e-5, (got, ref)
+    big = ref >= 1e-3
+    assert np.all(np.abs(got[big] - ref[big]) <= 1e-5 * ref[big]), (got, ref)
+    es.close()
+
+
+@pytest.mark.parametrize("widths,n", [([32, 64, 64, 64, 64, 16], 24),
+                                      ([256, 512, 512, 512, 512, 128], 6)])
+def test_mlp16_approximation_bound(widths, n):
+    """ES_FIT_MLP16 (N14', the fp16 parameter image) is a labelled approximation: (i) within the
+    Q24 1e-4 of the oracle's model of it (binary16 operands, fp32 vs binary64 accumulation flips
+    rare fp16 activation roundings) and (ii) within its derived distance to the
+    definition, |f16 - f| <= |model - f| + 1e-4 |model| per member, both oracle-computed."""
+    from paper_2212_04180_b200 import strategy as S
+    m = O.MLP(widths, 128, 7)
+    es = S.Strategy(W.OPENAI_ES, 16, m.D, [W.run_params(W.OPENAI_ES, 1)])
+    es.set_mlp_problem(widths, 128, 7)
+    theta, xs = _mlp_population(m, n, len(widths) + 1)
+    f0 = es.eval(W.MLP16, torch.from_numpy(theta[None]).cuda(), out=torch.empty(1, device="cuda"))
+    assert float(f0[0]) == 0.0
+    got = es.eval(W.MLP16, torch.from_numpy(xs).cuda(), out=torch.empty(n, device="cuda"))
+    got = got.cpu().numpy().astype(np.float64)
+    model = m.evaluate_f16(xs).astype(np.float64)
+    ref = m.evaluate(xs).astype(np.float64)
+    assert q24(got, model) <= 1e-4, (got, model)
+    bound = np.abs(model - ref) + 1e-4 * np.maximum(np.abs(model), 2 ** -10 * np.abs(model).max())
+    assert np.all(np.abs(got - ref) <= bound), (got, ref, model)
     es.close()
 
 
 def test_mlp_openai_es_generations_teacher_forced():
-    """Config-4 path (the bench's fused es_ask_eval with the fp16 image) at SURVEY §8(d)'s reduced
-    size ([32, 64x4, 16], D = 15,632, N = 256) for 100 generations: ask bit-exact every
-    generation, MLP fitness within the derived 1e-4 (Q24) on sampled generations, tell fed the
-    GPU's fitness within 1e-5 after one generation and 1e-3 after 100."""
+    """Config-4 path (es_ask_eval with the fp32-accurate MLP) at SURVEY §8(d)'s reduced size
+    ([32, 64x4, 16], D = 15,632, N = 256) for 100 generations: ask bit-exact every generation, MLP
+    fitness within 1e-5 (Q24) of the oracle on sampled generations, tell fed the GPU's fitness
+    within 1e-5 after one generation and 1e-3 after 100."""
     from paper_2212_04180_b200 import strategy as S
     widths = [32, 64, 64, 64, 64, 16]
     m = O.MLP(widths, 128, 3)
@@ -459,8 +485,8 @@ def test_mlp_openai_es_generations_teacher_forced():
         xo = pair.orc[0].ask()
         assert np.array_equal(bits(x[0].cpu().numpy()), bits(xo)), g
         if g in (0, 50, 99):
-            fo = m.evaluate_f16(xo[:32])
-            assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-4, g
+            fo = m.evaluate(xo[:32])
+            assert q24(f[0, :32].cpu().numpy(), fo) <= 1e-5, g
         pair.gpu.tell(f)
         pair.orc[0].tell(f[0].cpu().numpy())
         if g == 0:
@@ -496,34 +522,41 @@ def test_ask_eval_fused(algo, fn, N, D):
 @pytest.mark.parametrize("widths,N", [([32, 64, 64, 64, 64, 16], 64),
                                       ([256, 512, 512, 512, 512, 128], 32), ([96, 160, 48], 16)])
 def test_mlp_fused_fp16_image_path(widths, N):
-    """N14′: es_ask_eval(ES_FIT_MLP) — ask writes the fp16 image, the TMA-fed tcgen05 kernel
-    evaluates it — gives x bit-identical to es_ask and fitness bit-identical to es_eval_bbob on
-    the fp32 population (with or without materialising x), and within the derived bar of the
-    oracle."""
+    """N14′: es_ask_eval(ES_FIT_MLP16) — ask writes the fp16 image, the TMA-fed tcgen05 kernel
+    evaluates it — gives x bit-identical to es_ask and fitness bit-identical to es_eval_bbob(MLP16)
+    on the fp32 population (with or without materialising x), and within the Q24 1e-4 of the
+    oracle's model of the approximation; es_ask_eval(ES_FIT_MLP) likewise equals es_eval_bbob(MLP)
+    bit for bit (x given or internal)."""
     from paper_2212_04180_b200 import strategy as S
     m = O.MLP(widths, 128, 5)
     params = [W.run_params(W.OPENAI_ES, 3, init_min=-0.04, init_max=0.04)]
     es = S.Strategy(W.OPENAI_ES, N, m.D, params)
     es.set_mlp_problem(widths, 128, 5)
-    x1, f1 = es.ask_eval(W.MLP)
-    _, f2 = es.ask_eval(W.MLP, write_x=False)
+    x1, f1 = es.ask_eval(W.MLP16)
+    _, f2 = es.ask_eval(W.MLP16, write_x=False)
     x0 = es.ask()
-    f0 = es.eval(W.MLP, x0)
+    f0 = es.eval(W.MLP16, x0)
     assert torch.equal(x1, x0)
     assert np.array_equal(bits(f1.cpu().numpy()), bits(f0.cpu().numpy()))
     assert np.array_equal(bits(f2.cpu().numpy()), bits(f0.cpu().numpy()))
     ref = m.evaluate_f16(x0[0].cpu().numpy())
     assert q24(f1[0].cpu().numpy(), ref) <= 1e-4
-    es.tell(f1)
+    x3, f3 = es.ask_eval(W.MLP)
+    _, f4 = es.ask_eval(W.MLP, write_x=False)
+    f5 = es.eval(W.MLP, x0)
+    assert torch.equal(x3, x0)
+    assert np.array_equal(bits(f3.cpu().numpy()), bits(f5.cpu().numpy()))
+    assert np.array_equal(bits(f4.cpu().numpy()), bits(f5.cpu().numpy()))
+    es.tell(f3)
     es.close()
 
 
 def test_config4_full_size_sampled_members():
-    """C4 in the launch configuration bench.py times (es_ask_eval, the fp16 image and the TMA-fed
-    tcgen05 MLP, N = 4096, D = 985,216): the oracle's MLP fitness of sampled members (first, last,
-    both members of a middle pair) within the derived bar; the fp16 image of those members equals
-    fp16 of the oracle's x; one tell then moves sampled dims of the mean exactly as the oracle's
-    dimension-subset run fed the GPU's fitness."""
+    """C4 in the launch configuration bench.py times (es_ask_eval with the fp32-accurate tcgen05
+    MLP, N = 4096, D = 985,216): the oracle's MLP fitness (the definition) of sampled members
+    (first, last, both members of a middle pair) within 1e-5; the fp16-image approximation of the
+    same members within its model's 1e-4; one tell then moves sampled dims of the mean exactly as
+    the oracle's dimension-subset run fed the GPU's fitness."""
     from paper_2212_04180_b200 import strategy as S
     widths = [256, 512, 512, 512, 512, 128]
     cfg = W.CONFIGS["c4"]
@@ -532,13 +565,16 @@ def test_config4_full_size_sampled_members():
     params = [W.config_params(cfg, 0)]
     es = S.Strategy(W.OPENAI_ES, cfg["N"], cfg["D"], params)
     es.set_mlp_problem(widths, 128, 0)
+    _, f16 = es.ask_eval(W.MLP16, write_x=False)
     _, f = es.ask_eval(W.MLP, write_x=False)
-    fh = f.cpu().numpy()[0]
+    fh, fh16 = f.cpu().numpy()[0], f16.cpu().numpy()[0]
     run = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], **params[0])
     for j in (0, 2048, 2049, cfg["N"] - 1):
         xo = run.member(j)
-        fo = m.evaluate_f16(xo)[0]
-        assert abs(float(fh[j]) - float(fo)) <= 1e-5 * max(abs(float(fo)), 0.1), (j, fh[j], fo)
+        fo = m.evaluate(xo)[0]
+        assert abs(float(fh[j]) - float(fo)) <= 1e-5 * abs(float(fo)), (j, fh[j], fo)
+        fm = m.evaluate_f16(xo)[0]
+        assert abs(float(fh16[j]) - float(fm)) <= 1e-4 * abs(float(fm)), (j, fh16[j], fm)
     dims = np.sort(np.random.default_rng(3).choice(cfg["D"], 64, replace=False))
     sub = O.Run(W.OPENAI_ES, cfg["N"], cfg["D"], dims=dims, **params[0])
     es.tell(f)

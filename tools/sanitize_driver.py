@@ -106,6 +106,11 @@ def mlp():
     es.tell(es.eval(W.MLP, es.ask()))
     x, f = es.ask_eval(W.MLP)
     es.tell(f)
+    es.tell(es.eval(W.MLP16, es.ask()))
+    x, f = es.ask_eval(W.MLP16)
+    es.tell(f)
+    _, f = es.ask_eval(W.MLP, write_x=False)
+    es.tell(f)
     done(es)
 
 

@@ -12,8 +12,8 @@ OPENAI_ES, PGPE, SNES, SEP_CMA_ES, ARS, CMA_ES = 0, 1, 2, 3, 4, 5
 ALGO_NAMES = {OPENAI_ES: "openai_es", PGPE: "pgpe", SNES: "snes", SEP_CMA_ES: "sep_cma_es",
               ARS: "ars", CMA_ES: "cma_es"}
 ADAM, SGD, CLIPUP = 0, 1, 2
-SPHERE, ROSENBROCK, RASTRIGIN, MLP = 0, 1, 2, 3
-FN_NAMES = {SPHERE: "sphere", ROSENBROCK: "rosenbrock", RASTRIGIN: "rastrigin", MLP: "mlp"}
+SPHERE, ROSENBROCK, RASTRIGIN, MLP, MLP16 = 0, 1, 2, 3, 4
+FN_NAMES = {SPHERE: "sphere", ROSENBROCK: "rosenbrock", RASTRIGIN: "rastrigin", MLP: "mlp", MLP16: "mlp16"}
 
 # PAPER.md Appendix B, "Ant" column.
 ANT = {
