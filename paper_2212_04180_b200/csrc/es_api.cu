@@ -273,6 +273,8 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     while (npad < N) npad <<= 1;
     s.gkeys = nullptr;
     if (npad > 16384) TRY(dalloc(c, (void**)&s.gkeys, (size_t)R * npad * sizeof(uint64_t)));
+    TRY(dalloc(c, (void**)&s.rcnt, RN * sizeof(uint32_t)));
+    TRY(cudaMemsetAsync(s.rcnt, 0, RN * sizeof(uint32_t), st));
   }
   if (W > 1) TRY(dalloc(c, (void**)&c->fgather, RN * sizeof(float)));
   // per-run scalars and weight tables, computed on the host in binary64
@@ -454,12 +456,11 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
     return ES_SUCCESS;
   }
   if (fn == ES_FIT_MLP) {
-    // N14: the ask writes x (into the internal buffer when x is NULL), the fp32-accurate MLP reads it
-    float* xd = x;
-    if (!xd) {
-      if (!c->xstage) CUDA_OR(c, dalloc(c, (void**)&c->xstage, nloc * s.Dx * sizeof(float)));
-      xd = c->xstage;
-    }
+    // N14: the ask writes the split image (and x unless NULL); the fp32-accurate MLP streams the
+    // image's two binary16 planes with TMA
+    if (s.Dx % 4) return fail(c, ES_ERR_UNSUPPORTED, "MLP fitness needs D % 4 == 0");
+    __half* img = mlp_problem_image(c->mlp, (int64_t)nloc, st);
+    if (!img) return fail(c, ES_ERR_OOM, "MLP split image of %zu members", nloc);
     float* fd = f;
     const bool fh = !is_device_ptr(f);
     if (fh) {
@@ -467,12 +468,12 @@ es_status_t es_ask_eval(es_ctx_t* c, es_fitness_t fn, float* x, float* f, es_str
       fd = c->fstage;
     }
     {
-      ProfScope ps(c, "ask", st);
-      CUDA_OR(c, launch_ask(s, xd, st));
+      ProfScope ps(c, "ask32", st);
+      CUDA_OR(c, launch_ask_split(s, x, img, st));
     }
     {
       ProfScope ps(c, "eval_mlp", st);
-      CUDA_OR(c, launch_mlp_eval(c->mlp, xd, (int64_t)nloc, fd, st));
+      CUDA_OR(c, launch_mlp_eval_img(c->mlp, (int64_t)nloc, fd, st));
     }
     c->launches += 2;
     if (fh) {

@@ -20,6 +20,9 @@ namespace esb {
 cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
 cudaError_t launch_mlp_eval_f16(void* prob, const float* x, int64_t n, float* f, cudaStream_t st);
 cudaError_t mlp_problem_reserve(void* prob, int64_t n, cudaStream_t st);
+__half* mlp_problem_image(void* prob, int64_t n, cudaStream_t st);
+cudaError_t launch_mlp_eval_img(void* prob, int64_t n, float* f, cudaStream_t st);
+cudaError_t launch_ask_split(const DevState& s, float* x, __half* img, cudaStream_t st);
 inline bool is_mlp(int fn) { return fn == ES_FIT_MLP || fn == ES_FIT_MLP16; }
 void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint64_t seed,
                          cudaStream_t st, std::string* err);

@@ -87,6 +87,7 @@ struct DevState {
   uint32_t* arrive;    // [R][blocks_per_run] last-block counters
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
   uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
+  uint32_t* rcnt;      // [R][N] counting-rank positions (few runs), zero between tells
   int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
   double* n2;          // [R] D-shard Sep-CMA ‖p_σ'‖² share, summed over ranks before the finish
   // full-covariance CMA-ES (f4)

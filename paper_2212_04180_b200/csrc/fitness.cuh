@@ -2,8 +2,7 @@
 // evaluation kernel (k_eval.cu) and the fused ask+evaluate kernel (k_ask_eval.cu).
 // Binary64 accumulation; Sphere uses exact-product DFMAs (= the oracle's mul-then-add), Rastrigin
 // accumulates Σx² and ΣS² separately and combines them once as Σx² + 20·ΣS² (N7). The binary32 →
-// binary64 converts of S and |x| are bit assemblies on the FMA pipe, the floor an exact FADD
-// sequence: no XU-pipe instruction per element.
+// binary64 converts of S and |x| are bit assemblies on the FMA pipe; the floor stays on the XU.
 #pragma once
 #include "noise.cuh"
 
@@ -41,14 +40,12 @@ __device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has
   } else if (FN == FN_ROSENBROCK) {
     if (has_next) acc.a = __dadd_rn(acc.a, rosen_term(x, xn));
   } else {
-    // No XU-pipe instruction per element (the kernel was XU-bound on FRND + F2F.F64.F32):
-    // floor(|x|) for |x| < 2^23 by the 2^23 round-to-integer trick and a one-step correction
-    // (every operation exact), |x| ≥ 2^23 is an integer (fr = |x| − |x| = 0, NaN for inf, as
-    // the oracle's floorf path); (double)|x| by bit assembly as S. Both terms are the oracle's.
+    // One XU-pipe instruction per element (FRND for the floor); (double)|x| and (double)S are
+    // bit assemblies on the FMA pipe. (Both converts on the XU made the kernel XU-bound; moving
+    // the floor off the XU as well — an exact 2^23-shifter FADD sequence — made it issue-bound and
+    // slower: 114 → 138 µs at C2.)
     const float ab = fabsf(x);
-    float fl = __fsub_rn(__fadd_rn(ab, 0x1p23f), 0x1p23f);
-    fl = fl > ab ? __fsub_rn(fl, 1.0f) : fl;
-    const float fr = ab < 0x1p23f ? __fsub_rn(ab, fl) : __fsub_rn(ab, ab);
+    const float fr = __fsub_rn(ab, floorf(ab));
     const double S = pos_f2d(sinpi_half(fminf(fr, __fsub_rn(1.0f, fr))));   // S ∈ [0, 1]
     const double d = pos_f2d(ab);
     acc.a = __fma_rn(d, d, acc.a);

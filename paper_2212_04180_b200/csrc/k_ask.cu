@@ -60,10 +60,38 @@ __device__ __forceinline__ float ask_scale(const DevState& s, const RunScal& rs,
   return __fmul_rn(rs.sigma, __fsqrt_rn(s.vec[F_C][idx]));
 }
 
-// W16: also write fp16(x) into x16 (N14′, the MLP fitness's parameter image); x may be NULL then.
+// IMG 1: also write fp16(x) into x16 (N14′, the MLP fitness's parameter image); IMG 2: write the
+// split image of N14 — plane 0 fp16(x·2^8), plane 1 fp16(x·2^8 − hi), planes R·Nloc·D apart (the
+// fp32-accurate MLP's operands). x may be NULL with an image.
 // CLIP: clamp the members into the run's box [clip_lo, clip_hi] (the z the tell regenerates
 // is unclipped). Instantiated only when some run has bounds.
-template <int ALGO, bool V4, bool W16, bool CLIP>
+__device__ __forceinline__ void store_img(__half* h, const float* v, int mode, int64_t plane) {
+  if (mode == 1) {
+    __half2 a0 = __floats2half2_rn(v[0], v[1]), a1 = __floats2half2_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a0);
+    u.y = *reinterpret_cast<uint32_t*>(&a1);
+    __stcs(reinterpret_cast<uint2*>(h), u);
+  } else {
+    float sc[4], r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sc[k] = __fmul_rn(v[k], 256.0f);
+    __half2 a0 = __floats2half2_rn(sc[0], sc[1]), a1 = __floats2half2_rn(sc[2], sc[3]);
+    const float2 b0 = __half22float2(a0), b1 = __half22float2(a1);
+    r[0] = __fsub_rn(sc[0], b0.x); r[1] = __fsub_rn(sc[1], b0.y);
+    r[2] = __fsub_rn(sc[2], b1.x); r[3] = __fsub_rn(sc[3], b1.y);
+    __half2 c0 = __floats2half2_rn(r[0], r[1]), c1 = __floats2half2_rn(r[2], r[3]);
+    uint2 u, w;
+    u.x = *reinterpret_cast<uint32_t*>(&a0);
+    u.y = *reinterpret_cast<uint32_t*>(&a1);
+    w.x = *reinterpret_cast<uint32_t*>(&c0);
+    w.y = *reinterpret_cast<uint32_t*>(&c1);
+    __stcs(reinterpret_cast<uint2*>(h), u);
+    __stcs(reinterpret_cast<uint2*>(h + plane), w);
+  }
+}
+
+template <int ALGO, bool V4, int IMG, bool CLIP>
 __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
                                                            __half* __restrict__ x16, int bpr,
                                                            int dpt) {
@@ -92,9 +120,10 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   const int64_t step = (kAnti ? 2 : 1) * s.Dx;
   const int64_t first = (int64_t)r * s.Nloc * s.Dx + 4 * q + (int64_t)i0 * step;
   float* p0 = x ? x + first : nullptr;
-  __half* h0 = W16 ? x16 + first : nullptr;
+  __half* h0 = IMG ? x16 + first : nullptr;
+  const int64_t plane = (int64_t)s.R * s.Nloc * s.Dx;     // IMG 2: hi → lo plane distance
 #pragma unroll 4
-  for (int il = i0; il < i1; ++il, p0 += (x ? step : 0), h0 += (W16 ? step : 0)) {
+  for (int il = i0; il < i1; ++il, p0 += (x ? step : 0), h0 += (IMG ? step : 0)) {
     const float4 z = normal4(ph, (uint32_t)(q + s.q0), (uint32_t)(dir0 + il), t);
     const float zz[4] = {z.x, z.y, z.z, z.w};
     float xp[4], xm[4];
@@ -107,18 +136,9 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
         if (kAnti) xm[k] = fminf(fmaxf(xm[k], lo), hi);
       }
     }
-    if (W16) {            // D % 4 == 0 is required for this path (8-byte stores)
-      __half2 a0 = __floats2half2_rn(xp[0], xp[1]), a1 = __floats2half2_rn(xp[2], xp[3]);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&a0);
-      u.y = *reinterpret_cast<uint32_t*>(&a1);
-      __stcs(reinterpret_cast<uint2*>(h0), u);
-      if (kAnti) {
-        __half2 b0 = __floats2half2_rn(xm[0], xm[1]), b1 = __floats2half2_rn(xm[2], xm[3]);
-        u.x = *reinterpret_cast<uint32_t*>(&b0);
-        u.y = *reinterpret_cast<uint32_t*>(&b1);
-        __stcs(reinterpret_cast<uint2*>(h0 + s.Dx), u);
-      }
+    if (IMG) {            // D % 4 == 0 is required for this path (8-byte stores)
+      store_img(h0, xp, IMG, plane);
+      if (kAnti) store_img(h0 + s.Dx, xm, IMG, plane);
       if (!p0) continue;
     }
     if (V4) {
@@ -138,7 +158,7 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
 }
 
 template <int ALGO, bool CLIP>
-static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaStream_t st) {
+static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, int img, cudaStream_t st) {
   constexpr bool kAnti = is_anti(ALGO);
   const int Ploc = kAnti ? s.Nloc / 2 : s.Nloc;
   const int bpr = (int)((s.Qx + kAskThreads - 1) / kAskThreads);
@@ -151,29 +171,38 @@ static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, cudaSt
   const int dpt = (Ploc + nchunk - 1) / nchunk;
   nchunk = (Ploc + dpt - 1) / dpt;
   dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
+  if (x16 && img == 2) {
+    ask_kernel<ALGO, true, 2, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
+    return cudaGetLastError();
+  }
   if (x16) {
-    ask_kernel<ALGO, true, true, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
+    ask_kernel<ALGO, true, 1, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
     return cudaGetLastError();
   }
   const bool v4 = (s.Dx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if (v4) ask_kernel<ALGO, true, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
-  else ask_kernel<ALGO, false, false, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
+  if (v4) ask_kernel<ALGO, true, 0, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
+  else ask_kernel<ALGO, false, 0, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
   return cudaGetLastError();
 }
 
 template <bool CLIP>
-static cudaError_t launch_ask_c(const DevState& s, float* x, __half* x16, cudaStream_t st) {
+static cudaError_t launch_ask_c(const DevState& s, float* x, __half* x16, int img, cudaStream_t st) {
   switch (s.algo) {
-    case OPENAI_ES: return launch_ask_t<OPENAI_ES, CLIP>(s, x, x16, st);
-    case PGPE: return launch_ask_t<PGPE, CLIP>(s, x, x16, st);
-    case SNES: return launch_ask_t<SNES, CLIP>(s, x, x16, st);
-    case ARS: return launch_ask_t<ARS, CLIP>(s, x, x16, st);
-    default: return launch_ask_t<SEP_CMA_ES, CLIP>(s, x, x16, st);
+    case OPENAI_ES: return launch_ask_t<OPENAI_ES, CLIP>(s, x, x16, img, st);
+    case PGPE: return launch_ask_t<PGPE, CLIP>(s, x, x16, img, st);
+    case SNES: return launch_ask_t<SNES, CLIP>(s, x, x16, img, st);
+    case ARS: return launch_ask_t<ARS, CLIP>(s, x, x16, img, st);
+    default: return launch_ask_t<SEP_CMA_ES, CLIP>(s, x, x16, img, st);
   }
 }
 
 cudaError_t launch_ask16(const DevState& s, float* x, __half* x16, cudaStream_t st) {
-  return s.any_clip ? launch_ask_c<true>(s, x, x16, st) : launch_ask_c<false>(s, x, x16, st);
+  return s.any_clip ? launch_ask_c<true>(s, x, x16, 1, st) : launch_ask_c<false>(s, x, x16, 1, st);
+}
+
+// N14 split image (plane distance R·Nloc·D), x optional
+cudaError_t launch_ask_split(const DevState& s, float* x, __half* img, cudaStream_t st) {
+  return s.any_clip ? launch_ask_c<true>(s, x, img, 2, st) : launch_ask_c<false>(s, x, img, 2, st);
 }
 
 cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {

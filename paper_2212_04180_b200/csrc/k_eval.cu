@@ -17,15 +17,29 @@ __device__ __forceinline__ double row_partial(const float* __restrict__ row, int
                                               int64_t lane0, int64_t stride) {
   FitAcc acc;
   if (V4) {
+    // kU float4 loads issued before any is consumed (the loop was load-latency bound: one
+    // 16-byte load in flight per thread); the accumulation order per thread is unchanged
+    constexpr int kU = 4;
     const int64_t Q = D / 4;
-    for (int64_t q = lane0; q < Q; q += stride) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
-      const bool nn = (FN == FN_ROSENBROCK) && (4 * q + 4 < D);
-      const float nx = (FN == FN_ROSENBROCK && nn) ? __ldg(row + 4 * q + 4) : 0.0f;
-      fit_add<FN>(acc, v.x, v.y, true);
-      fit_add<FN>(acc, v.y, v.z, true);
-      fit_add<FN>(acc, v.z, v.w, true);
-      fit_add<FN>(acc, v.w, nx, nn);
+    for (int64_t q0 = lane0; q0 < Q; q0 += kU * stride) {
+      float4 v[kU];
+      float nx[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t q = q0 + u * stride;
+        v[u] = q < Q ? __ldcs(reinterpret_cast<const float4*>(row) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        nx[u] = (FN == FN_ROSENBROCK && 4 * q + 4 < D) ? __ldg(row + 4 * q + 4) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t q = q0 + u * stride;
+        if (q >= Q) break;
+        const bool nn = (FN == FN_ROSENBROCK) && (4 * q + 4 < D);
+        fit_add<FN>(acc, v[u].x, v[u].y, true);
+        fit_add<FN>(acc, v[u].y, v[u].z, true);
+        fit_add<FN>(acc, v[u].z, v[u].w, true);
+        fit_add<FN>(acc, v[u].w, nx[u], nn);
+      }
     }
   } else {
     for (int64_t d = lane0; d < D; d += stride) {

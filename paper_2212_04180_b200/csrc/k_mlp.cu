@@ -57,6 +57,8 @@ struct MlpParams {
   // fp32-accurate kernel (N14): per batch half, the layer-1 A image of the scaled hi/lo split of U
   const __half* uimg32[2];
   float* Y32;                   // [128][w_L] teacher outputs of the fp32-accurate kernel
+  const __half* img;            // split image [2][n][D] (hi plane, lo plane); biases read here
+  CUtensorMap tmap32[2][kMaxLayers + 1];   // per plane (hi, lo) and layer: [128 n × 32 k] tiles
   double* part;                 // [n][2] per-half squared-error sums
   uint32_t* cnt;                // [n] arrival counters (zero between launches)
 };
@@ -70,7 +72,8 @@ struct MlpProblem {
   float* Y32 = nullptr;
   double* part = nullptr;
   uint32_t* cnt = nullptr;
-  int64_t cap = 0;              // members part/cnt can hold
+  __half* img = nullptr;        // split image [2][cap][D] (hi, lo planes of x·2^8)
+  int64_t cap = 0;              // members part/cnt/img can hold
 };
 
 
@@ -427,14 +430,20 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 // its absolute error is ≤ 2^-33). D = Σ_k A·W with A = [A_hi; A_lo] stacked as the 128 MMA rows
 // (64 batch rows per CTA) and W = W_hi + W_lo accumulated into the same TMEM columns:
 // row b of D + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b] to fp32 accuracy.
-// Two CTAs per member (batch rows 0–63 and 64–127); each streams the member's weights (the pair's
-// second read is an L2 hit) and the pair's squared-error halves are combined in a fixed order by
-// whichever CTA finishes second. Warp roles as mlp_kernel; the epilogue's lane quarters 2–3 (the lo
-// rows) hand their accumulator to quarters 0–1 through shared memory.
-static constexpr int kStages32 = 2;
-static constexpr int kStage32Bytes = 2 * kTileBytes;            // hi tile + lo tile
-static constexpr int kXbufBytes = 8 * 32 * 32 * 4;               // 8 warp pairs × 32 lanes × 32 cols
+// The weights arrive as the population's split image — two binary16 planes [2][n][D] written by
+// the ask kernel (or by mlp_split_kernel from an fp32 x) — through TMA (one producer thread,
+// [128 n × 32 k] SWIZZLE_64B tiles of both planes per stage, an L2 prefetch look-ahead), so the
+// weight stream needs no producer registers. Two CTAs per member (batch rows 0–63 and 64–127); each
+// streams the member's weights (the pair's second read is an L2 hit) and the pair's squared-error
+// halves are combined in a fixed order by whichever CTA finishes second. The epilogue's lane
+// quarters 2–3 (the lo rows) hand their accumulator to quarters 0–1 through shared memory, 8
+// columns per round in two ping-pong buffers.
+static constexpr int kStages32 = 5;
+static constexpr int kT32Bytes = 128 * 64;                       // [128 n × 32 k] fp16 = 8 KB
+static constexpr int kStage32Bytes = 2 * kT32Bytes;              // hi tile + lo tile
+static constexpr int kXbufBytes = 8 * 2 * 32 * 8 * 4;            // 8 pairs × 2 bufs × 32 × 8 cols
 static constexpr int kSmem32Bytes = kABytes + kStages32 * kStage32Bytes + kXbufBytes + 1024;
+static constexpr int kThreads32 = (1 + kEpiWarps + 1) * 32;
 static constexpr float kSplitScale = 256.0f, kUnscale = 1.0f / 65536.0f;
 
 // hi / lo binary16 parts of 8 scaled values
@@ -449,10 +458,22 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   lo = pack8(r);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constant__ MlpParams P) {
+// UMMA shared-memory descriptor, K-major SWIZZLE_64B (64-byte rows, 8-row groups of 512 B).
+__device__ __forceinline__ uint64_t smem_desc64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads32, 1)
+    mlp32_kernel(const __grid_constant__ MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                              // [8][128 rows][64] fp16
-  uint8_t* Bst = smem + kABytes;                                  // [2][hi, lo][128][64] fp16
+  uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][128][32] fp16
   float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
                                                kXbufBytes);
@@ -470,14 +491,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages32; ++s) {
-      mbar_init(&full[s], kProdWarps);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
     mbar_init(aready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProdWarps + kEpiWarps) {
+  if (warp == 1 + kEpiWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -488,86 +509,63 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
   const uint32_t tmem = *tmem_slot;
   const int L = P.nl;
 
-  if (warp < kProdWarps) {
-    // ------------------------------------------------------------ producers: fp32 W → hi, lo
-    const int t = threadIdx.x;
-    int stage = 0;
-    uint32_t phase = 0;
-    auto block_of = [&](int64_t m, int l, int nt, const float** ptr, uint32_t* bytes) {
-      const int in = P.w[l - 1], out = P.w[l];
-      const int rows = min(128, out - nt * 128);
-      *ptr = P.x + m * P.D + P.off[l] + (int64_t)nt * 128 * in;
-      *bytes = rows > 0 ? (uint32_t)rows * in * 4u : 0u;
-    };
-    auto prefetch_block = [&](int64_t m, int l, int nt) {
-      if (++nt >= (P.npad[l] >> 7)) { nt = 0; if (++l > L) { l = 1; m += npair; } }
-      if (m >= P.n) return;
-      const float* ptr;
-      uint32_t bytes;
-      block_of(m, l, nt, &ptr, &bytes);
-      for (uint32_t o = lane * 8192u; o < bytes; o += 32 * 8192u)
-        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(8192u, bytes - o));
-    };
-    if (warp == 0 && pair < P.n) {
-      const float* ptr;
-      uint32_t bytes;
-      block_of(pair, 1, 0, &ptr, &bytes);
-      for (uint32_t o = lane * 8192u; o < bytes; o += 32 * 8192u)
-        prefetch_l2(reinterpret_cast<const char*>(ptr) + o, min(8192u, bytes - o));
-    }
-    for (int64_t m = pair; m < P.n; m += npair) {
-      const float* xm = P.x + m * P.D;
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (split image)
+    if (lane == 0) {
       for (int l = 1; l <= L; ++l) {
-        const int in = P.w[l - 1], out = P.w[l];
-        const float* W = xm + P.off[l];
-        const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
-        for (int tile = 0; tile < nt_n * kc_n; ++tile) {
-          const int nt = tile / kc_n, kc = tile % kc_n;
-          if (kc == 0 && warp == 0 && half == 0) prefetch_block(m, l, nt);
-          mbar_wait(&empty[stage], phase ^ 1);
-          float4 v[8];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
-            const int n = nt * 128 + r, k = kc * 64 + c * 8;
-            if (n < out && k < in) {
-              const float4* src = reinterpret_cast<const float4*>(W + (int64_t)n * in + k);
-              v[2 * j] = __ldg(src);
-              v[2 * j + 1] = __ldg(src + 1);
-            } else {
-              v[2 * j] = v[2 * j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[0][l])));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[1][l])));
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      // L2 look-ahead over the (member, layer, n-tile, k-chunk) stream: issued by one CTA of the
+      // pair only (both read the same tiles)
+      constexpr int kAhead = 24;
+      int64_t pm = pair;
+      int pl = 1, pt = 0;
+      auto ahead = [&]() {
+        if (half != 0 || pm >= P.n) return;
+        const int kcn = P.kpad[pl - 1] >> 5;
+        tma_prefetch_3d(&P.tmap32[0][pl], (pt % kcn) * 32, (pt / kcn) * 128, (int)pm);
+        tma_prefetch_3d(&P.tmap32[1][pl], (pt % kcn) * 32, (pt / kcn) * 128, (int)pm);
+        if (++pt == (P.npad[pl] >> 7) * kcn) {
+          pt = 0;
+          if (++pl > L) { pl = 1; pm += npair; }
+        }
+      };
+      for (int k = 0; k < kAhead; ++k) ahead();
+      for (int64_t m = pair; m < P.n; m += npair) {
+        for (int l = 1; l <= L; ++l) {
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
+          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
+            const int nt = tile / kc_n, kc = tile % kc_n;
+            ahead();
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], kStage32Bytes);
+            uint8_t* dst = Bst + stage * kStage32Bytes;
+            tma_load_3d(dst, &P.tmap32[0][l], kc * 32, nt * 128, (int)m, &full[stage]);
+            tma_load_3d(dst + kT32Bytes, &P.tmap32[1][l], kc * 32, nt * 128, (int)m, &full[stage]);
+            if (++stage == kStages32) { stage = 0; phase ^= 1; }
           }
-          uint8_t* dst = Bst + stage * kStage32Bytes;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ch = t + 256 * j, r = ch >> 3, c = ch & 7;
-            const float e[8] = {v[2 * j].x, v[2 * j].y, v[2 * j].z, v[2 * j].w,
-                                v[2 * j + 1].x, v[2 * j + 1].y, v[2 * j + 1].z, v[2 * j + 1].w};
-            uint4 hi, lo;
-            split8(e, hi, lo);
-            *reinterpret_cast<uint4*>(dst + swz(r, c)) = hi;
-            *reinterpret_cast<uint4*>(dst + kTileBytes + swz(r, c)) = lo;
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[stage]);
-          if (++stage == kStages32) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp < kProdWarps + kEpiWarps) {
+    __syncwarp();
+  } else if (warp < 1 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - kProdWarps;                 // 0..15
+    const int e = warp - 1;                          // 0..15
     const int q = warp & 3, part = e >> 2;           // TMEM lane quarter, 32-column quarter
     const bool hiw = q < 2;                          // lanes 0–63: the A_hi rows (and the result)
-    const int pr = part * 2 + (q & 1);               // warp pair (hi warp q, lo warp q + 2)
-    float* xb = xbuf + pr * 32 * 32;                 // [col][lane]
+    const int pr = e & 7;                            // warp pair: e and e ^ 2 share (q & 1, part)
+    const int prid = (part * 2 + (q & 1));           // named barrier of the pair
+    float* xb = xbuf + prid * (2 * 32 * 8);          // [2 bufs][8 cols][32 lanes]
+    (void)pr;
     const int brow = half * 64 + (q & 1) * 32 + lane;   // batch row of this lane
-    const int et = threadIdx.x - kProdWarps * 32;    // 0..511
+    const int et = threadIdx.x - 32;                 // 0..511
     uint32_t dphase = 0;
     for (int64_t m = pair; m < P.n; m += npair) {
-      const float* xm = P.x + m * P.D;
+      const __half* bhi = P.img + m * P.D;             // this member's hi / lo planes
+      const __half* blo = P.img + (P.n + m) * P.D;
       {
         const int bytes = (P.kpad[0] >> 6) * kTileBytes;
         const uint4* src = reinterpret_cast<const uint4*>(P.uimg32[half]);
@@ -580,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
       double sq = 0.0;
       for (int l = 1; l <= L; ++l) {
         const int in = P.w[l - 1], out = P.w[l];
-        const float* bias = xm + P.off[l] + (int64_t)out * in;
+        const int64_t boff = P.off[l] + (int64_t)out * in;   // b_l inside the layer block
         const int ntl = P.npad[l] >> 7;
         const int cend = l < L ? P.kpad[l] : out;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -591,21 +589,33 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
           if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
           float v[32];
           tmem_ld32(trow + (uint32_t)c0, v);
-          if (!hiw) {
+          // lo rows → hi rows, 8 columns per round through two ping-pong buffers
 #pragma unroll
-            for (int i = 0; i < 32; ++i) xb[i * 32 + lane] = v[i];
-            named_bar(2 + pr, 64);
-            named_bar(2 + pr, 64);                   // the hi warp has consumed xb
-            continue;
+          for (int rr = 0; rr < 4; ++rr) {
+            float* b = xb + (rr & 1) * (32 * 8);
+            if (!hiw) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) b[i * 32 + lane] = v[8 * rr + i];
+            }
+            named_bar(2 + prid, 64);
+            if (hiw) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * rr + i] = __fadd_rn(v[8 * rr + i], b[i * 32 + lane]);
+            }
           }
-          named_bar(2 + pr, 64);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(v[i], xb[i * 32 + lane]);
-          named_bar(2 + pr, 64);
+          named_bar(2 + prid, 64);                   // buffers free for the next chunk
+          if (!hiw) continue;
+          // b = (hi + lo)·2^-8 (the sum is exact in fp32: ≤ 22 significant bits)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int n = c0 + i;
-            v[i] = n < out ? tanhf(__fadd_rn(__fmul_rn(v[i], kUnscale), __ldg(bias + n))) : 0.0f;
+            if (n < out) {
+              const float b = __fmul_rn(__fadd_rn(__half2float(bhi[boff + n]),
+                                                  __half2float(blo[boff + n])), 1.0f / kSplitScale);
+              v[i] = tanhf(__fadd_rn(__fmul_rn(v[i], kUnscale), b));
+            } else {
+              v[i] = 0.0f;
+            }
           }
           if (l < L) {
             uint4 h[4], g[4];
@@ -689,19 +699,20 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
           mbar_wait(aready, aphase);
           aphase ^= 1;
           tc_fence_after();
-          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
           for (int tile = 0; tile < nt_n * kc_n; ++tile) {
             const int nt = tile / kc_n, kc = tile % kc_n;
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t bs = b_base + stage * kStage32Bytes;
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
-              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc(bs + ks * 32), idesc,
-                      (kc | ks) != 0);
-              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc(bs + kTileBytes + ks * 32), idesc,
-                      1u);
+            for (int j = 0; j < 2; ++j) {          // K = 16 per instruction, 32 per stage
+              const uint64_t ad = smem_desc(a_base + (kc >> 1) * kTileBytes +
+                                            (((kc & 1) * 2 + j) * 32));
+              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc64(bs + j * 32), idesc,
+                      (kc | j) != 0);
+              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc64(bs + kT32Bytes + j * 32),
+                      idesc, 1u);
             }
             mma_commit(&empty[stage]);
             if (kc == kc_n - 1) mma_commit(&dready[nt]);
@@ -714,9 +725,37 @@ __global__ void __launch_bounds__(kThreads, 1) mlp32_kernel(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kProdWarps + kEpiWarps) {
+  if (warp == 1 + kEpiWarps) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// fp32 parameters → the split image [2][n][D] (plane 0 = hi, plane 1 = lo), 8 values per thread.
+__global__ void mlp_split_kernel(const float* __restrict__ x, int64_t total, __half* __restrict__ img) {
+  const int64_t i8 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i8 >= total) return;
+  float v[8];
+  if (i8 + 8 <= total && ((reinterpret_cast<uintptr_t>(x + i8) & 15) == 0)) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(x + i8));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(x + i8) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i8 + i < total ? x[i8 + i] : 0.0f;
+  }
+  uint4 hi, lo;
+  split8(v, hi, lo);
+  if (i8 + 8 <= total) {
+    __stcs(reinterpret_cast<uint4*>(img + i8), hi);
+    __stcs(reinterpret_cast<uint4*>(img + total + i8), lo);
+  } else {
+    const __half* h = reinterpret_cast<const __half*>(&hi);
+    const __half* g = reinterpret_cast<const __half*>(&lo);
+    for (int i = 0; i < 8 && i8 + i < total; ++i) {
+      img[i8 + i] = h[i];
+      img[total + i8 + i] = g[i];
+    }
   }
 }
 
@@ -788,6 +827,7 @@ __global__ void mlp_teacher_kernel(uint64_t seed, int l, int in, int out, float 
 }
 
 void mlp_problem_destroy(void* prob);
+static cudaError_t mlp_reserve(MlpProblem* pr, int64_t n, cudaStream_t st);
 
 static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
   p.nl = nw - 1;
@@ -805,11 +845,43 @@ static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
   p.D = off;
 }
 
-static cudaError_t launch_mlp32(const MlpParams& p, cudaStream_t st) {
+// Per plane and layer: the split image viewed as a 3-D tensor (k = in, n = out, member) with
+// strides (2 B, in·2 B, D·2 B); a box of 32 k × 128 n × 1 member lands in smem in the UMMA K-major
+// SWIZZLE_64B layout of half a stage (rows past `out` / columns past `in` are zero-filled).
+static cudaError_t encode_maps32(MlpParams& q, const __half* img, int64_t n) {
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return cudaErrorNotSupported;
+  for (int pl = 0; pl < 2; ++pl) {
+    const __half* base = img + (size_t)pl * n * q.D;
+    for (int l = 1; l <= q.nl; ++l) {
+      const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};
+      const cuuint64_t strides[2] = {(cuuint64_t)q.w[l - 1] * 2, (cuuint64_t)q.D * 2};
+      const cuuint32_t box[3] = {32, 128, 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      CUresult r = enc(&q.tmap32[pl][l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                       const_cast<__half*>(base + q.off[l]), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  return cudaSuccess;
+}
+
+// fp32-accurate kernel on the split image img [2][n][D]
+static cudaError_t launch_mlp32(MlpParams q, const __half* img, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   if (cudaError_t e = smem_attr_once((const void*)mlp32_kernel, kSmem32Bytes, attr)) return e;
-  const int pairs = (int)std::min<int64_t>(p.n, std::max(1, sm_count() / 2));
-  mlp32_kernel<<<2 * pairs, kThreads, kSmem32Bytes, st>>>(p);
+  if (cudaError_t e = encode_maps32(q, img, q.n)) return e;
+  q.img = img;
+  const int pairs = (int)std::min<int64_t>(q.n, std::max(1, sm_count() / 2));
+  mlp32_kernel<<<2 * pairs, kThreads32, kSmem32Bytes, st>>>(q);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_split(const float* x, int64_t total, __half* img, cudaStream_t st) {
+  const int64_t thr = (total + 7) / 8;
+  mlp_split_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(x, total, img);
   return cudaGetLastError();
 }
 
@@ -897,7 +969,9 @@ void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint6
   q.n = 1;
   q.f = nullptr;
   q.mode = 1;                                   // write Y* = g_L(θ*) (both kernels)
-  if ((e = launch_mlp(q, st)) != cudaSuccess || (e = launch_mlp32(q, st)) != cudaSuccess ||
+  if ((e = mlp_reserve(pr, 1, st)) != cudaSuccess || (e = launch_mlp(q, st)) != cudaSuccess ||
+      (e = launch_split(pr->theta, p.D, pr->img, st)) != cudaSuccess ||
+      (e = launch_mlp32(q, pr->img, st)) != cudaSuccess ||
       (e = cudaStreamSynchronize(st)) != cudaSuccess) {
     *err = std::string("teacher forward: ") + cudaGetErrorString(e);
     mlp_problem_destroy(pr);
@@ -906,18 +980,23 @@ void* mlp_problem_create(const int32_t* widths, int32_t nw, int32_t batch, uint6
   return pr;
 }
 
-// per-member scratch of the fp32-accurate kernel (two half sums + a counter), grown on demand
+// per-member buffers of the fp32-accurate kernel — the split image [2][n][D] and the two half
+// sums + a counter — grown on demand (outside any stream capture: es_set_mlp_problem reserves a
+// whole population)
 static cudaError_t mlp_reserve(MlpProblem* pr, int64_t n, cudaStream_t st) {
   if (n <= pr->cap) return cudaSuccess;
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
   cudaFree(pr->part);
   cudaFree(pr->cnt);
+  cudaFree(pr->img);
   pr->part = nullptr;
   pr->cnt = nullptr;
+  pr->img = nullptr;
   pr->cap = 0;
   if ((e = cudaMalloc(&pr->part, (size_t)n * 2 * sizeof(double))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&pr->cnt, (size_t)n * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&pr->img, (size_t)n * 2 * pr->p.D * sizeof(__half))) != cudaSuccess) return e;
   if ((e = cudaMemset(pr->cnt, 0, (size_t)n * sizeof(uint32_t))) != cudaSuccess) return e;
   pr->cap = n;
   return cudaSuccess;
@@ -925,6 +1004,12 @@ static cudaError_t mlp_reserve(MlpProblem* pr, int64_t n, cudaStream_t st) {
 
 cudaError_t mlp_problem_reserve(void* prob, int64_t n, cudaStream_t st) {
   return mlp_reserve(static_cast<MlpProblem*>(prob), n, st);
+}
+
+// the split image buffer for n members (the fused ask writes it), or nullptr on failure
+__half* mlp_problem_image(void* prob, int64_t n, cudaStream_t st) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  return mlp_reserve(pr, n, st) == cudaSuccess ? pr->img : nullptr;
 }
 
 void mlp_problem_destroy(void* prob) {
@@ -937,6 +1022,7 @@ void mlp_problem_destroy(void* prob) {
   cudaFree(pr->Y32);
   cudaFree(pr->part);
   cudaFree(pr->cnt);
+  cudaFree(pr->img);
   delete pr;
 }
 
@@ -944,21 +1030,29 @@ int64_t mlp_problem_dims(const void* prob) {
   return prob ? static_cast<const MlpProblem*>(prob)->p.D : -1;
 }
 
-// N14 (the definition): the fp32-accurate kernel on the fp32 parameters.
-cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st) {
+// N14 (the definition) on the split image the ask already wrote into mlp_problem_image(n).
+cudaError_t launch_mlp_eval_img(void* prob, int64_t n, float* f, cudaStream_t st) {
   MlpProblem* pr = static_cast<MlpProblem*>(prob);
-  if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
   if (n == 0) return cudaSuccess;
-  if (cudaError_t e = mlp_reserve(pr, n, st)) return e;
+  if (n > pr->cap) return cudaErrorInvalidValue;
   MlpParams q = pr->p;
-  q.x = x;
+  q.x = nullptr;
   q.x16 = nullptr;
   q.n = n;
   q.f = f;
   q.mode = 0;
   q.part = pr->part;
   q.cnt = pr->cnt;
-  return launch_mlp32(q, st);
+  return launch_mlp32(q, pr->img, st);
+}
+
+// N14 (the definition) on fp32 parameters: split pass, then the fp32-accurate kernel.
+cudaError_t launch_mlp_eval(void* prob, const float* x, int64_t n, float* f, cudaStream_t st) {
+  MlpProblem* pr = static_cast<MlpProblem*>(prob);
+  if (n == 0) return cudaSuccess;
+  if (cudaError_t e = mlp_reserve(pr, n, st)) return e;
+  if (cudaError_t e = launch_split(x, n * pr->p.D, pr->img, st)) return e;
+  return launch_mlp_eval_img(prob, n, f, st);
 }
 
 // N14′ (the fp16-image approximation) on fp32 parameters: the producers round to binary16.

@@ -392,7 +392,83 @@ __global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkey
               s.fit + (int64_t)blockIdx.x * s.N);
 }
 
+// Few runs (R ≤ kCountMaxR), N ≤ kCountMaxN: rank by counting instead of sorting, spread over the
+// whole GPU. pos_j = #{i : (key_i, i) < (key_j, j)} — the position the (key, index) sort gives —
+// is a sum over i-ranges computed by independent CTAs (grid: j-tiles × i-ranges × runs) and added
+// with integer atomics (order-free, so deterministic). The finish kernel scatters every key to
+// its position (the sorted array), clears the counters for the next generation and runs the
+// common rank_finish. N² compare-adds per run, but over ~300 CTAs instead of one CTA's
+// log²N-stage network with a barrier per stage (the single-CTA sort is latency-bound at R = 1).
+static constexpr int kCountMaxR = 16, kCountMaxN = 16384, kCountT = 256;
+
+__device__ __forceinline__ uint64_t key_at(const DevState& s, const float* __restrict__ fsrc,
+                                           int r, int p) {
+  const int w = p / s.Nloc, jl = p % s.Nloc;
+  const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
+  return ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
+}
+
+__global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
+                                                             const float* __restrict__ fsrc,
+                                                             uint32_t* __restrict__ cnt,
+                                                             int ilen) {
+  __shared__ uint64_t tile[kCountT];
+  const int N = s.N, r = blockIdx.z;
+  const int j = blockIdx.x * kCountT + threadIdx.x;
+  const uint64_t kj = j < N ? key_at(s, fsrc, r, j) : ~0ull;
+  const int i0 = blockIdx.y * ilen, i1 = min(N, i0 + ilen);
+  uint32_t c = 0;
+  for (int b = i0; b < i1; b += kCountT) {
+    const int n = min(kCountT, i1 - b);
+    __syncthreads();
+    if (threadIdx.x < n) tile[threadIdx.x] = key_at(s, fsrc, r, b + threadIdx.x);
+    __syncthreads();
+    if (n == kCountT) {
+#pragma unroll 16
+      for (int e = 0; e < kCountT; ++e) c += tile[e] < kj;
+    } else {
+      for (int e = 0; e < n; ++e) c += tile[e] < kj;
+    }
+  }
+  if (j < N && c) atomicAdd(&cnt[(int64_t)r * N + j], c);
+}
+
+__global__ void rank_count_finish_kernel(DevState s, const float* __restrict__ fsrc,
+                                         uint32_t* __restrict__ cnt) {
+  extern __shared__ uint64_t keys[];              // [N] sorted keys, then [N] fitness values
+  __shared__ double red[32];
+  __shared__ int32_t sh_nw;
+  const int r = blockIdx.x, N = s.N;
+  float* fs = reinterpret_cast<float*>(keys + N);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const uint64_t k = load_key(s, fsrc, r, j, fs);
+    uint32_t* c = cnt + (int64_t)r * N + j;
+    keys[*c] = k;
+    *c = 0u;
+  }
+  __syncthreads();
+  rank_finish(s, r, keys, red, &sh_nw, fs);
+}
+
+static bool use_count(const DevState& s) { return s.R <= kCountMaxR && s.N <= kCountMaxN; }
+
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
+  if (use_count(s)) {
+    static std::atomic<uint64_t> attr{0};
+    if (cudaError_t e = smem_attr_once((const void*)rank_count_finish_kernel, 200 * 1024, attr))
+      return e;
+    const int jt = (s.N + kCountT - 1) / kCountT;
+    const int want = 2 * sm_count();
+    int ni = std::max(1, std::min(jt, want / std::max(1, s.R * jt)));
+    const int ilen = ((s.N + ni - 1) / ni + kCountT - 1) / kCountT * kCountT;
+    ni = (s.N + ilen - 1) / ilen;
+    rank_count_kernel<<<dim3((unsigned)jt, (unsigned)ni, (unsigned)s.R), kCountT, 0, st>>>(
+        s, fsrc, s.rcnt, ilen);
+    const int T = std::min(1024, std::max(32, (s.N + 31) / 32 * 32));
+    const size_t sm = (size_t)s.N * (sizeof(uint64_t) + sizeof(float));
+    rank_count_finish_kernel<<<s.R, T, sm, st>>>(s, fsrc, s.rcnt);
+    return cudaGetLastError();
+  }
   int npad = 1;
   while (npad < s.N) npad <<= 1;
   static std::atomic<uint64_t> attr[6];
@@ -432,6 +508,7 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
 }
 
 int rank_launches(const DevState& s) {
+  if (use_count(s)) return 2;
   int npad = 1, n = 1;
   while (npad < s.N) npad <<= 1;
   if (npad <= kChunk) return 1;

@@ -34,6 +34,48 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
 
 
+def es_state(es, algo, r, dims=None):
+    """Run r's state of any GPU context (sharded ones included) in the oracle's field names."""
+    st = {f: es.get(f)[r].cpu().numpy() for f in KEPT[algo]}
+    st["best_f"] = float(es.get("best_f")[r])
+    if algo in HAS_SIGMA:
+        st["sigma"] = float(es.get("sigma")[r])
+    if algo in HAS_LRATE:
+        st["lrate"] = float(es.get("lrate")[r])
+    st["gen"] = int(es.get("gen")[r])
+    if dims is not None:
+        for f in KEPT[algo]:
+            st[f] = st[f][dims]
+    return st
+
+
+def oracle_state(o, algo):
+    st = {f: o.vec[VEC_FIELDS.index(f)].copy() for f in KEPT[algo]}
+    st["best_f"] = float(o.best_f)
+    if algo in HAS_SIGMA:
+        st["sigma"] = float(o.sigma)
+    if algo in HAS_LRATE:
+        st["lrate"] = float(o.lr)
+    st["gen"] = int(o.t)
+    return st
+
+
+def compare_to_oracle(es, algo, r, o, tol, dims=None, d0=0):
+    """Q24 distance of run r of GPU context `es` (optionally a D-shard whose state starts at global
+    dim d0) to oracle run `o`, per field; asserts <= tol and returns the worst."""
+    g = es_state(es, algo, r)
+    ref = oracle_state(o, algo)
+    worst = 0.0
+    for k in g:
+        a, b = np.atleast_1d(g[k]), np.atleast_1d(ref[k])
+        if k in KEPT[algo] and a.size != b.size:       # a D-shard holds the dims [d0, d0 + n)
+            b = b[d0:d0 + a.size]
+        e = q24(a, b)
+        assert e <= tol, (k, r, e)
+        worst = max(worst, e)
+    return worst
+
+
 class Pair:
     """R runs of one algorithm on the GPU and R oracle runs with identical parameters."""
 

@@ -9,7 +9,7 @@ import torch
 
 import workloads as W
 from oracle import oracle as O
-from gpu_helpers import KEPT, bits, q24
+from gpu_helpers import KEPT, bits, compare_to_oracle, q24
 
 pytestmark = pytest.mark.gpu
 
@@ -45,6 +45,7 @@ def _run(algo, N, D, R, Wn, fn, gens, per=None):
     assert shards[0].d_begin == 0 and all(a.d_begin + a.x_dims == b.d_begin
                                           for a, b in zip(shards, shards[1:]))
     assert shards[-1].d_begin + shards[-1].x_dims == D
+    orcs = [O.Run(algo, N, D, **p) for p in params]
     for g in range(gens):
         x, f_ref = ref.ask_eval(fn)
         parts = []
@@ -60,6 +61,9 @@ def _run(algo, N, D, R, Wn, fn, gens, per=None):
         # the split sum differs from the unsharded block order only in binary64 rounding
         assert q24(f.cpu().numpy(), f_ref.cpu().numpy()) <= 2 ** -23
         ref.tell(f)
+        fh = f.cpu().numpy()
+        for r, o in enumerate(orcs):          # the oracle fed the same (summed) fitness
+            o.tell(fh[r])
         for sh in shards:
             if algo == W.SEP_CMA_ES:
                 sh.tell_local(f)
@@ -83,6 +87,8 @@ def _run(algo, N, D, R, Wn, fn, gens, per=None):
                 else:
                     assert q24(a, b) <= tol, (g, fld, d0)
             assert torch.equal(sh.get("perm"), ref.get("perm"))
+            for r, o in enumerate(orcs):      # each shard's dims against the oracle's
+                compare_to_oracle(sh, algo, r, o, 1e-5, d0=sh.d_begin)
     for es in shards + [ref]:
         es.close()
 

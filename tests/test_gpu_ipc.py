@@ -15,6 +15,7 @@ import torch
 
 import workloads as W
 from gpu_helpers import q24
+from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
@@ -91,8 +92,13 @@ def test_p2p_ipc_two_processes(case):
                            start_method="spawn")
         res = [torch.load(os.path.join(td, f"rank{w}.pt")) for w in range(WS)]
     ref = S.Strategy(algo, N, D, _params(algo, per))
+    orcs = [O.Run(algo, N, D, **p) for p in _params(algo, per)]
     for _ in range(GENS):
-        ref.tell(ref.eval(W.RASTRIGIN, ref.ask()))
+        f = ref.eval(W.RASTRIGIN, ref.ask())
+        ref.tell(f)
+        for r, o in enumerate(orcs):                     # the oracle fed the same fitness
+            o.ask()
+            o.tell(f[r].cpu().numpy())
     Q = (D + 3) // 4
     for w, got in enumerate(res):
         assert torch.equal(got["perm"], ref.get("perm").cpu()), w
@@ -105,4 +111,16 @@ def test_p2p_ipc_two_processes(case):
                 assert np.all(np.abs(a - b) <= 1e-6 * np.abs(b)), (k, w)
             else:
                 assert q24(a, b) <= 1e-6, (k, w)
+            # and against the oracle (each rank's copy of the all-gathered fields, its own
+            # optimizer-state slice)
+            vi = {"mean": 0, "sigma_d": 1, "adam_m": 2, "C": 6, "best_x": 7}
+            for r, o in enumerate(orcs):
+                if k == "sigma":
+                    assert abs(float(a[r]) - float(o.sigma)) <= 1e-5 * abs(float(o.sigma)), (k, w)
+                    continue
+                ob = o.vec[vi[k]]
+                ar = a[r]
+                if k == "adam_m":
+                    ob = ob[d0:d1]
+                assert q24(ar, ob) <= 1e-5, (k, w, r)
     ref.close()

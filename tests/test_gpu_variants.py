@@ -8,7 +8,7 @@ import torch
 
 import workloads as W
 from oracle import oracle as O
-from gpu_helpers import KEPT, Pair, bits, q24
+from gpu_helpers import KEPT, Pair, bits, compare_to_oracle, q24
 
 pytestmark = pytest.mark.gpu
 
@@ -175,17 +175,23 @@ def test_variants_hundred_generations(algo, fn, N, D, R, over):
 @pytest.mark.parametrize("Wn", [2, 4])
 def test_variants_emulated_shards(algo, per, Wn):
     """As test_gpu_parity.test_emulated_shards_match_single_gpu: ARS's k selected directions and
-    ClipUp's global norms split over W shards reproduce the unsharded run."""
+    ClipUp's global norms split over W shards reproduce the unsharded run, and every shard's state
+    is within 1e-5 of the oracle fed the same fitness."""
     from paper_2212_04180_b200 import strategy as S
     N, D, R = 32, 301, 4
     params = _params(algo, R, per)
     ref = S.Strategy(algo, N, D, params)
     shards = [S.Strategy(algo, N, D, params, shard=(w, Wn)) for w in range(Wn)]
+    orcs = [O.Run(algo, N, D, **p) for p in params]
     nl = N // Wn
     for gen in range(3):
         x = ref.ask()
         f = ref.eval(W.RASTRIGIN, x)
         ref.tell(f)
+        fh = f.cpu().numpy()
+        for r, o in enumerate(orcs):
+            o.ask()
+            o.tell(fh[r])
         locs = []
         for w, sh in enumerate(shards):
             xs = sh.ask()
@@ -203,6 +209,8 @@ def test_variants_emulated_shards(algo, per, Wn):
         for sh in shards:
             for fld in KEPT[algo]:
                 assert q24(sh.get(fld).cpu().numpy(), ref.get(fld).cpu().numpy()) <= 1e-6, fld
+            for r, o in enumerate(orcs):
+                compare_to_oracle(sh, algo, r, o, 1e-5)
     for es in shards + [ref]:
         es.close()
 

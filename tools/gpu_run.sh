@@ -2,7 +2,7 @@
 # One gpurun call driven by env vars (everything lands in gpurun_out/<TAG>_*):
 #   TESTS="-k expr"  pytest -m gpu selection ("" = skip, "all" = the whole suite)
 #   BENCH="args;args" bench.py invocations (";"-separated), each logged
-#   NCU="regex|count|bench args" one ncu --set full capture of the kernels matching regex
+#   NCU_K=regex NCU_C=count NCU_ARGS="bench args": one ncu --set full capture of those kernels
 #   LAUNCH="bench args" ncu launch list (gpu__time_duration) of one bench invocation
 # usage: TAG=r2b TESTS="-k mlp" BENCH="--config c4" bash tools/gpu_run.sh
 TAG=${TAG:-r2}
@@ -11,7 +11,7 @@ mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/${TAG}_build.log 2>&1 || { echo build failed; tail -20 $OUT/${TAG}_build.log; exit 1; }
 if [ -n "$TESTS" ]; then
   if [ "$TESTS" = "all" ]; then SEL=""; else SEL="$TESTS"; fi
-  timeout ${TEST_TIMEOUT:-1200} python -m pytest tests -m gpu -x -q $SEL > $OUT/${TAG}_tests.log 2>&1
+  timeout ${TEST_TIMEOUT:-1200} python -m pytest tests -m gpu -q --maxfail=25 $SEL > $OUT/${TAG}_tests.log 2>&1
   echo "tests rc=$?"; tail -4 $OUT/${TAG}_tests.log
 fi
 if [ -n "$BENCH" ]; then
@@ -28,9 +28,8 @@ if [ -n "$LAUNCH" ]; then
     --log-file $OUT/${TAG}_launches.csv python bench.py $LAUNCH --no-cpu-baseline > $OUT/${TAG}_launch.log 2>&1
   echo "launch list rc=$?"
 fi
-if [ -n "$NCU" ]; then
-  IFS='|' read -r KRE KCNT NARGS <<< "$NCU"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$KRE" -c ${KCNT:-4} \
-    -o $OUT/${TAG}_prof python bench.py $NARGS --no-cpu-baseline > $OUT/${TAG}_ncu.log 2>&1
+if [ -n "$NCU_K" ]; then
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$NCU_K" -c ${NCU_C:-4} \
+    -o $OUT/${TAG}_prof python bench.py $NCU_ARGS --no-cpu-baseline > $OUT/${TAG}_ncu.log 2>&1
   echo "ncu rc=$?"; tail -3 $OUT/${TAG}_ncu.log
 fi
