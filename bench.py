@@ -665,6 +665,10 @@ def main():
     tot_k = sum(v["ms"] for v in kinds.values()) or 1.0
     share = {k: round(v["ms"] / tot_k, 4) for k, v in kinds.items()}   # of the serialised pass
     kernels_ms = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in kinds.items()}
+    by_handle = {}
+    for k, lst in prof.items():
+        for label, _, t, n in lst:
+            by_handle.setdefault(label, {})[k] = round(t / max(n, 1), 4)
 
     # --- end to end through the C ABI with HOST buffers (fitness read back and fed to tell)
     e2e = e2e_run(hs, args, 1 if sharded else world, fused, write_x)
@@ -694,7 +698,8 @@ def main():
             "data": "synthetic", "config": cb,
             "generations_per_s": 1e3 / ms, "roofline": roof, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "kernel_share": share,
-            "kernel_ms_per_launch": kernels_ms, "kernel_rates": extra,
+            "kernel_ms_per_launch": kernels_ms, "kernel_ms_by_handle": by_handle,
+            "kernel_rates": extra,
             "timing": "CUDA-graph replays of one generation" if graph is not None else
                       "eager C-ABI calls, CUDA events on the stream"}
     for h in hs:

@@ -137,7 +137,9 @@ typedef struct es_ctx es_ctx_t;
  * (Listing 1 `strategy.initialize`; N6). popsize N is the GLOBAL population; each rank
  * owns N/W members (= N/(2W) antithetic pairs or N/W directions). For world_size > 1,
  * nccl_unique_id points at the 128-byte ncclUniqueId that rank 0 created and broadcast
- * (e.g. via torch.distributed); it is ignored when world_size == 1.
+ * (e.g. via torch.distributed). world_size == 1 with an id (from es_nccl_get_unique_id) creates a
+ * one-rank communicator and es_tell then runs the population-sharded data plane (fitness
+ * all-gather, direction-sum all-reduce, separate update kernel) on one GPU; NULL: the fused tell.
  * world_size > 1 with nccl_unique_id == NULL creates a communicator-less shard (split-phase tell only).
  * Errors: ES_ERR_INVALID_ARG if N < 2, D < 1, R < 1, N odd (OpenAI-ES/PGPE), N mod W != 0,
  * N/W odd (OpenAI-ES/PGPE), ⌊elite_ratio·N⌋ < 1 (Sep-CMA-ES), negative σ_init, non-positive

@@ -273,10 +273,16 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     while (npad < N) npad <<= 1;
     s.gkeys = nullptr;
     if (npad > 16384) TRY(dalloc(c, (void**)&s.gkeys, (size_t)R * npad * sizeof(uint64_t)));
-    TRY(dalloc(c, (void**)&s.rcnt, RN * sizeof(uint32_t)));
-    TRY(cudaMemsetAsync(s.rcnt, 0, RN * sizeof(uint32_t), st));
+    // counting rank: [3][R][N] counters, [R][64] j-tile and [R] run arrivals, [R][2] slots
+    const size_t nc = 3 * RN + (size_t)R * 64 + 3 * (size_t)R;
+    TRY(dalloc(c, (void**)&s.rcnt, nc * sizeof(uint32_t)));
+    TRY(cudaMemsetAsync(s.rcnt, 0, nc * sizeof(uint32_t), st));
+    TRY(dalloc(c, (void**)&s.rbpart, (size_t)R * 64 * sizeof(double)));
   }
-  if (W > 1) TRY(dalloc(c, (void**)&c->fgather, RN * sizeof(float)));
+  // population sharding with a communicator — also a one-rank one (W = 1 with an id: the
+  // collective data plane of es_tell executed on a single GPU)
+  const bool pcoll = !dsh && (W > 1 || uid);
+  if (pcoll) TRY(dalloc(c, (void**)&c->fgather, RN * sizeof(float)));
   // per-run scalars and weight tables, computed on the host in binary64
   c->host_rs.assign(R, RunScal{});
   std::vector<float> wpos(RN, 0.0f), wr(N);
@@ -317,6 +323,14 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     }
     std::copy(wr.begin(), wr.end(), wpos.begin() + (size_t)r * N);
   }
+  // the counting rank needs a shaping that is a per-member function of the ranks (no z-score,
+  // no ARS / elite-pair selection)
+  s.rank_par = algo != ES_ARS;
+  for (int r = 0; r < R; ++r) {
+    const RunScal& rs = c->host_rs[r];
+    if ((antithetic(algo) && rs.shaping == 2) || (algo == ES_PGPE && rs.ars_k < N / 2))
+      s.rank_par = 0;
+  }
   {
     // tell entry split from each run's expected entry count on this rank (Sep-CMA-ES: μ_r)
     std::vector<int> ent(R);
@@ -344,7 +358,7 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
   }
   c->host_t.assign(R, 0u);
   TRY(cudaStreamSynchronize(st));   // host tables above are stack-owned
-  if (W > 1 && uid) {
+  if ((W > 1 || pcoll) && uid) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     ncclResult_t nr = ncclCommInitRank(&c->comm, W, id, rank);
@@ -352,6 +366,7 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
       fail(c, ES_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
       return bail(ES_ERR_NCCL);
     }
+    c->pcoll = pcoll;
   }
 #undef TRY
   *out = c;
@@ -794,9 +809,11 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     if ((err = weight_decay_impl(c, fl, nullptr, st)) != ES_SUCCESS) return err;
     fl = c->wdbuf;
   }
-  const bool fused = s.W == 1;
+  // the collective path: W > 1, or a one-rank communicator (c->pcoll)
+  const bool coll = s.W > 1 || c->pcoll;
+  const bool fused = !coll;
   const float* fsrc = fl;
-  if (s.W > 1) {   // a5: every rank obtains all N fitness values
+  if (coll) {   // a5: every rank obtains all N fitness values
     ProfScope ps(c, "allgather", st);
     NCCL_OR(c, ncclAllGather(fl, c->fgather, nloc, ncclFloat, c->comm, st));
     fsrc = c->fgather;
@@ -826,7 +843,7 @@ es_status_t es_tell(es_ctx_t* c, const float* fitness, es_stream_t stream_) {
     return ES_SUCCESS;
   }
   if ((err = tell_local_impl(c, fsrc, fused, st)) != ES_SUCCESS) return err;
-  if (s.W > 1 && s.algo != CMA_ES) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
+  if (coll && s.algo != CMA_ES) {   // a8 (P:226 pmean): sum the binary64 direction sums over ranks
     const size_t cnt = (size_t)(s.algo == OPENAI_ES || s.algo == ARS ? 1 : 2) * s.R * s.D;
     ProfScope ps(c, "allreduce", st);
     NCCL_OR(c, ncclAllReduce(s.G, s.G, cnt, ncclFloat64, ncclSum, c->comm, st));

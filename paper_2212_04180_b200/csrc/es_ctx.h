@@ -63,6 +63,7 @@ struct es_ctx {
   bool broken = false;
   TellSplit split{1, 1};
   float* fgather = nullptr;     // [W][R][Nloc]
+  bool pcoll = false;           // population-sharded with a communicator (also W = 1)
   float* fstage = nullptr;      // [R][Nloc] staging of host fitness
   float* fgather_stage = nullptr;  // [W][R][Nloc] staging of host gathered fitness (split phase)
   // host inputs are first copied (CPU memcpy) into one of two pinned host buffers, so the

@@ -87,7 +87,10 @@ struct DevState {
   uint32_t* arrive;    // [R][blocks_per_run] last-block counters
   double* normpart;    // [R][blocks_per_run] Sep-CMA ‖p_σ‖² partials
   uint64_t* gkeys;     // [R][npad] sort keys in global memory (N > 16384 only)
-  uint32_t* rcnt;      // [R][N] counting-rank positions (few runs), zero between tells
+  uint32_t* rcnt;      // counting rank (few runs): [3][R][N] counters + arrivals + slots, zero
+                      // between tells (k_rank.cu)
+  double* rbpart;     // [R][64] counting rank: PGPE baseline partials per j-tile
+  int rank_par;       // every run's shaping is per-member in the ranks (counting rank allowed)
   int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
   double* n2;          // [R] D-shard Sep-CMA ‖p_σ'‖² share, summed over ranks before the finish
   // full-covariance CMA-ES (f4)

@@ -2,7 +2,7 @@
 // evaluation kernel (k_eval.cu) and the fused ask+evaluate kernel (k_ask_eval.cu).
 // Binary64 accumulation; Sphere uses exact-product DFMAs (= the oracle's mul-then-add), Rastrigin
 // accumulates Σx² and ΣS² separately and combines them once as Σx² + 20·ΣS² (N7). The binary32 →
-// binary64 converts of S and |x| are bit assemblies on the FMA pipe; the floor stays on the XU.
+// binary64 converts of S and |x| are bit assemblies on the FMA pipe; rint stays on the XU.
 #pragma once
 #include "noise.cuh"
 
@@ -40,14 +40,14 @@ __device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has
   } else if (FN == FN_ROSENBROCK) {
     if (has_next) acc.a = __dadd_rn(acc.a, rosen_term(x, xn));
   } else {
-    // One XU-pipe instruction per element (FRND for the floor); (double)|x| and (double)S are
-    // bit assemblies on the FMA pipe. (Both converts on the XU made the kernel XU-bound; moving
-    // the floor off the XU as well — an exact 2^23-shifter FADD sequence — made it issue-bound and
-    // slower: 114 → 138 µs at C2.)
-    const float ab = fabsf(x);
-    const float fr = __fsub_rn(ab, floorf(ab));
-    const double S = pos_f2d(sinpi_half(fminf(fr, __fsub_rn(1.0f, fr))));   // S ∈ [0, 1]
-    const double d = pos_f2d(ab);
+    // b = min(fr, 1 − fr) of N7 is the distance from x to the nearest integer: bq = x − rint(x)
+    // is exact (Sterbenz; rint(x) = 0 for |x| < 1/2) and |bq| = b bit for bit, ties and |x| ≥ 2^23
+    // included. S is odd in b and its polynomial even, so S = |bq|·P(bq²) (the |·| is an operand
+    // modifier). Per element: FRND (the one XU instruction), FADD, the 7-op polynomial, two
+    // IMAD.WIDE bit-assembled converts (FMA pipe), the |x| materialisation and two DFMAs.
+    const float bq = __fsub_rn(x, rintf(x));
+    const double S = pos_f2d(__fmul_rn(fabsf(bq), sinpi_P(__fmul_rn(bq, bq))));   // S ∈ [0, 1]
+    const double d = pos_f2d(fabsf(x));
     acc.a = __fma_rn(d, d, acc.a);
     acc.b = __fma_rn(S, S, acc.b);
   }

@@ -31,6 +31,44 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// The generation's scalars (one thread): best tracking, schedules, Adam bias
+// corrections, the tell's entry count. jbest = member at sorted position 0, fb its fitness,
+// nw = Sep-CMA-ES / CMA-ES weighted positions (end of μ−1's tie group + 1).
+__device__ void write_genscal(const DevState& s, int r, int jbest, float fb, int nw, double bbar,
+                              float ars_scale) {
+  const int N = s.N;
+  const bool anti = is_anti(s.algo);
+  RunScal& w = s.rs[r];
+  GenScal g;
+  g.t = w.t;
+  g.jbest = jbest;
+  g.improved = fb < w.best_f;                 // strict; false for NaN
+  if (g.improved) w.best_f = fb;
+  g.lr = w.lr;
+  g.sigma = w.sigma;
+  g.nentries = (s.algo == ARS || s.algo == PGPE) ? w.ars_k
+                                                 : (anti ? N / 2 : (s.algo == SNES ? N : nw));
+  g.ars_scale = ars_scale;
+  g.clip_inv = 0.0f;
+  g.bbar = bbar;
+  g.bc1 = g.bc2 = 1.0f;
+  g.sigma_new = w.sigma;
+  g.hsig = 0;
+  if (anti) {
+    const double b1 = __dmul_rn(w.b1pow, (double)w.beta1);
+    const double b2 = __dmul_rn(w.b2pow, (double)w.beta2);
+    g.bc1 = (float)__dsub_rn(1.0, b1);
+    g.bc2 = (float)__dsub_rn(1.0, b2);
+    w.b1pow = b1;
+    w.b2pow = b2;
+    w.lr = fmaxf(__fmul_rn(w.lr, w.lrate_decay), w.lrate_limit);
+    if (s.algo == OPENAI_ES || s.algo == ARS)
+      w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
+  }
+  w.t = g.t + 1;
+  s.gs[r] = g;
+}
+
 // Sorted (key, index) pairs → tie groups, shaping, tell coefficients and the generation's
 // scalars (N9–N12 bookkeeping). `keys` is the run's sorted array (shared or global memory).
 // fit: the run's fitness in sorted-input order (shared memory when the caller staged it there —
@@ -185,36 +223,8 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    RunScal& w = s.rs[r];
-    GenScal g;
-    g.t = w.t;
-    g.jbest = (int)(uint32_t)keys[0];            // = perm[0], without the global round trip
-    const float fb = fit[g.jbest];
-    g.improved = fb < w.best_f;                 // strict; false for NaN
-    if (g.improved) w.best_f = fb;
-    g.lr = w.lr;
-    g.sigma = w.sigma;
-    g.nentries = (s.algo == ARS || s.algo == PGPE) ? w.ars_k
-                                                   : (anti ? N / 2 : (s.algo == SNES ? N : sh_nw));
-    g.ars_scale = ars_scale;
-    g.clip_inv = 0.0f;
-    g.bbar = bbar;
-    g.bc1 = g.bc2 = 1.0f;
-    g.sigma_new = w.sigma;
-    g.hsig = 0;
-    if (anti) {
-      const double b1 = __dmul_rn(w.b1pow, (double)w.beta1);
-      const double b2 = __dmul_rn(w.b2pow, (double)w.beta2);
-      g.bc1 = (float)__dsub_rn(1.0, b1);
-      g.bc2 = (float)__dsub_rn(1.0, b2);
-      w.b1pow = b1;
-      w.b2pow = b2;
-      w.lr = fmaxf(__fmul_rn(w.lr, w.lrate_decay), w.lrate_limit);
-      if (s.algo == OPENAI_ES || s.algo == ARS)
-        w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
-    }
-    w.t = g.t + 1;
-    s.gs[r] = g;
+    const int jbest = (int)(uint32_t)keys[0];            // = perm[0], without the global round trip
+    write_genscal(s, r, jbest, fit[jbest], sh_nw, bbar, ars_scale);
   }
 }
 
@@ -392,81 +402,192 @@ __global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkey
               s.fit + (int64_t)blockIdx.x * s.N);
 }
 
-// Few runs (R ≤ kCountMaxR), N ≤ kCountMaxN: rank by counting instead of sorting, spread over the
-// whole GPU. pos_j = #{i : (key_i, i) < (key_j, j)} — the position the (key, index) sort gives —
-// is a sum over i-ranges computed by independent CTAs (grid: j-tiles × i-ranges × runs) and added
-// with integer atomics (order-free, so deterministic). The finish kernel scatters every key to
-// its position (the sorted array), clears the counters for the next generation and runs the
-// common rank_finish. N² compare-adds per run, but over ~300 CTAs instead of one CTA's
-// log²N-stage network with a barrier per stage (the single-CTA sort is latency-bound at R = 1).
+// Few runs (R ≤ kCountMaxR), N ≤ kCountMaxN, and a shaping that is a per-member function of the
+// ranks (centered rank, raw, SNES / Sep-CMA weights — s.rank_par): rank by COUNTING, in ONE launch
+// spread over the whole GPU (the single-CTA sort is latency-bound at R = 1). For member j with key
+// k_j (N9):  lt_j = #{i : k_i < k_j},  le_j = #{i : k_i ≤ k_j},  pos_j = #{i : (k_i, i) < (k_j, j)}
+// — the tie group is [s_j, e_j] = [lt_j, le_j − 1] and pos_j the (key, index) sort position, so
+// no sorted array is needed. Grid: j-tiles × i-ranges × runs; each CTA adds its i-range's counts
+// with integer atomics (order-free, deterministic). The last CTA of a j-tile (arrival counter)
+// finishes its 256 members: tie group, shaped value (N10 / N11 / raw), perm, the tell's
+// (direction, coefficient) entries; the last j-tile of a run writes the generation's scalars
+// (and subtracts PGPE's baseline, N12). Counters are cleared for the next generation on the way.
 static constexpr int kCountMaxR = 16, kCountMaxN = 16384, kCountT = 256;
+static constexpr int kCountMaxTiles = kCountMaxN / kCountT;
 
-__device__ __forceinline__ uint64_t key_at(const DevState& s, const float* __restrict__ fsrc,
-                                           int r, int p) {
+// rcnt layout: [3][R][N] counters (pos, lt, le), then [R][kCountMaxTiles] j-tile arrivals, [R]
+// run arrivals, [R][2] slots (jbest, nw).
+__device__ __forceinline__ uint32_t* rc_tile(const DevState& s) { return s.rcnt + 3 * (int64_t)s.R * s.N; }
+__device__ __forceinline__ uint32_t* rc_run(const DevState& s) { return rc_tile(s) + (int64_t)s.R * kCountMaxTiles; }
+__device__ __forceinline__ uint32_t* rc_slot(const DevState& s) { return rc_run(s) + s.R; }
+
+__device__ __forceinline__ float fit_at(const DevState& s, const float* __restrict__ fsrc, int r,
+                                        int p) {
   const int w = p / s.Nloc, jl = p % s.Nloc;
-  const float f = fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
-  return ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
+  return fsrc[((int64_t)w * s.R + r) * s.Nloc + jl];
 }
 
 __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
                                                              const float* __restrict__ fsrc,
-                                                             uint32_t* __restrict__ cnt,
                                                              int ilen) {
-  __shared__ uint64_t tile[kCountT];
-  const int N = s.N, r = blockIdx.z;
+  __shared__ uint32_t tile[kCountT];
+  __shared__ float sval[kCountT];
+  __shared__ double red[32];
+  __shared__ int sh_last;
+  const int N = s.N, r = blockIdx.z, jt = gridDim.x, ni = gridDim.y;
   const int j = blockIdx.x * kCountT + threadIdx.x;
-  const uint64_t kj = j < N ? key_at(s, fsrc, r, j) : ~0ull;
+  const float fj = j < N ? fit_at(s, fsrc, r, j) : 0.0f;
+  const uint32_t kj = j < N ? rank_key(fj) : 0xFFFFFFFFu;
   const int i0 = blockIdx.y * ilen, i1 = min(N, i0 + ilen);
-  uint32_t c = 0;
+  const int jt0 = blockIdx.x * kCountT;
+  uint32_t cpos = 0, clt = 0, cle = 0;
   for (int b = i0; b < i1; b += kCountT) {
     const int n = min(kCountT, i1 - b);
     __syncthreads();
-    if (threadIdx.x < n) tile[threadIdx.x] = key_at(s, fsrc, r, b + threadIdx.x);
+    if (threadIdx.x < n) tile[threadIdx.x] = rank_key(fit_at(s, fsrc, r, b + threadIdx.x));
     __syncthreads();
+    uint32_t lt = 0, le = 0;
     if (n == kCountT) {
 #pragma unroll 16
-      for (int e = 0; e < kCountT; ++e) c += tile[e] < kj;
+      for (int e = 0; e < kCountT; ++e) {
+        const uint32_t k = tile[e];
+        lt += k < kj;
+        le += k <= kj;
+      }
     } else {
-      for (int e = 0; e < n; ++e) c += tile[e] < kj;
+      for (int e = 0; e < n; ++e) {
+        const uint32_t k = tile[e];
+        lt += k < kj;
+        le += k <= kj;
+      }
+    }
+    clt += lt;
+    cle += le;
+    if (b + n <= jt0) {
+      cpos += le;                           // every i of the tile precedes every j of this j-tile
+    } else if (b >= jt0 + kCountT) {
+      cpos += lt;                           // every i follows
+    } else {                                // the j-tile itself: (key, index) order, i.e. lt
+      cpos += lt;                           // + the equal keys of smaller index (ties only)
+      if (le - lt > 1u) {
+        const int ne = min(j - b, n);
+        for (int e = 0; e < ne; ++e) cpos += tile[e] == kj;
+      }
     }
   }
-  if (j < N && c) atomicAdd(&cnt[(int64_t)r * N + j], c);
-}
-
-__global__ void rank_count_finish_kernel(DevState s, const float* __restrict__ fsrc,
-                                         uint32_t* __restrict__ cnt) {
-  extern __shared__ uint64_t keys[];              // [N] sorted keys, then [N] fitness values
-  __shared__ double red[32];
-  __shared__ int32_t sh_nw;
-  const int r = blockIdx.x, N = s.N;
-  float* fs = reinterpret_cast<float*>(keys + N);
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    const uint64_t k = load_key(s, fsrc, r, j, fs);
-    uint32_t* c = cnt + (int64_t)r * N + j;
-    keys[*c] = k;
-    *c = 0u;
+  const int64_t RN = (int64_t)s.R * N, rj = (int64_t)r * N + j;
+  if (j < N) {
+    if (cpos) atomicAdd(&s.rcnt[rj], cpos);
+    if (clt) atomicAdd(&s.rcnt[RN + rj], clt);
+    if (cle) atomicAdd(&s.rcnt[2 * RN + rj], cle);
+  }
+  // ---- the last i-range CTA of this j-tile finishes its members
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* tc = rc_tile(s) + (int64_t)r * kCountMaxTiles + blockIdx.x;
+    sh_last = atomicAdd(tc, 1u) == (uint32_t)(ni - 1);
+    if (sh_last) *tc = 0u;
   }
   __syncthreads();
-  rank_finish(s, r, keys, red, &sh_nw, fs);
+  if (!sh_last) return;
+  __threadfence();
+  const RunScal& rs = s.rs[r];
+  const bool anti = is_anti(s.algo), cmaish = s.algo == SEP_CMA_ES || s.algo == CMA_ES;
+  float val = 0.0f;
+  int pos = 0;
+  if (j < N) {
+    pos = (int)__ldcg(&s.rcnt[rj]);
+    const int sj = (int)__ldcg(&s.rcnt[RN + rj]);
+    const int ej = (int)__ldcg(&s.rcnt[2 * RN + rj]) - 1;
+    s.rcnt[rj] = 0u;
+    s.rcnt[RN + rj] = 0u;
+    s.rcnt[2 * RN + rj] = 0u;
+    s.perm[(int64_t)r * N + pos] = j;
+    s.rs_s[rj] = sj;
+    s.rs_e[rj] = ej;
+    s.pos[rj] = pos;
+    s.fit[rj] = fj;
+    if (anti && rs.shaping == 1) {
+      val = fj;                                                          // raw fitness
+    } else if (anti) {
+      val = __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));  // N10
+    } else {
+      const float* wpos = s.wpos + (int64_t)r * N;                        // N11
+      float acc = 0.0f;
+      for (int q = sj; q <= ej; ++q) acc = __fadd_rn(acc, wpos[q]);
+      val = __fdiv_rn(acc, (float)(ej - sj + 1));
+    }
+    s.shaped[rj] = val;
+    if (pos == 0) rc_slot(s)[2 * r] = (uint32_t)j;
+    if (cmaish && pos == rs.mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
+  }
+  sval[threadIdx.x] = val;
+  __syncthreads();
+  uint32_t* dir = s.dir + (int64_t)r * N;
+  double* cA = s.coefA + (int64_t)r * N;
+  double* cB = s.coefB + (int64_t)r * N;
+  double part = 0.0;
+  if (anti) {
+    if (j < N && !(j & 1)) {               // pair i = j/2 (N even; the partner is in this tile)
+      const int i = j >> 1;
+      const double cp = sval[threadIdx.x], cm = sval[threadIdx.x + 1];
+      dir[i] = (uint32_t)i;
+      cA[i] = __dsub_rn(cp, cm);
+      if (s.algo == PGPE) cB[i] = __dmul_rn(__dadd_rn(cp, cm), 0.5);   // − b̄ by the last tile
+    }
+    if (s.algo == PGPE) part = j < N ? (double)val : 0.0;
+  } else if (j < N) {
+    const int e = cmaish ? pos : j;         // Sep-CMA: entries in sorted order (the first nw count)
+    dir[e] = (uint32_t)j;
+    cA[e] = (double)val;
+  }
+  if (s.algo == PGPE) {
+    const double t = block_sum(part, red);
+    if (threadIdx.x == 0) s.rbpart[(int64_t)r * kCountMaxTiles + blockIdx.x] = t;
+  }
+  // ---- the last j-tile of the run: the generation's scalars
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* rc = rc_run(s) + r;
+    sh_last = atomicAdd(rc, 1u) == (uint32_t)(jt - 1);
+    if (sh_last) *rc = 0u;
+  }
+  __syncthreads();
+  if (!sh_last) return;
+  __threadfence();
+  double bbar = 0.0;
+  if (s.algo == PGPE) {
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int b = 0; b < jt; ++b) t = __dadd_rn(t, __ldcg(&s.rbpart[(int64_t)r * kCountMaxTiles + b]));
+      red[0] = t / (double)N;
+    }
+    __syncthreads();
+    bbar = red[0];
+    for (int i = threadIdx.x; i < N / 2; i += blockDim.x) cB[i] = __dsub_rn(__ldcg(&cB[i]), bbar);
+  }
+  if (threadIdx.x == 0) {
+    const int jbest = (int)__ldcg(&rc_slot(s)[2 * r]);
+    const int nw = cmaish ? (int)__ldcg(&rc_slot(s)[2 * r + 1]) : 0;
+    write_genscal(s, r, jbest, __ldcg(&s.fit[(int64_t)r * N + jbest]), nw, bbar, 0.0f);
+  }
 }
 
-static bool use_count(const DevState& s) { return s.R <= kCountMaxR && s.N <= kCountMaxN; }
+static bool use_count(const DevState& s) {
+  return s.rank_par && s.R <= kCountMaxR && s.N <= kCountMaxN;
+}
 
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
   if (use_count(s)) {
-    static std::atomic<uint64_t> attr{0};
-    if (cudaError_t e = smem_attr_once((const void*)rank_count_finish_kernel, 200 * 1024, attr))
-      return e;
     const int jt = (s.N + kCountT - 1) / kCountT;
     const int want = 2 * sm_count();
     int ni = std::max(1, std::min(jt, want / std::max(1, s.R * jt)));
     const int ilen = ((s.N + ni - 1) / ni + kCountT - 1) / kCountT * kCountT;
     ni = (s.N + ilen - 1) / ilen;
     rank_count_kernel<<<dim3((unsigned)jt, (unsigned)ni, (unsigned)s.R), kCountT, 0, st>>>(
-        s, fsrc, s.rcnt, ilen);
-    const int T = std::min(1024, std::max(32, (s.N + 31) / 32 * 32));
-    const size_t sm = (size_t)s.N * (sizeof(uint64_t) + sizeof(float));
-    rank_count_finish_kernel<<<s.R, T, sm, st>>>(s, fsrc, s.rcnt);
+        s, fsrc, ilen);
     return cudaGetLastError();
   }
   int npad = 1;
@@ -508,7 +629,7 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
 }
 
 int rank_launches(const DevState& s) {
-  if (use_count(s)) return 2;
+  if (use_count(s)) return 1;
   int npad = 1, n = 1;
   while (npad < s.N) npad <<= 1;
   if (npad <= kChunk) return 1;

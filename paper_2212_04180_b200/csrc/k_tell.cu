@@ -11,12 +11,16 @@
 // result does not depend on scheduling) and runs the update epilogue in the same kernel.
 // Bound: Philox + Box–Muller issue rate (ALU); the state traffic (16–32 B/dim) is ~0.1 % of time.
 #include <algorithm>
+#include <cstdlib>
 
 #include "es_internal.h"
 #include "noise.cuh"
 
 namespace esb {
 
+#ifndef ES_TELL_MINB
+#define ES_TELL_MINB 8
+#endif
 static constexpr int TT = kTellThreads;
 
 // s.G layout [2][R][D]: the first R·D doubles are the only ones OpenAI-ES all-reduces.
@@ -182,7 +186,7 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
 // (Sep-CMA-ES elite ratios vmapped over runs) occupy few CTAs and the block scheduler packs
 // the SMs instead of one wave waiting on the longest runs. CTAs past nch_r exit at once.
 template <int ALGO>
-__global__ void __launch_bounds__(TT, 8) tell_kernel(DevState s, int bpr, int echunk, int fused) {
+__global__ void __launch_bounds__(TT, ES_TELL_MINB) tell_kernel(DevState s, int bpr, int echunk, int fused) {
   __shared__ uint32_t sdir[kTile];
   __shared__ double sA[kTile];
   __shared__ double sB[kTile];
@@ -641,6 +645,12 @@ static TellSplit pick_split_t(const DevState& s, const std::vector<int>& ent) {
 }
 
 TellSplit tell_pick_split(const DevState& s, const std::vector<int>& ent) {
+  if (const char* e = std::getenv("ES_TELL_ECHUNK")) {     // A/B switch for profiling
+    int emax = 1;
+    for (int v : ent) emax = std::max(emax, v);
+    const int ec = std::max(1, std::min(emax, std::atoi(e)));
+    return TellSplit{(emax + ec - 1) / ec, ec};
+  }
   switch (s.algo) {
     case OPENAI_ES: return pick_split_t<OPENAI_ES>(s, ent);
     case PGPE: return pick_split_t<PGPE>(s, ent);

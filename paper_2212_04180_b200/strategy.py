@@ -45,11 +45,14 @@ class Strategy:
     """R independent runs of one algorithm (vmap over seeds / hyperparameters)."""
 
     def __init__(self, algo, popsize, num_dims, params, device="cuda", group=None, stream=None,
-                 shard=None, split="population"):
+                 shard=None, split="population", single_comm=False):
         """params: one dict per run (es_run_params_t fields; 'seed' required).
         group: torch.distributed group for sharding with NCCL inside the library.
         shard: (rank, world_size) for a communicator-less shard (split-phase exchange).
-        split: "population" (es_init) or "dims" (f1 D-sharding, es_init_dshard)."""
+        split: "population" (es_init) or "dims" (f1 D-sharding, es_init_dshard).
+        single_comm: without a group, give the context a ONE-rank NCCL communicator so es_tell
+        runs the population-sharded data plane (all-gather, all-reduce, separate update) on one
+        GPU."""
         if isinstance(params, dict):
             params = [params]
         self.algo, self.popsize, self.num_dims = int(algo), int(popsize), int(num_dims)
@@ -75,6 +78,12 @@ class Strategy:
             torch.distributed.broadcast(bbuf, src=torch.distributed.get_global_rank(group, 0),
                                         group=group)
             buf = bbuf.cpu()
+            self._uid = buf
+            uid = C.c_void_p(buf.data_ptr())
+        elif single_comm:
+            n = lib().es_nccl_unique_id_size()
+            buf = torch.zeros(n, dtype=torch.uint8)
+            check(lib().es_nccl_get_unique_id(C.c_void_p(buf.data_ptr())))
             self._uid = buf
             uid = C.c_void_p(buf.data_ptr())
         if shard is not None:
