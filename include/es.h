@@ -362,6 +362,7 @@ int32_t es_profile_read(es_ctx_t *ctx, char *names /* [max_kinds][32] */, double
  *   which = 3  normals (N2):       in uint32 [n][6] = (q, i, t, tag, k0, k1)    → out float [n][4]
  *   which = 4  ρ square root:      in float [n] (= −2·LN(u))                    → out float [n]
  *   which = 5  sin(πb), b ≤ 1/2 (N7): in float [n]                              → out float [n]
+ *   which = 6  tanh of the MLP (N14): in float [n]                              → out float [n]
  * in/out are device pointers. Errors: ES_ERR_INVALID_ARG for unknown `which` or n < 0. */
 es_status_t es_debug_primitive(int32_t which, const void *in, void *out, int64_t n,
                                es_stream_t stream);

@@ -344,6 +344,16 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     c->split = tell_pick_split(s, ent);
     if (c->split.nchunk > 1)
       TRY(dalloc(c, (void**)&s.Gchunk, (size_t)c->split.nchunk * 2 * RD * sizeof(double)));
+    const std::vector<int4> items = tell_items(R, ent, c->split);
+    if (items.size() > 65535) {
+      fail(c, ES_ERR_UNSUPPORTED, "tell: %zu work items > 65535", items.size());
+      return bail(ES_ERR_UNSUPPORTED);
+    }
+    int4* dit = nullptr;
+    TRY(dalloc(c, (void**)&dit, items.size() * sizeof(int4)));
+    TRY(cudaMemcpyAsync(dit, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    c->split.items = dit;
+    c->split.nitems = (int)items.size();
   }
   TRY(cudaMemcpyAsync(s.rs, c->host_rs.data(), R * sizeof(RunScal), cudaMemcpyHostToDevice, st));
   TRY(cudaMemcpyAsync(s.wpos, wpos.data(), RN * sizeof(float), cudaMemcpyHostToDevice, st));
@@ -1130,7 +1140,7 @@ int32_t es_profile_read(es_ctx_t* c, char* names, double* ms, int64_t* counts, i
 
 es_status_t es_debug_primitive(int32_t which, const void* in, void* out, int64_t n,
                                es_stream_t stream_) {
-  if (which < 0 || which > 5 || n < 0) return fail(nullptr, ES_ERR_INVALID_ARG, "bad which/n");
+  if (which < 0 || which > 6 || n < 0) return fail(nullptr, ES_ERR_INVALID_ARG, "bad which/n");
   if (n > 0 && (!in || !out)) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
   CUDA_OR(nullptr, launch_primitive(which, in, out, n, (cudaStream_t)stream_));
   return ES_SUCCESS;

@@ -169,7 +169,16 @@ cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st);
 // applies them. Sep-CMA-ES additionally needs launch_sepcma_finish (global ‖p_σ‖, σ, h_σ, p_c, C).
 // Each returns the number of kernels it launched through *nk.
 // grid.y = nchunk; run r's entries are cut into chunks of echunk (see tell_kernel)
-struct TellSplit { int nchunk, echunk; };
+// The tell grid: x = quad block of a run, y = work item (run, entry chunk, the run's chunk count)
+// from a host-built table — runs with few entries get few items, so no CTA starts only to exit and
+// no CTA divides blockIdx to find its run. echunk entries per chunk (the last chunk of a run also
+// takes any tie-extended entries, Sep-CMA-ES N11).
+struct TellSplit {
+  int nchunk, echunk;    // largest chunk count of a run, entries per chunk
+  int nitems = 0;        // work items (grid.y)
+  const int4* items = nullptr;   // device [nitems] (run, chunk, chunks of the run, 0)
+};
+std::vector<int4> tell_items(int R, const std::vector<int>& ent, const TellSplit& sp);
 cudaError_t launch_tell_reduce(const DevState& s, bool fused, TellSplit sp, cudaStream_t st);
 cudaError_t launch_tell_update(const DevState& s, cudaStream_t st);
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk);

@@ -1,6 +1,7 @@
 // k_diag.cu — device evaluation of single NUMERICS primitives for the exhaustive parity tests
 // (es_debug_primitive). Uses exactly the device functions the hot kernels use.
 #include "es_internal.h"
+#include "fitness.cuh"
 #include "noise.cuh"
 
 namespace esb {
@@ -23,6 +24,8 @@ __global__ void prim_kernel(int which, const void* __restrict__ in, void* __rest
     static_cast<float*>(out)[k] = sinpi_half(static_cast<const float*>(in)[k]);
   } else if (which == 4) {
     static_cast<float*>(out)[k] = rho_sqrt(static_cast<const float*>(in)[k]);
+  } else if (which == 6) {
+    static_cast<float*>(out)[k] = tanh32(static_cast<const float*>(in)[k]);
   } else if (which == 1) {
     static_cast<float*>(out)[k] = ln_poly(static_cast<const float*>(in)[k]);
   } else {

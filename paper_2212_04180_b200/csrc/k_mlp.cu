@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "es_internal.h"
+#include "fitness.cuh"   // tanh32 (N14)
 #include "noise.cuh"
 #include "tcgen05.cuh"   // PTX helpers: mbarriers, TMA, UMMA descriptors, tcgen05 mma/ld/st
 
@@ -38,6 +39,17 @@ static constexpr int kThreadsTma = (1 + kEpiWarps + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
 static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 2048;   // + barriers, bias
+
+// ES_MLP_TRACE (profiling builds only): per-role wait / busy cycle totals of CTA 0, printed at exit.
+#ifdef ES_MLP_TRACE
+#define TR_DECL(v) long long v = 0
+#define TR_T0(t) const long long t = clock64()
+#define TR_ACC(v, t) v += clock64() - t
+#else
+#define TR_DECL(v)
+#define TR_T0(t)
+#define TR_ACC(v, t)
+#endif
 
 struct MlpParams {
   int nl;                       // layers L
@@ -106,9 +118,9 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   uint64_t* full = bars;                             // [kStages]
   uint64_t* empty = bars + kStages;                  // [kStages]
   uint64_t* dready = bars + 2 * kStages;             // [4] per 128-column n-tile of a layer
-  uint64_t* aready = bars + 2 * kStages + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
-  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 6);   // [kEpiWarps] (64 B)
+  uint64_t* aready = bars + 2 * kStages + 4;         // [4] per 128-k group of A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
+  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 9);   // [kEpiWarps] (64 B)
   // TMA mode: the layer's fp16 bias, staged once per layer (≤ 512 values)
   __half* bias_s = reinterpret_cast<__half*>(smem + kABytes + kStages * kTileBytes + 512);
 
@@ -121,7 +133,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
-    mbar_init(aready, 1);
+    for (int k = 0; k < 4; ++k) mbar_init(&aready[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kProd + kEpiWarps) {                   // TMEM: 512 fp32 columns × 128 lanes
@@ -136,41 +148,61 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   const int L = P.nl;
 
   if (TMA && warp == 0) {
-    // ------------------------------------------------------------ TMA producer (fp16 image)
-    if (lane == 0) {
-      for (int l = 1; l <= L; ++l)
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap[l])));
+    // ------------------------------------------------------------ TMA producer (fp16 image):
+    // whole warp, warp-uniform counters, one elected lane issues
+    {
+      if (lane == 0)
+        for (int l = 1; l <= L; ++l)
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap[l])));
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
-      // L2 look-ahead: keep kAhead tiles (256 KB) of the stream requested from HBM, so that the
-      // weight stream continues while the ring is full during the epilogues
-      constexpr int kAhead = 16;
+      TR_DECL(tr_empty);
+      TR_T0(tr_start);
+      // L2 look-ahead by (layer, n-tile) block: contiguous rows, plain bulk L2 prefetches of 16 KB
+      // per lane, two blocks ahead (the TMA engine only serves the tile loads)
       int64_t pm = blockIdx.x;
-      int pl = 1, pt = 0;
-      auto ahead = [&]() {
+      int pl = 1, pnt = 0;
+      const uintptr_t img_end = reinterpret_cast<uintptr_t>(P.x16) + (uintptr_t)P.n * P.D * 2;
+      auto prefetch_block = [&]() {
         if (pm >= P.n) return;
-        const int kcn = P.kpad[pl - 1] >> 6;
-        tma_prefetch_3d(&P.tmap[pl], (pt % kcn) * 64, (pt / kcn) * 128, (int)pm);
-        if (++pt == (P.npad[pl] >> 7) * kcn) {
-          pt = 0;
+        const int in = P.w[pl - 1], rows = min(128, P.w[pl] - pnt * 128);
+        if (rows > 0) {
+          const uintptr_t b0 = reinterpret_cast<uintptr_t>(P.x16) +
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 128 * in) * 2;
+          const uintptr_t lo = b0 & ~(uintptr_t)15;
+          const uintptr_t hi = min(img_end, b0 + (uintptr_t)rows * in * 2 + 15) & ~(uintptr_t)15;
+          for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
+            prefetch_l2(reinterpret_cast<const void*>(o), (uint32_t)min((uintptr_t)16384u, hi - o));
+        }
+        if (++pnt == (P.npad[pl] >> 7)) {
+          pnt = 0;
           if (++pl > L) { pl = 1; pm += gridDim.x; }
         }
       };
-      for (int k = 0; k < kAhead; ++k) ahead();
+      prefetch_block();
+      prefetch_block();
       for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
         for (int l = 1; l <= L; ++l) {
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
-          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
-            const int nt = tile / kc_n, kc = tile % kc_n;
-            ahead();
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], kTileBytes);
-            tma_load_3d(Bst + stage * kTileBytes, &P.tmap[l], kc * 64, nt * 128, (int)m,
-                        &full[stage]);
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          for (int nt = 0; nt < nt_n; ++nt) {
+            prefetch_block();
+            for (int kc = 0; kc < kc_n; ++kc) {
+              TR_T0(tw);
+              mbar_wait(&empty[stage], phase ^ 1);
+              TR_ACC(tr_empty, tw);
+              mbar_expect_tx_w(&full[stage], kTileBytes);
+              tma_load_3d_w(Bst + stage * kTileBytes, &P.tmap[l], kc * 64, nt * 128, (int)m,
+                            &full[stage]);
+              if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
           }
         }
       }
+#ifdef ES_MLP_TRACE
+      if (blockIdx.x == 0 && lane == 0)
+        printf("mlp16 trace producer: total %lld wait_empty %lld\n", clock64() - tr_start, tr_empty);
+#endif
     }
     __syncwarp();
   } else if (!TMA && warp < kProdWarps) {
@@ -252,6 +284,8 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
     const int row = q * 32 + lane;                   // batch row = TMEM lane
     const int et = threadIdx.x - kProd * 32;         // 0..511
     uint32_t dphase = 0;                             // bit k: parity of dready[k]
+    TR_DECL(tr_dready);
+    TR_T0(tr_start);
     for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
       const float* xm = P.x + m * P.D;
       // A <- layer-1 inputs (fp16 image, L2-resident)
@@ -262,7 +296,8 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
           reinterpret_cast<uint4*>(A)[o] = __ldg(src + o);
         fence_async_smem();
         named_bar(1, kEpiWarps * 32);
-        if (et == 0) mbar_arrive(aready);
+        if (et == 0)
+          for (int g = 0; g < (P.kpad[0] + 127) >> 7; ++g) mbar_arrive(&aready[g]);
       }
       float sq = 0.0f;
       for (int l = 1; l <= L; ++l) {
@@ -287,9 +322,34 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         // soon as it completes and the last tile's epilogue is short.
         const int cend = l < L ? P.kpad[l] : out;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        // next layer's A, k group t, from the packed fp16 results parked in TMEM (zeros past out)
+        auto write_a = [&](int t) {
+          const int c0 = t * 128 + part * 32;
+          if (c0 >= cend) return;
+          uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                        make_uint4(0, 0, 0, 0)};
+          if (c0 < out) tmem_ld16(trow + (uint32_t)c0, h);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {              // 4 chunks of 8 k in k-block c0/64
+            const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
+            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = h[c];
+          }
+        };
         for (int t = 0; t < ntl; ++t) {
+          TR_T0(td);
           mbar_wait(&dready[t], (dphase >> t) & 1u);
+          TR_ACC(tr_dready, td);
           tc_fence_after();
+          if (l < L && t == ntl - 1 && t > 0) {
+            // every MMA of this layer is done: A is free. k groups 0 … ntl−2 go first, so the
+            // next layer's MMAs start on them while this last tile's epilogue runs
+            for (int g = 0; g < ntl - 1; ++g) write_a(g);
+            fence_async_smem();
+            tc_fence_before();
+            named_bar(1, kEpiWarps * 32);
+            if (et == 0)
+              for (int g = 0; g < ntl - 1; ++g) mbar_arrive(&aready[g]);
+          }
           const int c0 = t * 128 + part * 32;
           if (c0 >= cend || c0 >= out) continue;     // padded K columns: zeros, written below
           float v[32];
@@ -303,7 +363,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
                 const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + n);
                 const __half* hh = reinterpret_cast<const __half*>(&hb);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[i + u] = tanhf(__fadd_rn(v[i + u], __half2float(hh[u])));
+                for (int u = 0; u < 8; ++u) v[i + u] = tanh32(__fadd_rn(v[i + u], __half2float(hh[u])));
               } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) v[i + u] = 0.0f;
@@ -313,16 +373,16 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
-              v[i] = tanhf(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
-              v[i + 1] = tanhf(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
-              v[i + 2] = tanhf(__fadd_rn(v[i + 2], __half2float(__float2half_rn(b4.z))));
-              v[i + 3] = tanhf(__fadd_rn(v[i + 3], __half2float(__float2half_rn(b4.w))));
+              v[i] = tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
+              v[i + 1] = tanh32(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
+              v[i + 2] = tanh32(__fadd_rn(v[i + 2], __half2float(__float2half_rn(b4.z))));
+              v[i + 3] = tanh32(__fadd_rn(v[i + 3], __half2float(__float2half_rn(b4.w))));
             }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int n = c0 + i;
-              v[i] = n < out ? tanhf(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
+              v[i] = n < out ? tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
                              : 0.0f;
             }
           }
@@ -347,26 +407,13 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
               if (c0 + i < out) P.Y[(int64_t)row * out + c0 + i] = v[i];
           }
         }
-        if (l < L) {
-          for (int t = 0; t < ntl; ++t) {
-            const int c0 = t * 128 + part * 32;
-            if (c0 >= cend) continue;
-            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
-                          make_uint4(0, 0, 0, 0)};
-            if (c0 < out) tmem_ld16(trow + (uint32_t)c0, h);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {            // 4 chunks of 8 k in k-block c0/64
-              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = h[c];
-            }
-          }
-        }
+        if (l < L) write_a(ntl - 1);
         dphase ^= (1u << ntl) - 1u;                  // every n-tile barrier completed once
         tc_fence_before();
         if (l < L) {
           fence_async_smem();
           named_bar(1, kEpiWarps * 32);
-          if (et == 0) mbar_arrive(aready);
+          if (et == 0) mbar_arrive(&aready[ntl - 1]);
         }
       }
       // fitness = Σ squares / (B · w_L)
@@ -381,37 +428,58 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
       }
       named_bar(1, kEpiWarps * 32);
     }
+#ifdef ES_MLP_TRACE
+    if (TMA && blockIdx.x == 0 && et == 0)
+      printf("mlp16 trace epi: total %lld dready %lld\n", clock64() - tr_start, tr_dready);
+#endif
   } else {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp: the
+    // loop's values stay warp-uniform; one elected lane issues each tcgen05 instruction)
+    {
       const uint32_t idesc = idesc_f16(128, 128);
       int stage = 0;
       uint32_t phase = 0, aphase = 0;
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      TR_DECL(tr_aready); TR_DECL(tr_full);
+      TR_T0(tr_start);
       for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
         for (int l = 1; l <= L; ++l) {
-          mbar_wait(aready, aphase);
-          aphase ^= 1;
-          tc_fence_after();
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
-          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
-            const int nt = tile / kc_n, kc = tile % kc_n;
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
+          for (int nt = 0; nt < nt_n; ++nt) {
+            const uint32_t dt = tmem + (uint32_t)(nt * 128);
+            for (int kc = 0; kc < kc_n; ++kc) {
+              if (nt == 0 && (kc & 1) == 0) {        // A's k group kc/2 (128 k) is written
+                const int g = kc >> 1;
+                TR_T0(ta);
+                mbar_wait(&aready[g], (aphase >> g) & 1u);
+                TR_ACC(tr_aready, ta);
+                aphase ^= 1u << g;
+                tc_fence_after();
+              }
+              TR_T0(tf);
+              mbar_wait(&full[stage], phase);
+              TR_ACC(tr_full, tf);
+              tc_fence_after();
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {          // K = 16 per instruction, 64 per tile
-              const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
-              const uint64_t bd = smem_desc(b_base + stage * kTileBytes + ks * 32);
-              mma_f16(tmem + (uint32_t)(nt * 128), ad, bd, idesc, (kc | ks) != 0);
+              for (int ks = 0; ks < 4; ++ks) {        // K = 16 per instruction, 64 per tile
+                const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
+                const uint64_t bd = smem_desc(b_base + stage * kTileBytes + ks * 32);
+                mma_f16_w(dt, ad, bd, idesc, (kc | ks) != 0);
+              }
+              mma_commit_w(&empty[stage]);           // frees the stage when these MMAs finish
+              // n-tile nt's accumulator is complete: its epilogue quarter starts while the
+              // remaining n-tiles of the layer are still being multiplied
+              if (kc == kc_n - 1) mma_commit_w(&dready[nt]);
+              if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
-            mma_commit(&empty[stage]);               // frees the stage when these MMAs finish
-            // n-tile nt's accumulator is complete: its epilogue quarter starts while the
-            // remaining n-tiles of the layer are still being multiplied
-            if (kc == kc_n - 1) mma_commit(&dready[nt]);
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
       }
+#ifdef ES_MLP_TRACE
+      if (TMA && blockIdx.x == 0 && lane == 0)
+        printf("mlp16 trace mma: total %lld wait_aready %lld wait_full %lld\n", clock64() - tr_start,
+               tr_aready, tr_full);
+#endif
     }
     __syncwarp();
   }
@@ -441,8 +509,11 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 static constexpr int kStages32 = 5;
 static constexpr int kT32Bytes = 128 * 64;                       // [128 n × 32 k] fp16 = 8 KB
 static constexpr int kStage32Bytes = 2 * kT32Bytes;              // hi tile + lo tile
-static constexpr int kXbufBytes = 8 * 2 * 32 * 8 * 4;            // 8 pairs × 2 bufs × 32 × 8 cols
-static constexpr int kSmem32Bytes = kABytes + kStages32 * kStage32Bytes + kXbufBytes + 1024;
+static constexpr int kXbufBytes = 8 * 2 * 8 * 32 * 4;            // 8 pairs × 2 dirs × 8 cols × 32
+static constexpr int kBias32Bytes = 512 * 4;                     // the layer's fp32 bias
+static constexpr int kSmem32Bytes =
+    kABytes + kStages32 * kStage32Bytes + kXbufBytes + kBias32Bytes + 1024;
+static_assert(kSmem32Bytes <= 232448, "fp32 MLP kernel exceeds 227 KB of shared memory");
 static constexpr int kThreads32 = (1 + kEpiWarps + 1) * 32;
 static constexpr float kSplitScale = 256.0f, kUnscale = 1.0f / 65536.0f;
 
@@ -469,20 +540,21 @@ __device__ __forceinline__ uint64_t smem_desc64(uint32_t addr) {
   return d;
 }
 
-__global__ void __launch_bounds__(kThreads32, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     mlp32_kernel(const __grid_constant__ MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                              // [8][128 rows][64] fp16
   uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][128][32] fp16
   float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
+  float* bias_s = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes + kXbufBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
-                                               kXbufBytes);
+                                               kXbufBytes + kBias32Bytes);
   uint64_t* full = bars;                                          // [kStages32]
   uint64_t* empty = bars + kStages32;
   uint64_t* dready = bars + 2 * kStages32;                        // [4]
-  uint64_t* aready = bars + 2 * kStages32 + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages32 + 5);
-  double* red = reinterpret_cast<double*>(bars + 2 * kStages32 + 6);   // [kEpiWarps]
+  uint64_t* aready = bars + 2 * kStages32 + 4;                    // [4] per 128-k group of A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages32 + 8);
+  double* red = reinterpret_cast<double*>(bars + 2 * kStages32 + 9);   // [kEpiWarps]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = blockIdx.x & 1;
@@ -492,10 +564,10 @@ __global__ void __launch_bounds__(kThreads32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages32; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);                   // the MMA commits of BOTH CTAs of the pair
     }
     for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
-    mbar_init(aready, 1);
+    for (int k = 0; k < 4; ++k) mbar_init(&aready[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1 + kEpiWarps) {
@@ -505,64 +577,96 @@ __global__ void __launch_bounds__(kThreads32, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();                            // the peer's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int L = P.nl;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (split image)
-    if (lane == 0) {
-      for (int l = 1; l <= L; ++l) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[0][l])));
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[1][l])));
-      }
+    // ------------------------------------------------------------ TMA producer (split image):
+    // the whole warp runs the loop (warp-uniform counters, no divisions); one elected lane issues
+    {
+      if (lane == 0)
+        for (int l = 1; l <= L; ++l) {
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[0][l])));
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmap32[1][l])));
+        }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
-      // L2 look-ahead over the (member, layer, n-tile, k-chunk) stream: issued by one CTA of the
-      // pair only (both read the same tiles)
-      constexpr int kAhead = 24;
+      TR_DECL(tr_empty);
+      TR_T0(tr_start);
+      // L2 look-ahead by (layer, n-tile) block: the block's rows of this CTA's plane are one
+      // contiguous range (≤ 128 rows × in × 2 B), prefetched with plain bulk L2 prefetches, 16 KB
+      // per lane, two blocks ahead of the loads — the TMA engine only serves the tile loads
+      // (tensor prefetches, one per tile and plane, had doubled its 64-B row requests)
       int64_t pm = pair;
-      int pl = 1, pt = 0;
-      auto ahead = [&]() {
-        if (half != 0 || pm >= P.n) return;
-        const int kcn = P.kpad[pl - 1] >> 5;
-        tma_prefetch_3d(&P.tmap32[0][pl], (pt % kcn) * 32, (pt / kcn) * 128, (int)pm);
-        tma_prefetch_3d(&P.tmap32[1][pl], (pt % kcn) * 32, (pt / kcn) * 128, (int)pm);
-        if (++pt == (P.npad[pl] >> 7) * kcn) {
-          pt = 0;
+      int pl = 1, pnt = 0;
+      const char* plane0 = reinterpret_cast<const char*>(P.img + (int64_t)half * P.n * P.D);
+      const uintptr_t plane_end = reinterpret_cast<uintptr_t>(plane0) + (uintptr_t)P.n * P.D * 2;
+      auto prefetch_block = [&]() {
+        if (pm >= P.n) return;
+        const int in = P.w[pl - 1], rows = min(128, P.w[pl] - pnt * 128);
+        if (rows > 0) {
+          const uintptr_t b0 = reinterpret_cast<uintptr_t>(plane0) +
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 128 * in) * 2;
+          const uintptr_t lo = b0 & ~(uintptr_t)15;
+          const uintptr_t hi = min(plane_end, b0 + (uintptr_t)rows * in * 2 + 15) & ~(uintptr_t)15;
+          for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
+            prefetch_l2(reinterpret_cast<const void*>(o), (uint32_t)min((uintptr_t)16384u, hi - o));
+        }
+        if (++pnt == (P.npad[pl] >> 7)) {
+          pnt = 0;
           if (++pl > L) { pl = 1; pm += npair; }
         }
       };
-      for (int k = 0; k < kAhead; ++k) ahead();
+      prefetch_block();
+      prefetch_block();
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
-          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
-            const int nt = tile / kc_n, kc = tile % kc_n;
-            ahead();
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], kStage32Bytes);
-            uint8_t* dst = Bst + stage * kStage32Bytes;
-            tma_load_3d(dst, &P.tmap32[0][l], kc * 32, nt * 128, (int)m, &full[stage]);
-            tma_load_3d(dst + kT32Bytes, &P.tmap32[1][l], kc * 32, nt * 128, (int)m, &full[stage]);
-            if (++stage == kStages32) { stage = 0; phase ^= 1; }
+          for (int nt = 0; nt < nt_n; ++nt) {
+            prefetch_block();
+            for (int kc = 0; kc < kc_n; ++kc) {
+              // both CTAs multiply the same weight tile: each loads one plane and multicasts it
+              // to the pair (every tile crosses L2 → SM once); the stage is reused once both
+              // CTAs' MMAs have read it (empty counts two commits)
+              TR_T0(tw);
+              mbar_wait(&empty[stage], phase ^ 1);
+              TR_ACC(tr_empty, tw);
+              mbar_expect_tx_w(&full[stage], kStage32Bytes);
+              uint8_t* dst = Bst + stage * kStage32Bytes + half * kT32Bytes;
+              tma_load_3d_mc_w(dst, &P.tmap32[half][l], kc * 32, nt * 128, (int)m, &full[stage], 3);
+              if (++stage == kStages32) { stage = 0; phase ^= 1; }
+            }
           }
         }
       }
+#ifdef ES_MLP_TRACE
+      if (blockIdx.x == 0 && lane == 0)
+        printf("mlp32 trace producer: total %lld wait_empty %lld\n", clock64() - tr_start, tr_empty);
+#endif
     }
     __syncwarp();
   } else if (warp < 1 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
+    // Warp pair (hi, lo) = (q, q ^ 2) of one 32-column part: the hi warp's lanes hold the A_hi
+    // rows' accumulators D[b], the lo warp's D[64 + b], both for batch row b. They swap 16 columns
+    // through shared memory, so BOTH finish 16 columns of b = D[b] + D[64+b]: the hi warp columns
+    // 0–15 of the part, the lo warp 16–31 (+ bias, tanh, split, or the squared error).
     const int e = warp - 1;                          // 0..15
     const int q = warp & 3, part = e >> 2;           // TMEM lane quarter, 32-column quarter
-    const bool hiw = q < 2;                          // lanes 0–63: the A_hi rows (and the result)
-    const int pr = e & 7;                            // warp pair: e and e ^ 2 share (q & 1, part)
-    const int prid = (part * 2 + (q & 1));           // named barrier of the pair
-    float* xb = xbuf + prid * (2 * 32 * 8);          // [2 bufs][8 cols][32 lanes]
-    (void)pr;
-    const int brow = half * 64 + (q & 1) * 32 + lane;   // batch row of this lane
+    const bool hiw = q < 2;                          // lanes 0–63: the A_hi rows
+    const int prid = part * 2 + (q & 1);             // named barrier of the pair
+    const int side = hiw ? 0 : 16;                   // this warp's 16 result columns in the part
+    float* xmine = xbuf + (prid * 2 + (hiw ? 0 : 1)) * (8 * 32);    // [8 cols][32 lanes] I write
+    const float* xpeer = xbuf + (prid * 2 + (hiw ? 1 : 0)) * (8 * 32);
+    const int rh = (q & 1) * 32 + lane;              // batch row within the half (A rows rh, 64+rh)
+    const int brow = half * 64 + rh;                 // batch row of this lane
     const int et = threadIdx.x - 32;                 // 0..511
     uint32_t dphase = 0;
+    TR_DECL(tr_dready); TR_DECL(tr_tile); TR_DECL(tr_awrite); TR_DECL(tr_bias);
+    TR_T0(tr_start);
     for (int64_t m = pair; m < P.n; m += npair) {
       const __half* bhi = P.img + m * P.D;             // this member's hi / lo planes
       const __half* blo = P.img + (P.n + m) * P.D;
@@ -573,7 +677,8 @@ __global__ void __launch_bounds__(kThreads32, 1)
           reinterpret_cast<uint4*>(A)[o] = __ldg(src + o);
         fence_async_smem();
         named_bar(1, kEpiWarps * 32);
-        if (et == 0) mbar_arrive(aready);
+        if (et == 0)
+          for (int g = 0; g < (P.kpad[0] + 127) >> 7; ++g) mbar_arrive(&aready[g]);
       }
       double sq = 0.0;
       for (int l = 1; l <= L; ++l) {
@@ -581,91 +686,107 @@ __global__ void __launch_bounds__(kThreads32, 1)
         const int64_t boff = P.off[l] + (int64_t)out * in;   // b_l inside the layer block
         const int ntl = P.npad[l] >> 7;
         const int cend = l < L ? P.kpad[l] : out;
+        // b = (hi + lo)·2^-8 (exact in fp32: ≤ 22 significant bits), staged while the MMAs run
+        TR_T0(tb);
+        for (int n = et; n < P.npad[l]; n += kEpiWarps * 32)
+          bias_s[n] = n < out ? __fmul_rn(__fadd_rn(__half2float(bhi[boff + n]),
+                                                    __half2float(blo[boff + n])), 1.0f / kSplitScale)
+                              : 0.0f;
+        named_bar(1, kEpiWarps * 32);
+        TR_ACC(tr_bias, tb);
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        // next layer's A, k group t (rows rh: hi split, 64 + rh: lo split) from the split values
+        // parked in TMEM; padded K columns [out, kpad) written as zeros
+        auto write_a = [&](int t) {
+          const int cb = t * 128 + part * 32 + side;
+          if (cb >= cend) return;
+          uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                        make_uint4(0, 0, 0, 0)};
+          if (cb - side < out) tmem_ld16(trow + (uint32_t)cb, h);
+          const int kb = cb >> 6, ck = (cb & 63) >> 3;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck + c)) = h[c];
+            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck + c)) = h[2 + c];
+          }
+        };
         for (int t = 0; t < ntl; ++t) {
+          TR_T0(td);
           mbar_wait(&dready[t], (dphase >> t) & 1u);
+          TR_ACC(tr_dready, td);
+          TR_T0(tt);
           tc_fence_after();
+          if (l < L && t == ntl - 1 && t > 0) {
+            // every MMA of this layer is done: A is free. Groups 0 … ntl−2 go first, so the next
+            // layer's MMAs start on them while this last tile's epilogue runs
+            for (int g = 0; g < ntl - 1; ++g) write_a(g);
+            fence_async_smem();
+            tc_fence_before();
+            named_bar(1, kEpiWarps * 32);
+            if (et == 0)
+              for (int g = 0; g < ntl - 1; ++g) mbar_arrive(&aready[g]);
+          }
           const int c0 = t * 128 + part * 32;
           if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
           float v[32];
           tmem_ld32(trow + (uint32_t)c0, v);
-          // lo rows → hi rows, 8 columns per round through two ping-pong buffers
+          // swap the peer's half of the 32 columns in two rounds of 8 through one 8-column buffer
+          // per direction (4 barriers of the pair: the buffer is rewritten only after the peer
+          // has read it)
+          float x[16];
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            float* b = xb + (rr & 1) * (32 * 8);
-            if (!hiw) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) b[i * 32 + lane] = v[8 * rr + i];
-            }
+          for (int rr = 0; rr < 2; ++rr) {
             named_bar(2 + prid, 64);
-            if (hiw) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[8 * rr + i] = __fadd_rn(v[8 * rr + i], b[i * 32 + lane]);
-            }
+            for (int i = 0; i < 8; ++i)
+              xmine[i * 32 + lane] = hiw ? v[16 + 8 * rr + i] : v[8 * rr + i];
+            named_bar(2 + prid, 64);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              x[8 * rr + i] = __fadd_rn(hiw ? v[8 * rr + i] : v[16 + 8 * rr + i], xpeer[i * 32 + lane]);
           }
-          named_bar(2 + prid, 64);                   // buffers free for the next chunk
-          if (!hiw) continue;
-          // b = (hi + lo)·2^-8 (the sum is exact in fp32: ≤ 22 significant bits)
+          const int cb = c0 + side;                  // first of this warp's 16 columns
+          // a = D·2^-16 + b (the product by 2^-16 is exact), h = tanh(a)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int n = c0 + i;
-            if (n < out) {
-              const float b = __fmul_rn(__fadd_rn(__half2float(bhi[boff + n]),
-                                                  __half2float(blo[boff + n])), 1.0f / kSplitScale);
-              v[i] = tanhf(__fadd_rn(__fmul_rn(v[i], kUnscale), b));
-            } else {
-              v[i] = 0.0f;
-            }
+          for (int i = 0; i < 16; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias_s + cb + i);
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              x[i + u] = cb + i + u < out ? tanh32(__fmaf_rn(x[i + u], kUnscale, bb[u])) : 0.0f;
           }
           if (l < L) {
-            uint4 h[4], g[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) split8(v + 8 * c, h[c], g[c]);
-            tmem_st16(trow + (uint32_t)c0, h);        // parked in the tile's consumed columns
-            tmem_st16(trow + (uint32_t)c0 + 16, g);
+            uint4 h[4];                              // hi split of 16 columns, then the lo split
+            split8(x, h[0], h[2]);
+            split8(x + 8, h[1], h[3]);
+            tmem_st16(trow + (uint32_t)cb, h);       // parked in this lane's consumed columns
           } else if (P.mode == 0) {
             const float* yr = P.Y32 + (int64_t)brow * out;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int n = c0 + i;
+            for (int i = 0; i < 16; ++i) {
+              const int n = cb + i;
               if (n < out) {
-                const double d = (double)v[i] - (double)__ldg(yr + n);
+                const double d = (double)x[i] - (double)__ldg(yr + n);
                 sq = __fma_rn(d, d, sq);
               }
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c0 + i < out) P.Y32[(int64_t)brow * out + c0 + i] = v[i];
+            for (int i = 0; i < 16; ++i)
+              if (cb + i < out) P.Y32[(int64_t)brow * out + cb + i] = x[i];
           }
+          TR_ACC(tr_tile, tt);
         }
-        if (l < L && hiw) {
-          const int rh = (q & 1) * 32 + lane;        // A rows: rh (hi), 64 + rh (lo)
-          for (int t = 0; t < ntl; ++t) {
-            const int c0 = t * 128 + part * 32;
-            if (c0 >= cend) continue;
-            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
-                          make_uint4(0, 0, 0, 0)};
-            uint4 g[4] = {h[0], h[1], h[2], h[3]};
-            if (c0 < out) {
-              tmem_ld16(trow + (uint32_t)c0, h);
-              tmem_ld16(trow + (uint32_t)c0 + 16, g);
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck)) = h[c];
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck)) = g[c];
-            }
-          }
-        }
+        TR_T0(ta);
+        if (l < L) write_a(ntl - 1);
         dphase ^= (1u << ntl) - 1u;
         tc_fence_before();
         if (l < L) {
           fence_async_smem();
           named_bar(1, kEpiWarps * 32);
-          if (et == 0) mbar_arrive(aready);
+          if (et == 0) mbar_arrive(&aready[ntl - 1]);
         }
+        TR_ACC(tr_awrite, ta);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
@@ -687,44 +808,65 @@ __global__ void __launch_bounds__(kThreads32, 1)
       }
       named_bar(1, kEpiWarps * 32);
     }
+#ifdef ES_MLP_TRACE
+    if (blockIdx.x == 0 && (et == 0 || et == 32 * 8))
+      printf("mlp32 trace epi warp %d: total %lld dready %lld tiles %lld awrite %lld bias %lld\n", e,
+             clock64() - tr_start, tr_dready, tr_tile, tr_awrite, tr_bias);
+#endif
   } else {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, one
+    // elected lane issues)
+    {
       const uint32_t idesc = idesc_f16(128, 128);
       int stage = 0;
-      uint32_t phase = 0, aphase = 0;
+      uint32_t phase = 0, aphase = 0;                // aphase bit g: parity of aready[g]
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      TR_DECL(tr_aready); TR_DECL(tr_full);
+      TR_T0(tr_start);
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
-          mbar_wait(aready, aphase);
-          aphase ^= 1;
-          tc_fence_after();
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
-          for (int tile = 0; tile < nt_n * kc_n; ++tile) {
-            const int nt = tile / kc_n, kc = tile % kc_n;
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t bs = b_base + stage * kStage32Bytes;
+          for (int nt = 0; nt < nt_n; ++nt) {
+            const uint32_t dt = tmem + (uint32_t)(nt * 128);
+            for (int kc = 0; kc < kc_n; ++kc) {
+              if (nt == 0 && (kc & 3) == 0) {        // A's k group kc/4 is written
+                const int g = kc >> 2;
+                TR_T0(ta);
+                mbar_wait(&aready[g], (aphase >> g) & 1u);
+                TR_ACC(tr_aready, ta);
+                aphase ^= 1u << g;
+                tc_fence_after();
+              }
+              TR_T0(tf);
+              mbar_wait(&full[stage], phase);
+              TR_ACC(tr_full, tf);
+              tc_fence_after();
+              const uint32_t bs = b_base + stage * kStage32Bytes;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {          // K = 16 per instruction, 32 per stage
-              const uint64_t ad = smem_desc(a_base + (kc >> 1) * kTileBytes +
-                                            (((kc & 1) * 2 + j) * 32));
-              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc64(bs + j * 32), idesc,
-                      (kc | j) != 0);
-              mma_f16(tmem + (uint32_t)(nt * 128), ad, smem_desc64(bs + kT32Bytes + j * 32),
-                      idesc, 1u);
+              for (int j = 0; j < 2; ++j) {        // K = 16 per instruction, 32 per stage
+                const uint64_t ad = smem_desc(a_base + (kc >> 1) * kTileBytes +
+                                              (((kc & 1) * 2 + j) * 32));
+                mma_f16_w(dt, ad, smem_desc64(bs + j * 32), idesc, (kc | j) != 0);
+                mma_f16_w(dt, ad, smem_desc64(bs + kT32Bytes + j * 32), idesc, 1u);
+              }
+              mma_commit_mc_w(&empty[stage], 3);    // frees the stage in both CTAs' rings
+              if (kc == kc_n - 1) mma_commit_w(&dready[nt]);
+              if (++stage == kStages32) { stage = 0; phase ^= 1; }
             }
-            mma_commit(&empty[stage]);
-            if (kc == kc_n - 1) mma_commit(&dready[nt]);
-            if (++stage == kStages32) { stage = 0; phase ^= 1; }
           }
         }
       }
+#ifdef ES_MLP_TRACE
+      if (blockIdx.x == 0 && lane == 0)
+        printf("mlp32 trace mma: total %lld wait_aready %lld wait_full %lld\n", clock64() - tr_start,
+               tr_aready, tr_full);
+#endif
     }
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();                            // no CTA leaves while its peer may still signal it
   if (warp == 1 + kEpiWarps) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -874,7 +1016,25 @@ static cudaError_t launch_mlp32(MlpParams q, const __half* img, cudaStream_t st)
   if (cudaError_t e = smem_attr_once((const void*)mlp32_kernel, kSmem32Bytes, attr)) return e;
   if (cudaError_t e = encode_maps32(q, img, q.n)) return e;
   q.img = img;
-  const int pairs = (int)std::min<int64_t>(q.n, std::max(1, sm_count() / 2));
+  // persistent: as many CTA pairs as can be co-resident (not every SM has a cluster partner),
+  // so that no pair waits for a second wave
+  static std::atomic<int> max_pairs{0};
+  int mp = max_pairs.load();
+  if (mp == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (unsigned)std::max(1, sm_count() / 2));
+    cfg.blockDim = dim3(kThreads32);
+    cfg.dynamicSmemBytes = kSmem32Bytes;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&mp, (const void*)mlp32_kernel, &cfg) != cudaSuccess || mp < 1)
+      mp = std::max(1, sm_count() / 2);
+    max_pairs.store(mp);
+  }
+  const int pairs = (int)std::min<int64_t>(q.n, mp);
   mlp32_kernel<<<2 * pairs, kThreads32, kSmem32Bytes, st>>>(q);
   return cudaGetLastError();
 }

@@ -575,6 +575,8 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   }
 }
 
+// (For many runs the per-run register bitonic sort stays faster: counting at R = 512, N = 256
+// measured 22.8 vs 15 µs per launch.)
 static bool use_count(const DevState& s) {
   return s.rank_par && s.R <= kCountMaxR && s.N <= kCountMaxN;
 }

@@ -186,24 +186,25 @@ __device__ void apply_update(const DevState& s, int r, int64_t q, bool active, c
 // (Sep-CMA-ES elite ratios vmapped over runs) occupy few CTAs and the block scheduler packs
 // the SMs instead of one wave waiting on the longest runs. CTAs past nch_r exit at once.
 template <int ALGO>
-__global__ void __launch_bounds__(TT, ES_TELL_MINB) tell_kernel(DevState s, int bpr, int echunk, int fused) {
+__global__ void __launch_bounds__(TT, ES_TELL_MINB) tell_kernel(DevState s,
+                                                                 const int4* __restrict__ items,
+                                                                 int echunk, int fused) {
   __shared__ uint32_t sdir[kTile];
   __shared__ double sA[kTile];
   __shared__ double sB[kTile];
   __shared__ double red[TT / 32];
   __shared__ int sh_last;
-  const int r = blockIdx.x / bpr;
-  const int qb = blockIdx.x % bpr;
+  const int4 it = items[blockIdx.y];
+  const int r = it.x, chunk = it.y, nchunk = it.z;
+  const int qb = blockIdx.x, bpr = gridDim.x;
   const int64_t q = (int64_t)qb * TT + threadIdx.x;
   const bool active = q < s.Q;
-  const int chunk = blockIdx.y;
   const GenScal& gs = s.gs[r];
   const int ne = gs.nentries;
-  int e0, e1;
-  shard_range(ne, s.W, s.rank, e0, e1);
-  const int nchunk = max(1, (e1 - e0 + echunk - 1) / echunk);
-  if (chunk >= nchunk) return;
-  const int c0 = min(e1, e0 + chunk * echunk), c1 = min(e1, c0 + echunk);
+  int e0 = 0, e1 = ne;
+  if (s.W > 1) shard_range(ne, s.W, s.rank, e0, e1);
+  const int c0 = min(e1, e0 + chunk * echunk);
+  const int c1 = chunk == nchunk - 1 ? e1 : min(e1, c0 + echunk);
   const Philox ph(s.rs[r].seed);
   const uint32_t t = gs.t;
   const uint32_t* dir = s.dir + (int64_t)r * s.N;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(TT) update_kernel(DevState s, int bpr) {
 // Fixed-order sum of run r's per-block norm partials (valid in thread 0).
 __device__ __forceinline__ double normpart_total(const DevState& s, int r, int bpr, double* red) {
   double v = 0.0;
-  for (int b = threadIdx.x; b < bpr; b += blockDim.x) v = __dadd_rn(v, s.normpart[(int64_t)r * bpr + b]);
+  for (int b = threadIdx.x; b < bpr; b += blockDim.x) v = __dadd_rn(v, __ldcg(&s.normpart[(int64_t)r * bpr + b]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -362,8 +363,8 @@ __device__ __forceinline__ void sepcma_pc_elem(const DevState& s, int r, int64_t
   const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
   const float aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
   const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
-  const float Z = (float)s.G[gidx(s, 0, r, d)];
-  const float Qv = (float)s.G[gidx(s, 1, r, d)];
+  const float Z = (float)__ldcg(&s.G[gidx(s, 0, r, d)]);
+  const float Qv = (float)__ldcg(&s.G[gidx(s, 1, r, d)]);
   const int64_t idx = (int64_t)r * s.D + d;
   const float C0 = s.vec[F_C][idx];
   const float y = __fmul_rn(__fsqrt_rn(C0), Z);
@@ -613,13 +614,16 @@ static TellSplit pick_split_t(const DevState& s, const std::vector<int>& ent) {
   const int64_t blocks = (int64_t)s.R * bpr;
   int emax = 1;
   for (int e : ent) emax = std::max(emax, e);
-  const double c0 = 8.0, cempty = 0.25;
+  const double c0 = 8.0;
   TellSplit best{1, emax};
   double best_t = 1e300;
   std::vector<double> heap;
   for (int n = 1; n <= std::min(64, emax); ++n) {
     const int ec = (emax + n - 1) / n;
     if (n > 1 && (emax + ec - 1) / ec != n) continue;         // same echunk as a smaller n
+    int64_t nit = 0;                                           // grid.y ≤ 65535 work items
+    for (int e : ent) nit += std::max(1, (e + ec - 1) / ec);
+    if (n > 1 && nit > 65535) break;
     double tn;
     if (blocks * n <= 65536) {
       heap.assign((size_t)slots, 0.0);                         // min-heap of slot free times
@@ -627,7 +631,8 @@ static TellSplit pick_split_t(const DevState& s, const std::vector<int>& ent) {
       for (int y = 0; y < n; ++y) {
         for (int r = 0; r < s.R; ++r) {
           const int nch = std::max(1, (ent[r] + ec - 1) / ec);
-          const double len = y < nch ? std::min(ec, ent[r] - y * ec) + c0 : cempty;
+          if (y >= nch) continue;                    // no CTA: the item table skips it
+          const double len = std::min(ec, ent[r] - y * ec) + c0;
           for (int b = 0; b < bpr; ++b) {
             std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
             heap.back() += len;
@@ -660,11 +665,20 @@ TellSplit tell_pick_split(const DevState& s, const std::vector<int>& ent) {
   }
 }
 
+std::vector<int4> tell_items(int R, const std::vector<int>& ent, const TellSplit& sp) {
+  std::vector<int4> it;
+  for (int y = 0; y < sp.nchunk; ++y)            // chunk-major: the block scheduler starts every
+    for (int r = 0; r < R; ++r) {                // run's first chunk before anyone's second
+      const int nch = std::max(1, (ent[r] + sp.echunk - 1) / sp.echunk);
+      if (y < nch) it.push_back(make_int4(r, y, nch, 0));
+    }
+  return it;
+}
+
 template <int ALGO>
 static void launch_tell_t(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {
-  const int bpr = tell_blocks_per_run(s);
-  dim3 grid((unsigned)(s.R * bpr), (unsigned)sp.nchunk);
-  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, bpr, sp.echunk, fused ? 1 : 0);
+  dim3 grid((unsigned)tell_blocks_per_run(s), (unsigned)sp.nitems);
+  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, sp.items, sp.echunk, fused ? 1 : 0);
 }
 
 cudaError_t launch_tell_reduce(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {

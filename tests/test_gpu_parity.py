@@ -88,6 +88,22 @@ def test_sincos_exhaustive_bit_exact():
     assert np.array_equal(bits(dev[:, 0]), bits(c)) and np.array_equal(bits(dev[:, 1]), bits(s))
 
 
+def test_mlp_tanh_accuracy():
+    """N14's activation: the device tanh (odd rational x p(x^2)/q(x^2), one MUFU rcp) is
+    within 5e-7 relative of binary64 tanh over a dense sweep of [-12, 12], tiny and huge values
+    (odd, saturating at +-1, tanh(0) = 0)."""
+    rng = np.random.default_rng(11)
+    x = np.concatenate([np.linspace(-12, 12, 1 << 22), rng.uniform(-0.7, 0.7, 1 << 20),
+                        np.exp2(rng.uniform(-40, 3, 1 << 18)) * rng.choice([-1, 1], 1 << 18),
+                        [0.0, -0.0, 0.625, -0.625, 0.62499997, 30.0, -30.0, 1e30, -1e30]])
+    x = x.astype(np.float32)
+    dev = _prim(6, torch.from_numpy(x).cuda(), torch.empty(x.size, device="cuda")).cpu().numpy()
+    ref = np.tanh(x.astype(np.float64))
+    rel = np.abs(dev.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1e-30)
+    assert rel.max() <= 5e-7, (rel.max(), x[rel.argmax()])
+    assert np.all(dev[x == 0] == 0.0)
+
+
 @pytest.mark.parametrize("seed,i,t,tag", [(0, 0, 0, 0), (12345, 7, 3, 0), (2 ** 40 + 5, 99, 1000, 1),
                                           (77, 0, 0, 4)])
 def test_normals_bit_exact(seed, i, t, tag):
