@@ -175,6 +175,14 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
           for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
             prefetch_l2(reinterpret_cast<const void*>(o), (uint32_t)min((uintptr_t)16384u, hi - o));
         }
+        if (pnt == 0 && lane == 31) {                // the layer's bias (staged at layer start)
+          const int out = P.w[pl];
+          const uintptr_t b0 = reinterpret_cast<uintptr_t>(P.x16) +
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)out * in) * 2;
+          const uintptr_t lo = b0 & ~(uintptr_t)15;
+          const uintptr_t hi = min(img_end, b0 + (uintptr_t)out * 2 + 15) & ~(uintptr_t)15;
+          if (hi > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
+        }
         if (++pnt == (P.npad[pl] >> 7)) {
           pnt = 0;
           if (++pl > L) { pl = 1; pm += gridDim.x; }
@@ -614,6 +622,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           const uintptr_t hi = min(plane_end, b0 + (uintptr_t)rows * in * 2 + 15) & ~(uintptr_t)15;
           for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
             prefetch_l2(reinterpret_cast<const void*>(o), (uint32_t)min((uintptr_t)16384u, hi - o));
+        }
+        if (pnt == 0 && lane == 31) {                // the layer's bias (this plane's part)
+          const int out = P.w[pl];
+          const uintptr_t b0 = reinterpret_cast<uintptr_t>(plane0) +
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)out * in) * 2;
+          const uintptr_t lo = b0 & ~(uintptr_t)15;
+          const uintptr_t hi = min(plane_end, b0 + (uintptr_t)out * 2 + 15) & ~(uintptr_t)15;
+          if (hi > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
         }
         if (++pnt == (P.npad[pl] >> 7)) {
           pnt = 0;

@@ -476,33 +476,46 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
     }
   }
   const int64_t RN = (int64_t)s.R * N, rj = (int64_t)r * N + j;
-  if (j < N) {
-    if (cpos) atomicAdd(&s.rcnt[rj], cpos);
-    if (clt) atomicAdd(&s.rcnt[RN + rj], clt);
-    if (cle) atomicAdd(&s.rcnt[2 * RN + rj], cle);
+  // one CTA covers the whole run (N ≤ 256): the counts are final in registers — no atomics,
+  // arrival counters or fences (the multi-CTA path's four global round trips are its latency)
+  const bool solo = jt == 1 && ni == 1;
+  if (!solo) {
+    if (j < N) {
+      if (cpos) atomicAdd(&s.rcnt[rj], cpos);
+      if (clt) atomicAdd(&s.rcnt[RN + rj], clt);
+      if (cle) atomicAdd(&s.rcnt[2 * RN + rj], cle);
+    }
+    // ---- the last i-range CTA of this j-tile finishes its members
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t* tc = rc_tile(s) + (int64_t)r * kCountMaxTiles + blockIdx.x;
+      sh_last = atomicAdd(tc, 1u) == (uint32_t)(ni - 1);
+      if (sh_last) *tc = 0u;
+    }
+    __syncthreads();
+    if (!sh_last) return;
+    __threadfence();
   }
-  // ---- the last i-range CTA of this j-tile finishes its members
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t* tc = rc_tile(s) + (int64_t)r * kCountMaxTiles + blockIdx.x;
-    sh_last = atomicAdd(tc, 1u) == (uint32_t)(ni - 1);
-    if (sh_last) *tc = 0u;
-  }
-  __syncthreads();
-  if (!sh_last) return;
-  __threadfence();
   const RunScal& rs = s.rs[r];
   const bool anti = is_anti(s.algo), cmaish = s.algo == SEP_CMA_ES || s.algo == CMA_ES;
   float val = 0.0f;
   int pos = 0;
+  __shared__ int sh_jbest, sh_nw;
   if (j < N) {
-    pos = (int)__ldcg(&s.rcnt[rj]);
-    const int sj = (int)__ldcg(&s.rcnt[RN + rj]);
-    const int ej = (int)__ldcg(&s.rcnt[2 * RN + rj]) - 1;
-    s.rcnt[rj] = 0u;
-    s.rcnt[RN + rj] = 0u;
-    s.rcnt[2 * RN + rj] = 0u;
+    int sj, ej;
+    if (solo) {
+      pos = (int)cpos;
+      sj = (int)clt;
+      ej = (int)cle - 1;
+    } else {
+      pos = (int)__ldcg(&s.rcnt[rj]);
+      sj = (int)__ldcg(&s.rcnt[RN + rj]);
+      ej = (int)__ldcg(&s.rcnt[2 * RN + rj]) - 1;
+      s.rcnt[rj] = 0u;
+      s.rcnt[RN + rj] = 0u;
+      s.rcnt[2 * RN + rj] = 0u;
+    }
     s.perm[(int64_t)r * N + pos] = j;
     s.rs_s[rj] = sj;
     s.rs_e[rj] = ej;
@@ -519,8 +532,13 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       val = __fdiv_rn(acc, (float)(ej - sj + 1));
     }
     s.shaped[rj] = val;
-    if (pos == 0) rc_slot(s)[2 * r] = (uint32_t)j;
-    if (cmaish && pos == rs.mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
+    if (solo) {
+      if (pos == 0) sh_jbest = j;
+      if (cmaish && pos == rs.mu - 1) sh_nw = ej + 1;
+    } else {
+      if (pos == 0) rc_slot(s)[2 * r] = (uint32_t)j;
+      if (cmaish && pos == rs.mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
+    }
   }
   sval[threadIdx.x] = val;
   __syncthreads();
@@ -544,7 +562,20 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   }
   if (s.algo == PGPE) {
     const double t = block_sum(part, red);
+    if (solo) {                               // the baseline and the generation's scalars here
+      const double bbar = t / (double)N;
+      __syncthreads();
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) cB[i] = __dsub_rn(cB[i], bbar);
+      if (threadIdx.x == 0) write_genscal(s, r, sh_jbest, s.fit[(int64_t)r * N + sh_jbest], 0, bbar, 0.0f);
+      return;
+    }
     if (threadIdx.x == 0) s.rbpart[(int64_t)r * kCountMaxTiles + blockIdx.x] = t;
+  }
+  if (solo) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      write_genscal(s, r, sh_jbest, s.fit[(int64_t)r * N + sh_jbest], cmaish ? sh_nw : 0, 0.0, 0.0f);
+    return;
   }
   // ---- the last j-tile of the run: the generation's scalars
   __threadfence();

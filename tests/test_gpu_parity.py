@@ -139,7 +139,7 @@ def test_ask_bit_exact(algo, N, D):
 
 # ------------------------------------------------------------------------ fitness
 @pytest.mark.parametrize("fn", FNS)
-@pytest.mark.parametrize("n,D", [(7, 1), (33, 2), (64, 7), (64, 1000), (12000, 21), (16, 4097), (4, 70001),
+@pytest.mark.parametrize("n,D", [(7, 1), (33, 2), (64, 7), (64, 1000), (12000, 21), (50, 6000), (16, 4097), (4, 70001),
                                  (3, 262144)])
 def test_eval_parity(fn, n, D):
     from paper_2212_04180_b200 import strategy as S
