@@ -310,7 +310,11 @@ def config_block(cfg_key, world):
                             f"{MLP_WIDTHS} (D=985,216), popsize 4096, batch 128",
                 "R": 1, "N": c["N"], "D": c["D"],
                 "parallelism": f"population sharded x{world}" if world > 1 else "1 GPU",
-                "l2": "inputs larger than L2: x is 16.1 GB per step"}
+                "l2": ("inputs larger than L2: the MLP reads the population's split binary16 "
+                       "image (hi and lo planes, 16.1 GB per step) the ask wrote; x itself is not "
+                       "materialised in fp32" if MLP_MODE["mode"] == "fp32" else
+                       "inputs larger than L2: the MLP reads the population's fp16 image (8.07 GB "
+                       "per step) the ask wrote; x itself is not materialised in fp32")}
     if cfg_key == "c5":
         cfg = sweep_cfg(SWEEP["N"], SWEEP["D"])
         return {"workload": f"c5 cell: {cfg['name']} (tell only on synthetic fitness, the north-star "
@@ -685,8 +689,10 @@ def main():
                       "the fp16 parameter image (N14', a labelled approximation of N14), "
                       "TMA-fed tcgen05 MLP fitness, then tell")
     elif fused and hs[0][1]["fn"] == W.MLP:
-        cb["path"] = ("es_ask_eval: ask writes x (fp32, internal buffer), fp32-accurate tcgen05 MLP "
-                      "fitness (N14: binary16 hi/lo split, three products in TMEM), then tell")
+        cb["path"] = ("es_ask_eval: the ask writes the population's split binary16 image (N14: hi "
+                      "and lo parts of x*2^8" + (", and x" if write_x else "; x not materialised") +
+                      "), the fp32-accurate tcgen05 MLP fitness streams it (2-CTA pair MMAs, three "
+                      "products summed in TMEM), then tell")
     elif fused:
         cb["path"] = "fused ask+evaluate kernel" + (" (x written)" if write_x else "") + ", tell"
     else:

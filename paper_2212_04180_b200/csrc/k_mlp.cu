@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
               if (nt == 0 && (kc & 1) == 0) {        // A's k group kc/2 (128 k) is written
                 const int g = kc >> 1;
                 TR_T0(ta);
-                mbar_wait(&aready[g], (aphase >> g) & 1u);
+                mbar_wait_cluster(&aready[g], (aphase >> g) & 1u);
                 TR_ACC(tr_aready, ta);
                 aphase ^= 1u << g;
                 tc_fence_after();
@@ -514,9 +514,9 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 // halves are combined in a fixed order by whichever CTA finishes second. The epilogue's lane
 // quarters 2–3 (the lo rows) hand their accumulator to quarters 0–1 through shared memory, 8
 // columns per round in two ping-pong buffers.
-static constexpr int kStages32 = 5;
-static constexpr int kT32Bytes = 128 * 64;                       // [128 n × 32 k] fp16 = 8 KB
-static constexpr int kStage32Bytes = 2 * kT32Bytes;              // hi tile + lo tile
+static constexpr int kStages32 = 10;
+static constexpr int kH32Bytes = 64 * 64;                        // [64 n × 32 k] fp16 = 4 KB
+static constexpr int kStage32Bytes = 2 * kH32Bytes;              // this CTA's hi half + lo half
 static constexpr int kXbufBytes = 8 * 2 * 8 * 32 * 4;            // 8 pairs × 2 dirs × 8 cols × 32
 static constexpr int kBias32Bytes = 512 * 4;                     // the layer's fp32 bias
 static constexpr int kSmem32Bytes =
@@ -552,7 +552,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     mlp32_kernel(const __grid_constant__ MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                              // [8][128 rows][64] fp16
-  uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][128][32] fp16
+  uint8_t* Bst = smem + kABytes;                                  // [10][hi, lo][64][32] fp16
   float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
   float* bias_s = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes + kXbufBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
@@ -571,21 +571,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages32; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);                   // the MMA commits of BOTH CTAs of the pair
+      mbar_init(&full[s], 1);                    // CTA 0's: its producer's expect_tx
+      mbar_init(&empty[s], 1);                   // the pair MMA's multicast commit
     }
     for (int k = 0; k < 4; ++k) mbar_init(&dready[k], 1);
-    for (int k = 0; k < 4; ++k) mbar_init(&aready[k], 1);
+    for (int k = 0; k < 4; ++k) mbar_init(&aready[k], 2);   // CTA 0's: both CTAs' epilogues
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1 + kEpiWarps) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+  if (warp == 1 + kEpiWarps) {                   // the same warp in both CTAs of the pair
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();                            // the peer's barriers exist before any multicast
+  cluster_sync_all();                            // the peer's barriers exist before any signal
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int L = P.nl;
@@ -644,15 +644,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           for (int nt = 0; nt < nt_n; ++nt) {
             prefetch_block();
             for (int kc = 0; kc < kc_n; ++kc) {
-              // both CTAs multiply the same weight tile: each loads one plane and multicasts it
-              // to the pair (every tile crosses L2 → SM once); the stage is reused once both
-              // CTAs' MMAs have read it (empty counts two commits)
+              // the pair MMA (M = 256, N = 128) takes B rows 0–63 from CTA 0 and 64–127 from CTA 1:
+              // each CTA loads its 64 rows of both planes; the bytes count on CTA 0's barrier
               TR_T0(tw);
               mbar_wait(&empty[stage], phase ^ 1);
               TR_ACC(tr_empty, tw);
-              mbar_expect_tx_w(&full[stage], kStage32Bytes);
-              uint8_t* dst = Bst + stage * kStage32Bytes + half * kT32Bytes;
-              tma_load_3d_mc_w(dst, &P.tmap32[half][l], kc * 32, nt * 128, (int)m, &full[stage], 3);
+              if (half == 0) mbar_expect_tx_w(&full[stage], 2 * kStage32Bytes);
+              uint8_t* dst = Bst + stage * kStage32Bytes;
+              const int n0 = nt * 128 + half * 64;
+              tma_load_3d_2sm_w(dst, &P.tmap32[0][l], kc * 32, n0, (int)m, &full[stage]);
+              tma_load_3d_2sm_w(dst + kH32Bytes, &P.tmap32[1][l], kc * 32, n0, (int)m, &full[stage]);
               if (++stage == kStages32) { stage = 0; phase ^= 1; }
             }
           }
@@ -694,7 +695,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         fence_async_smem();
         named_bar(1, kEpiWarps * 32);
         if (et == 0)
-          for (int g = 0; g < (P.kpad[0] + 127) >> 7; ++g) mbar_arrive(&aready[g]);
+          for (int g = 0; g < (P.kpad[0] + 127) >> 7; ++g) mbar_arrive_remote(&aready[g], 0);
       }
       double sq = 0.0;
       for (int l = 1; l <= L; ++l) {
@@ -740,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             tc_fence_before();
             named_bar(1, kEpiWarps * 32);
             if (et == 0)
-              for (int g = 0; g < ntl - 1; ++g) mbar_arrive(&aready[g]);
+              for (int g = 0; g < ntl - 1; ++g) mbar_arrive_remote(&aready[g], 0);
           }
           const int c0 = t * 128 + part * 32;
           if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
@@ -800,7 +801,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         if (l < L) {
           fence_async_smem();
           named_bar(1, kEpiWarps * 32);
-          if (et == 0) mbar_arrive(&aready[ntl - 1]);
+          if (et == 0) mbar_arrive_remote(&aready[ntl - 1], 0);
         }
         TR_ACC(tr_awrite, ta);
       }
@@ -830,13 +831,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
              clock64() - tr_start, tr_dready, tr_tile, tr_awrite, tr_bias);
 #endif
   } else {
-    // ------------------------------------------------------------ MMA issuer (whole warp, one
-    // elected lane issues)
-    {
-      const uint32_t idesc = idesc_f16(128, 128);
+    // ------------------------------------------------------------ MMA issuer: CTA 0 of the pair
+    // (whole warp, one elected lane issues); M = 256 = both CTAs' [A_hi; A_lo] rows, N = 128
+    if (half == 0) {
+      const uint32_t idesc = idesc_f16(256, 128);
       int stage = 0;
       uint32_t phase = 0, aphase = 0;                // aphase bit g: parity of aready[g]
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      const uint64_t da0 = smem_desc(a_base), db0 = smem_desc64(b_base);
       TR_DECL(tr_aready); TR_DECL(tr_full);
       TR_T0(tr_start);
       for (int64_t m = pair; m < P.n; m += npair) {
@@ -857,16 +859,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
               mbar_wait(&full[stage], phase);
               TR_ACC(tr_full, tf);
               tc_fence_after();
-              const uint32_t bs = b_base + stage * kStage32Bytes;
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {        // K = 16 per instruction, 32 per stage
-                const uint64_t ad = smem_desc(a_base + (kc >> 1) * kTileBytes +
-                                              (((kc & 1) * 2 + j) * 32));
-                mma_f16_w(dt, ad, smem_desc64(bs + j * 32), idesc, (kc | j) != 0);
-                mma_f16_w(dt, ad, smem_desc64(bs + kT32Bytes + j * 32), idesc, 1u);
-              }
-              mma_commit_mc_w(&empty[stage], 3);    // frees the stage in both CTAs' rings
-              if (kc == kc_n - 1) mma_commit_w(&dready[nt]);
+              // K = 16 per instruction, 32 per stage: descriptors = base + (byte offset >> 4)
+              // (the 14-bit address field cannot carry: shared memory < 256 KB)
+              const uint32_t ao = (uint32_t)((kc >> 1) * kTileBytes + (kc & 1) * 64) >> 4;
+              const uint32_t bo = (uint32_t)(stage * kStage32Bytes) >> 4;
+              mma4_commit_2sm_w(dt, da0 + ao, da0 + ao + 2, db0 + bo, db0 + bo + (kH32Bytes >> 4),
+                                db0 + bo + 2, db0 + bo + (kH32Bytes >> 4) + 2, idesc, kc != 0,
+                                &empty[stage], 3);      // ... and frees the stage in both CTAs
+              if (kc == kc_n - 1) mma_commit_2sm_mc_w(&dready[nt], 3);
               if (++stage == kStages32) { stage = 0; phase ^= 1; }
             }
           }
@@ -885,7 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
   cluster_sync_all();                            // no CTA leaves while its peer may still signal it
   if (warp == 1 + kEpiWarps) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -1014,7 +1014,7 @@ static cudaError_t encode_maps32(MlpParams& q, const __half* img, int64_t n) {
     for (int l = 1; l <= q.nl; ++l) {
       const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};
       const cuuint64_t strides[2] = {(cuuint64_t)q.w[l - 1] * 2, (cuuint64_t)q.D * 2};
-      const cuuint32_t box[3] = {32, 128, 1};
+      const cuuint32_t box[3] = {32, 64, 1};        // one CTA's half of a [128 n × 32 k] tile
       const cuuint32_t es[3] = {1, 1, 1};
       CUresult r = enc(&q.tmap32[pl][l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
                        const_cast<__half*>(base + q.off[l]), dims, strides, box, es,

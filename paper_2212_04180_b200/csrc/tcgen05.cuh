@@ -156,6 +156,71 @@ __device__ __forceinline__ void tma_prefetch_3d_w(const CUtensorMap* map, int c0
       "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// ---- CTA pairs (cta_group::2): one MMA spans the two SMs of a cluster pair — A rows 0–127 from
+// CTA 0's shared memory and 128–255 from CTA 1's, B's N rows split the same way, D rows in each
+// CTA's own TMEM. Issued by CTA 0 only.
+__device__ __forceinline__ void mma_f16_2sm_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_2sm_mc_w(uint64_t* b, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n\t}" ::"r"(smem_u32(b)), "h"(mask)
+      : "memory");
+}
+// One 32-k stage of the fp32-accurate MLP: 4 pair MMAs (k-steps 0/1 × weight planes hi/lo) and
+// the multicast commit that frees the stage, under ONE elect (the single issuing lane spends
+// its time on tcgen05 instructions, not on per-instruction ELECT / predicate sequences).
+__device__ __forceinline__ void mma4_commit_2sm_w(uint32_t tmem_d, uint64_t a0, uint64_t a1,
+                                                  uint64_t bh0, uint64_t bl0, uint64_t bh1,
+                                                  uint64_t bl1, uint32_t idesc, uint32_t acc,
+                                                  uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\tsetp.ne.b32 p, %8, 0;\n\tsetp.eq.b32 t, %8, %8;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %5, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %6, %7, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%9], %10;\n\t}" ::"r"(tmem_d),
+      "l"(a0), "l"(a1), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc), "r"(acc),
+      "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// TMA load into this CTA's shared memory whose completion is counted on CTA 0's mbarrier at
+// bar's offset (the peer bit of the shared::cluster address cleared)
+__device__ __forceinline__ void tma_load_3d_2sm_w(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                  int c2, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "r"(c2), "l"(0x1000000000000000ull)
+      : "memory");
+}
+// arrive on the mbarrier at b's offset in cluster CTA `cta` (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(b)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 // the MMAs' completion arrives on the mbarrier at b's offset in every CTA of ctaMask
 __device__ __forceinline__ void mma_commit_mc(uint64_t* b, uint16_t mask) {
   asm volatile(

@@ -1,12 +1,7 @@
 mkdir -p gpurun_out
-T=${TAG:-r2p}
+T=${TAG:-r2y}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail gpurun_out/${T}_build.log; exit 1; }
 timeout 300 python -m pytest tests -m gpu -q -x -k "mlp or tanh" > gpurun_out/${T}_tests_mlp.log 2>&1; echo mlp tests rc=$?; tail -2 gpurun_out/${T}_tests_mlp.log; grep -E "^FAILED|Error" gpurun_out/${T}_tests_mlp.log | head
-cp paper_2212_04180_b200/lib/libes_b200.so /tmp/keep.so
-cp exp/libes_trace.so paper_2212_04180_b200/lib/libes_b200.so
-timeout 300 python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_trace_c4.log 2>&1; echo trace rc=$?
-cp /tmp/keep.so paper_2212_04180_b200/lib/libes_b200.so
-grep "mlp32 trace" gpurun_out/${T}_trace_c4.log | tail -4
 timeout 1500 python -m pytest tests -m gpu -q --maxfail=10 -k "not mlp" > gpurun_out/${T}_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/${T}_tests.log; grep -E "^FAILED|Error" gpurun_out/${T}_tests.log | head
 for c in "--steps 20 --warmup 5 --no-cpu-baseline --sub 0" "--config c5 --steps 10 --warmup 3 --no-cpu-baseline" "--config c3 --steps 50 --warmup 5 --no-cpu-baseline" "--config c4 --steps 3 --warmup 3 --no-cpu-baseline" "--config c4 --steps 3 --warmup 3 --no-cpu-baseline --mlp fp16"; do
   timeout 300 python bench.py $c > /tmp/o.log 2>&1; echo "bench $c rc=$?"
