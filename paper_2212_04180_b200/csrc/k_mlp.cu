@@ -1,19 +1,18 @@
-// k_mlp.cu — K4: synthetic-MLP fitness on the 5th-generation tensor cores (NUMERICS N14; P:212
-// "MLP", topology P:268–270). Per population member: L chained [128 × w_{l-1}]·[w_{l-1} × w_l]
-// GEMMs (batch 128), tanh, and the MSE against the teacher's outputs.
+// k_mlp.cu — K4: synthetic-MLP fitness on the 5th-generation tensor cores (NUMERICS N14, N14′;
+// P:212 "MLP", topology P:268–270). Per population member: L chained [128 × w_{l-1}]·[w_{l-1} × w_l]
+// GEMMs (batch 128), tanh, and the MSE against the teacher's outputs. Two kernels:
 //
-// One persistent CTA per SM walks the members. Warp roles (544 threads):
-//   warps 0–7   producers: prefetch the next (layer, n-tile) weight block into L2 with the TMA
-//               engine (cp.async.bulk.prefetch.L2), stream the current one with LDG.128, round to
-//               fp16, and store it into a 6-stage ring of [128 n × 64 k] fp16 tiles in the UMMA
-//               K-major SWIZZLE_128B layout; arrive on full[s].
-//   warps 8–15  epilogue: tcgen05.ld the fp32 accumulator (TMEM lane = batch row), + bias, tanh,
-//               round to fp16 and write the next layer's A operand (smem, same layout); last layer:
-//               squared error vs. the teacher.
-//   warp 16     TMEM allocator + a single elected thread issuing tcgen05.mma.kind::f16
-//               (M=128, N=128, K=16; fp32 accumulation in TMEM, 512 columns = one whole layer).
+// mlp_kernel (N14′, the fp16-image approximation): one persistent CTA per SM walks the members.
+//   warp 0 (TMA mode)  producer: the ask's fp16 image streamed with TMA in [128 n × 64 k]
+//                      SWIZZLE_128B tiles (6-stage ring), one bulk L2 prefetch per (layer,
+//                      n-tile) block ahead; (non-TMA mode: 8 warps converting fp32 x to fp16)
+//   warps 1–16         epilogue: tcgen05.ld the fp32 accumulator (TMEM lane = batch row), + bias,
+//                      tanh, round to fp16, park in TMEM, then write the next layer's A operand
+//                      (smem) per 128-k group; last layer: squared error vs. the teacher
+//   warp 17            TMEM allocator + the MMA loop (whole warp, one elected lane issuing
+//                      tcgen05.mma.kind::f16 M=128 N=128 K=16; fp32 accumulation in 512 TMEM columns)
+// mlp32_kernel (N14, the definition, fp32-accurate): CTA pairs (2-CTA clusters), see below.
 // The activations never leave the SM (A: 128 KB smem); weights are read from HBM exactly once.
-// Bound: HBM (4 B/parameter/member); tensor work is ~20 % of the HBM time at B = 128.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -39,6 +38,10 @@ static constexpr int kThreadsTma = (1 + kEpiWarps + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
 static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 2048;   // + barriers, bias
+#ifndef ES_MLP16_AHEAD
+#define ES_MLP16_AHEAD 1   // L2 look-ahead of the fp16-image MLP producer, in (layer, n-tile) blocks
+                           // (measured at C4: 1 → 1.72 ms, 2 → 1.79)
+#endif
 
 // ES_MLP_TRACE (profiling builds only): per-role wait / busy cycle totals of CTA 0, printed at exit.
 #ifdef ES_MLP_TRACE
@@ -188,8 +191,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
           if (++pl > L) { pl = 1; pm += gridDim.x; }
         }
       };
-      prefetch_block();
-      prefetch_block();
+      for (int k = 0; k < ES_MLP16_AHEAD; ++k) prefetch_block();
       for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
         for (int l = 1; l <= L; ++l) {
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
@@ -448,6 +450,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
       int stage = 0;
       uint32_t phase = 0, aphase = 0;
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
+      const uint64_t da0 = smem_desc(a_base), db0 = smem_desc(b_base);
       TR_DECL(tr_aready); TR_DECL(tr_full);
       TR_T0(tr_start);
       for (int64_t m = blockIdx.x; m < P.n; m += gridDim.x) {
@@ -468,13 +471,10 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
               mbar_wait(&full[stage], phase);
               TR_ACC(tr_full, tf);
               tc_fence_after();
-#pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {        // K = 16 per instruction, 64 per tile
-                const uint64_t ad = smem_desc(a_base + kc * kTileBytes + ks * 32);
-                const uint64_t bd = smem_desc(b_base + stage * kTileBytes + ks * 32);
-                mma_f16_w(dt, ad, bd, idesc, (kc | ks) != 0);
-              }
-              mma_commit_w(&empty[stage]);           // frees the stage when these MMAs finish
+              // K = 16 per instruction, 64 per tile; descriptor = base + (byte offset >> 4)
+              mma4k_commit_w(dt, da0 + (uint32_t)((kc * kTileBytes) >> 4),
+                             db0 + (uint32_t)((stage * kTileBytes) >> 4), idesc, kc != 0,
+                             &empty[stage]);          // ... and frees the stage when they finish
               // n-tile nt's accumulator is complete: its epilogue quarter starts while the
               // remaining n-tiles of the layer are still being multiplied
               if (kc == kc_n - 1) mma_commit_w(&dready[nt]);
@@ -503,17 +503,23 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 // The definition (N14) is the MLP of the fp32 parameters. Each operand a is split into two binary16
 // parts of the scaled value a·2^8: hi = fp16(a·2^8), lo = fp16(a·2^8 − hi) (≈ 22 significant bits
 // together; the 2^8 scale keeps lo out of the binary16 subnormal range for |a| ≥ 2^-10, below which
-// its absolute error is ≤ 2^-33). D = Σ_k A·W with A = [A_hi; A_lo] stacked as the 128 MMA rows
-// (64 batch rows per CTA) and W = W_hi + W_lo accumulated into the same TMEM columns:
-// row b of D + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b] to fp32 accuracy.
-// The weights arrive as the population's split image — two binary16 planes [2][n][D] written by
-// the ask kernel (or by mlp_split_kernel from an fp32 x) — through TMA (one producer thread,
-// [128 n × 32 k] SWIZZLE_64B tiles of both planes per stage, an L2 prefetch look-ahead), so the
-// weight stream needs no producer registers. Two CTAs per member (batch rows 0–63 and 64–127); each
-// streams the member's weights (the pair's second read is an L2 hit) and the pair's squared-error
-// halves are combined in a fixed order by whichever CTA finishes second. The epilogue's lane
-// quarters 2–3 (the lo rows) hand their accumulator to quarters 0–1 through shared memory, 8
-// columns per round in two ping-pong buffers.
+// its absolute error is ≤ 2^-33). One 2-CTA cluster per member, CTA h holding batch rows
+// 64h … 64h+63 as A = [A_hi; A_lo] (128 rows). CTA 0 issues `tcgen05.mma.cta_group::2` with M = 256
+// (both CTAs' rows) and N = 128 output columns, W_hi and W_lo products accumulated into the same
+// TMEM columns, so in each CTA row b + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b]
+// to fp32 accuracy (the lo·lo product is negligible and free). The weights are the population's
+// split image — two binary16 planes [2][n][D] written by the ask (or mlp_split_kernel) — and each
+// CTA TMA-loads ITS 64 of the tile's 128 weight rows of both planes (the pair MMA takes B rows
+// 0–63 from CTA 0's shared memory and 64–127 from CTA 1's), the bytes counted on CTA 0's barrier;
+// the MMA's multicast commits free both CTAs' stages and signal both epilogues; the epilogues
+// arrive on CTA 0's per-128-k-group `aready` barriers remotely. The pair's squared-error halves are
+// combined in a fixed order by whichever CTA finishes second. Epilogue: the hi warp (lanes 0–63)
+// and lo warp (64–127) of a column part swap 16 columns through shared memory so both finish 16
+// columns (bias, tanh, split into the next A, parked in TMEM until A is free).
+#ifndef ES_MLP_AHEAD
+#define ES_MLP_AHEAD 1   // L2 look-ahead of the fp32 MLP producer, in (layer, n-tile) blocks
+                         // (measured at C4: 1 → 4.54 ms, 2 → 4.66, 3 → 4.94)
+#endif
 static constexpr int kStages32 = 10;
 static constexpr int kH32Bytes = 64 * 64;                        // [64 n × 32 k] fp16 = 4 KB
 static constexpr int kStage32Bytes = 2 * kH32Bytes;              // this CTA's hi half + lo half
@@ -636,8 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           if (++pl > L) { pl = 1; pm += npair; }
         }
       };
-      prefetch_block();
-      prefetch_block();
+      for (int k = 0; k < ES_MLP_AHEAD; ++k) prefetch_block();
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
           const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;

@@ -715,8 +715,24 @@ cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Small D (≤ 16384 dims per run): phase 2 in ONE launch, a CTA per run — ‖p_σ'‖, σ', h_σ, then
+// p_c and C of the run's dims by the same CTA (saves the second launch and its ramp; C2: 2 → 1).
+__global__ void __launch_bounds__(256) sepcma_finish_kernel(DevState s, int bpr) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
+  if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
+  __syncthreads();                               // h_σ (global, this CTA's own write) visible
+  for (int64_t d = threadIdx.x; d < s.D; d += blockDim.x) sepcma_pc_elem(s, r, d);
+}
+
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk) {
   const int bpr = tell_blocks_per_run(s);
+  if (s.D <= 16384) {
+    sepcma_finish_kernel<<<s.R, 256, 0, st>>>(s, bpr);
+    if (nk) *nk = 1;
+    return cudaGetLastError();
+  }
   sepcma_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr);
   const int64_t n = (int64_t)s.R * s.D;
   sepcma_pc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s);

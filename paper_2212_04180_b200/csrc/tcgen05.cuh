@@ -173,6 +173,25 @@ __device__ __forceinline__ void mma_commit_2sm_mc_w(uint64_t* b, uint16_t mask) 
       "[%0], %1;\n\t}" ::"r"(smem_u32(b)), "h"(mask)
       : "memory");
 }
+// One 64-k stage (4 × K = 16 along the same A / B tiles) + the commit that frees it, under one
+// elect (single-CTA form). Descriptors advance by 32 B (2 in descriptor units) per K step.
+__device__ __forceinline__ void mma4k_commit_w(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t acc, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(
+          tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(smem_u32(bar))
+      : "memory");
+}
 // One 32-k stage of the fp32-accurate MLP: 4 pair MMAs (k-steps 0/1 × weight planes hi/lo) and
 // the multicast commit that frees the stage, under ONE elect (the single issuing lane spends
 // its time on tcgen05 instructions, not on per-instruction ELECT / predicate sequences).
