@@ -278,6 +278,13 @@ static es_status_t init_impl(es_ctx_t** out, es_algo_t algo, int32_t R, int32_t 
     TRY(dalloc(c, (void**)&s.rcnt, nc * sizeof(uint32_t)));
     TRY(cudaMemsetAsync(s.rcnt, 0, nc * sizeof(uint32_t), st));
     TRY(dalloc(c, (void**)&s.rbpart, (size_t)R * 64 * sizeof(double)));
+    s.rrad = nullptr;
+    s.rrad_bar = nullptr;
+    if (R <= 16 && N <= 65536) {
+      TRY(dalloc(c, (void**)&s.rrad, ((size_t)4 * R * N + (size_t)R * 256 * 32) * sizeof(uint32_t)));
+      TRY(dalloc(c, (void**)&s.rrad_bar, 2 * sizeof(unsigned)));
+      TRY(cudaMemsetAsync(s.rrad_bar, 0, 2 * sizeof(unsigned), st));
+    }
   }
   // population sharding with a communicator — also a one-rank one (W = 1 with an id: the
   // collective data plane of es_tell executed on a single GPU)

@@ -90,6 +90,8 @@ struct DevState {
   uint32_t* rcnt;      // counting rank (few runs): [3][R][N] counters + arrivals + slots, zero
                       // between tells (k_rank.cu)
   double* rbpart;     // [R][64] counting rank: PGPE baseline partials per j-tile
+  unsigned* rrad_bar; // radix rank: grid-barrier counters [2] (zero between launches)
+  uint32_t* rrad;     // radix rank (few runs, 4096 < N ≤ 65536): keys / indices ping-pong [4][R][N] + digit totals [R][256][32]
   int rank_par;       // every run's shaping is per-member in the ranks (counting rank allowed)
   int32_t* pos;        // [R][N] member → sorted position (ARS pair selection)
   double* n2;          // [R] D-shard Sep-CMA ‖p_σ'‖² share, summed over ranks before the finish

@@ -7,6 +7,10 @@
 // utilities; P:286 Sep-CMA elite weights) and the tell's per-direction coefficients are written
 // here so that the tell kernel only streams (direction, coefficient) pairs.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "es_internal.h"
 
@@ -608,11 +612,319 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
 
 // (For many runs the per-run register bitonic sort stays faster: counting at R = 512, N = 256
 // measured 22.8 vs 15 µs per launch.)
+
+// Few runs (R ≤ kCountMaxR) with 4096 < N ≤ 65536 and per-member shaping: an LSD radix RANK in
+// ONE cooperative launch. A tile of 2048 keys per CTA (256 threads × 8, striped so that position
+// = tile·2048 + slot·256 + thread); four 8-bit passes of a stable counting sort of the (key,
+// index) pairs — warp-level __match_any_sync ranks, a (slot, warp) prefix per digit in shared
+// memory, per-tile digit totals in global memory, every CTA deriving its own digit offsets after a
+// grid sync (no separate scan phase) — then the finish over the sorted keys spread over all CTAs
+// (tie groups by neighbour checks, binary search only inside a tie run). Sorting by (key, index)
+// through a stable LSD sort gives exactly N9's order. Nine grid syncs replace the counting path's
+// N² compares (88 µs at N = 16384) and the hybrid sort's single-CTA finish (0.52 ms at 65536).
+static constexpr int kRadT = 256, kRadE = 8, kRadTile = kRadT * kRadE, kRadMaxBlk = 32;
+static constexpr int kRadMinN = 4097, kRadMaxN = kRadTile * kRadMaxBlk;
+
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int k = 0; k < w; ++k) base += wsum[k];
+  return base + x - v;
+}
+
+// Grid barrier for the cooperative launch (all CTAs co-resident): a monotone arrival counter,
+// spun on without back-off (the cooperative-groups grid sync measured ~4 µs per barrier here).
+// `ctr[0]` counts arrivals, `ctr[1]` departures; the last CTA to leave the kernel resets both.
+__device__ __forceinline__ unsigned __smid_dummy() { unsigned r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+struct GridBar {
+  unsigned* ctr;
+  unsigned n, k = 0;
+  __device__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++k;
+      __threadfence();                           // cumulative: the CTA's writes, ordered by the barrier
+      atomicAdd(&ctr[0], 1u);
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < k * n);
+    }
+    __syncthreads();
+  }
+  __device__ void leave() {
+    if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1u) == n - 1) {
+      ctr[0] = 0u;                               // every CTA has passed every barrier
+      ctr[1] = 0u;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kRadT, 4) rank_radix_kernel(DevState s, const float* __restrict__ fsrc,
+                                                           int nblk) {
+  GridBar grid{s.rrad_bar, gridDim.x * gridDim.y};
+#ifdef ES_RADIX_TRACE
+  long long tr[16];
+  int ntr = 0;
+  tr[ntr++] = clock64();
+#define RTR() do { if (ntr < 16) tr[ntr++] = clock64(); } while (0)
+#else
+#define RTR() do { } while (0)
+#endif
+  __shared__ uint16_t cnt[kRadE][kRadT / 32][256];
+  __shared__ uint32_t off[256];
+  __shared__ uint32_t wsum[kRadT / 32];
+  __shared__ double red[32];
+  const int N = s.N, R = s.R, r = blockIdx.y, b = blockIdx.x, t = threadIdx.x;
+  const int w = t >> 5, lane = t & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t* const base = s.rrad;
+  uint32_t* const K0 = base + (size_t)r * N;
+  uint32_t* const K1 = base + (size_t)(2 * R + r) * N;
+  uint32_t* const I0 = base + (size_t)(R + r) * N;
+  uint32_t* const I1 = base + (size_t)(3 * R + r) * N;
+  uint32_t* hist = base + (size_t)4 * R * N + (size_t)r * 256 * kRadMaxBlk;   // [digit][tile]
+  uint32_t k[kRadE], id[kRadE];
+  bool v[kRadE];
+#pragma unroll
+  for (int e = 0; e < kRadE; ++e) {
+    const int i = b * kRadTile + e * kRadT + t;
+    v[e] = i < N;
+    k[e] = v[e] ? rank_key(fit_at(s, fsrc, r, i)) : 0u;
+    id[e] = (uint32_t)i;
+  }
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 8 * pass;
+    uint32_t* cz = reinterpret_cast<uint32_t*>(&cnt[0][0][0]);
+    for (int i = t; i < kRadE * (kRadT / 32) * 256 / 2; i += kRadT) cz[i] = 0u;
+    __syncthreads();
+    uint32_t rk[kRadE];
+#pragma unroll
+    for (int e = 0; e < kRadE; ++e) {
+      const uint32_t act = __ballot_sync(0xffffffffu, v[e]);
+      rk[e] = 0u;
+      if (v[e]) {
+        const uint32_t d = (k[e] >> sh) & 255u;
+        const uint32_t peers = __match_any_sync(act, d);
+        rk[e] = __popc(peers & lt_mask);
+        if (rk[e] == 0u) cnt[e][w][d] = (uint16_t)__popc(peers);
+      }
+    }
+    __syncthreads();
+    uint32_t run = 0;                             // thread t = digit: prefix over (slot, warp)
+    {
+      uint16_t c[kRadE * (kRadT / 32)];           // all 64 loads in flight, then the prefix
+#pragma unroll
+      for (int k2 = 0; k2 < kRadE * (kRadT / 32); ++k2) c[k2] = cnt[k2 / (kRadT / 32)][k2 % (kRadT / 32)][t];
+#pragma unroll
+      for (int k2 = 0; k2 < kRadE * (kRadT / 32); ++k2) {
+        cnt[k2 / (kRadT / 32)][k2 % (kRadT / 32)][t] = (uint16_t)run;
+        run += c[k2];
+      }
+    }
+    hist[t * kRadMaxBlk + b] = run;
+    RTR();
+    grid.sync();
+    RTR();
+    uint32_t T = 0, Pb = 0;
+    {
+      uint32_t h[kRadMaxBlk];                     // all tile totals in flight at once
+#pragma unroll
+      for (int bb = 0; bb < kRadMaxBlk; ++bb) h[bb] = bb < nblk ? __ldcg(&hist[t * kRadMaxBlk + bb]) : 0u;
+#pragma unroll
+      for (int bb = 0; bb < kRadMaxBlk; ++bb) {
+        T += h[bb];
+        if (bb < b) Pb += h[bb];
+      }
+    }
+    off[t] = block_excl_scan256(T, wsum) + Pb;
+    __syncthreads();
+    uint32_t* Ko = (pass & 1) ? K1 : K0;
+    uint32_t* Io = (pass & 1) ? I1 : I0;
+#pragma unroll
+    for (int e = 0; e < kRadE; ++e) {
+      if (!v[e]) continue;
+      const uint32_t d = (k[e] >> sh) & 255u;
+      const uint32_t dst = off[d] + cnt[e][w][d] + rk[e];
+      Ko[dst] = k[e];
+      Io[dst] = id[e];
+    }
+    grid.sync();
+#pragma unroll
+    for (int e = 0; e < kRadE; ++e) {
+      const int i = b * kRadTile + e * kRadT + t;
+      if (v[e]) {
+        k[e] = __ldcg(&Ko[i]);
+        id[e] = __ldcg(&Io[i]);
+      }
+    }
+  }
+  RTR();
+  // ---- finish: positions of this tile in the sorted order (pass 3 wrote buffer 1)
+  const uint32_t* SK = K1;
+  const RunScal& rs = s.rs[r];
+  const bool anti = is_anti(s.algo), cmaish = s.algo == SEP_CMA_ES || s.algo == CMA_ES;
+  uint32_t* dir = s.dir + (int64_t)r * N;
+  double* cA = s.coefA + (int64_t)r * N;
+  double* cB = s.coefB + (int64_t)r * N;
+  double part = 0.0;
+  // the tile's sorted keys in shared memory (the digit counters are free now): neighbour checks and
+  // tie-run searches stay on chip unless a tie run crosses the tile edge; the fitness values of
+  // the tile's members are fetched up front (independent loads)
+  uint32_t* skt = reinterpret_cast<uint32_t*>(&cnt[0][0][0]);
+  const int tlen = min(kRadTile, N - b * kRadTile);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kRadE; ++e) skt[e * kRadT + t] = k[e];
+  float fv[kRadE];
+#pragma unroll
+  for (int e = 0; e < kRadE; ++e) fv[e] = v[e] ? fit_at(s, fsrc, r, (int)id[e]) : 0.0f;
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kRadE; ++e) {
+    if (!v[e]) continue;
+    const int pl = e * kRadT + t, p = b * kRadTile + pl;
+    const uint32_t key = k[e];
+    const int j = (int)id[e];
+    int sj = p, ej = p;
+    const uint32_t kprev = pl > 0 ? skt[pl - 1] : (p > 0 ? __ldcg(&SK[p - 1]) : ~key);
+    if (kprev == key) {                           // inside a tie run: its first position
+      int lo, hi;
+      if (skt[0] != key) { lo = 0; hi = pl; } else { lo = -b * kRadTile; hi = 0; }
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t km = mid >= 0 ? skt[mid] : __ldcg(&SK[b * kRadTile + mid]);
+        if (km < key) lo = mid + 1; else hi = mid;
+      }
+      sj = b * kRadTile + lo;
+    }
+    const uint32_t knext = pl + 1 < tlen ? skt[pl + 1] : (p + 1 < N ? __ldcg(&SK[p + 1]) : ~key);
+    if (knext == key) {                           // its last position
+      int lo, hi;
+      if (skt[tlen - 1] != key) { lo = pl; hi = tlen; } else { lo = tlen - 1; hi = N - b * kRadTile; }
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t km = mid < tlen ? skt[mid] : __ldcg(&SK[b * kRadTile + mid]);
+        if (km <= key) lo = mid + 1; else hi = mid;
+      }
+      ej = b * kRadTile + lo - 1;
+    }
+    const int64_t rj = (int64_t)r * N + j;
+    const float fj = fv[e];
+    s.perm[(int64_t)r * N + p] = j;
+    s.rs_s[rj] = sj;
+    s.rs_e[rj] = ej;
+    s.pos[rj] = p;
+    s.fit[rj] = fj;
+    float val;
+    if (anti && rs.shaping == 1) {
+      val = fj;
+    } else if (anti) {
+      val = __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));   // N10
+    } else {
+      const float* wpos = s.wpos + (int64_t)r * N;                         // N11
+      float acc = 0.0f;
+      for (int q = sj; q <= ej; ++q) acc = __fadd_rn(acc, wpos[q]);
+      val = __fdiv_rn(acc, (float)(ej - sj + 1));
+    }
+    s.shaped[rj] = val;
+    if (cmaish) { dir[p] = (uint32_t)j; cA[p] = (double)val; }
+    else if (!anti) { dir[j] = (uint32_t)j; cA[j] = (double)val; }
+    if (p == 0) rc_slot(s)[2 * r] = (uint32_t)j;
+    if (cmaish && p == rs.mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
+    part += (double)val;
+  }
+  RTR();
+  if (s.algo == PGPE) {
+    const double tsum = block_sum(part, red);
+    if (t == 0) s.rbpart[(int64_t)r * kCountMaxTiles + b] = tsum;
+  }
+  grid.sync();
+  RTR();
+  double bbar = 0.0;
+  if (s.algo == PGPE) {                           // every CTA sums the tile partials in order
+    double pb[kRadMaxBlk];
+#pragma unroll
+    for (int bb = 0; bb < kRadMaxBlk; ++bb)
+      pb[bb] = bb < nblk ? __ldcg(&s.rbpart[(int64_t)r * kCountMaxTiles + bb]) : 0.0;
+    double tsum = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < kRadMaxBlk; ++bb) tsum = __dadd_rn(tsum, pb[bb]);
+    bbar = tsum / (double)N;
+  }
+  if (anti) {                                     // pair coefficients, 1024 pairs per tile
+    const float* sh = s.shaped + (int64_t)r * N;
+    for (int i = b * (kRadTile / 2) + t; i < min(N / 2, (b + 1) * (kRadTile / 2)); i += kRadT) {
+      const double cp = __ldcg(&sh[2 * i]), cm = __ldcg(&sh[2 * i + 1]);
+      dir[i] = (uint32_t)i;
+      cA[i] = __dsub_rn(cp, cm);
+      if (s.algo == PGPE) cB[i] = __dsub_rn(__dmul_rn(__dadd_rn(cp, cm), 0.5), bbar);
+    }
+  }
+  if (b == 0 && t == 0) {
+    const int jbest = (int)__ldcg(&rc_slot(s)[2 * r]);
+    const int nw = cmaish ? (int)__ldcg(&rc_slot(s)[2 * r + 1]) : 0;
+    write_genscal(s, r, jbest, __ldcg(&s.fit[(int64_t)r * N + jbest]), nw, bbar, 0.0f);
+  }
+  grid.leave();
+#ifdef ES_RADIX_TRACE
+  RTR();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    printf("radix trace:");
+    for (int i = 1; i < ntr; ++i) printf(" %lld", tr[i] - tr[i - 1]);
+    printf("\n");
+  }
+  if (threadIdx.x == 0 && ntr >= 12)
+    printf("radix cta %d finish %lld smid %u\n", blockIdx.x, tr[10] - tr[9], __smid_dummy());
+#endif
+}
+
+static int radix_min_n() {                      // A/B switch for profiling (ES_RADIX_MIN_N)
+  static const int v = [] {
+    const char* e = std::getenv("ES_RADIX_MIN_N");
+    return e ? std::max(2, std::atoi(e)) : kRadMinN;
+  }();
+  return v;
+}
+// the cooperative grid (tiles × runs) must be co-resident
+static int radix_max_ctas() {
+  static std::atomic<int> v{0};
+  int m = v.load();
+  if (m == 0) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rank_radix_kernel, kRadT, 0);
+    m = std::max(1, occ) * sm_count();
+    v.store(m);
+  }
+  return m;
+}
+static bool use_radix(const DevState& s) {
+  return s.rank_par && s.rrad && s.R <= kCountMaxR && s.N >= radix_min_n() && s.N <= kRadMaxN &&
+         s.R * ((s.N + kRadTile - 1) / kRadTile) <= radix_max_ctas();
+}
+
 static bool use_count(const DevState& s) {
-  return s.rank_par && s.R <= kCountMaxR && s.N <= kCountMaxN;
+  return s.rank_par && s.R <= kCountMaxR && s.N <= kCountMaxN && !use_radix(s);
 }
 
 cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
+  if (use_radix(s)) {
+    int nblk = (s.N + kRadTile - 1) / kRadTile;
+    dim3 grid((unsigned)nblk, (unsigned)s.R);
+    DevState sc = s;
+    const float* fs = fsrc;
+    void* args[] = {(void*)&sc, (void*)&fs, (void*)&nblk};
+    return cudaLaunchCooperativeKernel((const void*)rank_radix_kernel, grid, dim3(kRadT), args, 0, st);
+  }
   if (use_count(s)) {
     const int jt = (s.N + kCountT - 1) / kCountT;
     const int want = 2 * sm_count();
@@ -662,7 +974,7 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
 }
 
 int rank_launches(const DevState& s) {
-  if (use_count(s)) return 1;
+  if (use_radix(s) || use_count(s)) return 1;
   int npad = 1, n = 1;
   while (npad < s.N) npad <<= 1;
   if (npad <= kChunk) return 1;

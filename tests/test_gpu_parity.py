@@ -212,7 +212,7 @@ def test_rank_and_shaping_bit_exact(algo, N, R):
 
 
 # ------------------------------------------------------------------------ one generation
-SHAPES = [(3, 16, 10), (2, 64, 1003), (1, 256, 5000), (2, 32, 130), (1, 2, 1), (2, 1030, 40)]
+SHAPES = [(3, 16, 10), (2, 64, 1003), (1, 256, 5000), (2, 32, 130), (1, 2, 1), (2, 1030, 40), (2, 8200, 12)]
 
 
 @pytest.mark.parametrize("algo", ALGOS)
