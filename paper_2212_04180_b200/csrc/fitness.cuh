@@ -15,11 +15,13 @@ struct FitAcc {
 };
 
 // Rosenbrock term of the pair (x_d, x_{d+1}), every operation in double as the oracle.
-__device__ __forceinline__ double rosen_term(float a, float b) {
-  const double da = a, db = b;
+__device__ __forceinline__ double rosen_term_d(double da, double db) {
   const double t1 = __dsub_rn(db, __dmul_rn(da, da));
   const double t2 = __dsub_rn(1.0, da);
   return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
+}
+__device__ __forceinline__ double rosen_term(float a, float b) {
+  return rosen_term_d((double)a, (double)b);
 }
 
 // (double)v for v ≥ 0 without the XU-pipe F2F convert: the binary64 bits of a positive normal

@@ -34,7 +34,10 @@ static constexpr int kStages = 6;
 static constexpr int kProdWarps = 8, kEpiWarps = 16;
 static constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
 // TMA mode: one producer warp (a single thread issues the tile copies) instead of eight.
-static constexpr int kThreadsTma = (1 + kEpiWarps + 1) * 32;
+// (32 epilogue warps of 16 columns would double the warps per scheduler for the latency-bound
+// epilogue, but 34 warps exceed the 1024-thread CTA limit; the code is generic in the count)
+static constexpr int kEpiWarpsTma = 16;
+static constexpr int kThreadsTma = (1 + kEpiWarpsTma + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
 static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 2048;   // + barriers, bias
@@ -114,6 +117,8 @@ template <bool TMA>
 __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
     mlp_kernel(const __grid_constant__ MlpParams P) {
   constexpr int kProd = TMA ? 1 : kProdWarps;          // producer warps
+  constexpr int EW = TMA ? kEpiWarpsTma : kEpiWarps;    // epilogue warps
+  constexpr int CW = 128 / (EW / 4);                    // columns per epilogue warp per n-tile
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                 // [8][128 rows][64] fp16
   uint8_t* Bst = smem + kABytes;                     // [kStages][128 rows][64] fp16
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   uint64_t* dready = bars + 2 * kStages;             // [4] per 128-column n-tile of a layer
   uint64_t* aready = bars + 2 * kStages + 4;         // [4] per 128-k group of A
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
-  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 9);   // [kEpiWarps] (64 B)
+  float* red = reinterpret_cast<float*>(bars + 2 * kStages + 9);   // [EW] (≤ 128 B)
   // TMA mode: the layer's fp16 bias, staged once per layer (≤ 512 values)
   __half* bias_s = reinterpret_cast<__half*>(smem + kABytes + kStages * kTileBytes + 512);
 
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
     for (int k = 0; k < 4; ++k) mbar_init(&aready[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProd + kEpiWarps) {                   // TMEM: 512 fp32 columns × 128 lanes
+  if (warp == kProd + EW) {                          // TMEM: 512 fp32 columns × 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -286,10 +291,10 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         }
       }
     }
-  } else if (warp < kProd + kEpiWarps) {
+  } else if (warp < kProd + EW) {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - kProd;                      // 0..15
-    // a warp may only tcgen05.ld the TMEM lane quarter (warp id mod 4); part = column quarter
+    const int e = warp - kProd;                      // 0..EW-1
+    // a warp may only tcgen05.ld the TMEM lane quarter (warp id mod 4); part = CW-column group
     const int q = warp & 3, part = e >> 2;
     const int row = q * 32 + lane;                   // batch row = TMEM lane
     const int et = threadIdx.x - kProd * 32;         // 0..511
@@ -302,10 +307,10 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
       {
         const int bytes = (P.kpad[0] >> 6) * kTileBytes;
         const uint4* src = reinterpret_cast<const uint4*>(P.uimg);
-        for (int o = et; o < bytes / 16; o += kEpiWarps * 32)
+        for (int o = et; o < bytes / 16; o += EW * 32)
           reinterpret_cast<uint4*>(A)[o] = __ldg(src + o);
         fence_async_smem();
-        named_bar(1, kEpiWarps * 32);
+        named_bar(1, EW * 32);
         if (et == 0)
           for (int g = 0; g < (P.kpad[0] + 127) >> 7; ++g) mbar_arrive(&aready[g]);
       }
@@ -317,11 +322,11 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         const int ntl = P.npad[l] >> 7;              // n-tiles (dready barriers) of this layer
         if (TMA) {
           // stage the bias while the layer's MMAs run (its HBM latency was exposed per chunk)
-          for (int o = et; o < (out >> 3); o += kEpiWarps * 32)
+          for (int o = et; o < (out >> 3); o += EW * 32)
             reinterpret_cast<uint4*>(bias_s)[o] = __ldg(reinterpret_cast<const uint4*>(bias16) + o);
-          for (int n = (out & ~7) + et; n < P.npad[l]; n += kEpiWarps * 32)
+          for (int n = (out & ~7) + et; n < P.npad[l]; n += EW * 32)
             bias_s[n] = n < out ? bias16[n] : __float2half_rn(0.0f);   // padded columns finite
-          named_bar(1, kEpiWarps * 32);
+          named_bar(1, EW * 32);
         }
 
         // hidden layers also zero-fill the padded K columns [out, kpad) of the next A. The next
@@ -334,13 +339,16 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
         // next layer's A, k group t, from the packed fp16 results parked in TMEM (zeros past out)
         auto write_a = [&](int t) {
-          const int c0 = t * 128 + part * 32;
+          const int c0 = t * 128 + part * CW;
           if (c0 >= cend) return;
           uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
                         make_uint4(0, 0, 0, 0)};
-          if (c0 < out) tmem_ld16(trow + (uint32_t)c0, h);
+          if (c0 < out) {
+            if (CW == 32) tmem_ld16(trow + (uint32_t)c0, h);
+            else tmem_ld8(trow + (uint32_t)c0, h);
+          }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {              // 4 chunks of 8 k in k-block c0/64
+          for (int c = 0; c < CW / 8; ++c) {         // CW/8 chunks of 8 k in k-block c0/64
             const int kb = c0 >> 6, ck = ((c0 & 63) >> 3) + c;
             *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(row, ck)) = h[c];
           }
@@ -356,18 +364,19 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
             for (int g = 0; g < ntl - 1; ++g) write_a(g);
             fence_async_smem();
             tc_fence_before();
-            named_bar(1, kEpiWarps * 32);
+            named_bar(1, EW * 32);
             if (et == 0)
               for (int g = 0; g < ntl - 1; ++g) mbar_arrive(&aready[g]);
           }
-          const int c0 = t * 128 + part * 32;
+          const int c0 = t * 128 + part * CW;
           if (c0 >= cend || c0 >= out) continue;     // padded K columns: zeros, written below
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+          float v[CW];
+          if (CW == 32) tmem_ld32(trow + (uint32_t)c0, v);
+          else tmem_ld16f(trow + (uint32_t)c0, v);
           // bias (N14: fp16(b), uniform across the warp → broadcast loads)
           if (TMA) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 8) {
+            for (int i = 0; i < CW; i += 8) {
               const int n = c0 + i;
               if (n < out) {
                 const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + n);
@@ -379,9 +388,9 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
                 for (int u = 0; u < 8; ++u) v[i + u] = 0.0f;
               }
             }
-          } else if (c0 + 32 <= out) {
+          } else if (c0 + CW <= out) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
+            for (int i = 0; i < CW; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
               v[i] = tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
               v[i + 1] = tanh32(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
@@ -390,21 +399,22 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < CW; ++i) {
               const int n = c0 + i;
               v[i] = n < out ? tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
                              : 0.0f;
             }
           }
           if (l < L) {
-            uint4 h[4];
+            uint4 h[CW / 8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) h[c] = pack8(v + 8 * c);
-            tmem_st16(trow + (uint32_t)c0, h);
+            for (int c = 0; c < CW / 8; ++c) h[c] = pack8(v + 8 * c);
+            if (CW == 32) tmem_st16(trow + (uint32_t)c0, h);
+            else tmem_st8(trow + (uint32_t)c0, h);
           } else if (P.mode == 0) {
             const float* yr = P.Y + (int64_t)row * out;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < CW; ++i) {
               const int n = c0 + i;
               if (n < out) {
                 const float d = __fsub_rn(v[i], __ldg(yr + n));
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < CW; ++i)
               if (c0 + i < out) P.Y[(int64_t)row * out + c0 + i] = v[i];
           }
         }
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         tc_fence_before();
         if (l < L) {
           fence_async_smem();
-          named_bar(1, kEpiWarps * 32);
+          named_bar(1, EW * 32);
           if (et == 0) mbar_arrive(&aready[ntl - 1]);
         }
       }
@@ -430,13 +440,13 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
       if (lane == 0) red[e] = sq;
-      named_bar(1, kEpiWarps * 32);
+      named_bar(1, EW * 32);
       if (et == 0 && P.mode == 0) {
         double tot = 0.0;
-        for (int k = 0; k < kEpiWarps; ++k) tot += (double)red[k];
+        for (int k = 0; k < EW; ++k) tot += (double)red[k];
         P.f[m] = (float)(tot / ((double)kBatch * P.w[L]));
       }
-      named_bar(1, kEpiWarps * 32);
+      named_bar(1, EW * 32);
     }
 #ifdef ES_MLP_TRACE
     if (TMA && blockIdx.x == 0 && et == 0)
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kProd + kEpiWarps) {
+  if (warp == kProd + EW) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
