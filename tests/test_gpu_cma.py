@@ -138,6 +138,32 @@ def test_sampling_through_the_factor_is_fp32_accurate(R, N, D):
     pair.close()
 
 
+@pytest.mark.parametrize("R,N,D", [(2, 64, 128), (1, 256, 1024)])
+def test_sampling_per_entry_bound(R, N, D):
+    """Per entry, not normwise: |y_gpu - y_ref|[i, d] <= 2^-17 (|A| |z|)[i, d] + the rounding of
+    x = fma(sigma, y, m) to binary32 seen through (x - m) / sigma. The 3-pass tf32 split drops
+    small*small (<= 2^-20 |a b|) and small's truncation (<= 2^-21 |a b|) per product (N17), and
+    the fp32 accumulation over K terms adds a few 2^-24 of the absolute sum, so no entry may
+    carry an error beyond a small multiple of 2^-23 of its own absolute product sum."""
+    pair = CmaPair(N, D, _params(R))
+    pair.step(W.ROSENBROCK)
+    A = pair.gpu.get("chol").cpu().numpy().astype(np.float64)
+    m = pair.gpu.get("mean").cpu().numpy().astype(np.float64)
+    sg = pair.gpu.get("sigma").cpu().numpy().astype(np.float64)
+    x = pair.gpu.ask().cpu().numpy().astype(np.float64)
+    for r in range(R):
+        pair.orc[r].ask()
+        Z = pair.orc[r].Z
+        y_ref = Z @ A[r].T
+        absum = np.abs(Z) @ np.abs(A[r]).T
+        y_gpu = (x[r] - m[r][None, :]) / sg[r]
+        xr = np.abs(x[r]) + np.abs(m[r][None, :])
+        bound = 2.0 ** -17 * absum + 2.0 ** -23 * xr / sg[r]
+        err = np.abs(y_gpu - y_ref)
+        assert np.all(err <= bound), (r, float((err / bound).max()))
+    pair.close()
+
+
 def test_graph_replay_equals_eager_with_lazy_refresh():
     """D = 300, N = 8: the factor is refreshed every k = 6 generations (Hansen's lazy schedule).
     Eager calls skip the refresh launches on the other generations; a generation captured as a
