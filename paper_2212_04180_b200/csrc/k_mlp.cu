@@ -375,18 +375,14 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
           else tmem_ld16f(trow + (uint32_t)c0, v);
           // bias (N14: fp16(b), uniform across the warp → broadcast loads)
           if (TMA) {
+            // branch-free (the tanh chains interleave): past `out` the accumulator (zero-filled
+            // weight rows) and the staged bias (padded with 0) are 0, and tanh(0) = 0
 #pragma unroll
             for (int i = 0; i < CW; i += 8) {
-              const int n = c0 + i;
-              if (n < out) {
-                const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + n);
-                const __half* hh = reinterpret_cast<const __half*>(&hb);
+              const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + c0 + i);
+              const __half* hh = reinterpret_cast<const __half*>(&hb);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[i + u] = tanh32(__fadd_rn(v[i + u], __half2float(hh[u])));
-              } else {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[i + u] = 0.0f;
-              }
+              for (int u = 0; u < 8; ++u) v[i + u] = tanh32(__fadd_rn(v[i + u], __half2float(hh[u])));
             }
           } else if (c0 + CW <= out) {
 #pragma unroll
@@ -515,12 +511,13 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 // together; the 2^8 scale keeps lo out of the binary16 subnormal range for |a| ≥ 2^-10, below which
 // its absolute error is ≤ 2^-33). One 2-CTA cluster per member, CTA h holding batch rows
 // 64h … 64h+63 as A = [A_hi; A_lo] (128 rows). CTA 0 issues `tcgen05.mma.cta_group::2` with M = 256
-// (both CTAs' rows) and N = 128 output columns, W_hi and W_lo products accumulated into the same
-// TMEM columns, so in each CTA row b + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b]
-// to fp32 accuracy (the lo·lo product is negligible and free). The weights are the population's
-// split image — two binary16 planes [2][n][D] written by the ask (or mlp_split_kernel) — and each
-// CTA TMA-loads ITS 64 of the tile's 128 weight rows of both planes (the pair MMA takes B rows
-// 0–63 from CTA 0's shared memory and 64–127 from CTA 1's), the bytes counted on CTA 0's barrier;
+// (both CTAs' rows) and N = 256 output columns (a 512-wide layer is 2 n-tiles = the 512 TMEM
+// columns), W_hi and W_lo products accumulated into the same TMEM columns, so in each CTA row b +
+// row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b] to fp32 accuracy (the lo·lo product
+// is negligible and free). The weights are the population's split image — two binary16 planes
+// [2][n][D] written by the ask (or mlp_split_kernel) — and each CTA TMA-loads ITS 128 of the
+// tile's 256 weight rows of both planes (the pair MMA takes B rows 0–127 from CTA 0's shared
+// memory and 128–255 from CTA 1's), [128 × 32 k] SWIZZLE_64B, the bytes counted on CTA 0's barrier;
 // the MMA's multicast commits free both CTAs' stages and signal both epilogues; the epilogues
 // arrive on CTA 0's per-128-k-group `aready` barriers remotely. The pair's squared-error halves are
 // combined in a fixed order by whichever CTA finishes second. Epilogue: the hi warp (lanes 0–63)
@@ -530,8 +527,8 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 #define ES_MLP_AHEAD 1   // L2 look-ahead of the fp32 MLP producer, in (layer, n-tile) blocks
                          // (measured at C4: 1 → 4.54 ms, 2 → 4.66, 3 → 4.94)
 #endif
-static constexpr int kStages32 = 10;
-static constexpr int kH32Bytes = 64 * 64;                        // [64 n × 32 k] fp16 = 4 KB
+static constexpr int kStages32 = 5;
+static constexpr int kH32Bytes = 128 * 64;                       // [128 n × 32 k] fp16 = 8 KB
 static constexpr int kStage32Bytes = 2 * kH32Bytes;              // this CTA's hi half + lo half
 static constexpr int kXbufBytes = 8 * 2 * 8 * 32 * 4;            // 8 pairs × 2 dirs × 8 cols × 32
 static constexpr int kBias32Bytes = 512 * 4;                     // the layer's fp32 bias
@@ -568,7 +565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     mlp32_kernel(const __grid_constant__ MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                              // [8][128 rows][64] fp16
-  uint8_t* Bst = smem + kABytes;                                  // [10][hi, lo][64][32] fp16
+  uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][128][32] fp16
   float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
   float* bias_s = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes + kXbufBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
@@ -630,10 +627,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       const uintptr_t plane_end = reinterpret_cast<uintptr_t>(plane0) + (uintptr_t)P.n * P.D * 2;
       auto prefetch_block = [&]() {
         if (pm >= P.n) return;
-        const int in = P.w[pl - 1], rows = min(128, P.w[pl] - pnt * 128);
+        const int in = P.w[pl - 1], rows = min(256, P.w[pl] - pnt * 256);
         if (rows > 0) {
           const uintptr_t b0 = reinterpret_cast<uintptr_t>(plane0) +
-                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 128 * in) * 2;
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 256 * in) * 2;
           const uintptr_t lo = b0 & ~(uintptr_t)15;
           const uintptr_t hi = min(plane_end, b0 + (uintptr_t)rows * in * 2 + 15) & ~(uintptr_t)15;
           for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
@@ -647,7 +644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           const uintptr_t hi = min(plane_end, b0 + (uintptr_t)out * 2 + 15) & ~(uintptr_t)15;
           if (hi > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
         }
-        if (++pnt == (P.npad[pl] >> 7)) {
+        if (++pnt == ((P.w[pl] + 255) >> 8)) {
           pnt = 0;
           if (++pl > L) { pl = 1; pm += npair; }
         }
@@ -655,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       for (int k = 0; k < ES_MLP_AHEAD; ++k) prefetch_block();
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
-          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
+          const int nt_n = (P.w[l] + 255) >> 8, kc_n = P.kpad[l - 1] >> 5;
           for (int nt = 0; nt < nt_n; ++nt) {
             prefetch_block();
             for (int kc = 0; kc < kc_n; ++kc) {
@@ -666,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
               TR_ACC(tr_empty, tw);
               if (half == 0) mbar_expect_tx_w(&full[stage], 2 * kStage32Bytes);
               uint8_t* dst = Bst + stage * kStage32Bytes;
-              const int n0 = nt * 128 + half * 64;
+              const int n0 = nt * 256 + half * 128;
               tma_load_3d_2sm_w(dst, &P.tmap32[0][l], kc * 32, n0, (int)m, &full[stage]);
               tma_load_3d_2sm_w(dst + kH32Bytes, &P.tmap32[1][l], kc * 32, n0, (int)m, &full[stage]);
               if (++stage == kStages32) { stage = 0; phase ^= 1; }
@@ -716,11 +713,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       for (int l = 1; l <= L; ++l) {
         const int in = P.w[l - 1], out = P.w[l];
         const int64_t boff = P.off[l] + (int64_t)out * in;   // b_l inside the layer block
-        const int ntl = P.npad[l] >> 7;
+        const int ntl = (out + 255) >> 8;            // 256-output n-tiles (the pair MMA's N)
         const int cend = l < L ? P.kpad[l] : out;
+        const int ng_next = (cend + 127) >> 7;       // k groups of the next layer's A
         // b = (hi + lo)·2^-8 (exact in fp32: ≤ 22 significant bits), staged while the MMAs run
         TR_T0(tb);
-        for (int n = et; n < P.npad[l]; n += kEpiWarps * 32)
+        for (int n = et; n < 256 * ntl; n += kEpiWarps * 32)
           bias_s[n] = n < out ? __fmul_rn(__fadd_rn(__half2float(bhi[boff + n]),
                                                     __half2float(blo[boff + n])), 1.0f / kSplitScale)
                               : 0.0f;
@@ -729,17 +727,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
         // next layer's A, k group t (rows rh: hi split, 64 + rh: lo split) from the split values
         // parked in TMEM; padded K columns [out, kpad) written as zeros
-        auto write_a = [&](int t) {
-          const int cb = t * 128 + part * 32 + side;
-          if (cb >= cend) return;
-          uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
-                        make_uint4(0, 0, 0, 0)};
-          if (cb - side < out) tmem_ld16(trow + (uint32_t)cb, h);
-          const int kb = cb >> 6, ck = (cb & 63) >> 3;
+        auto write_a = [&](int t) {                  // a part owns 64 columns of a tile
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck + c)) = h[c];
-            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck + c)) = h[2 + c];
+          for (int cc = 0; cc < 2; ++cc) {
+            const int cb = t * 256 + part * 64 + cc * 32 + side;
+            if (cb >= cend) continue;
+            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                          make_uint4(0, 0, 0, 0)};
+            if (cb - side < out) tmem_ld16(trow + (uint32_t)cb, h);
+            const int kb = cb >> 6, ck = (cb & 63) >> 3;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck + c)) = h[c];
+              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck + c)) = h[2 + c];
+            }
           }
         };
         for (int t = 0; t < ntl; ++t) {
@@ -756,9 +757,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             tc_fence_before();
             named_bar(1, kEpiWarps * 32);
             if (et == 0)
-              for (int g = 0; g < ntl - 1; ++g) mbar_arrive_remote(&aready[g], 0);
+              for (int g = 0; g < min(2 * (ntl - 1), ng_next); ++g) mbar_arrive_remote(&aready[g], 0);
           }
-          const int c0 = t * 128 + part * 32;
+          for (int cc = 0; cc < 2; ++cc) {
+          const int c0 = t * 256 + part * 64 + cc * 32;
           if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
           float v[32];
           tmem_ld32(trow + (uint32_t)c0, v);
@@ -783,9 +785,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           for (int i = 0; i < 16; i += 4) {
             const float4 b4 = *reinterpret_cast<const float4*>(bias_s + cb + i);
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            // branch-free over the 16 columns (so the 16 tanh chains interleave): past `out` the
+            // accumulator (zero-filled weight rows) and the staged bias are 0, and tanh(0) = 0
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              x[i + u] = cb + i + u < out ? tanh32(__fmaf_rn(x[i + u], kUnscale, bb[u])) : 0.0f;
+            for (int u = 0; u < 4; ++u) x[i + u] = tanh32(__fmaf_rn(x[i + u], kUnscale, bb[u]));
           }
           if (l < L) {
             uint4 h[4];                              // hi split of 16 columns, then the lo split
@@ -807,6 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             for (int i = 0; i < 16; ++i)
               if (cb + i < out) P.Y32[(int64_t)brow * out + cb + i] = x[i];
           }
+          }
           TR_ACC(tr_tile, tt);
         }
         TR_T0(ta);
@@ -816,7 +820,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         if (l < L) {
           fence_async_smem();
           named_bar(1, kEpiWarps * 32);
-          if (et == 0) mbar_arrive_remote(&aready[ntl - 1], 0);
+          if (et == 0)
+            for (int g = 2 * (ntl - 1); g < ng_next; ++g) mbar_arrive_remote(&aready[g], 0);
         }
         TR_ACC(tr_awrite, ta);
       }
@@ -849,7 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     // ------------------------------------------------------------ MMA issuer: CTA 0 of the pair
     // (whole warp, one elected lane issues); M = 256 = both CTAs' [A_hi; A_lo] rows, N = 128
     if (half == 0) {
-      const uint32_t idesc = idesc_f16(256, 128);
+      const uint32_t idesc = idesc_f16(256, 256);
       int stage = 0;
       uint32_t phase = 0, aphase = 0;                // aphase bit g: parity of aready[g]
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
@@ -858,9 +863,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       TR_T0(tr_start);
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
-          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 5;
+          const int nt_n = (P.w[l] + 255) >> 8, kc_n = P.kpad[l - 1] >> 5;
           for (int nt = 0; nt < nt_n; ++nt) {
-            const uint32_t dt = tmem + (uint32_t)(nt * 128);
+            const uint32_t dt = tmem + (uint32_t)(nt * 256);
             for (int kc = 0; kc < kc_n; ++kc) {
               if (nt == 0 && (kc & 3) == 0) {        // A's k group kc/4 is written
                 const int g = kc >> 2;
@@ -1029,7 +1034,7 @@ static cudaError_t encode_maps32(MlpParams& q, const __half* img, int64_t n) {
     for (int l = 1; l <= q.nl; ++l) {
       const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};
       const cuuint64_t strides[2] = {(cuuint64_t)q.w[l - 1] * 2, (cuuint64_t)q.D * 2};
-      const cuuint32_t box[3] = {32, 64, 1};        // one CTA's half of a [128 n × 32 k] tile
+      const cuuint32_t box[3] = {32, 128, 1};       // one CTA's half of a [256 n × 32 k] tile
       const cuuint32_t es[3] = {1, 1, 1};
       CUresult r = enc(&q.tmap32[pl][l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
                        const_cast<__half*>(base + q.off[l]), dims, strides, box, es,

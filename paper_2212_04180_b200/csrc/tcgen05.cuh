@@ -212,6 +212,32 @@ __device__ __forceinline__ void mma4_commit_2sm_w(uint32_t tmem_d, uint64_t a0, 
       "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// One 64-k stage of the fp32-accurate MLP with SWIZZLE_128B operands: 8 pair MMAs (k-steps 0–3 ×
+// weight planes hi/lo; descriptors advance 32 B = 2 units per k-step) + the multicast commit, under
+// one elect.
+__device__ __forceinline__ void mma8_commit_2sm_w(uint32_t tmem_d, uint64_t a, uint64_t bh,
+                                                  uint64_t bl, uint32_t idesc, uint32_t acc,
+                                                  uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 a1, a2, a3, h1, h2, h3, l1, l2, l3;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 h1, %2, 2;\n\tadd.s64 h2, %2, 4;\n\tadd.s64 h3, %2, 6;\n\t"
+      "add.s64 l1, %3, 2;\n\tadd.s64 l2, %3, 4;\n\tadd.s64 l3, %3, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, h1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, l1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, h2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, l2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, h3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, l3, %4, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%6], %7;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 // TMA load into this CTA's shared memory whose completion is counted on CTA 0's mbarrier at
 // bar's offset (the peer bit of the shared::cluster address cleared)
 __device__ __forceinline__ void tma_load_3d_2sm_w(void* dst, const CUtensorMap* map, int c0, int c1,
