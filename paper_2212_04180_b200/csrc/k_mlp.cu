@@ -76,7 +76,7 @@ struct MlpParams {
   const __half* uimg32[2];
   float* Y32;                   // [128][w_L] teacher outputs of the fp32-accurate kernel
   const __half* img;            // split image [2][n][D] (hi plane, lo plane); biases read here
-  CUtensorMap tmap32[2][kMaxLayers + 1];   // per plane (hi, lo) and layer: [128 n × 32 k] tiles
+  CUtensorMap tmap32[2][kMaxLayers + 1];   // per plane (hi, lo) and layer: [64 n × 64 k] boxes
   double* part;                 // [n][2] per-half squared-error sums
   uint32_t* cnt;                // [n] arrival counters (zero between launches)
 };
@@ -511,24 +511,25 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
 // together; the 2^8 scale keeps lo out of the binary16 subnormal range for |a| ≥ 2^-10, below which
 // its absolute error is ≤ 2^-33). One 2-CTA cluster per member, CTA h holding batch rows
 // 64h … 64h+63 as A = [A_hi; A_lo] (128 rows). CTA 0 issues `tcgen05.mma.cta_group::2` with M = 256
-// (both CTAs' rows) and N = 256 output columns (a 512-wide layer is 2 n-tiles = the 512 TMEM
-// columns), W_hi and W_lo products accumulated into the same TMEM columns, so in each CTA row b +
-// row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b] to fp32 accuracy (the lo·lo product
-// is negligible and free). The weights are the population's split image — two binary16 planes
-// [2][n][D] written by the ask (or mlp_split_kernel) — and each CTA TMA-loads ITS 128 of the
-// tile's 256 weight rows of both planes (the pair MMA takes B rows 0–127 from CTA 0's shared
-// memory and 128–255 from CTA 1's), [128 × 32 k] SWIZZLE_64B, the bytes counted on CTA 0's barrier;
+// (both CTAs' rows) and N = 128 output columns, W_hi and W_lo products accumulated into the same
+// TMEM columns, so in each CTA row b + row 64+b of D = (A_hi + A_lo)(W_hi + W_lo)[b] = 2^16·(h·W)[b]
+// to fp32 accuracy (the lo·lo product is negligible and free). The weights are the population's
+// split image — two binary16 planes [2][n][D] written by the ask (or mlp_split_kernel) — and each
+// CTA TMA-loads ITS 64 of the tile's 128 weight rows of both planes (the pair MMA takes B rows
+// 0–63 from CTA 0's shared memory and 64–127 from CTA 1's), the bytes counted on CTA 0's barrier;
 // the MMA's multicast commits free both CTAs' stages and signal both epilogues; the epilogues
 // arrive on CTA 0's per-128-k-group `aready` barriers remotely. The pair's squared-error halves are
 // combined in a fixed order by whichever CTA finishes second. Epilogue: the hi warp (lanes 0–63)
 // and lo warp (64–127) of a column part swap 16 columns through shared memory so both finish 16
-// columns (bias, tanh, split into the next A, parked in TMEM until A is free).
+// columns (bias, tanh, split into the next A, parked in TMEM until A is free). Stages hold 64 k
+// (128-byte SWIZZLE_128B rows): the TMA unit's cost goes with the number of rows it moves, and
+// 128-byte rows halve it against [128 n × 32 k] 64-byte-row tiles (C4: 4.31 vs 4.62 ms).
 #ifndef ES_MLP_AHEAD
 #define ES_MLP_AHEAD 1   // L2 look-ahead of the fp32 MLP producer, in (layer, n-tile) blocks
                          // (measured at C4: 1 → 4.54 ms, 2 → 4.66, 3 → 4.94)
 #endif
 static constexpr int kStages32 = 5;
-static constexpr int kH32Bytes = 128 * 64;                       // [128 n × 32 k] fp16 = 8 KB
+static constexpr int kH32Bytes = 64 * 128;                       // [64 n × 64 k] fp16 = 8 KB
 static constexpr int kStage32Bytes = 2 * kH32Bytes;              // this CTA's hi half + lo half
 static constexpr int kXbufBytes = 8 * 2 * 8 * 32 * 4;            // 8 pairs × 2 dirs × 8 cols × 32
 static constexpr int kBias32Bytes = 512 * 4;                     // the layer's fp32 bias
@@ -550,22 +551,11 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   lo = pack8(r);
 }
 
-// UMMA shared-memory descriptor, K-major SWIZZLE_64B (64-byte rows, 8-row groups of 512 B).
-__device__ __forceinline__ uint64_t smem_desc64(uint32_t addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
-  return d;
-}
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     mlp32_kernel(const __grid_constant__ MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                              // [8][128 rows][64] fp16
-  uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][128][32] fp16
+  uint8_t* Bst = smem + kABytes;                                  // [5][hi, lo][64][64] fp16
   float* xbuf = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes);
   float* bias_s = reinterpret_cast<float*>(smem + kABytes + kStages32 * kStage32Bytes + kXbufBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kABytes + kStages32 * kStage32Bytes +
@@ -627,10 +617,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       const uintptr_t plane_end = reinterpret_cast<uintptr_t>(plane0) + (uintptr_t)P.n * P.D * 2;
       auto prefetch_block = [&]() {
         if (pm >= P.n) return;
-        const int in = P.w[pl - 1], rows = min(256, P.w[pl] - pnt * 256);
+        const int in = P.w[pl - 1], rows = min(128, P.w[pl] - pnt * 128);
         if (rows > 0) {
           const uintptr_t b0 = reinterpret_cast<uintptr_t>(plane0) +
-                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 256 * in) * 2;
+                               (uintptr_t)(pm * P.D + P.off[pl] + (int64_t)pnt * 128 * in) * 2;
           const uintptr_t lo = b0 & ~(uintptr_t)15;
           const uintptr_t hi = min(plane_end, b0 + (uintptr_t)rows * in * 2 + 15) & ~(uintptr_t)15;
           for (uintptr_t o = lo + (uintptr_t)lane * 16384u; o < hi; o += 32u * 16384u)
@@ -644,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
           const uintptr_t hi = min(plane_end, b0 + (uintptr_t)out * 2 + 15) & ~(uintptr_t)15;
           if (hi > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
         }
-        if (++pnt == ((P.w[pl] + 255) >> 8)) {
+        if (++pnt == (P.npad[pl] >> 7)) {
           pnt = 0;
           if (++pl > L) { pl = 1; pm += npair; }
         }
@@ -652,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       for (int k = 0; k < ES_MLP_AHEAD; ++k) prefetch_block();
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
-          const int nt_n = (P.w[l] + 255) >> 8, kc_n = P.kpad[l - 1] >> 5;
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
           for (int nt = 0; nt < nt_n; ++nt) {
             prefetch_block();
             for (int kc = 0; kc < kc_n; ++kc) {
@@ -663,9 +653,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
               TR_ACC(tr_empty, tw);
               if (half == 0) mbar_expect_tx_w(&full[stage], 2 * kStage32Bytes);
               uint8_t* dst = Bst + stage * kStage32Bytes;
-              const int n0 = nt * 256 + half * 128;
-              tma_load_3d_2sm_w(dst, &P.tmap32[0][l], kc * 32, n0, (int)m, &full[stage]);
-              tma_load_3d_2sm_w(dst + kH32Bytes, &P.tmap32[1][l], kc * 32, n0, (int)m, &full[stage]);
+              const int n0 = nt * 128 + half * 64;
+              tma_load_3d_2sm_w(dst, &P.tmap32[0][l], kc * 64, n0, (int)m, &full[stage]);
+              tma_load_3d_2sm_w(dst + kH32Bytes, &P.tmap32[1][l], kc * 64, n0, (int)m, &full[stage]);
               if (++stage == kStages32) { stage = 0; phase ^= 1; }
             }
           }
@@ -713,12 +703,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
       for (int l = 1; l <= L; ++l) {
         const int in = P.w[l - 1], out = P.w[l];
         const int64_t boff = P.off[l] + (int64_t)out * in;   // b_l inside the layer block
-        const int ntl = (out + 255) >> 8;            // 256-output n-tiles (the pair MMA's N)
+        const int ntl = P.npad[l] >> 7;
         const int cend = l < L ? P.kpad[l] : out;
-        const int ng_next = (cend + 127) >> 7;       // k groups of the next layer's A
         // b = (hi + lo)·2^-8 (exact in fp32: ≤ 22 significant bits), staged while the MMAs run
         TR_T0(tb);
-        for (int n = et; n < 256 * ntl; n += kEpiWarps * 32)
+        for (int n = et; n < P.npad[l]; n += kEpiWarps * 32)
           bias_s[n] = n < out ? __fmul_rn(__fadd_rn(__half2float(bhi[boff + n]),
                                                     __half2float(blo[boff + n])), 1.0f / kSplitScale)
                               : 0.0f;
@@ -727,20 +716,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
         // next layer's A, k group t (rows rh: hi split, 64 + rh: lo split) from the split values
         // parked in TMEM; padded K columns [out, kpad) written as zeros
-        auto write_a = [&](int t) {                  // a part owns 64 columns of a tile
+        auto write_a = [&](int t) {
+          const int cb = t * 128 + part * 32 + side;
+          if (cb >= cend) return;
+          uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                        make_uint4(0, 0, 0, 0)};
+          if (cb - side < out) tmem_ld16(trow + (uint32_t)cb, h);
+          const int kb = cb >> 6, ck = (cb & 63) >> 3;
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int cb = t * 256 + part * 64 + cc * 32 + side;
-            if (cb >= cend) continue;
-            uint4 h[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
-                          make_uint4(0, 0, 0, 0)};
-            if (cb - side < out) tmem_ld16(trow + (uint32_t)cb, h);
-            const int kb = cb >> 6, ck = (cb & 63) >> 3;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck + c)) = h[c];
-              *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck + c)) = h[2 + c];
-            }
+          for (int c = 0; c < 2; ++c) {
+            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(rh, ck + c)) = h[c];
+            *reinterpret_cast<uint4*>(A + kb * kTileBytes + swz(64 + rh, ck + c)) = h[2 + c];
           }
         };
         for (int t = 0; t < ntl; ++t) {
@@ -757,10 +743,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             tc_fence_before();
             named_bar(1, kEpiWarps * 32);
             if (et == 0)
-              for (int g = 0; g < min(2 * (ntl - 1), ng_next); ++g) mbar_arrive_remote(&aready[g], 0);
+              for (int g = 0; g < ntl - 1; ++g) mbar_arrive_remote(&aready[g], 0);
           }
-          for (int cc = 0; cc < 2; ++cc) {
-          const int c0 = t * 256 + part * 64 + cc * 32;
+          const int c0 = t * 128 + part * 32;
           if (c0 >= cend || c0 >= out) continue;     // both warps of the pair skip together
           float v[32];
           tmem_ld32(trow + (uint32_t)c0, v);
@@ -810,7 +795,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             for (int i = 0; i < 16; ++i)
               if (cb + i < out) P.Y32[(int64_t)brow * out + cb + i] = x[i];
           }
-          }
           TR_ACC(tr_tile, tt);
         }
         TR_T0(ta);
@@ -820,8 +804,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
         if (l < L) {
           fence_async_smem();
           named_bar(1, kEpiWarps * 32);
-          if (et == 0)
-            for (int g = 2 * (ntl - 1); g < ng_next; ++g) mbar_arrive_remote(&aready[g], 0);
+          if (et == 0) mbar_arrive_remote(&aready[ntl - 1], 0);
         }
         TR_ACC(tr_awrite, ta);
       }
@@ -854,21 +837,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     // ------------------------------------------------------------ MMA issuer: CTA 0 of the pair
     // (whole warp, one elected lane issues); M = 256 = both CTAs' [A_hi; A_lo] rows, N = 128
     if (half == 0) {
-      const uint32_t idesc = idesc_f16(256, 256);
+      const uint32_t idesc = idesc_f16(256, 128);
       int stage = 0;
       uint32_t phase = 0, aphase = 0;                // aphase bit g: parity of aready[g]
       const uint32_t a_base = smem_u32(A), b_base = smem_u32(Bst);
-      const uint64_t da0 = smem_desc(a_base), db0 = smem_desc64(b_base);
+      const uint64_t da0 = smem_desc(a_base), db0 = smem_desc(b_base);   // SWIZZLE_128B, 64-k rows
       TR_DECL(tr_aready); TR_DECL(tr_full);
       TR_T0(tr_start);
       for (int64_t m = pair; m < P.n; m += npair) {
         for (int l = 1; l <= L; ++l) {
-          const int nt_n = (P.w[l] + 255) >> 8, kc_n = P.kpad[l - 1] >> 5;
+          const int nt_n = P.npad[l] >> 7, kc_n = P.kpad[l - 1] >> 6;
           for (int nt = 0; nt < nt_n; ++nt) {
-            const uint32_t dt = tmem + (uint32_t)(nt * 256);
+            const uint32_t dt = tmem + (uint32_t)(nt * 128);
             for (int kc = 0; kc < kc_n; ++kc) {
-              if (nt == 0 && (kc & 3) == 0) {        // A's k group kc/4 is written
-                const int g = kc >> 2;
+              if (nt == 0 && (kc & 1) == 0) {        // A's k group kc/2 (128 k) is written
+                const int g = kc >> 1;
                 TR_T0(ta);
                 mbar_wait(&aready[g], (aphase >> g) & 1u);
                 TR_ACC(tr_aready, ta);
@@ -879,12 +862,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
               mbar_wait(&full[stage], phase);
               TR_ACC(tr_full, tf);
               tc_fence_after();
-              // K = 16 per instruction, 32 per stage: descriptors = base + (byte offset >> 4)
+              // K = 16 per instruction, 64 per stage: descriptors = base + (byte offset >> 4)
               // (the 14-bit address field cannot carry: shared memory < 256 KB)
-              const uint32_t ao = (uint32_t)((kc >> 1) * kTileBytes + (kc & 1) * 64) >> 4;
+              const uint32_t ao = (uint32_t)(kc * kTileBytes) >> 4;
               const uint32_t bo = (uint32_t)(stage * kStage32Bytes) >> 4;
-              mma4_commit_2sm_w(dt, da0 + ao, da0 + ao + 2, db0 + bo, db0 + bo + (kH32Bytes >> 4),
-                                db0 + bo + 2, db0 + bo + (kH32Bytes >> 4) + 2, idesc, kc != 0,
+              mma8_commit_2sm_w(dt, da0 + ao, db0 + bo, db0 + bo + (kH32Bytes >> 4), idesc, kc != 0,
                                 &empty[stage], 3);      // ... and frees the stage in both CTAs
               if (kc == kc_n - 1) mma_commit_2sm_mc_w(&dready[nt], 3);
               if (++stage == kStages32) { stage = 0; phase ^= 1; }
@@ -1024,8 +1006,8 @@ static void fill_params(MlpParams& p, const int32_t* widths, int nw) {
 }
 
 // Per plane and layer: the split image viewed as a 3-D tensor (k = in, n = out, member) with
-// strides (2 B, in·2 B, D·2 B); a box of 32 k × 128 n × 1 member lands in smem in the UMMA K-major
-// SWIZZLE_64B layout of half a stage (rows past `out` / columns past `in` are zero-filled).
+// strides (2 B, in·2 B, D·2 B); a box of 64 k × 64 n × 1 member lands in smem in the UMMA K-major
+// SWIZZLE_128B layout of one plane of a stage (rows past `out` / columns past `in` are zero-filled).
 static cudaError_t encode_maps32(MlpParams& q, const __half* img, int64_t n) {
   EncodeTiledFn enc = encode_tiled_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -1034,11 +1016,11 @@ static cudaError_t encode_maps32(MlpParams& q, const __half* img, int64_t n) {
     for (int l = 1; l <= q.nl; ++l) {
       const cuuint64_t dims[3] = {(cuuint64_t)q.w[l - 1], (cuuint64_t)q.w[l], (cuuint64_t)n};
       const cuuint64_t strides[2] = {(cuuint64_t)q.w[l - 1] * 2, (cuuint64_t)q.D * 2};
-      const cuuint32_t box[3] = {32, 128, 1};       // one CTA's half of a [256 n × 32 k] tile
+      const cuuint32_t box[3] = {64, 64, 1};        // one CTA's half of a [128 n × 64 k] tile
       const cuuint32_t es[3] = {1, 1, 1};
       CUresult r = enc(&q.tmap32[pl][l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
                        const_cast<__half*>(base + q.off[l]), dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
