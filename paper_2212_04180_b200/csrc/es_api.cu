@@ -11,6 +11,14 @@
 thread_local std::string g_err;
 
 namespace esb {
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("ES_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int sm_count() {
   static std::atomic<int> n[64];
   int dev = 0;

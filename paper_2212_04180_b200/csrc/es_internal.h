@@ -225,6 +225,33 @@ TellSplit tell_pick_split(const DevState& s, const std::vector<int>& ent);
 constexpr int kTellThreads = 128;
 int sm_count();   // of the current device
 
+// Programmatic dependent launch (PDL) for the generation's short kernels (ask → evaluate → rank →
+// tell → finish): each is launched with programmatic stream serialization, so its CTAs are
+// scheduled while its predecessor drains; its first statement waits for the predecessor grid's
+// completion and memory flush (griddepcontrol.wait, a no-op without the attribute), then lets
+// its own successor launch. Nothing is read or written before the wait, so stream order holds.
+// ES_PDL=0 launches them plainly (A/B switch).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_on();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is per device:
 // a process driving several GPUs sets it on each). `done` is the call site's device bitmask.
 inline cudaError_t smem_attr_once(const void* kernel, int bytes, std::atomic<uint64_t>& done) {

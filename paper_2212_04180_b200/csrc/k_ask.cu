@@ -96,6 +96,7 @@ template <int ALGO, bool V4, int IMG, bool CLIP>
 __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __restrict__ x,
                                                            __half* __restrict__ x16, int bpr,
                                                            int dpt) {
+  pdl_enter();
   constexpr bool kAnti = is_anti(ALGO);
   const int r = blockIdx.x / bpr;
   const int64_t q = (int64_t)(blockIdx.x % bpr) * kAskThreads + threadIdx.x;
@@ -176,18 +177,13 @@ static cudaError_t launch_ask_t(const DevState& s, float* x, __half* x16, int im
   const int dpt = (Ploc + nchunk - 1) / nchunk;
   nchunk = (Ploc + dpt - 1) / dpt;
   dim3 grid((unsigned)(s.R * bpr), (unsigned)nchunk);
-  if (x16 && img == 2) {
-    ask_kernel<ALGO, true, 2, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
-    return cudaGetLastError();
-  }
-  if (x16) {
-    ask_kernel<ALGO, true, 1, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, x16, bpr, dpt);
-    return cudaGetLastError();
-  }
+  const dim3 blk(kAskThreads);
+  if (x16 && img == 2) return launch_pdl(ask_kernel<ALGO, true, 2, CLIP>, grid, blk, 0, st, s, x, x16, bpr, dpt);
+  if (x16) return launch_pdl(ask_kernel<ALGO, true, 1, CLIP>, grid, blk, 0, st, s, x, x16, bpr, dpt);
   const bool v4 = (s.Dx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if (v4) ask_kernel<ALGO, true, 0, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
-  else ask_kernel<ALGO, false, 0, CLIP><<<grid, kAskThreads, 0, st>>>(s, x, nullptr, bpr, dpt);
-  return cudaGetLastError();
+  __half* none = nullptr;
+  if (v4) return launch_pdl(ask_kernel<ALGO, true, 0, CLIP>, grid, blk, 0, st, s, x, none, bpr, dpt);
+  return launch_pdl(ask_kernel<ALGO, false, 0, CLIP>, grid, blk, 0, st, s, x, none, bpr, dpt);
 }
 
 template <bool CLIP>
@@ -216,6 +212,7 @@ cudaError_t launch_ask(const DevState& s, float* x, cudaStream_t st) {
 
 // N15: f_j = u_b(o_{j mod 4}) of counter (⌊j/4⌋, 0, t, 4), for this rank's members.
 __global__ void synth_kernel(DevState s, float* __restrict__ f) {
+  pdl_enter();
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)s.R * s.Nloc) return;
   const int r = (int)(gid / s.Nloc);
@@ -230,8 +227,7 @@ __global__ void synth_kernel(DevState s, float* __restrict__ f) {
 
 cudaError_t launch_synth(const DevState& s, float* f, cudaStream_t st) {
   const int64_t n = (int64_t)s.R * s.Nloc;
-  synth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, f);
-  return cudaGetLastError();
+  return launch_pdl(synth_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, s, f);
 }
 
 }  // namespace esb

@@ -69,6 +69,7 @@ __device__ __forceinline__ double warp_sum(double v) { return warp_sum_d(v); }
 template <int FN, bool V4>
 __global__ void __launch_bounds__(256) eval_warp_kernel(const float* __restrict__ x, int64_t n,
                                                         int64_t D, float* __restrict__ f) {
+  pdl_enter();
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= n) return;
   const int lane = threadIdx.x & 31;
@@ -80,6 +81,7 @@ template <int FN, bool V4, int T>
 __global__ void __launch_bounds__(T) eval_block_kernel(const float* __restrict__ x, int64_t D,
                                                        float* __restrict__ f) {
   __shared__ double part[T / 32];
+  pdl_enter();
   const int64_t row = blockIdx.x;
   double acc = warp_sum(row_partial<FN, V4>(x + row * D, D, threadIdx.x, T));
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
@@ -93,13 +95,15 @@ __global__ void __launch_bounds__(T) eval_block_kernel(const float* __restrict__
 
 template <int FN, bool V4>
 static void launch_fn(const float* x, int64_t n, int64_t D, float* f, cudaStream_t st) {
+  cudaError_t e;
   if (D <= 4096) {
-    eval_warp_kernel<FN, V4><<<(unsigned)((n + 7) / 8), 256, 0, st>>>(x, n, D, f);
+    e = launch_pdl(eval_warp_kernel<FN, V4>, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, x, n, D, f);
   } else if (D <= 65536 || n >= 4 * sm_count()) {
-    eval_block_kernel<FN, V4, 256><<<(unsigned)n, 256, 0, st>>>(x, D, f);
+    e = launch_pdl(eval_block_kernel<FN, V4, 256>, dim3((unsigned)n), dim3(256), 0, st, x, D, f);
   } else {
-    eval_block_kernel<FN, V4, 1024><<<(unsigned)n, 1024, 0, st>>>(x, D, f);
+    e = launch_pdl(eval_block_kernel<FN, V4, 1024>, dim3((unsigned)n), dim3(1024), 0, st, x, D, f);
   }
+  (void)e;   // a launch error stays the thread's last error (launch_eval_bbob returns it)
 }
 
 cudaError_t launch_eval_bbob(int fn, const float* x, int64_t n, int64_t D, float* f,

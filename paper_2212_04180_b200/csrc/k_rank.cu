@@ -330,6 +330,7 @@ __global__ void rank_kernel_smem(DevState s, const float* __restrict__ fsrc, int
   extern __shared__ uint64_t keys[];              // [npad] keys, then [npad] fitness values
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
+  pdl_enter();
   const int r = blockIdx.x;
   float* fs = reinterpret_cast<float*>(keys + npad);
   for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
@@ -344,6 +345,7 @@ __global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad
   extern __shared__ uint64_t keys[];
   __shared__ double red[32];
   __shared__ int32_t sh_nw;
+  pdl_enter();
   const int r = blockIdx.x;
   float* fs = reinterpret_cast<float*>(keys + npad);   // the fitness, kept on chip for the finish
   for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   __shared__ float sval[kCountT];
   __shared__ double red[32];
   __shared__ int sh_last;
+  pdl_enter();
   const int N = s.N, r = blockIdx.z, jt = gridDim.x, ni = gridDim.y;
   const int j = blockIdx.x * kCountT + threadIdx.x;
   const float fj = j < N ? fit_at(s, fsrc, r, j) : 0.0f;
@@ -931,9 +934,8 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
     int ni = std::max(1, std::min(jt, want / std::max(1, s.R * jt)));
     const int ilen = ((s.N + ni - 1) / ni + kCountT - 1) / kCountT * kCountT;
     ni = (s.N + ilen - 1) / ilen;
-    rank_count_kernel<<<dim3((unsigned)jt, (unsigned)ni, (unsigned)s.R), kCountT, 0, st>>>(
-        s, fsrc, ilen);
-    return cudaGetLastError();
+    return launch_pdl(rank_count_kernel, dim3((unsigned)jt, (unsigned)ni, (unsigned)s.R),
+                      dim3(kCountT), 0, st, s, fsrc, ilen);
   }
   int npad = 1;
   while (npad < s.N) npad <<= 1;
@@ -952,12 +954,11 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
     const int E = pad / T;
     const size_t sm = (size_t)pad * (sizeof(uint64_t) + sizeof(float));   // keys + fitness
     switch (E) {
-      case 2: rank_kernel<2><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
-      case 4: rank_kernel<4><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
-      case 8: rank_kernel<8><<<s.R, T, sm, st>>>(s, fsrc, pad); break;
-      default: rank_kernel_smem<<<s.R, T, sm, st>>>(s, fsrc, pad); break;
+      case 2: return launch_pdl(rank_kernel<2>, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
+      case 4: return launch_pdl(rank_kernel<4>, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
+      case 8: return launch_pdl(rank_kernel<8>, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
+      default: return launch_pdl(rank_kernel_smem, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
     }
-    return cudaGetLastError();
   }
   const int nch = npad / kChunk;
   const size_t smem = (size_t)kChunk * sizeof(uint64_t);

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(TT, ES_TELL_MINB) tell_kernel(DevState s,
   __shared__ double sB[kTile];
   __shared__ double red[TT / 32];
   __shared__ int sh_last;
+  pdl_enter();
   const int4 it = items[blockIdx.y];
   const int r = it.x, chunk = it.y, nchunk = it.z;
   const int qb = blockIdx.x, bpr = gridDim.x;
@@ -349,6 +350,7 @@ __device__ __forceinline__ void sepcma_sigma(const DevState& s, int r, double n2
 
 __global__ void sepcma_norm_kernel(DevState s, int bpr) {
   __shared__ double red[32];
+  pdl_enter();
   const int r = blockIdx.x;
   const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
   if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
@@ -678,7 +680,9 @@ std::vector<int4> tell_items(int R, const std::vector<int>& ent, const TellSplit
 template <int ALGO>
 static void launch_tell_t(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {
   dim3 grid((unsigned)tell_blocks_per_run(s), (unsigned)sp.nitems);
-  tell_kernel<ALGO><<<grid, TT, 0, st>>>(s, sp.items, sp.echunk, fused ? 1 : 0);
+  // a launch error stays the thread's last error (launch_tell_reduce returns it)
+  (void)launch_pdl(tell_kernel<ALGO>, grid, dim3(TT), 0, st, s, (const int4*)sp.items, sp.echunk,
+                   fused ? 1 : 0);
 }
 
 cudaError_t launch_tell_reduce(const DevState& s, bool fused, TellSplit sp, cudaStream_t st) {
@@ -719,6 +723,7 @@ cudaError_t launch_sepcma_n2(const DevState& s, cudaStream_t st) {
 // p_c and C of the run's dims by the same CTA (saves the second launch and its ramp; C2: 2 → 1).
 __global__ void __launch_bounds__(256) sepcma_finish_kernel(DevState s, int bpr) {
   __shared__ double red[32];
+  pdl_enter();
   const int r = blockIdx.x;
   const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
   if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
@@ -729,9 +734,8 @@ __global__ void __launch_bounds__(256) sepcma_finish_kernel(DevState s, int bpr)
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk) {
   const int bpr = tell_blocks_per_run(s);
   if (s.D <= 16384) {
-    sepcma_finish_kernel<<<s.R, 256, 0, st>>>(s, bpr);
     if (nk) *nk = 1;
-    return cudaGetLastError();
+    return launch_pdl(sepcma_finish_kernel, dim3(s.R), dim3(256), 0, st, s, bpr);
   }
   sepcma_norm_kernel<<<s.R, 256, 0, st>>>(s, bpr);
   const int64_t n = (int64_t)s.R * s.D;
