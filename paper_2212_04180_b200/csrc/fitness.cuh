@@ -14,14 +14,15 @@ struct FitAcc {
   double a = 0.0, b = 0.0;
 };
 
-// Rosenbrock term of the pair (x_d, x_{d+1}), every operation in double as the oracle.
-__device__ __forceinline__ double rosen_term_d(double da, double db) {
-  const double t1 = __dsub_rn(db, __dmul_rn(da, da));
+// acc + Rosenbrock term of the pair (x_d, x_{d+1}) in binary64 with contracted operations
+// (NUMERICS N7, GPU detail): t1 = fma(−a, a, b), acc = fma(1 − a, 1 − a, acc), then
+// acc = fma(100·t1, t1, acc) — 5 FP64 instructions instead of the oracle's 7 + the sum's add; each
+// result is binary64-accurate (a few 2⁻⁵³ relative), the same ≤ 1 ulp binary32 bar.
+__device__ __forceinline__ double rosen_acc_d(double acc, double da, double db) {
+  const double t1 = __fma_rn(-da, da, db);
   const double t2 = __dsub_rn(1.0, da);
-  return __dadd_rn(__dmul_rn(100.0, __dmul_rn(t1, t1)), __dmul_rn(t2, t2));
-}
-__device__ __forceinline__ double rosen_term(float a, float b) {
-  return rosen_term_d((double)a, (double)b);
+  acc = __fma_rn(t2, t2, acc);
+  return __fma_rn(__dmul_rn(100.0, t1), t1, acc);
 }
 
 // (double)v for v ≥ 0 without the XU-pipe F2F convert: the binary64 bits of a positive normal
@@ -40,7 +41,7 @@ __device__ __forceinline__ void fit_add(FitAcc& acc, float x, float xn, bool has
     const double d = (double)x;
     acc.a = __fma_rn(d, d, acc.a);
   } else if (FN == FN_ROSENBROCK) {
-    if (has_next) acc.a = __dadd_rn(acc.a, rosen_term(x, xn));
+    if (has_next) acc.a = rosen_acc_d(acc.a, (double)x, (double)xn);
   } else {
     // b = min(fr, 1 − fr) of N7 is the distance from x to the nearest integer: bq = x − rint(x)
     // is exact (Sterbenz; rint(x) = 0 for |x| < 1/2) and |bq| = b bit for bit, ties and |x| ≥ 2^23
