@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-T=${TAG:-r2f2}
+T=${TAG:-r2final2}
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --sub 0 > gpurun_out/${T}_plain_c2.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --sub 0 > gpurun_out/${T}_ncu_launch_c2.log 2>&1; echo launch c2 rc=$?
