@@ -43,33 +43,41 @@ __device__ void write_genscal(const DevState& s, int r, int jbest, float fb, int
   const int N = s.N;
   const bool anti = is_anti(s.algo);
   RunScal& w = s.rs[r];
+  // every field is read before the first store: the stores may alias them, so a field read after
+  // one would be another dependent global round trip on this single thread
+  const uint32_t t = w.t;
+  const float best_f = w.best_f, lr = w.lr, sigma = w.sigma;
+  const int ars_k = w.ars_k;
+  const double b1pow = w.b1pow, b2pow = w.b2pow;
+  const float beta1 = w.beta1, beta2 = w.beta2, lrate_decay = w.lrate_decay,
+              lrate_limit = w.lrate_limit, sigma_decay = w.sigma_decay, sigma_limit = w.sigma_limit;
   GenScal g;
-  g.t = w.t;
+  g.t = t;
   g.jbest = jbest;
-  g.improved = fb < w.best_f;                 // strict; false for NaN
-  if (g.improved) w.best_f = fb;
-  g.lr = w.lr;
-  g.sigma = w.sigma;
-  g.nentries = (s.algo == ARS || s.algo == PGPE) ? w.ars_k
+  g.improved = fb < best_f;                   // strict; false for NaN
+  g.lr = lr;
+  g.sigma = sigma;
+  g.nentries = (s.algo == ARS || s.algo == PGPE) ? ars_k
                                                  : (anti ? N / 2 : (s.algo == SNES ? N : nw));
   g.ars_scale = ars_scale;
   g.clip_inv = 0.0f;
   g.bbar = bbar;
   g.bc1 = g.bc2 = 1.0f;
-  g.sigma_new = w.sigma;
+  g.sigma_new = sigma;
   g.hsig = 0;
+  if (g.improved) w.best_f = fb;
   if (anti) {
-    const double b1 = __dmul_rn(w.b1pow, (double)w.beta1);
-    const double b2 = __dmul_rn(w.b2pow, (double)w.beta2);
+    const double b1 = __dmul_rn(b1pow, (double)beta1);
+    const double b2 = __dmul_rn(b2pow, (double)beta2);
     g.bc1 = (float)__dsub_rn(1.0, b1);
     g.bc2 = (float)__dsub_rn(1.0, b2);
     w.b1pow = b1;
     w.b2pow = b2;
-    w.lr = fmaxf(__fmul_rn(w.lr, w.lrate_decay), w.lrate_limit);
+    w.lr = fmaxf(__fmul_rn(lr, lrate_decay), lrate_limit);
     if (s.algo == OPENAI_ES || s.algo == ARS)
-      w.sigma = fmaxf(__fmul_rn(w.sigma, w.sigma_decay), w.sigma_limit);
+      w.sigma = fmaxf(__fmul_rn(sigma, sigma_decay), sigma_limit);
   }
-  w.t = g.t + 1;
+  w.t = t + 1;
   s.gs[r] = g;
 }
 
@@ -442,6 +450,9 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   __shared__ int sh_last;
   pdl_enter();
   const int N = s.N, r = blockIdx.z, jt = gridDim.x, ni = gridDim.y;
+  // the run's hyperparameters, loaded before any store (a load after a store to another array
+  // cannot be hoisted above it: one more dependent round trip each)
+  const int rs_shaping = s.rs[r].shaping, rs_mu = s.rs[r].mu;
   const int j = blockIdx.x * kCountT + threadIdx.x;
   const float fj = j < N ? fit_at(s, fsrc, r, j) : 0.0f;
   const uint32_t kj = j < N ? rank_key(fj) : 0xFFFFFFFFu;
@@ -504,11 +515,11 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
     if (!sh_last) return;
     __threadfence();
   }
-  const RunScal& rs = s.rs[r];
   const bool anti = is_anti(s.algo), cmaish = s.algo == SEP_CMA_ES || s.algo == CMA_ES;
   float val = 0.0f;
   int pos = 0;
   __shared__ int sh_jbest, sh_nw;
+  __shared__ float sh_fbest;
   if (j < N) {
     int sj, ej;
     if (solo) {
@@ -523,12 +534,8 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       s.rcnt[RN + rj] = 0u;
       s.rcnt[2 * RN + rj] = 0u;
     }
-    s.perm[(int64_t)r * N + pos] = j;
-    s.rs_s[rj] = sj;
-    s.rs_e[rj] = ej;
-    s.pos[rj] = pos;
-    s.fit[rj] = fj;
-    if (anti && rs.shaping == 1) {
+    // the shaped value first: its weight loads then precede this thread's stores
+    if (anti && rs_shaping == 1) {
       val = fj;                                                          // raw fitness
     } else if (anti) {
       val = __fdiv_rn((float)(sj + ej - (N - 1)), (float)(2 * (N - 1)));  // N10
@@ -538,13 +545,21 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       for (int q = sj; q <= ej; ++q) acc = __fadd_rn(acc, wpos[q]);
       val = __fdiv_rn(acc, (float)(ej - sj + 1));
     }
+    s.perm[(int64_t)r * N + pos] = j;
+    s.rs_s[rj] = sj;
+    s.rs_e[rj] = ej;
+    s.pos[rj] = pos;
+    s.fit[rj] = fj;
     s.shaped[rj] = val;
     if (solo) {
-      if (pos == 0) sh_jbest = j;
-      if (cmaish && pos == rs.mu - 1) sh_nw = ej + 1;
+      if (pos == 0) {
+        sh_jbest = j;
+        sh_fbest = fj;
+      }
+      if (cmaish && pos == rs_mu - 1) sh_nw = ej + 1;
     } else {
       if (pos == 0) rc_slot(s)[2 * r] = (uint32_t)j;
-      if (cmaish && pos == rs.mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
+      if (cmaish && pos == rs_mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
     }
   }
   sval[threadIdx.x] = val;
@@ -573,7 +588,7 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       const double bbar = t / (double)N;
       __syncthreads();
       for (int i = threadIdx.x; i < N / 2; i += blockDim.x) cB[i] = __dsub_rn(cB[i], bbar);
-      if (threadIdx.x == 0) write_genscal(s, r, sh_jbest, s.fit[(int64_t)r * N + sh_jbest], 0, bbar, 0.0f);
+      if (threadIdx.x == 0) write_genscal(s, r, sh_jbest, sh_fbest, 0, bbar, 0.0f);
       return;
     }
     if (threadIdx.x == 0) s.rbpart[(int64_t)r * kCountMaxTiles + blockIdx.x] = t;
@@ -581,7 +596,7 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   if (solo) {
     __syncthreads();
     if (threadIdx.x == 0)
-      write_genscal(s, r, sh_jbest, s.fit[(int64_t)r * N + sh_jbest], cmaish ? sh_nw : 0, 0.0, 0.0f);
+      write_genscal(s, r, sh_jbest, sh_fbest, cmaish ? sh_nw : 0, 0.0, 0.0f);
     return;
   }
   // ---- the last j-tile of the run: the generation's scalars
