@@ -17,6 +17,7 @@ namespace esb {
 
 static constexpr int kAE = 128;      // threads per block (4 warps, 512 dims)
 static constexpr int kMaxDpt = 32;   // directions per thread-chunk (red buffer bound)
+static constexpr int kAEB = 8;       // directions per batch of the warp's column sums
 
 template <int ALGO>
 __device__ __forceinline__ float ae_scale(const DevState& s, const RunScal& rs, int64_t idx) {
@@ -32,6 +33,9 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
   constexpr bool kAnti = is_anti(ALGO);
   constexpr int M = kAnti ? 2 : 1;
   __shared__ double red[4][kMaxDpt * 2];
+  // per warp: each lane's binary64 partial of the batch's members, [member][lane] with a 33-word
+  // row pitch (the column sums below read down a row: no bank conflicts)
+  __shared__ double col[4][kAEB * M][33];
   const int r = blockIdx.x / bpr, qb = blockIdx.x % bpr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = (int64_t)qb * kAE + threadIdx.x;
@@ -61,64 +65,78 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
   const bool clip = rs.clip != 0;                     // box bounds, block-uniform
   const float lo = rs.clip_lo, hi = rs.clip_hi;
   float* xr = x ? x + (int64_t)r * s.Nloc * s.Dx + 4 * q : nullptr;
-  for (int il = i0; il < i1; ++il) {
-    const uint32_t dir = (uint32_t)(dir0 + il);
-    const float4 z = normal4(ph, (uint32_t)(q + s.q0), dir, t);
-    const float zz[4] = {z.x, z.y, z.z, z.w};
-    float xv[M][4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      xv[0][k] = __fmaf_rn(sc[k], zz[k], m[k]);
-      if (kAnti) xv[M - 1][k] = __fmaf_rn(-sc[k], zz[k], m[k]);
-      if (clip) {
-#pragma unroll
-        for (int h = 0; h < M; ++h) xv[h][k] = fminf(fmaxf(xv[h][k], lo), hi);
-      }
-    }
-    if (WX && q < s.Qx) {                             // owned quads only
-      const int64_t row = kAnti ? 2 * (int64_t)il : il;
-#pragma unroll
-      for (int h = 0; h < M; ++h) {
-        float* p0 = xr + (row + h) * s.Dx;
-        if (V4) {
-          __stcs(reinterpret_cast<float4*>(p0), make_float4(xv[h][0], xv[h][1], xv[h][2], xv[h][3]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (4 * q + k < s.Dx) p0[k] = xv[h][k];
-        }
-      }
-    }
-    float nx[M];
-#pragma unroll
-    for (int h = 0; h < M; ++h) nx[h] = 0.0f;
-    if (FN == FN_ROSENBROCK) {
-#pragma unroll
-      for (int h = 0; h < M; ++h) nx[h] = __shfl_down_sync(0xffffffffu, xv[h][0], 1);
-      if (lane == 31 && has_next) {
-        const float zN = normal4(ph, (uint32_t)(q + 1 + s.q0), dir, t).x;
-        nx[0] = __fmaf_rn(scN, zN, mN);
-        if (kAnti) nx[M - 1] = __fmaf_rn(-scN, zN, mN);
-        if (clip) {
-#pragma unroll
-          for (int h = 0; h < M; ++h) nx[h] = fminf(fmaxf(nx[h], lo), hi);
-        }
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < M; ++h) {
-      FitAcc acc;
-#pragma unroll
+  for (int ib = i0; ib < i1; ib += kAEB) {
+    const int ie = min(i1, ib + kAEB);
+#pragma unroll 2
+    for (int il = ib; il < ie; ++il) {
+      const uint32_t dir = (uint32_t)(dir0 + il);
+      const float4 z = normal4(ph, (uint32_t)(q + s.q0), dir, t);
+      const float zz[4] = {z.x, z.y, z.z, z.w};
+      float xv[M][4];
+  #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int64_t d = 4 * q + k;
-        if (active && d < s.Dx) {                    // a D-shard's halo dim only feeds xn
-          const float xn = k < 3 ? xv[h][k + 1] : nx[h];
-          fit_add<FN>(acc, xv[h][k], xn, d + 1 < s.D);
+        xv[0][k] = __fmaf_rn(sc[k], zz[k], m[k]);
+        if (kAnti) xv[M - 1][k] = __fmaf_rn(-sc[k], zz[k], m[k]);
+        if (clip) {
+  #pragma unroll
+          for (int h = 0; h < M; ++h) xv[h][k] = fminf(fmaxf(xv[h][k], lo), hi);
         }
       }
-      const double tot = warp_sum_d(fit_total<FN>(acc));
-      if (lane == 0) red[warp][M * (il - i0) + h] = tot;
+      if (WX && q < s.Qx) {                             // owned quads only
+        const int64_t row = kAnti ? 2 * (int64_t)il : il;
+  #pragma unroll
+        for (int h = 0; h < M; ++h) {
+          float* p0 = xr + (row + h) * s.Dx;
+          if (V4) {
+            __stcs(reinterpret_cast<float4*>(p0), make_float4(xv[h][0], xv[h][1], xv[h][2], xv[h][3]));
+          } else {
+  #pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (4 * q + k < s.Dx) p0[k] = xv[h][k];
+          }
+        }
+      }
+      float nx[M];
+  #pragma unroll
+      for (int h = 0; h < M; ++h) nx[h] = 0.0f;
+      if (FN == FN_ROSENBROCK) {
+  #pragma unroll
+        for (int h = 0; h < M; ++h) nx[h] = __shfl_down_sync(0xffffffffu, xv[h][0], 1);
+        if (lane == 31 && has_next) {
+          const float zN = normal4(ph, (uint32_t)(q + 1 + s.q0), dir, t).x;
+          nx[0] = __fmaf_rn(scN, zN, mN);
+          if (kAnti) nx[M - 1] = __fmaf_rn(-scN, zN, mN);
+          if (clip) {
+  #pragma unroll
+            for (int h = 0; h < M; ++h) nx[h] = fminf(fmaxf(nx[h], lo), hi);
+          }
+        }
+      }
+  #pragma unroll
+      for (int h = 0; h < M; ++h) {
+        FitAcc acc;
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t d = 4 * q + k;
+          if (active && d < s.Dx) {                    // a D-shard's halo dim only feeds xn
+            const float xn = k < 3 ? xv[h][k + 1] : nx[h];
+            fit_add<FN>(acc, xv[h][k], xn, d + 1 < s.D);
+          }
+        }
+        col[warp][M * (il - ib) + h][lane] = fit_total<FN>(acc);
+      }
     }
+    // the members' sums over the warp's 32 lanes, one member per lane, in lane order (instead of a
+    // 5-round shuffle reduction per member: the reduction cost per member falls from 15 warp
+    // instructions to 2 × 32 / (8·M) plus one store)
+    __syncwarp();
+    if (lane < M * (ie - ib)) {
+      double v = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) v = __dadd_rn(v, col[warp][lane][k]);
+      red[warp][M * (ib - i0) + lane] = v;
+    }
+    __syncwarp();
   }
   __syncthreads();
   const int cnt = M * (i1 - i0);
