@@ -73,49 +73,49 @@ __global__ void __launch_bounds__(kAE) ask_eval_kernel(DevState s, float* __rest
       const float4 z = normal4(ph, (uint32_t)(q + s.q0), dir, t);
       const float zz[4] = {z.x, z.y, z.z, z.w};
       float xv[M][4];
-  #pragma unroll
+#pragma unroll
       for (int k = 0; k < 4; ++k) {
         xv[0][k] = __fmaf_rn(sc[k], zz[k], m[k]);
         if (kAnti) xv[M - 1][k] = __fmaf_rn(-sc[k], zz[k], m[k]);
         if (clip) {
-  #pragma unroll
+#pragma unroll
           for (int h = 0; h < M; ++h) xv[h][k] = fminf(fmaxf(xv[h][k], lo), hi);
         }
       }
       if (WX && q < s.Qx) {                             // owned quads only
         const int64_t row = kAnti ? 2 * (int64_t)il : il;
-  #pragma unroll
+#pragma unroll
         for (int h = 0; h < M; ++h) {
           float* p0 = xr + (row + h) * s.Dx;
           if (V4) {
             __stcs(reinterpret_cast<float4*>(p0), make_float4(xv[h][0], xv[h][1], xv[h][2], xv[h][3]));
           } else {
-  #pragma unroll
+#pragma unroll
             for (int k = 0; k < 4; ++k)
               if (4 * q + k < s.Dx) p0[k] = xv[h][k];
           }
         }
       }
       float nx[M];
-  #pragma unroll
+#pragma unroll
       for (int h = 0; h < M; ++h) nx[h] = 0.0f;
       if (FN == FN_ROSENBROCK) {
-  #pragma unroll
+#pragma unroll
         for (int h = 0; h < M; ++h) nx[h] = __shfl_down_sync(0xffffffffu, xv[h][0], 1);
         if (lane == 31 && has_next) {
           const float zN = normal4(ph, (uint32_t)(q + 1 + s.q0), dir, t).x;
           nx[0] = __fmaf_rn(scN, zN, mN);
           if (kAnti) nx[M - 1] = __fmaf_rn(-scN, zN, mN);
           if (clip) {
-  #pragma unroll
+#pragma unroll
             for (int h = 0; h < M; ++h) nx[h] = fminf(fmaxf(nx[h], lo), hi);
           }
         }
       }
-  #pragma unroll
+#pragma unroll
       for (int h = 0; h < M; ++h) {
         FitAcc acc;
-  #pragma unroll
+#pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int64_t d = 4 * q + k;
           if (active && d < s.Dx) {                    // a D-shard's halo dim only feeds xn
