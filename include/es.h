@@ -363,6 +363,7 @@ int32_t es_profile_read(es_ctx_t *ctx, char *names /* [max_kinds][32] */, double
  *   which = 4  ρ square root:      in float [n] (= −2·LN(u))                    → out float [n]
  *   which = 5  sin(πb), b ≤ 1/2 (N7): in float [n]                              → out float [n]
  *   which = 6  tanh of the MLP (N14): in float [n]                              → out float [n]
+ *   which = 7  tanh of N14′'s hidden layers (rounded to binary16 next): float [n] → float [n]
  * in/out are device pointers. Errors: ES_ERR_INVALID_ARG for unknown `which` or n < 0. */
 es_status_t es_debug_primitive(int32_t which, const void *in, void *out, int64_t n,
                                es_stream_t stream);

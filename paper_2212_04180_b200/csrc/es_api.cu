@@ -1155,7 +1155,7 @@ int32_t es_profile_read(es_ctx_t* c, char* names, double* ms, int64_t* counts, i
 
 es_status_t es_debug_primitive(int32_t which, const void* in, void* out, int64_t n,
                                es_stream_t stream_) {
-  if (which < 0 || which > 6 || n < 0) return fail(nullptr, ES_ERR_INVALID_ARG, "bad which/n");
+  if (which < 0 || which > 7 || n < 0) return fail(nullptr, ES_ERR_INVALID_ARG, "bad which/n");
   if (n > 0 && (!in || !out)) return fail(nullptr, ES_ERR_INVALID_ARG, "NULL argument");
   CUDA_OR(nullptr, launch_primitive(which, in, out, n, (cudaStream_t)stream_));
   return ES_SUCCESS;

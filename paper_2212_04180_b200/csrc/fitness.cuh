@@ -61,28 +61,48 @@ __device__ __forceinline__ double fit_total(const FitAcc& acc) {
   return FN == FN_RASTRIGIN ? __fma_rn(20.0, acc.b, acc.a) : acc.a;
 }
 
-// tanh to ≤ 5·10⁻⁷ relative (NUMERICS N14): the odd [13/6] rational x·p(x²)/q(x²) on x clamped
-// to ±7.9053 (where it reaches ±1 in binary32); ONE MUFU (rcp) —
-// the epilogues that call it are bound by the XU pipe, which a 1 − 2/(1 + e^{2x}) form loads twice.
-// 4.3·10⁻⁷ modelled in binary32 with the reciprocal 1 ulp off; tested on a dense sweep.
+// tanh to ≤ 5·10⁻⁷ relative (NUMERICS N14): the odd [9/8] rational x·p(x²)/q(x²) (p₀ = q₀ = 1) on
+// x clamped to ±7.9053 (where it reaches ±1 in binary32); ONE MUFU (rcp) — a 1 − 2/(1 + e^{2x})
+// form loads the XU pipe twice. 3.0·10⁻⁷ modelled in binary32 (+ the reciprocal's ulp: ≤ 4.2·10⁻⁷);
+// tested on a dense sweep. 14 instructions per value (the earlier [13/6] form took 15).
 __device__ __forceinline__ float tanh32(float x) {
   const float xc = fminf(fmaxf(x, -7.90531110763549805f), 7.90531110763549805f);
   const float s = __fmul_rn(xc, xc);
-  float p = -2.76076847742355e-16f;
-  p = __fmaf_rn(p, s, 2.00018790482477e-13f);
-  p = __fmaf_rn(p, s, -8.60467152213735e-11f);
-  p = __fmaf_rn(p, s, 5.12229709037114e-08f);
-  p = __fmaf_rn(p, s, 1.48572235717979e-05f);
-  p = __fmaf_rn(p, s, 6.37261928875436e-04f);
-  p = __fmaf_rn(p, s, 4.89352455891786e-03f);
+  float p = 0x1.08dd48p-26f;
+  p = __fmaf_rn(p, s, 0x1.715eecp-16f);
+  p = __fmaf_rn(p, s, 0x1.d50d80p-9f);
+  p = __fmaf_rn(p, s, 0x1.13763cp-3f);
+  p = __fmaf_rn(p, s, 1.0f);
   p = __fmul_rn(xc, p);
-  float q = 1.19825839466702e-06f;
-  q = __fmaf_rn(q, s, 1.18534705686654e-04f);
-  q = __fmaf_rn(q, s, 2.26843463243900e-03f);
-  q = __fmaf_rn(q, s, 4.89352518554385e-03f);
+  float q = 0x1.cd6b4ap-21f;
+  q = __fmaf_rn(q, s, 0x1.66ecccp-12f);
+  q = __fmaf_rn(q, s, 0x1.ad1bd8p-6f);
+  q = __fmaf_rn(q, s, 0x1.df1070p-2f);
+  q = __fmaf_rn(q, s, 1.0f);
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
-  return __fmul_rn(p, r);     // tiny |x|: p/q = x·α₁/β₀ = x·(1 − 1.3·10⁻⁷), no select needed
+  return __fmul_rn(p, r);     // tiny |x|: p/q = x (p0 = q0 = 1), no select needed
+}
+
+// tanh of an activation that is rounded to binary16 next (N14′ hidden layers): the odd [7/6]
+// rational x·p(x²)/q(x²) on x clamped to ±4.6 — past it tanh rounds to ±1 in binary16, and the
+// rational's value there, 0.99979794, is above 1 − 2⁻¹² — ≤ 2.8·10⁻⁷ relative inside (modelled in
+// binary32); 12 instructions per value instead of tanh32's 14.
+__device__ __forceinline__ float tanh16h(float x) {
+  const float xc = fminf(fmaxf(x, -4.6f), 4.6f);
+  const float s = __fmul_rn(xc, xc);
+  float p = 0x1.6cb52ep-18f;
+  p = __fmaf_rn(p, s, 0x1.4e0136p-9f);
+  p = __fmaf_rn(p, s, 0x1.01c874p-3f);
+  p = __fmaf_rn(p, s, 1.0f);
+  p = __fmul_rn(xc, p);
+  float q = 0x1.6cb002p-13f;
+  q = __fmaf_rn(q, s, 0x1.6d1718p-6f);
+  q = __fmaf_rn(q, s, 0x1.d6397cp-2f);
+  q = __fmaf_rn(q, s, 1.0f);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+  return __fmul_rn(p, r);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {

@@ -26,6 +26,8 @@ __global__ void prim_kernel(int which, const void* __restrict__ in, void* __rest
     static_cast<float*>(out)[k] = rho_sqrt(static_cast<const float*>(in)[k]);
   } else if (which == 6) {
     static_cast<float*>(out)[k] = tanh32(static_cast<const float*>(in)[k]);
+  } else if (which == 7) {
+    static_cast<float*>(out)[k] = tanh16h(static_cast<const float*>(in)[k]);
   } else if (which == 1) {
     static_cast<float*>(out)[k] = ln_poly(static_cast<const float*>(in)[k]);
   } else {

@@ -40,7 +40,8 @@ static constexpr int kEpiWarpsTma = 16;
 static constexpr int kThreadsTma = (1 + kEpiWarpsTma + 1) * 32;
 static constexpr int kTileBytes = 128 * 128;              // [128 rows × 64 k] fp16 = 16 KB
 static constexpr int kABytes = 8 * kTileBytes;            // A: up to K = 512 (8 k-blocks)
-static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 2048;   // + barriers, bias
+static constexpr int kSmemBytes = kABytes + kStages * kTileBytes + 3072;   // + barriers, fp32 bias
+static_assert(kSmemBytes <= 232448, "fp16-image MLP kernel exceeds 227 KB of shared memory");
 #ifndef ES_MLP16_AHEAD
 #define ES_MLP16_AHEAD 1   // L2 look-ahead of the fp16-image MLP producer, in (layer, n-tile) blocks
                            // (measured at C4: 1 → 1.72 ms, 2 → 1.79)
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
   float* red = reinterpret_cast<float*>(bars + 2 * kStages + 9);   // [EW] (≤ 128 B)
   // TMA mode: the layer's fp16 bias, staged once per layer (≤ 512 values)
-  __half* bias_s = reinterpret_cast<__half*>(smem + kABytes + kStages * kTileBytes + 512);
+  float* bias_s = reinterpret_cast<float*>(smem + kABytes + kStages * kTileBytes + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (smem_u32(smem) & 1023) __trap();               // SWIZZLE_128B needs 1024-B alignment
@@ -322,10 +323,16 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
         const int ntl = P.npad[l] >> 7;              // n-tiles (dready barriers) of this layer
         if (TMA) {
           // stage the bias while the layer's MMAs run (its HBM latency was exposed per chunk)
-          for (int o = et; o < (out >> 3); o += EW * 32)
-            reinterpret_cast<uint4*>(bias_s)[o] = __ldg(reinterpret_cast<const uint4*>(bias16) + o);
+          // staged as fp32 (the fp16 values exactly): one conversion per column, not per element
+          for (int o = et; o < (out >> 3); o += EW * 32) {
+            const uint4 hb = __ldg(reinterpret_cast<const uint4*>(bias16) + o);
+            const __half* hh = reinterpret_cast<const __half*>(&hb);
+            float4* d4 = reinterpret_cast<float4*>(bias_s + 8 * o);
+            d4[0] = make_float4(__half2float(hh[0]), __half2float(hh[1]), __half2float(hh[2]), __half2float(hh[3]));
+            d4[1] = make_float4(__half2float(hh[4]), __half2float(hh[5]), __half2float(hh[6]), __half2float(hh[7]));
+          }
           for (int n = (out & ~7) + et; n < P.npad[l]; n += EW * 32)
-            bias_s[n] = n < out ? bias16[n] : __float2half_rn(0.0f);   // padded columns finite
+            bias_s[n] = n < out ? __half2float(bias16[n]) : 0.0f;   // padded columns finite
           named_bar(1, EW * 32);
         }
 
@@ -377,27 +384,44 @@ __global__ void __launch_bounds__(TMA ? kThreadsTma : kThreads, 1)
           if (TMA) {
             // branch-free (the tanh chains interleave): past `out` the accumulator (zero-filled
             // weight rows) and the staged bias (padded with 0) are 0, and tanh(0) = 0
+            // hidden layers: tanh16h (the value is rounded to binary16 next); the output layer
+            // keeps tanh32 (its activation enters the squared error in fp32)
+            if (l < L) {
 #pragma unroll
-            for (int i = 0; i < CW; i += 8) {
-              const uint4 hb = *reinterpret_cast<const uint4*>(bias_s + c0 + i);
-              const __half* hh = reinterpret_cast<const __half*>(&hb);
+              for (int i = 0; i < CW; i += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c0 + i);
+                v[i] = tanh16h(__fadd_rn(v[i], b4.x));
+                v[i + 1] = tanh16h(__fadd_rn(v[i + 1], b4.y));
+                v[i + 2] = tanh16h(__fadd_rn(v[i + 2], b4.z));
+                v[i + 3] = tanh16h(__fadd_rn(v[i + 3], b4.w));
+              }
+            } else {
 #pragma unroll
-              for (int u = 0; u < 8; ++u) v[i + u] = tanh32(__fadd_rn(v[i + u], __half2float(hh[u])));
+              for (int i = 0; i < CW; i += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c0 + i);
+                v[i] = tanh32(__fadd_rn(v[i], b4.x));
+                v[i + 1] = tanh32(__fadd_rn(v[i + 1], b4.y));
+                v[i + 2] = tanh32(__fadd_rn(v[i + 2], b4.z));
+                v[i + 3] = tanh32(__fadd_rn(v[i + 3], b4.w));
+              }
             }
           } else if (c0 + CW <= out) {
+            // the same activations as the TMA path: tanh16h for hidden layers, tanh32 last
+            auto act = [&](float a) { return l < L ? tanh16h(a) : tanh32(a); };
 #pragma unroll
             for (int i = 0; i < CW; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
-              v[i] = tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
-              v[i + 1] = tanh32(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
-              v[i + 2] = tanh32(__fadd_rn(v[i + 2], __half2float(__float2half_rn(b4.z))));
-              v[i + 3] = tanh32(__fadd_rn(v[i + 3], __half2float(__float2half_rn(b4.w))));
+              v[i] = act(__fadd_rn(v[i], __half2float(__float2half_rn(b4.x))));
+              v[i + 1] = act(__fadd_rn(v[i + 1], __half2float(__float2half_rn(b4.y))));
+              v[i + 2] = act(__fadd_rn(v[i + 2], __half2float(__float2half_rn(b4.z))));
+              v[i + 3] = act(__fadd_rn(v[i + 3], __half2float(__float2half_rn(b4.w))));
             }
           } else {
+            auto act = [&](float a) { return l < L ? tanh16h(a) : tanh32(a); };
 #pragma unroll
             for (int i = 0; i < CW; ++i) {
               const int n = c0 + i;
-              v[i] = n < out ? tanh32(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
+              v[i] = n < out ? act(__fadd_rn(v[i], __half2float(__float2half_rn(__ldg(bias + n)))))
                              : 0.0f;
             }
           }

@@ -104,6 +104,26 @@ def test_mlp_tanh_accuracy():
     assert np.all(dev[x == 0] == 0.0)
 
 
+def test_mlp16_hidden_tanh():
+    """N14′'s hidden-layer tanh (its value is rounded to binary16 next): within 3.5e-7 relative
+    of binary64 tanh on |x| <= 4.6, and beyond the clamp its binary16 rounding is exactly +-1
+    (as tanh's is: tanh(4.6) > 1 - 2^-12); odd, tanh(0) = 0."""
+    rng = np.random.default_rng(12)
+    x = np.concatenate([np.linspace(-12, 12, 1 << 22), rng.uniform(-0.7, 0.7, 1 << 20),
+                        np.exp2(rng.uniform(-40, 3, 1 << 18)) * rng.choice([-1, 1], 1 << 18),
+                        [0.0, 4.6, -4.6, 4.59999, 4.60001, 30.0, -30.0, 1e30, -1e30]])
+    x = x.astype(np.float32)
+    dev = _prim(7, torch.from_numpy(x).cuda(), torch.empty(x.size, device="cuda")).cpu().numpy()
+    ref = np.tanh(x.astype(np.float64))
+    inr = np.abs(x) <= np.float32(4.6)
+    rel = np.abs(dev[inr].astype(np.float64) - ref[inr]) / np.maximum(np.abs(ref[inr]), 1e-30)
+    assert rel.max() <= 3.5e-7, (rel.max(), x[inr][rel.argmax()])
+    h = dev[~inr].astype(np.float16)
+    assert np.array_equal(h, np.sign(x[~inr]).astype(np.float16)), h
+    assert np.all(dev[x == 0] == 0.0)
+    assert np.array_equal(dev[x == 4.6], -dev[x == -4.6])
+
+
 @pytest.mark.parametrize("seed,i,t,tag", [(0, 0, 0, 0), (12345, 7, 3, 0), (2 ** 40 + 5, 99, 1000, 1),
                                           (77, 0, 0, 4)])
 def test_normals_bit_exact(seed, i, t, tag):
