@@ -10,4 +10,4 @@ for c in c1 c3 c5 c4 c6; do
 done
 timeout 600 python bench.py --config c4 --mlp fp16 --no-cpu-baseline > gpurun_out/${T}_bench_c4fp16.log 2>&1; echo "bench c4 fp16 rc=$?"
 tail -1 gpurun_out/${T}_bench_c4fp16.log | python -c 'import json,sys; d=json.load(sys.stdin); print(round(d["ms_per_step"],4), json.dumps(d.get("kernel_ms_by_handle")))'
-TAG=$T bash tools/_prof_final.sh
+TAG=$T bash tools/runs/_prof_final.sh
