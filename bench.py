@@ -751,14 +751,18 @@ def e2e_run(hs, args, world, fused=False, write_x=True):
     from paper_2212_04180_b200._lib import check, lib
     import ctypes as C
 
-    # independent handles on their own streams (as a user driving two batches would): each phase
-    # is issued for every handle before the next, so a host-buffer call that waits on one
-    # handle's stream leaves the other's work running
+    # independent handles on their own streams (as a user driving two batches would): the asks
+    # are issued for every handle first; then, handle by handle, the evaluation into host memory
+    # (which waits on that handle's stream only) and the tell from it, so one handle's tell is
+    # already queued while the host waits for the next handle's fitness; best_fitness last
     streams = [torch.cuda.Stream() for _ in hs] if len(hs) > 1 else [torch.cuda.current_stream()]
     ss = [C.c_void_p(st.cuda_stream) for st in streams]
 
     def step():
-        for (label, cfg, es, x, _), f, s, st in zip(hs, fh, ss, streams):
+        if not fused and hs[0][1]["fn"] is not None:
+            for (label, cfg, es, x, _), st in zip(hs, streams):
+                es.ask(out=x, stream=st)
+        for (label, cfg, es, x, _), f, s in zip(hs, fh, ss):
             n = cfg["R"] * es.local_popsize
             if cfg["fn"] is None:
                 check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
@@ -767,13 +771,8 @@ def e2e_run(hs, args, world, fused=False, write_x=True):
                                         C.c_void_p(x.data_ptr()) if write_x else None,
                                         C.c_void_p(f.data_ptr()), s), es.ctx)
             else:
-                es.ask(out=x, stream=st)
-        if not fused and hs[0][1]["fn"] is not None:
-            for (label, cfg, es, x, _), f, s in zip(hs, fh, ss):
-                n = cfg["R"] * es.local_popsize
                 check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n,
                                          cfg["D"], C.c_void_p(f.data_ptr()), s), es.ctx)
-        for (label, cfg, es, x, _), f, s in zip(hs, fh, ss):
             check(lib().es_tell(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
         for (label, cfg, es, x, _), b, s in zip(hs, bh, ss):
             check(lib().es_get(es.ctx, 8, C.c_void_p(b.data_ptr()), s), es.ctx)
