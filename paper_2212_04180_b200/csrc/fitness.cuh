@@ -84,6 +84,28 @@ __device__ __forceinline__ float tanh32(float x) {
   return __fmul_rn(p, r);     // tiny |x|: p/q = x (p0 = q0 = 1), no select needed
 }
 
+// 2⁸·tanh(x) — tanh32 with p's coefficients scaled by 2⁸ (exact: a power of two), so the value is
+// bit for bit fmul(tanh32(x), 256): the fp32 MLP's hidden activations enter the binary16 split
+// pre-scaled without a multiply per value.
+__device__ __forceinline__ float tanh32_x256(float x) {
+  const float xc = fminf(fmaxf(x, -7.90531110763549805f), 7.90531110763549805f);
+  const float s = __fmul_rn(xc, xc);
+  float p = 0x1.08dd48p-18f;
+  p = __fmaf_rn(p, s, 0x1.715eecp-8f);
+  p = __fmaf_rn(p, s, 0x1.d50d80p-1f);
+  p = __fmaf_rn(p, s, 0x1.13763cp+5f);
+  p = __fmaf_rn(p, s, 256.0f);
+  p = __fmul_rn(xc, p);
+  float q = 0x1.cd6b4ap-21f;
+  q = __fmaf_rn(q, s, 0x1.66ecccp-12f);
+  q = __fmaf_rn(q, s, 0x1.ad1bd8p-6f);
+  q = __fmaf_rn(q, s, 0x1.df1070p-2f);
+  q = __fmaf_rn(q, s, 1.0f);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+  return __fmul_rn(p, r);
+}
+
 // tanh of an activation that is rounded to binary16 next (N14′ hidden layers): the odd [7/6]
 // rational x·p(x²)/q(x²) on x clamped to ±4.6 — past it tanh rounds to ±1 in binary16, and the
 // rational's value there, 0.99979794, is above 1 − 2⁻¹² — ≤ 2.8·10⁻⁷ relative inside (modelled in

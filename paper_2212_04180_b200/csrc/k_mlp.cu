@@ -563,6 +563,16 @@ static_assert(kSmem32Bytes <= 232448, "fp32 MLP kernel exceeds 227 KB of shared 
 static constexpr int kThreads32 = (1 + kEpiWarps + 1) * 32;
 static constexpr float kSplitScale = 256.0f, kUnscale = 1.0f / 65536.0f;
 
+// hi / lo binary16 parts of 8 values already scaled by 2⁸
+__device__ __forceinline__ void split8s(const float* s, uint4& hi, uint4& lo) {
+  float r[8];
+  hi = pack8(s);
+  const __half* h = reinterpret_cast<const __half*>(&hi);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = __fsub_rn(s[i], __half2float(h[i]));
+  lo = pack8(r);
+}
+
 // hi / lo binary16 parts of 8 scaled values
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   float s[8], r[8];
@@ -702,8 +712,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
     const bool hiw = q < 2;                          // lanes 0–63: the A_hi rows
     const int prid = part * 2 + (q & 1);             // named barrier of the pair
     const int side = hiw ? 0 : 16;                   // this warp's 16 result columns in the part
-    float* xmine = xbuf + (prid * 2 + (hiw ? 0 : 1)) * (8 * 32);    // [8 cols][32 lanes] I write
-    const float* xpeer = xbuf + (prid * 2 + (hiw ? 1 : 0)) * (8 * 32);
+    // [2 col quads][32 lanes] float4 I write / the peer wrote (16-byte accesses: 4 per round)
+    float4* xmine = reinterpret_cast<float4*>(xbuf + (prid * 2 + (hiw ? 0 : 1)) * (8 * 32));
+    const float4* xpeer = reinterpret_cast<const float4*>(xbuf + (prid * 2 + (hiw ? 1 : 0)) * (8 * 32));
     const int rh = (q & 1) * 32 + lane;              // batch row within the half (A rows rh, 64+rh)
     const int brow = half * 64 + rh;                 // batch row of this lane
     const int et = threadIdx.x - 32;                 // 0..511
@@ -780,13 +791,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
             named_bar(2 + prid, 64);
+            float sv[8], mv[8];                        // the peer's 8 columns, this warp's 8
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              xmine[i * 32 + lane] = hiw ? v[16 + 8 * rr + i] : v[8 * rr + i];
+            for (int i = 0; i < 8; ++i) {
+              sv[i] = hiw ? v[16 + 8 * rr + i] : v[8 * rr + i];
+              mv[i] = hiw ? v[8 * rr + i] : v[16 + 8 * rr + i];
+            }
+            xmine[lane] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+            xmine[32 + lane] = make_float4(sv[4], sv[5], sv[6], sv[7]);
             named_bar(2 + prid, 64);
+            const float4 p0 = xpeer[lane], p1 = xpeer[32 + lane];
+            const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              x[8 * rr + i] = __fadd_rn(hiw ? v[8 * rr + i] : v[16 + 8 * rr + i], xpeer[i * 32 + lane]);
+            for (int i = 0; i < 8; ++i) x[8 * rr + i] = __fadd_rn(mv[i], pv[i]);
           }
           const int cb = c0 + side;                  // first of this warp's 16 columns
           // a = D·2^-16 + b (the product by 2^-16 is exact), h = tanh(a)
@@ -796,13 +813,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
             // branch-free over the 16 columns (so the 16 tanh chains interleave): past `out` the
             // accumulator (zero-filled weight rows) and the staged bias are 0, and tanh(0) = 0
+            // hidden layers: 2⁸·tanh (the split's scale folded into the rational's numerator)
+            if (l < L) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[i + u] = tanh32(__fmaf_rn(x[i + u], kUnscale, bb[u]));
+              for (int u = 0; u < 4; ++u) x[i + u] = tanh32_x256(__fmaf_rn(x[i + u], kUnscale, bb[u]));
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) x[i + u] = tanh32(__fmaf_rn(x[i + u], kUnscale, bb[u]));
+            }
           }
           if (l < L) {
             uint4 h[4];                              // hi split of 16 columns, then the lo split
-            split8(x, h[0], h[2]);
-            split8(x + 8, h[1], h[3]);
+            split8s(x, h[0], h[2]);
+            split8s(x + 8, h[1], h[3]);
             tmem_st16(trow + (uint32_t)cb, h);       // parked in this lane's consumed columns
           } else if (P.mode == 0) {
             const float* yr = P.Y32 + (int64_t)brow * out;
