@@ -791,19 +791,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads32, 1)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
             named_bar(2 + prid, 64);
-            float sv[8], mv[8];                        // the peer's 8 columns, this warp's 8
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              sv[i] = hiw ? v[16 + 8 * rr + i] : v[8 * rr + i];
-              mv[i] = hiw ? v[8 * rr + i] : v[16 + 8 * rr + i];
+            // warp-uniform roles (no per-value selects): the hi warp hands over columns 16–31
+            // of the part and finishes 0–15, the lo warp the reverse
+            if (hiw) {
+              xmine[lane] = make_float4(v[16 + 8 * rr], v[17 + 8 * rr], v[18 + 8 * rr], v[19 + 8 * rr]);
+              xmine[32 + lane] = make_float4(v[20 + 8 * rr], v[21 + 8 * rr], v[22 + 8 * rr], v[23 + 8 * rr]);
+            } else {
+              xmine[lane] = make_float4(v[8 * rr], v[1 + 8 * rr], v[2 + 8 * rr], v[3 + 8 * rr]);
+              xmine[32 + lane] = make_float4(v[4 + 8 * rr], v[5 + 8 * rr], v[6 + 8 * rr], v[7 + 8 * rr]);
             }
-            xmine[lane] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-            xmine[32 + lane] = make_float4(sv[4], sv[5], sv[6], sv[7]);
             named_bar(2 + prid, 64);
             const float4 p0 = xpeer[lane], p1 = xpeer[32 + lane];
             const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+            if (hiw) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) x[8 * rr + i] = __fadd_rn(mv[i], pv[i]);
+              for (int i = 0; i < 8; ++i) x[8 * rr + i] = __fadd_rn(v[8 * rr + i], pv[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[8 * rr + i] = __fadd_rn(v[16 + 8 * rr + i], pv[i]);
+            }
           }
           const int cb = c0 + side;                  // first of this warp's 16 columns
           // a = D·2^-16 + b (the product by 2^-16 is exact), h = tanh(a)
