@@ -73,10 +73,9 @@ __device__ __forceinline__ void store_img(__half* h, const float* v, int mode, i
     u.x = *reinterpret_cast<uint32_t*>(&a0);
     u.y = *reinterpret_cast<uint32_t*>(&a1);
     __stcs(reinterpret_cast<uint2*>(h), u);
-  } else {
-    float sc[4], r[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sc[k] = __fmul_rn(v[k], 256.0f);
+  } else {                                  // mode 2: v is already x·2⁸ (see ask_kernel)
+    float r[4];
+    const float* sc = v;
     __half2 a0 = __floats2half2_rn(sc[0], sc[1]), a1 = __floats2half2_rn(sc[2], sc[3]);
     const float2 b0 = __half22float2(a0), b1 = __half22float2(a1);
     r[0] = __fsub_rn(sc[0], b0.x); r[1] = __fsub_rn(sc[1], b0.y);
@@ -109,15 +108,19 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
   const Philox ph(rs.seed);
   const uint32_t t = rs.t;
   const int64_t base = (int64_t)r * s.D + 4 * q;
+  // IMG 2 (the split image of x·2⁸): m, the scale and the box are pre-multiplied by 2⁸, so the
+  // FFMA yields x·2⁸ directly — fma(2⁸σ, z, 2⁸m) = 2⁸·fma(σ, z, m) exactly (a power of two), and
+  // so is the clamp; x itself, when written, is that times 2⁻⁸ (exact)
+  constexpr float kPre = IMG == 2 ? 256.0f : 1.0f;
   float m[4], sc[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const bool ok = 4 * q + k < s.D;
-    m[k] = ok ? s.vec[F_MEAN][base + k] : 0.0f;
-    sc[k] = ok ? ask_scale<ALGO>(s, rs, base + k) : 0.0f;
+    m[k] = ok ? __fmul_rn(s.vec[F_MEAN][base + k], kPre) : 0.0f;
+    sc[k] = ok ? __fmul_rn(ask_scale<ALGO>(s, rs, base + k), kPre) : 0.0f;
   }
   const int dir0 = s.rank * Ploc;
-  const float lo = CLIP ? rs.clip_lo : 0.0f, hi = CLIP ? rs.clip_hi : 0.0f;
+  const float lo = CLIP ? __fmul_rn(rs.clip_lo, kPre) : 0.0f, hi = CLIP ? __fmul_rn(rs.clip_hi, kPre) : 0.0f;
   // row pointers advance by one direction's rows per iteration (no per-iteration 64-bit multiply)
   const int64_t step = (kAnti ? 2 : 1) * s.Dx;
   const int64_t first = (int64_t)r * s.Nloc * s.Dx + 4 * q + (int64_t)i0 * step;
@@ -142,6 +145,13 @@ __global__ void __launch_bounds__(kAskThreads) ask_kernel(DevState s, float* __r
       store_img(h0, xp, IMG, plane);
       if (kAnti) store_img(h0 + s.Dx, xm, IMG, plane);
       if (!p0) continue;
+      if (IMG == 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          xp[k] = __fmul_rn(xp[k], 1.0f / 256.0f);
+          if (kAnti) xm[k] = __fmul_rn(xm[k], 1.0f / 256.0f);
+        }
+      }
     }
     if (V4) {
       __stcs(reinterpret_cast<float4*>(p0), make_float4(xp[0], xp[1], xp[2], xp[3]));
