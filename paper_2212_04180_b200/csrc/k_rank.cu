@@ -85,8 +85,19 @@ __device__ void write_genscal(const DevState& s, int r, int jbest, float fb, int
 // scalars (N9–N12 bookkeeping). `keys` is the run's sorted array (shared or global memory).
 // fit: the run's fitness in sorted-input order (shared memory when the caller staged it there —
 // load_key also writes the global copy es_get reads).
+// aux (optional, N ≤ kAuxMaxN): on-chip copies — [N] shaped, [N] tie ends, [N] perm, and the
+// run's position weights prefetched by the caller — so the second half reads no global value
+// this CTA has just written (each such read was a dependent L2 round trip).
+static constexpr int kAuxMaxN = 4096;
+struct RankAux {
+  float* shaped;
+  int32_t* E;
+  int32_t* perm;
+  const float* wpos;
+};
+
 __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, double* red,
-                            int32_t* sh_nw_p, const float* fit) {
+                            int32_t* sh_nw_p, const float* fit, RankAux aux = RankAux{}) {
   const int N = s.N, T = blockDim.x;
   int32_t& sh_nw = *sh_nw_p;
   // tie groups and shaping
@@ -95,7 +106,11 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
   int32_t* S = s.rs_s + (int64_t)r * N;
   int32_t* E = s.rs_e + (int64_t)r * N;
   float* shaped = s.shaped + (int64_t)r * N;
-  const float* wpos = s.wpos + (int64_t)r * N;
+  const float* wpos = aux.wpos ? aux.wpos : s.wpos + (int64_t)r * N;
+  const bool on_chip = aux.shaped != nullptr;
+  const float* shaped_r = on_chip ? aux.shaped : shaped;   // read side after the barrier
+  const int32_t* E_r = on_chip ? aux.E : E;
+  const int32_t* perm_r = on_chip ? aux.perm : perm;
   const bool anti = is_anti(s.algo);
   // z-score shaping: population mean and std of the fitness, binary64
   double zmu = 0.0, zsd = 1.0;
@@ -131,6 +146,10 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     S[j] = sj;
     E[j] = ej;
     s.pos[(int64_t)r * N + j] = p;
+    if (on_chip) {
+      aux.perm[p] = j;
+      aux.E[j] = ej;
+    }
     float val;
     if (s.algo == ARS || (anti && rs.shaping == 1)) {
       val = fit[j];                                                      // raw fitness
@@ -144,6 +163,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
       val = __fdiv_rn(acc, (float)(ej - sj + 1));
     }
     shaped[j] = val;
+    if (on_chip) aux.shaped[j] = val;
   }
   __syncthreads();
   // per-entry tell coefficients
@@ -153,7 +173,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
   double bbar = 0.0;
   if (s.algo == PGPE) {
     double part = 0.0;
-    for (int j = threadIdx.x; j < N; j += T) part = __dadd_rn(part, (double)shaped[j]);
+    for (int j = threadIdx.x; j < N; j += T) part = __dadd_rn(part, (double)shaped_r[j]);
     bbar = block_sum(part, red) / (double)N;
   }
   float ars_scale = 0.0f;
@@ -167,7 +187,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     const int k = rs.ars_k;
     const int per = (N + T - 1) / T, p0 = threadIdx.x * per, p1 = min(N, p0 + per);
     int cnt = 0;
-    for (int p = p0; p < p1; ++p) cnt += pos[perm[p] ^ 1] > p;
+    for (int p = p0; p < p1; ++p) cnt += pos[perm_r[p] ^ 1] > p;
     // exclusive scan of cnt over the block (fixed order)
     int* scan = reinterpret_cast<int*>(red);          // ≤ 32 warps: warp totals
     int v = cnt;
@@ -184,15 +204,15 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     int idx = wbase + v - cnt;
     double psum = 0.0;
     for (int p = p0; p < p1; ++p) {
-      if (pos[perm[p] ^ 1] > p) {
+      if (pos[perm_r[p] ^ 1] > p) {
         if (idx < k) {
-          const int i = perm[p] >> 1;
+          const int i = perm_r[p] >> 1;
           dir[idx] = (uint32_t)i;
           if (s.algo == ARS) {         // raw differences; σ_R below
             cA[idx] = __dsub_rn((double)fit[2 * i], (double)fit[2 * i + 1]);
             psum = __dadd_rn(psum, __dadd_rn((double)fit[2 * i], (double)fit[2 * i + 1]));
           } else {                     // PGPE: shaped coefficients, whole-population baseline
-            const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
+            const double cp = shaped_r[2 * i], cm = shaped_r[2 * i + 1];
             cA[idx] = __dsub_rn(cp, cm);
             cB[idx] = __dsub_rn(__dmul_rn(__dadd_rn(cp, cm), 0.5), bbar);
           }
@@ -214,7 +234,7 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
     }
   } else if (anti) {
     for (int i = threadIdx.x; i < N / 2; i += T) {
-      const double cp = shaped[2 * i], cm = shaped[2 * i + 1];
+      const double cp = shaped_r[2 * i], cm = shaped_r[2 * i + 1];
       dir[i] = (uint32_t)i;
       cA[i] = __dsub_rn(cp, cm);
       if (s.algo == PGPE) cB[i] = __dsub_rn(__dmul_rn(__dadd_rn(cp, cm), 0.5), bbar);
@@ -222,15 +242,15 @@ __device__ void rank_finish(const DevState& s, int r, const uint64_t* keys, doub
   } else if (s.algo == SNES) {
     for (int j = threadIdx.x; j < N; j += T) {
       dir[j] = (uint32_t)j;
-      cA[j] = (double)shaped[j];
+      cA[j] = (double)shaped_r[j];
     }
   } else {
-    if (threadIdx.x == 0) sh_nw = E[(uint32_t)keys[rs.mu - 1]] + 1;   // end of μ−1's tie group
+    if (threadIdx.x == 0) sh_nw = E_r[(uint32_t)keys[rs.mu - 1]] + 1;   // end of μ−1's tie group
     __syncthreads();
     for (int p = threadIdx.x; p < sh_nw; p += T) {
-      const int j = perm[p];
+      const int j = perm_r[p];
       dir[p] = (uint32_t)j;
-      cA[p] = (double)shaped[j];
+      cA[p] = (double)shaped_r[j];
     }
   }
   __syncthreads();
@@ -249,6 +269,21 @@ __device__ __forceinline__ uint64_t load_key(const DevState& s, const float* __r
   s.fit[(int64_t)r * s.N + p] = f;
   if (fs) fs[p] = f;
   return ((uint64_t)rank_key(f) << 32) | (uint32_t)p;
+}
+
+// The on-chip finish arrays after the keys and fitness (N ≤ kAuxMaxN; the launch sizes the shared
+// memory accordingly), with the run's position weights prefetched while the keys load and sort.
+__device__ __forceinline__ RankAux rank_aux(const DevState& s, int r, float* base, int npad) {
+  if (npad > kAuxMaxN) return RankAux{};
+  RankAux a;
+  a.shaped = base;
+  a.E = reinterpret_cast<int32_t*>(base + npad);
+  a.perm = reinterpret_cast<int32_t*>(base + 2 * npad);
+  float* w = base + 3 * npad;
+  const float* wg = s.wpos + (int64_t)r * s.N;
+  for (int p = threadIdx.x; p < s.N; p += blockDim.x) w[p] = wg[p];
+  a.wpos = w;                                      // visible after the caller's barrier
+  return a;
 }
 
 // In-shared-memory bitonic steps k ∈ [k0, k1], all j < k (indices global: direction (g & k)).
@@ -341,10 +376,11 @@ __global__ void rank_kernel_smem(DevState s, const float* __restrict__ fsrc, int
   pdl_enter();
   const int r = blockIdx.x;
   float* fs = reinterpret_cast<float*>(keys + npad);
+  const RankAux aux = rank_aux(s, r, fs + npad, npad);
   for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
   __syncthreads();
   bitonic_smem(keys, npad, 0, 2, npad, npad);
-  rank_finish(s, r, keys, red, &sh_nw, fs);
+  rank_finish(s, r, keys, red, &sh_nw, fs, aux);
 }
 
 // N ≤ 8192: one CTA per run, the sort in registers (+ shared memory for the long strides).
@@ -356,10 +392,11 @@ __global__ void rank_kernel(DevState s, const float* __restrict__ fsrc, int npad
   pdl_enter();
   const int r = blockIdx.x;
   float* fs = reinterpret_cast<float*>(keys + npad);   // the fitness, kept on chip for the finish
+  const RankAux aux = rank_aux(s, r, fs + npad, npad);
   for (int p = threadIdx.x; p < npad; p += blockDim.x) keys[p] = load_key(s, fsrc, r, p, fs);
   __syncthreads();
   bitonic_regs<E>(keys, npad);
-  rank_finish(s, r, keys, red, &sh_nw, fs);
+  rank_finish(s, r, keys, red, &sh_nw, fs, aux);
 }
 
 // N > 16384: hybrid bitonic sort over global memory. Chunks of kChunk keys are sorted and merged
@@ -967,7 +1004,9 @@ cudaError_t launch_rank(const DevState& s, const float* fsrc, cudaStream_t st) {
     const int pad = std::max(npad, 64);
     const int T = std::min(1024, pad / 2);
     const int E = pad / T;
-    const size_t sm = (size_t)pad * (sizeof(uint64_t) + sizeof(float));   // keys + fitness
+    // keys + fitness (+ the finish's on-chip arrays and weights for pad ≤ kAuxMaxN)
+    const size_t sm = (size_t)pad * (sizeof(uint64_t) + sizeof(float)) +
+                      (pad <= kAuxMaxN ? (size_t)pad * 16 : 0);
     switch (E) {
       case 2: return launch_pdl(rank_kernel<2>, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
       case 4: return launch_pdl(rank_kernel<4>, dim3(s.R), dim3(T), sm, st, s, fsrc, pad);
