@@ -485,7 +485,16 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   __shared__ float sval[kCountT];
   __shared__ double red[32];
   __shared__ int sh_last;
+#ifdef ES_RANK_TRACE
+  long long rtr[12];
+  int nrt = 0;
+#define RKT() do { if (nrt < 12) rtr[nrt++] = clock64(); } while (0)
+#else
+#define RKT() do { } while (0)
+#endif
+  RKT();
   pdl_enter();
+  RKT();
   const int N = s.N, r = blockIdx.z, jt = gridDim.x, ni = gridDim.y;
   // the run's hyperparameters, loaded before any store (a load after a store to another array
   // cannot be hoisted above it: one more dependent round trip each)
@@ -493,21 +502,26 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
   const int j = blockIdx.x * kCountT + threadIdx.x;
   const float fj = j < N ? fit_at(s, fsrc, r, j) : 0.0f;
   const uint32_t kj = j < N ? rank_key(fj) : 0xFFFFFFFFu;
+  RKT();
   const int i0 = blockIdx.y * ilen, i1 = min(N, i0 + ilen);
   const int jt0 = blockIdx.x * kCountT;
   uint32_t cpos = 0, clt = 0, cle = 0;
+  const bool solo = jt == 1 && ni == 1;
   for (int b = i0; b < i1; b += kCountT) {
     const int n = min(kCountT, i1 - b);
     __syncthreads();
-    if (threadIdx.x < n) tile[threadIdx.x] = rank_key(fit_at(s, fsrc, r, b + threadIdx.x));
+    // one CTA for the run: the tile is its own keys (no second load of the fitness)
+    if (threadIdx.x < n) tile[threadIdx.x] = solo ? kj : rank_key(fit_at(s, fsrc, r, b + threadIdx.x));
     __syncthreads();
     uint32_t lt = 0, le = 0;
     if (n == kCountT) {
-#pragma unroll 16
-      for (int e = 0; e < kCountT; ++e) {
-        const uint32_t k = tile[e];
-        lt += k < kj;
-        le += k <= kj;
+      // 16-byte broadcast reads, 8 in flight (a scalar read per key was ≈ 22 cycles per key)
+      const uint4* t4 = reinterpret_cast<const uint4*>(tile);
+#pragma unroll 8
+      for (int e = 0; e < kCountT / 4; ++e) {
+        const uint4 k4 = t4[e];
+        lt += (k4.x < kj) + (k4.y < kj) + (k4.z < kj) + (k4.w < kj);
+        le += (k4.x <= kj) + (k4.y <= kj) + (k4.z <= kj) + (k4.w <= kj);
       }
     } else {
       for (int e = 0; e < n; ++e) {
@@ -530,10 +544,10 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       }
     }
   }
+  RKT();
   const int64_t RN = (int64_t)s.R * N, rj = (int64_t)r * N + j;
   // one CTA covers the whole run (N ≤ 256): the counts are final in registers — no atomics,
   // arrival counters or fences (the multi-CTA path's four global round trips are its latency)
-  const bool solo = jt == 1 && ni == 1;
   if (!solo) {
     if (j < N) {
       if (cpos) atomicAdd(&s.rcnt[rj], cpos);
@@ -599,19 +613,25 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
       if (cmaish && pos == rs_mu - 1) rc_slot(s)[2 * r + 1] = (uint32_t)(ej + 1);
     }
   }
+  RKT();
   sval[threadIdx.x] = val;
   __syncthreads();
+  RKT();
   uint32_t* dir = s.dir + (int64_t)r * N;
   double* cA = s.coefA + (int64_t)r * N;
   double* cB = s.coefB + (int64_t)r * N;
   double part = 0.0;
+  double cb_pre = 0.0;                      // PGPE (cp + cm)/2 of this thread's pair
   if (anti) {
     if (j < N && !(j & 1)) {               // pair i = j/2 (N even; the partner is in this tile)
       const int i = j >> 1;
       const double cp = sval[threadIdx.x], cm = sval[threadIdx.x + 1];
       dir[i] = (uint32_t)i;
       cA[i] = __dsub_rn(cp, cm);
-      if (s.algo == PGPE) cB[i] = __dmul_rn(__dadd_rn(cp, cm), 0.5);   // − b̄ by the last tile
+      if (s.algo == PGPE) {
+        cb_pre = __dmul_rn(__dadd_rn(cp, cm), 0.5);
+        if (!solo) cB[i] = cb_pre;         // − b̄ by the last tile
+      }
     }
     if (s.algo == PGPE) part = j < N ? (double)val : 0.0;
   } else if (j < N) {
@@ -623,17 +643,35 @@ __global__ void __launch_bounds__(kCountT) rank_count_kernel(DevState s,
     const double t = block_sum(part, red);
     if (solo) {                               // the baseline and the generation's scalars here
       const double bbar = t / (double)N;
-      __syncthreads();
-      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) cB[i] = __dsub_rn(cB[i], bbar);
+      // the pair's thread still holds (cp + cm)/2: one store, no read back of cB
+      if (j < N && !(j & 1)) cB[j >> 1] = __dsub_rn(cb_pre, bbar);
+      RKT();
       if (threadIdx.x == 0) write_genscal(s, r, sh_jbest, sh_fbest, 0, bbar, 0.0f);
+#ifdef ES_RANK_TRACE
+      RKT();
+      if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+        printf("rank trace pgpe:");
+        for (int i = 1; i < nrt; ++i) printf(" %lld", rtr[i] - rtr[i - 1]);
+        printf("\n");
+      }
+#endif
       return;
     }
     if (threadIdx.x == 0) s.rbpart[(int64_t)r * kCountMaxTiles + blockIdx.x] = t;
   }
   if (solo) {
     __syncthreads();
+    RKT();
     if (threadIdx.x == 0)
       write_genscal(s, r, sh_jbest, sh_fbest, cmaish ? sh_nw : 0, 0.0, 0.0f);
+#ifdef ES_RANK_TRACE
+    RKT();
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+      printf("rank trace:");
+      for (int i = 1; i < nrt; ++i) printf(" %lld", rtr[i] - rtr[i - 1]);
+      printf("\n");
+    }
+#endif
     return;
   }
   // ---- the last j-tile of the run: the generation's scalars

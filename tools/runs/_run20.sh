@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-T=${TAG:-r2bf}
+T=${TAG:-r2bh}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail gpurun_out/${T}_build.log; exit 1; }
 timeout 600 python -m pytest tests -m gpu -q -x -k "rank or tell or shap or variant or ars or pgpe" > gpurun_out/${T}_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/${T}_tests.log; grep -E "^FAILED|Error" gpurun_out/${T}_tests.log | head
 for c in "--steps 20 --warmup 5 --no-cpu-baseline" "--config c3 --steps 50 --warmup 5 --no-cpu-baseline" "--config c1 --steps 50 --warmup 5 --no-cpu-baseline" "--config c5 --steps 10 --warmup 3 --no-cpu-baseline"; do
