@@ -18,7 +18,28 @@ template <int FN, bool V4>
 __device__ __forceinline__ double row_partial(const float* __restrict__ row, int64_t D, int64_t qa,
                                               int64_t qb, int64_t lane0, int64_t stride) {
   FitAcc acc;
-  if (V4) {
+  if (V4 && FN != FN_ROSENBROCK) {
+    // quad indices within a row fit 32 bits: 32-bit compares and increments; a quad past the
+    // range is neither loaded nor zero-filled (the consuming loop stops before it). Same
+    // per-thread order as the general loop below.
+    constexpr int kU = 4;
+    const int Q = (int)qb, st = (int)stride;
+    const float4* row4 = reinterpret_cast<const float4*>(row);
+    for (int q0 = (int)(qa + lane0); q0 < Q; q0 += kU * st) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (q0 + u * st < Q) v[u] = __ldcs(row4 + q0 + u * st);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (q0 + u * st >= Q) break;
+        fit_add<FN>(acc, v[u].x, v[u].y, true);
+        fit_add<FN>(acc, v[u].y, v[u].z, true);
+        fit_add<FN>(acc, v[u].z, v[u].w, true);
+        fit_add<FN>(acc, v[u].w, 0.0f, false);
+      }
+    }
+  } else if (V4) {
     // kU float4 loads issued before any is consumed (the loop was load-latency bound: one
     // 16-byte load in flight per thread); the accumulation order per thread is unchanged
     constexpr int kU = 4;
@@ -69,7 +90,7 @@ __device__ __forceinline__ double warp_sum(double v) { return warp_sum_d(v); }
 // measured slower at C2: 121.5 vs 115 µs — the per-row load → reduce → next-row chain of a
 // persistent warp hides less latency than fresh warps do.)
 template <int FN, bool V4>
-__global__ void __launch_bounds__(256) eval_warp_kernel(const float* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(256, FN == FN_ROSENBROCK ? 6 : 8) eval_warp_kernel(const float* __restrict__ x, int64_t n,
                                                         int64_t D, float* __restrict__ f) {
   pdl_enter();
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
