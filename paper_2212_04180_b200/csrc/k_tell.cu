@@ -356,15 +356,27 @@ __global__ void sepcma_norm_kernel(DevState s, int bpr) {
   if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
 }
 
-// p_c and C of element idx (run r, dim d) from Z, Q (s.G) and h_σ.
-__device__ __forceinline__ void sepcma_pc_elem(const DevState& s, int r, int64_t d) {
+// The run's p_c / C coefficients (binary64 → binary32, as the oracle rounds them), once per run.
+struct PcCoef {
+  float omcc, kc, aC, c1f, cmuf;
+};
+__device__ __forceinline__ PcCoef sepcma_pc_coef(const DevState& s, int r) {
   const RunScal& rs = s.rs[r];
   const GenScal& gs = s.gs[r];
   const double hs = gs.hsig ? 1.0 : 0.0;
-  const float omcc = (float)(1.0 - rs.c_c);
-  const float kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
-  const float aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
-  const float c1f = (float)rs.c_1, cmuf = (float)rs.c_mu;
+  PcCoef k;
+  k.omcc = (float)(1.0 - rs.c_c);
+  k.kc = gs.hsig ? (float)sqrt(rs.c_c * (2.0 - rs.c_c) * rs.mueff) : 0.0f;
+  k.aC = (float)(1.0 - rs.c_1 - rs.c_mu + (1.0 - hs) * rs.c_1 * rs.c_c * (2.0 - rs.c_c));
+  k.c1f = (float)rs.c_1;
+  k.cmuf = (float)rs.c_mu;
+  return k;
+}
+
+// p_c and C of element idx (run r, dim d) from Z, Q (s.G) and h_σ.
+__device__ __forceinline__ void sepcma_pc_elem(const DevState& s, int r, int64_t d,
+                                               const PcCoef& k) {
+  const float omcc = k.omcc, kc = k.kc, aC = k.aC, c1f = k.c1f, cmuf = k.cmuf;
   const float Z = (float)__ldcg(&s.G[gidx(s, 0, r, d)]);
   const float Qv = (float)__ldcg(&s.G[gidx(s, 1, r, d)]);
   const int64_t idx = (int64_t)r * s.D + d;
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(256) p2p_sepcma_pc_kernel(DevState s, PeerTabl
   const int r = blockIdx.y;
   const int64_t d = d0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= d1) return;
-  sepcma_pc_elem(s, r, d);
+  sepcma_pc_elem(s, r, d, sepcma_pc_coef(s, r));
   const int64_t idx = (int64_t)r * s.D + d;
   const float c = s.vec[F_C][idx];
   for (int v = 0; v < pt.W; ++v)
@@ -535,7 +547,7 @@ cudaError_t launch_nvls_apply(const DevState& s, const NvlsView& v, cudaStream_t
 __global__ void __launch_bounds__(256) sepcma_pc_kernel(DevState s) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)s.R * s.D) return;
-  sepcma_pc_elem(s, (int)(gid / s.D), gid % s.D);
+  sepcma_pc_elem(s, (int)(gid / s.D), gid % s.D, sepcma_pc_coef(s, (int)(gid / s.D)));
 }
 
 // ClipUp (Toklu et al. 2020), phases after the gradient g is parked in s.G:
@@ -728,7 +740,8 @@ __global__ void __launch_bounds__(256) sepcma_finish_kernel(DevState s, int bpr)
   const double n2 = s.dshard ? s.n2[r] : normpart_total(s, r, bpr, red);
   if (threadIdx.x == 0) sepcma_sigma(s, r, n2);
   __syncthreads();                               // h_σ (global, this CTA's own write) visible
-  for (int64_t d = threadIdx.x; d < s.D; d += blockDim.x) sepcma_pc_elem(s, r, d);
+  const PcCoef k = sepcma_pc_coef(s, r);          // once per thread, not per element
+  for (int64_t d = threadIdx.x; d < s.D; d += blockDim.x) sepcma_pc_elem(s, r, d, k);
 }
 
 cudaError_t launch_sepcma_finish(const DevState& s, cudaStream_t st, int* nk) {
