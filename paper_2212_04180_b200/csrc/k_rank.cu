@@ -1006,6 +1006,13 @@ static bool use_radix(const DevState& s) {
 }
 
 static bool use_count(const DevState& s) {
+  // N ≤ 256: one counting CTA per run (no cross-CTA traffic) for any number of runs (A/B switch
+  // ES_COUNT_MANY=0 keeps the per-run bitonic sort for R > 16)
+  static const bool many = [] {
+    const char* e = std::getenv("ES_COUNT_MANY");
+    return !(e && e[0] == '0');
+  }();
+  if (s.rank_par && many && s.N <= kCountT && s.R <= 65535) return true;
   return s.rank_par && s.R <= kCountMaxR && s.N <= kCountMaxN && !use_radix(s);
 }
 
