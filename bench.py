@@ -658,7 +658,12 @@ def main():
         achieved = d["bytes"] / secs / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
-    roof.update(kernel=dom, launches=d["launches"], peak_source=peaks["src"],
+    src = peaks["src"]
+    if roof["bound"] == "alu":   # derived, not measured: unit counts x the max SM clock
+        src = (f"derived: 148 SMs x 4 SMSPs x 32 lanes x {peaks['sm_max_mhz']:.0f} MHz "
+               f"(clock from MEASURED_PEAKS.json)" if src == "measured" else
+               "derived: 148 SMs x 4 SMSPs x 32 lanes x 1965 MHz (B200_PROFILING.md)")
+    roof.update(kernel=dom, launches=d["launches"], peak_source=src,
                 traffic=ncu_traffic(args.config, dom))
     extra = {}
     for k, v in kinds.items():
