@@ -747,37 +747,44 @@ def ncu_traffic(cfg_key, kernel):
 
 def e2e_run(hs, args, world, fused=False, write_x=True):
     """Same metric through the public API with host buffers: per step and handle, ask on the
-    device, evaluate into PINNED HOST fitness (D2H), tell from that host buffer (H2D), and read
-    best_fitness back (D2H)."""
+    device, evaluate, copy the fitness into PINNED HOST memory (D2H), tell from that host buffer
+    (H2D), and read best_fitness back (D2H)."""
     import torch
     fh = [torch.empty((cfg["R"], es.local_popsize), dtype=torch.float32).pin_memory()
+          for _, cfg, es, _, _ in hs]
+    fd = [torch.empty((cfg["R"], es.local_popsize), dtype=torch.float32, device="cuda")
           for _, cfg, es, _, _ in hs]
     bh = [torch.empty(cfg["R"], dtype=torch.float32).pin_memory() for _, cfg, _, _, _ in hs]
     from paper_2212_04180_b200._lib import check, lib
     import ctypes as C
 
-    # independent handles on their own streams (as a user driving two batches would): the asks
-    # are issued for every handle first; then, handle by handle, the evaluation into host memory
-    # (which waits on that handle's stream only) and the tell from it, so one handle's tell is
-    # already queued while the host waits for the next handle's fitness; best_fitness last
+    # independent handles on their own streams (as a user driving two batches would): every
+    # handle's ask, evaluation and fitness D2H copy (cudaMemcpyAsync into pinned memory) is
+    # queued first; then, handle by handle, the host waits for that handle's copy and tells from
+    # the host buffer (the library's H2D), so the GPU queue never drains while the host waits;
+    # best_fitness last
     streams = [torch.cuda.Stream() for _ in hs] if len(hs) > 1 else [torch.cuda.current_stream()]
     ss = [C.c_void_p(st.cuda_stream) for st in streams]
+    evs = [torch.cuda.Event() for _ in hs]
 
     def step():
-        if not fused and hs[0][1]["fn"] is not None:
-            for (label, cfg, es, x, _), st in zip(hs, streams):
-                es.ask(out=x, stream=st)
-        for (label, cfg, es, x, _), f, s in zip(hs, fh, ss):
+        for (label, cfg, es, x, _), f, d, s, st, ev in zip(hs, fh, fd, ss, streams, evs):
             n = cfg["R"] * es.local_popsize
             if cfg["fn"] is None:
-                check(lib().es_synth_fitness(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
+                check(lib().es_synth_fitness(es.ctx, C.c_void_p(d.data_ptr()), s), es.ctx)
             elif fused:
                 check(lib().es_ask_eval(es.ctx, cfg["fn"],
                                         C.c_void_p(x.data_ptr()) if write_x else None,
-                                        C.c_void_p(f.data_ptr()), s), es.ctx)
+                                        C.c_void_p(d.data_ptr()), s), es.ctx)
             else:
+                es.ask(out=x, stream=st)
                 check(lib().es_eval_bbob(es.ctx, cfg["fn"], C.c_void_p(x.data_ptr()), n,
-                                         cfg["D"], C.c_void_p(f.data_ptr()), s), es.ctx)
+                                         cfg["D"], C.c_void_p(d.data_ptr()), s), es.ctx)
+            with torch.cuda.stream(st):
+                f.copy_(d, non_blocking=True)                  # D2H into pinned host memory
+                ev.record(st)
+        for (label, cfg, es, x, _), f, s, ev in zip(hs, fh, ss, evs):
+            ev.synchronize()                                   # this handle's fitness on the host
             check(lib().es_tell(es.ctx, C.c_void_p(f.data_ptr()), s), es.ctx)
         for (label, cfg, es, x, _), b, s in zip(hs, bh, ss):
             check(lib().es_get(es.ctx, 8, C.c_void_p(b.data_ptr()), s), es.ctx)
