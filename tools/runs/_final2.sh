@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-T=${TAG:-r2final4}
+T=${TAG:-r2final5}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail gpurun_out/${T}_build.log; exit 1; }
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/${T}_smoke.log
 timeout 900 python bench.py > gpurun_out/${T}_bench_default.log 2>&1; echo bench default rc=$?; tail -1 gpurun_out/${T}_bench_default.log | cut -c1-300
