@@ -463,6 +463,7 @@ __global__ void rank_finish_kernel(DevState s, const uint64_t* __restrict__ gkey
 // finishes its 256 members: tie group, shaped value (N10 / N11 / raw), perm, the tell's
 // (direction, coefficient) entries; the last j-tile of a run writes the generation's scalars
 // (and subtracts PGPE's baseline, N12). Counters are cleared for the next generation on the way.
+// N ≤ 256 at any run count: one CTA per run holds the whole run (no atomics, no arrivals).
 static constexpr int kCountMaxR = 16, kCountMaxN = 16384, kCountT = 256;
 static constexpr int kCountMaxTiles = kCountMaxN / kCountT;
 
